@@ -1,0 +1,247 @@
+/* duchess_b200.h — C-ABI of the B200 DUCHESS probe + orchestration hot path.
+ *
+ * The reference (arxiv 2509.24957, `branchsim`, pure Python) has no FFI; its
+ * seams for this path are Python callables. Each entry point below replaces
+ * one of them, batched over many requests, and is what a ctypes / cffi binding
+ * of the reference would call:
+ *
+ *   duchess_score            <- predictor.py:126-151  mlp_forward (linear probe),
+ *                               called per survivor via the predictor seam
+ *                               orchestrator.py:358-363; + token pooling (extension)
+ *   duchess_advance          <- orchestrator.py:344-355  DuchessRun.step phase 1
+ *                               (_decode_chunk :273-279, _probe :281-285, _collect :287-290)
+ *                               + RequestRun.__init__ seeding :242-248 on refill
+ *   duchess_decide           <- orchestrator.py:357-402  DuchessRun.step phases 2-5
+ *                               (make_correctness_predictor :211-224, branch_out_sample
+ *                               :188-197, _spawn :254-268, check_request_termination
+ *                               :200-208, majority_vote core.py:76-83)
+ *   duchess_sort_difficulty  <- scheduler.py:60-96  next_request pops over a snapshot
+ *   duchess_fork_cow         <- orchestrator.py:254-268 _spawn(offset_base=source.position)
+ *                               executed on a paged KV block table (extension)
+ *   duchess_lr_grad          <- probe training (absent in reference)
+ *
+ * Conventions: every pointer is caller-owned DEVICE memory unless stated;
+ * every call is stream-ordered and non-blocking on `stream` (a cudaStream_t,
+ * NULL = legacy default stream) and returns DUCHESS_OK (0) or an error code.
+ * No C++ exception crosses this boundary.
+ */
+#ifndef DUCHESS_B200_H
+#define DUCHESS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DUCHESS_F32 0
+#define DUCHESS_BF16 1
+
+/* Branch status (orchestrator.py:35-40). */
+#define DUCHESS_ACTIVE 0
+#define DUCHESS_EARLY_TERMINATED 1
+#define DUCHESS_NATURAL_END 2
+#define DUCHESS_CAPPED 3
+#define DUCHESS_CANCELLED 4
+
+/* Request termination reasons (orchestrator.py:42-45). */
+#define DUCHESS_REASON_NONE 0
+#define DUCHESS_REASON_CONSENSUS 1
+#define DUCHESS_REASON_COVERAGE 2
+#define DUCHESS_REASON_EXHAUSTED 3
+
+/* Branch actions (orchestrator.py:128-132). */
+#define DUCHESS_ACT_CONTINUE 1
+#define DUCHESS_ACT_TERMINATE 2
+#define DUCHESS_ACT_BRANCH_OUT 3
+
+/* Correctness-prediction source for DuchessRun.step phase 2. */
+#define DUCHESS_PRED_DEVICE 0 /* probabilities from duchess_score (K1), by branch slot */
+#define DUCHESS_PRED_TRACE 1  /* make_correctness_predictor: pred_probs else synthetic */
+#define DUCHESS_PRED_HOST 2   /* caller-supplied probabilities by slot (predictor= callable) */
+
+#define DUCHESS_MT_WORDS 625 /* 624 MT19937 words + index, as random.Random.getstate() */
+#define DUCHESS_MAX_SLOTS 64 /* max_branches limit of the warp-per-request kernel */
+#define DUCHESS_REC_WORDS 12
+
+/* Round record fields (RoundReport, orchestrator.py:149-159, plus bookkeeping). */
+#define DUCHESS_REC_ROUND 0     /* round_index; 0 = slot ran no round this step */
+#define DUCHESS_REC_DECODING 1  /* decoding_branches */
+#define DUCHESS_REC_MAX_CHUNK 2 /* max_chunk */
+#define DUCHESS_REC_DECODE 3    /* decode_tokens */
+#define DUCHESS_REC_PROBES 4    /* probes */
+#define DUCHESS_REC_NACTIONS 5  /* len(actions) */
+#define DUCHESS_REC_DONE 6      /* done */
+#define DUCHESS_REC_NFORKS 7    /* branch_out actions this round */
+#define DUCHESS_REC_NSURV 8     /* survivors scored + decided (branch-steps) */
+#define DUCHESS_REC_REQ 9       /* pool index of the request in this slot */
+#define DUCHESS_REC_REASON 10   /* termination reason if done */
+#define DUCHESS_REC_FINAL 11    /* majority-vote answer id if done */
+
+/* Counters (int64). */
+#define DUCHESS_CNT_AMBIGUOUS 0 /* branch-out draws within 4 ulp of a CDF boundary */
+#define DUCHESS_CNT_ERRORS 1    /* requests that hit "no answers collected" */
+#define DUCHESS_CNT_FINISHED 2  /* requests finished */
+#define DUCHESS_CNT_BRANCH_STEPS 3
+#define DUCHESS_CNT_FORKS 4
+#define DUCHESS_N_COUNTERS 8
+
+typedef struct DuchessPolicy {
+  int32_t max_branches;      /* c, orchestrator.py:66 */
+  int32_t interval_tokens;   /* i, :67 */
+  int32_t early_term_rounds; /* S, :69 */
+  int32_t token_cap;         /* :73 */
+  int32_t probe_cost_tokens; /* :74 */
+  int32_t need_consensus;    /* _at_least(consensus_frac, c), :162-164, :204 */
+  int32_t need_coverage;     /* _at_least(coverage_frac, c), :206 */
+  int32_t pred_source;       /* DUCHESS_PRED_* */
+  int32_t n_layers;          /* probability columns per slot in `probs` */
+  int32_t combine;           /* 0 = layer 0, 1 = mean over layers */
+  double early_term_threshold; /* tau, :68; +inf disables (:58-59) */
+  double inv_temperature;      /* 1.0 / branch_out_temperature, computed by the host (:182) */
+  double rho;                  /* SyntheticPredictorConfig.rho, predictor.py:321 */
+} DuchessPolicy;
+
+/* Read-only workload tables for a pool of P requests (workload.py:35-60).
+ * Answers are interned per request in sorted string order with "" (NO_ANSWER)
+ * as id 0, so min(id) == min(str) as majority_vote needs (core.py:83). */
+typedef struct DuchessWorkload {
+  int32_t n_requests;       /* P */
+  int32_t queue_len;        /* entries in `queue` */
+  int32_t cycle;            /* 1 = restart the queue when exhausted (steady-state bench) */
+  int32_t _pad;
+  const int32_t* tmpl_off;  /* [P+1] template CSR */
+  const int32_t* ground_truth; /* [P] */
+  const uint32_t* mt_init;  /* [P*625] random.Random(seed).getstate() */
+  const int32_t* nat_len;   /* [NT] */
+  const int32_t* final_ans; /* [NT] */
+  const int32_t* conv;      /* [NT] oracle_convergence, -1 = None */
+  const int32_t* probe_off; /* [NT+1] */
+  const int32_t* probe_at;  /* [NP] */
+  const int32_t* probe_ans; /* [NP] */
+  const int32_t* pred_off;  /* [NT+1] */
+  const int32_t* pred_at;   /* [NQ] */
+  const double* pred_p;     /* [NQ] */
+  const int32_t* queue;     /* [queue_len] pool indices in service order */
+} DuchessWorkload;
+
+/* Mutable engine state: R request slots x C branch slots, Bmax branch ids. */
+typedef struct DuchessState {
+  int32_t n_slots;     /* R */
+  int32_t branch_cap;  /* Bmax >= templates of any request */
+  int32_t answer_cap;  /* A >= distinct answers of any request */
+  int32_t _pad;
+  /* per request slot [R] */
+  int32_t* slot_req;
+  int32_t* needs_refill;
+  int32_t* n_branches;
+  int32_t* next_template;
+  int32_t* tokens_decode;
+  int32_t* tokens_probe;
+  int32_t* rounds;
+  int32_t* done;
+  int32_t* tally;      /* [R*A] */
+  uint32_t* mt;        /* [R*625] */
+  /* per branch [R*Bmax] */
+  int32_t* br_offset;
+  int32_t* br_decoded;
+  int32_t* br_streak;
+  int32_t* br_status;
+  int32_t* br_final;
+  int32_t* br_npred;
+  int32_t* br_slot;
+  double* br_last_pred;
+  /* per branch slot [R*C] */
+  int32_t* slot_branch;
+  uint8_t* row_mask;   /* survivors to score this round */
+  int32_t* row_pos;
+  int32_t* row_tmpl;
+  int64_t* row_req;
+  /* latest round */
+  int32_t* round_rec;  /* [R*DUCHESS_REC_WORDS] */
+  int32_t* actions;    /* [R*2C*3] (kind, branch_id, source_branch_id or -1) */
+  int32_t* forks;      /* [R*C*4]  (child, source, table_root, prefix_tokens) */
+  double* step_pred;   /* [R*C] prediction used for each survivor, by slot */
+  int32_t* queue_head; /* [2] */
+  /* outcomes by pool index [P] */
+  int32_t* out_final;
+  int32_t* out_reason;
+  int32_t* out_tokens_decode;
+  int32_t* out_tokens_probe;
+  int32_t* out_rounds;
+  int32_t* out_error;
+  int32_t* out_tally;  /* [P*A] */
+  long long* counters; /* [DUCHESS_N_COUNTERS] */
+} DuchessState;
+
+/* ---- K1: pooled LayerNorm + linear-probe scoring ------------------------ */
+size_t duchess_score_workspace_bytes(int64_t n_units, int32_t nsplit_max);
+int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers, int32_t T,
+                  int32_t H, int64_t row_stride, int64_t layer_stride, int64_t token_stride,
+                  const float* wg, const float* c1, const uint8_t* row_mask, float* out_logit,
+                  double* out_prob, void* workspace, size_t workspace_bytes, int32_t nsplit,
+                  int32_t threads, void* stream);
+int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                             int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                             int64_t token_stride, uint64_t seed, const int64_t* row_req,
+                             const int32_t* row_tmpl, const int32_t* row_pos,
+                             const uint8_t* row_mask, void* stream);
+
+/* ---- K2: per-request decisions (host pointers to the POD structs) -------- */
+int duchess_advance(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                    const DuchessState* state, void* stream);
+int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                   const DuchessState* state, const double* probs, void* stream);
+
+/* Rule primitives (orchestrator.py:177-197, :200-208; core.py:76-83). */
+int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,
+                              uint32_t* mt_state, int32_t n_draws, int32_t* out_idx,
+                              double* out_weights, long long* out_ambiguous, void* stream);
+int duchess_vote(const int32_t* counts, int32_t n_sets, int32_t n_answers,
+                 int32_t need_consensus, int32_t need_coverage, int32_t* out_final,
+                 int32_t* out_reason, void* stream);
+int duchess_template_lookup(const DuchessWorkload* workload, const int32_t* tmpl,
+                            const int32_t* pos, int32_t n, int32_t* out_probe_answer,
+                            double* out_trace_pred, void* stream);
+
+/* ---- difficulty ordering (scheduler.py:60-96) --------------------------- */
+int duchess_sort_difficulty(const uint64_t* keys, const int32_t* seg_offsets, int32_t n_segs,
+                            int32_t* out_perm, void* stream);
+
+/* ---- K3: copy-on-write block-table fork ----------------------------------
+ * Fork records are (child, source, table_root, prefix_tokens) int32 quads laid
+ * out as [n_groups][group_cap]; group g holds group_counts[g*counts_stride]
+ * valid records (group_counts NULL: group_cap each). Branch ids map to block-
+ * table rows g*rows_per_group + id. Forks are applied in (group, record)
+ * order: the child row receives the root's first prefix/block_tokens entries
+ * (refcount += 1 each); a partial tail block is taken from
+ * free_list[*free_cursor + k] (k = rank among tail-needing forks), gets
+ * refcount 1 and a copy of the root's first prefix%block_tokens tokens of KV
+ * bytes. Remaining child entries are set to -1. *free_cursor advances by the
+ * number of tail blocks taken. status[0] is set to 1 if the free list ran out. */
+size_t duchess_fork_workspace_bytes(int32_t n_groups, int32_t group_cap);
+int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const int32_t* group_counts,
+                     int32_t counts_stride, int32_t n_groups, int32_t rows_per_group,
+                     int32_t* block_table, int32_t table_stride, int32_t* refcount,
+                     const int32_t* free_list, int32_t free_list_len, int32_t* free_cursor,
+                     void* kv_pool, int64_t kv_bytes_per_token, int32_t block_tokens,
+                     int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K4: logistic-regression gradient for probe training ------------------
+ * grad[h] = inv_n * sum_i (sigmoid(x_i . w + w[H]) - y_i) x_ih, grad[H] = the
+ * bias term; w and grad are [H+1] fp32 (bias last). One HBM pass over X. */
+size_t duchess_lr_grad_workspace_bytes(int32_t H);
+int duchess_lr_grad(const void* X, int32_t dtype, const float* y, const float* w,
+                    int64_t n_rows, int32_t H, float inv_n, float* grad_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+int duchess_sgd_update(float* w, const float* grad, int32_t n, float lr, void* stream);
+
+/* Build/runtime introspection. */
+const char* duchess_version(void);
+int duchess_device_arch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DUCHESS_B200_H */

@@ -1,0 +1,83 @@
+// Shared device helpers for the DUCHESS B200 hot path (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "duchess_b200 targets sm_100a only"
+#endif
+
+#define DUCHESS_OK 0
+#define DUCHESS_EINVAL 1
+#define DUCHESS_ECUDA 2
+
+namespace duchess {
+
+constexpr float kLayerNormEps = 1e-5f;   // predictor.py:21 LAYERNORM_EPS
+constexpr double kProbClip = 1e-12;      // predictor.py:24 _PROB_CLIP
+
+// ---------------------------------------------------------------------------
+// Counter-based synthetic activation generator. Parity inputs for the probe
+// are keyed by (seed, request, template index, position, layer, token, hidden)
+// so the CPU oracle (oracle/activations.py) regenerates them bit for bit.
+// Only integer ops plus one fp32 multiply (two for outlier channels).
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t row_key(uint64_t seed, uint64_t req,
+                                                     uint64_t tmpl, uint64_t pos,
+                                                     uint64_t layer) {
+  uint64_t k = mix64(seed);
+  k = mix64(k ^ req);
+  k = mix64(k ^ tmpl);
+  return mix64(k ^ ((pos << 8) | layer));
+}
+
+constexpr float kActScale = 0x1.bb67aep-16f;  // float32(sqrt(3) / 65536), bits 0x37ddb3d7
+constexpr float kOutlierGain = 20.0f;
+
+// Irwin-Hall(4) of 16-bit lanes -> ~N(0,1) in fp32; 8 outlier channels per 4096.
+__device__ __forceinline__ float synth_value(uint64_t rk, uint32_t t, uint32_t h) {
+  uint64_t e = mix64(rk ^ ((uint64_t(t) << 32) | h));
+  int s = int(e & 0xFFFF) + int((e >> 16) & 0xFFFF) + int((e >> 32) & 0xFFFF) +
+          int(e >> 48);
+  float x = __fmul_rn(float(s - 131070), kActScale);
+  if ((h & 511u) == 257u) x = __fmul_rn(x, kOutlierGain);
+  return x;
+}
+
+// fp32 -> bf16 round-to-nearest-even (finite inputs), as bit pattern.
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u = __float_as_uint(f);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// Streaming 128-bit load: read-once activation data, no L1 allocation.
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void add_counter(long long* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace duchess

@@ -1,0 +1,661 @@
+// K2: per-request orchestration decisions, one warp per request slot.
+//
+// Restates DuchessRun.step (reference pkg/src/branchsim/orchestrator.py:329-402)
+// for every request slot at once, bit-exact:
+//   duchess_advance: refill finished slots from the service queue
+//                    (RequestRun.__init__ seeding, :242-248) then phase 1,
+//                    decode chunk + natural-end / cap collection (:344-355).
+//   [K1 scores the survivors' activation windows between the two launches]
+//   duchess_decide : phase 2 predictions (:357-363), phase 3 early termination
+//                    (:365-373), phase 4 branch-out refill (:375-388), phase 5
+//                    request termination + majority vote (:390-399).
+//
+// IEEE fidelity: this translation unit is compiled with --fmad=false and uses
+// explicit _rn intrinsics wherever the reference's double arithmetic could
+// otherwise be contracted; random draws replay CPython's MT19937
+// genrand_res53; the branch-out normaliser replays CPython >= 3.12's
+// compensated (Neumaier) builtin sum().
+#include "common.cuh"
+#include "../../include/duchess_b200.h"
+
+namespace duchess {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kMaxC = DUCHESS_MAX_SLOTS;
+constexpr int kMtN = 624, kMtM = 397;
+constexpr double kProbFloor = 1e-6;   // orchestrator.py:56 BRANCH_PROB_FLOOR
+
+// ---------------------------------------------------------------------------
+// MT19937, CPython flavour (Modules/_randommodule.c genrand_uint32 / random()).
+
+__device__ __forceinline__ uint32_t mt_temper(uint32_t y) {
+  y ^= (y >> 11);
+  y ^= (y << 7) & 0x9d2c5680u;
+  y ^= (y << 15) & 0xefc60000u;
+  y ^= (y >> 18);
+  return y;
+}
+
+__device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t m) {
+  const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+  return m ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+}
+
+// Regenerate all 624 words, warp-cooperatively. The serial recurrence splits
+// into phases whose members only read words finalised by earlier phases.
+__device__ void mt_twist_warp(uint32_t* mt, int lane) {
+  auto phase = [&](int lo, int hi, bool old_m) {
+    for (int base = lo; base < hi; base += 32) {
+      const int kk = base + lane;
+      uint32_t nv = 0;
+      const bool act = kk < hi;
+      if (act) {
+        const uint32_t m = old_m ? mt[kk + kMtM] : mt[kk + kMtM - kMtN];
+        nv = mt_mix(mt[kk], mt[kk + 1], m);
+      }
+      __syncwarp();
+      if (act) mt[kk] = nv;
+      __syncwarp();
+    }
+  };
+  phase(0, kMtN - kMtM, true);               // [0, 227): mt[kk+397] still old
+  phase(kMtN - kMtM, 2 * (kMtN - kMtM), false);  // [227, 454): mt[kk-227] from phase A
+  phase(2 * (kMtN - kMtM), kMtN - 1, false);     // [454, 623): mt[kk-227] from phase B
+  if (lane == 0) mt[kMtN - 1] = mt_mix(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+  __syncwarp();
+}
+
+// Produce n tempered words into out[] (shared), advancing the stream.
+__device__ void mt_words_warp(uint32_t* mt, int n, uint32_t* out, int lane) {
+  int idx = int(mt[kMtN]);
+  int k = 0;
+  while (k < n) {
+    if (idx >= kMtN) {
+      mt_twist_warp(mt, lane);
+      idx = 0;
+    }
+    const int take = min(n - k, kMtN - idx);
+    for (int j = lane; j < take; j += 32) out[k + j] = mt_temper(mt[idx + j]);
+    k += take;
+    idx += take;
+  }
+  __syncwarp();
+  if (lane == 0) mt[kMtN] = uint32_t(idx);
+  __syncwarp();
+}
+
+// random.random(): (a*67108864.0 + b) * (1.0/9007199254740992.0), exact.
+__device__ __forceinline__ double mt_res53(uint32_t w0, uint32_t w1) {
+  const double a = double(w0 >> 5), b = double(w1 >> 6);
+  return __dmul_rn(__dadd_rn(__dmul_rn(a, 67108864.0), b), 1.0 / 9007199254740992.0);
+}
+
+// ---------------------------------------------------------------------------
+// Template lookups (workload.py:82-106).
+
+__device__ __forceinline__ int upper_bound(const int32_t* a, int lo, int hi, int key) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// probe_answer (workload.py:82-94). Answer id 0 is NO_ANSWER ("").
+__device__ __forceinline__ int probe_answer(const DuchessWorkload& w, int t, int pos) {
+  const int conv = w.conv[t];
+  if (conv >= 0 && pos >= conv) return w.final_ans[t];
+  const int lo = w.probe_off[t], hi = w.probe_off[t + 1];
+  if (hi > lo) {
+    const int idx = upper_bound(w.probe_at, lo, hi, pos) - 1;
+    if (idx >= lo) return w.probe_ans[idx];
+  }
+  return 0;
+}
+
+// trace_prediction (workload.py:97-106).
+__device__ __forceinline__ double trace_prediction(const DuchessWorkload& w, int t, int pos) {
+  const int lo = w.pred_off[t], hi = w.pred_off[t + 1];
+  if (hi <= lo) return 0.0;
+  const int idx = upper_bound(w.pred_at, lo, hi, pos) - 1;
+  return idx < lo ? 0.0 : w.pred_p[idx];
+}
+
+// min(max(p, 1e-6), 1.0) ** exponent (orchestrator.py:183).
+__device__ __forceinline__ double branch_raw(double p, double inv_temp) {
+  const double x = fmin(fmax(p, kProbFloor), 1.0);
+  if (inv_temp == 1.0 || x == 1.0) return x;
+  return pow(x, inv_temp);
+}
+
+// CPython >= 3.12 builtin sum() over floats: Neumaier compensation.
+struct NeumaierSum {
+  double f = 0.0, c = 0.0;
+  __device__ __forceinline__ void add(double x) {
+    const double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+    f = t;
+  }
+  __device__ __forceinline__ double result() const {
+    return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f;
+  }
+};
+
+// branch_out_sample (orchestrator.py:188-197) given precomputed raws and
+// their compensated sum; flags draws within 4 ulp of a CDF boundary.
+__device__ int sample_index(const double* raw, int n, double total, double u, bool* ambiguous) {
+  double acc = 0.0, prev = 0.0;
+  int pick = n - 1;
+  for (int j = 0; j < n; ++j) {
+    const double w = __ddiv_rn(raw[j], total);
+    prev = acc;
+    acc = __dadd_rn(acc, w);
+    if (u < acc) { pick = j; break; }
+  }
+  const double tol = 4.0 * 2.220446049250313e-16;
+  *ambiguous = fabs(u - acc) <= tol * fmax(acc, 1e-300) ||
+               (pick > 0 && fabs(u - prev) <= tol * fmax(prev, 1e-300));
+  return pick;
+}
+
+// ---------------------------------------------------------------------------
+
+struct WarpScratch {
+  uint32_t words[4 * kMaxC];
+  double draws[2 * kMaxC];
+  double raw[kMaxC];
+  int alive[kMaxC];
+  int root[kMaxC];
+};
+
+__device__ __forceinline__ int warp_count_lt(const int32_t* flags, int n, int upto, int lane) {
+  int cnt = 0;
+  for (int base = 0; base < upto; base += 32) {
+    const int j = base + lane;
+    const bool f = j < upto && j < n && flags[j] != 0;
+    cnt += __popc(__ballot_sync(0xffffffffu, f));
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= s.n_slots) return;
+  const int C = pol.max_branches;
+  const int64_t rC = int64_t(r) * C;
+  const int64_t rB = int64_t(r) * s.branch_cap;
+  int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
+
+  for (int j = lane; j < C; j += 32) s.row_mask[rC + j] = 0;
+  if (lane < DUCHESS_REC_WORDS) rec[lane] = 0;
+  __syncwarp();
+
+  // ---- refill: the k-th empty slot (slot order) takes queue[head + k] ----
+  const int head = s.queue_head[0];
+  if (r == 0) {
+    const int total = warp_count_lt(s.needs_refill, s.n_slots, s.n_slots, lane);
+    const int avail = w.cycle ? total : max(0, min(total, w.queue_len - head));
+    if (lane == 0) s.queue_head[1] = head + avail;
+  }
+  if (s.needs_refill[r]) {
+    const int rank = warp_count_lt(s.needs_refill, s.n_slots, r, lane);
+    int q = head + rank;
+    int p = -1;
+    if (w.queue_len > 0) {
+      if (w.cycle) p = w.queue[q % w.queue_len];
+      else if (q < w.queue_len) p = w.queue[q];
+    }
+    if (lane == 0) s.slot_req[r] = p;
+    if (p < 0) {
+      if (lane == 0) s.done[r] = 1;
+      return;
+    }
+    const int n_tmpl = w.tmpl_off[p + 1] - w.tmpl_off[p];
+    const int seeded = min(C, n_tmpl);   // RequestRun.__init__ :242-248
+    for (int b = lane; b < s.branch_cap; b += 32) {
+      const bool live = b < seeded;
+      s.br_offset[rB + b] = 0;
+      s.br_decoded[rB + b] = 0;
+      s.br_streak[rB + b] = 0;
+      s.br_status[rB + b] = live ? DUCHESS_ACTIVE : DUCHESS_CANCELLED;
+      s.br_final[rB + b] = -1;
+      s.br_npred[rB + b] = 0;
+      s.br_slot[rB + b] = live ? b : -1;
+      s.br_last_pred[rB + b] = 0.5;
+    }
+    for (int j = lane; j < C; j += 32) s.slot_branch[rC + j] = j < seeded ? j : -1;
+    for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
+    const uint32_t* src = w.mt_init + int64_t(p) * DUCHESS_MT_WORDS;
+    uint32_t* dst = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
+    for (int j = lane; j < DUCHESS_MT_WORDS; j += 32) dst[j] = src[j];
+    if (lane == 0) {
+      s.n_branches[r] = seeded;
+      s.next_template[r] = seeded;
+      s.tokens_decode[r] = 0;
+      s.tokens_probe[r] = 0;
+      s.rounds[r] = 0;
+      s.done[r] = 0;
+    }
+    __syncwarp();
+  }
+  if (s.done[r] || s.slot_req[r] < 0) return;
+
+  // ---- phase 1: decode one interval per active branch (:344-355) ----
+  const int p = s.slot_req[r];
+  const int t0 = w.tmpl_off[p];
+  const int nb = s.n_branches[r];
+  int decoding = 0, max_chunk = 0, dtok = 0, probes = 0;
+  for (int b = lane; b < nb; b += 32) {
+    const int64_t bi = rB + b;
+    if (s.br_status[bi] != DUCHESS_ACTIVE) continue;
+    const int t = t0 + b;                      // branch_id == template_index (:260-266)
+    const int nat = w.nat_len[t];
+    int pos = s.br_offset[bi] + s.br_decoded[bi];
+    const int room = min(nat, pol.token_cap) - pos;            // _decode_chunk :273-279
+    const int chunk = max(0, min(pol.interval_tokens, room));
+    s.br_decoded[bi] += chunk;
+    pos += chunk;
+    if (chunk > 0) { decoding++; max_chunk = max(max_chunk, chunk); dtok += chunk; }
+    int ans = -1, status = DUCHESS_ACTIVE;
+    if (pos >= nat) { ans = w.final_ans[t]; status = DUCHESS_NATURAL_END; }
+    else if (pos >= pol.token_cap) { ans = probe_answer(w, t, pos); status = DUCHESS_CAPPED; probes++; }
+    const int slot = s.br_slot[bi];
+    if (status != DUCHESS_ACTIVE) {
+      s.br_status[bi] = status;
+      s.br_final[bi] = ans;
+      atomicAdd(&s.tally[int64_t(r) * s.answer_cap + ans], 1);
+      if (slot >= 0) s.slot_branch[rC + slot] = -1;
+      s.br_slot[bi] = -1;
+    } else {
+      s.row_mask[rC + slot] = 1;
+      s.row_pos[rC + slot] = pos;
+      s.row_tmpl[rC + slot] = b;
+      s.row_req[rC + slot] = p;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    decoding += __shfl_xor_sync(0xffffffffu, decoding, o);
+    dtok += __shfl_xor_sync(0xffffffffu, dtok, o);
+    probes += __shfl_xor_sync(0xffffffffu, probes, o);
+    max_chunk = max(max_chunk, __shfl_xor_sync(0xffffffffu, max_chunk, o));
+  }
+  if (lane == 0) {
+    s.rounds[r] += 1;
+    s.tokens_decode[r] += dtok;
+    s.tokens_probe[r] += probes * pol.probe_cost_tokens;
+    rec[DUCHESS_REC_ROUND] = s.rounds[r];
+    rec[DUCHESS_REC_DECODING] = decoding;
+    rec[DUCHESS_REC_MAX_CHUNK] = max_chunk;
+    rec[DUCHESS_REC_DECODE] = dtok;
+    rec[DUCHESS_REC_PROBES] = probes;
+    rec[DUCHESS_REC_REQ] = p;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
+  __shared__ WarpScratch scratch[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int wi = threadIdx.x >> 5;
+  const int r = blockIdx.x * kWarpsPerBlock + wi;
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.queue_head[0] = s.queue_head[1];
+  if (r >= s.n_slots) return;
+  WarpScratch& sc = scratch[wi];
+  const int C = pol.max_branches;
+  const int64_t rC = int64_t(r) * C;
+  const int64_t rB = int64_t(r) * s.branch_cap;
+  const int64_t rA = int64_t(r) * s.answer_cap;
+  int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
+  if (rec[DUCHESS_REC_ROUND] == 0) return;   // slot idle or finished
+  const int p = s.slot_req[r];
+  const int t0 = w.tmpl_off[p];
+  const int n_tmpl = w.tmpl_off[p + 1] - t0;
+  int nb = s.n_branches[r];
+  uint32_t* mt = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
+  int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
+
+  // ---- phase 2: predictions for survivors, creation order (:357-363) ----
+  // Synthetic draws happen in survivor order for templates without pred_probs.
+  int n_need = 0;
+  if (pol.pred_source == DUCHESS_PRED_TRACE) {
+    for (int base = 0; base < nb; base += 32) {
+      const int b = base + lane;
+      bool need = false;
+      if (b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE) {
+        const int t = t0 + b;
+        need = w.pred_off[t + 1] <= w.pred_off[t];
+      }
+      n_need += __popc(__ballot_sync(0xffffffffu, need));
+    }
+    if (n_need > 0) {
+      mt_words_warp(mt, 2 * n_need, sc.words, lane);
+      for (int k = lane; k < n_need; k += 32) sc.draws[k] = mt_res53(sc.words[2 * k], sc.words[2 * k + 1]);
+      __syncwarp();
+    }
+  }
+  int need_rank = 0, surv_rank = 0, n_term = 0;
+  const double tau = pol.early_term_threshold;
+  for (int base = 0; base < nb; base += 32) {
+    const int b = base + lane;
+    const bool surv = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
+    const unsigned sm = __ballot_sync(0xffffffffu, surv);
+    bool need = false;
+    if (surv && pol.pred_source == DUCHESS_PRED_TRACE) {
+      const int t = t0 + b;
+      need = w.pred_off[t + 1] <= w.pred_off[t];
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    const unsigned lower = (1u << lane) - 1u;
+    bool term = false;
+    if (surv) {
+      const int64_t bi = rB + b;
+      const int slot = s.br_slot[bi];
+      const int pos = s.br_offset[bi] + s.br_decoded[bi];
+      const int t = t0 + b;
+      double pr;
+      if (pol.pred_source == DUCHESS_PRED_TRACE) {
+        if (!need) {
+          pr = trace_prediction(w, t, pos);
+        } else {
+          const double u = sc.draws[need_rank + __popc(nm & lower)];
+          // synthetic_predict (predictor.py:328-335) on probe_answer == ground truth
+          const double oracle = probe_answer(w, t, pos) == w.ground_truth[p] ? 1.0 : 0.0;
+          const double v = __dadd_rn(__dmul_rn(pol.rho, oracle), __dmul_rn(__dsub_rn(1.0, pol.rho), u));
+          pr = fmin(fmax(v, 0.0), 1.0);
+        }
+      } else if (pol.pred_source == DUCHESS_PRED_HOST || pol.n_layers == 1 || pol.combine == 0) {
+        pr = probs[(rC + slot) * pol.n_layers];
+      } else {
+        double acc = 0.0;
+        for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, probs[(rC + slot) * pol.n_layers + l]);
+        pr = __ddiv_rn(acc, double(pol.n_layers));
+      }
+      s.step_pred[rC + slot] = pr;
+      s.br_last_pred[bi] = pr;
+      s.br_npred[bi] += 1;
+      const int streak = pr > tau ? s.br_streak[bi] + 1 : 0;   // strict > (:363)
+      s.br_streak[bi] = streak;
+      // ---- phase 3: early termination (:365-373) ----
+      term = streak >= pol.early_term_rounds;
+      const int k = surv_rank + __popc(sm & lower);
+      act[k * 3 + 0] = term ? DUCHESS_ACT_TERMINATE : DUCHESS_ACT_CONTINUE;
+      act[k * 3 + 1] = b;
+      act[k * 3 + 2] = -1;
+      if (term) {
+        const int ans = probe_answer(w, t, pos);
+        s.br_status[bi] = DUCHESS_EARLY_TERMINATED;
+        s.br_final[bi] = ans;
+        atomicAdd(&s.tally[rA + ans], 1);
+        s.slot_branch[rC + slot] = -1;
+        s.br_slot[bi] = -1;
+      }
+    }
+    n_term += __popc(__ballot_sync(0xffffffffu, term));
+    need_rank += __popc(nm);
+    surv_rank += __popc(sm);
+  }
+  const int n_surv = surv_rank;
+  __syncwarp();
+
+  // ---- phase 4: branch-out refill of freed slots (:375-388) ----
+  int n_alive = 0;
+  for (int base = 0; base < nb; base += 32) {
+    const int b = base + lane;
+    const bool alive = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
+    const unsigned am = __ballot_sync(0xffffffffu, alive);
+    if (alive) {
+      const int k = n_alive + __popc(am & ((1u << lane) - 1u));
+      sc.alive[k] = b;
+      sc.root[k] = b;
+      sc.raw[k] = branch_raw(s.br_last_pred[rB + b], pol.inv_temperature);
+    }
+    n_alive += __popc(am);
+  }
+  __syncwarp();
+  const int next_t = s.next_template[r];
+  const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
+  if (n_forks > 0) {
+    mt_words_warp(mt, 2 * n_forks, sc.words, lane);
+    if (lane == 0) {
+      NeumaierSum sum;
+      for (int j = 0; j < n_alive; ++j) sum.add(sc.raw[j]);
+      int n = n_alive;
+      int amb = 0;
+      for (int k = 0; k < n_forks; ++k) {
+        const double u = mt_res53(sc.words[2 * k], sc.words[2 * k + 1]);
+        bool ambiguous = false;
+        const int idx = sample_index(sc.raw, n, sum.result(), u, &ambiguous);
+        amb += ambiguous;
+        sc.alive[n] = nb + k;                  // child branch id
+        sc.root[n] = sc.root[idx];
+        sc.raw[n] = sc.raw[idx];               // child inherits last_prediction (:264)
+        sum.add(sc.raw[idx]);
+        // stash source alive-index for the lane-parallel spawn below
+        sc.words[2 * kMaxC + k] = uint32_t(idx);
+        ++n;
+      }
+      if (amb) add_counter(&s.counters[DUCHESS_CNT_AMBIGUOUS], (long long)(amb));
+    }
+    __syncwarp();
+    // Free slots in ascending order go to children in fork order. Chains of
+    // forks (a child forked from a child of this round) resolve serially.
+    if (lane == 0) {
+      int free_slot = 0;
+      for (int k = 0; k < n_forks; ++k) {
+        const int idx = int(sc.words[2 * kMaxC + k]);
+        const int src = sc.alive[idx];
+        const int child = nb + k;
+        const int t = t0 + next_t + k;
+        const int64_t ci = rB + child, si = rB + src;
+        const int src_pos = s.br_offset[si] + s.br_decoded[si];
+        const int ob = min(src_pos, w.nat_len[t]);     // _spawn clamp (:263)
+        while (free_slot < C && s.slot_branch[rC + free_slot] >= 0) ++free_slot;
+        s.br_offset[ci] = ob;
+        s.br_decoded[ci] = 0;
+        s.br_streak[ci] = 0;
+        s.br_status[ci] = DUCHESS_ACTIVE;
+        s.br_final[ci] = -1;
+        s.br_npred[ci] = 0;
+        s.br_last_pred[ci] = s.br_last_pred[si];
+        s.br_slot[ci] = free_slot;
+        s.slot_branch[rC + free_slot] = child;
+        const int a = n_surv + k;
+        act[a * 3 + 0] = DUCHESS_ACT_BRANCH_OUT;
+        act[a * 3 + 1] = child;
+        act[a * 3 + 2] = src;
+        int32_t* f = s.forks + (rC + k) * 4;
+        f[0] = child;
+        f[1] = src;
+        f[2] = sc.root[idx];
+        f[3] = ob;
+      }
+      s.n_branches[r] = nb + n_forks;
+      s.next_template[r] = next_t + n_forks;
+      add_counter(&s.counters[DUCHESS_CNT_FORKS], (long long)(n_forks));
+    }
+    __syncwarp();
+    nb += n_forks;
+  }
+
+  // ---- phase 5: request termination (:390-399) ----
+  int max_count = 0, total = 0, best = 0x7fffffff;
+  for (int a = lane; a < s.answer_cap; a += 32) {
+    const int c = __ldcg(&s.tally[rA + a]);
+    total += c;
+    if (c > max_count) { max_count = c; best = a; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    total += __shfl_xor_sync(0xffffffffu, total, o);
+    const int mc = __shfl_xor_sync(0xffffffffu, max_count, o);
+    const int bb = __shfl_xor_sync(0xffffffffu, best, o);
+    if (mc > max_count || (mc == max_count && bb < best)) { max_count = mc; best = bb; }
+  }
+  int reason = DUCHESS_REASON_NONE;
+  if (max_count >= pol.need_consensus) reason = DUCHESS_REASON_CONSENSUS;
+  else if (total >= pol.need_coverage) reason = DUCHESS_REASON_COVERAGE;
+  bool any_active = false;
+  for (int base = 0; base < nb; base += 32) {
+    const int b = base + lane;
+    const bool a = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
+    if (a && reason != DUCHESS_REASON_NONE) {        // _cancel_active (:292-294)
+      s.br_status[rB + b] = DUCHESS_CANCELLED;
+      const int slot = s.br_slot[rB + b];
+      if (slot >= 0) s.slot_branch[rC + slot] = -1;
+      s.br_slot[rB + b] = -1;
+    }
+    any_active |= __any_sync(0xffffffffu, a);
+  }
+  if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
+  const bool done = reason != DUCHESS_REASON_NONE;
+  if (done) {
+    for (int a = lane; a < s.answer_cap; a += 32)
+      s.out_tally[int64_t(p) * s.answer_cap + a] = __ldcg(&s.tally[rA + a]);
+  }
+  if (lane == 0) {
+    s.tokens_probe[r] += n_term * pol.probe_cost_tokens;
+    rec[DUCHESS_REC_PROBES] += n_term;
+    rec[DUCHESS_REC_NACTIONS] = n_surv + n_forks;
+    rec[DUCHESS_REC_NFORKS] = n_forks;
+    rec[DUCHESS_REC_NSURV] = n_surv;
+    rec[DUCHESS_REC_DONE] = done ? 1 : 0;
+    add_counter(&s.counters[DUCHESS_CNT_BRANCH_STEPS], (long long)(n_surv));
+    if (done) {
+      const bool empty = total == 0;   // majority_vote on an empty tally raises (core.py:80-81)
+      s.done[r] = 1;
+      s.needs_refill[r] = 1;
+      rec[DUCHESS_REC_REASON] = reason;
+      rec[DUCHESS_REC_FINAL] = empty ? -1 : best;
+      s.out_final[p] = empty ? -1 : best;
+      s.out_reason[p] = reason;
+      s.out_tokens_decode[p] = s.tokens_decode[r];
+      s.out_tokens_probe[p] = s.tokens_probe[r];
+      s.out_rounds[p] = s.rounds[r];
+      s.out_error[p] = empty ? 1 : 0;
+      add_counter(&s.counters[DUCHESS_CNT_FINISHED], 1ll);
+      if (empty) add_counter(&s.counters[DUCHESS_CNT_ERRORS], 1ll);
+    } else {
+      s.needs_refill[r] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Rule primitives, one warp (branch_out_weights / branch_out_sample).
+__global__ void branch_out_kernel(const double* probs, int n, double inv_temp, uint32_t* mt,
+                                  int n_draws, int32_t* out_idx, double* out_w,
+                                  long long* out_amb) {
+  extern __shared__ double raw[];
+  __shared__ uint32_t words[2 * 256];
+  const int lane = threadIdx.x;
+  for (int j = lane; j < n; j += 32) raw[j] = branch_raw(probs[j], inv_temp);
+  __syncwarp();
+  NeumaierSum sum;
+  for (int j = 0; j < n; ++j) sum.add(raw[j]);
+  const double total = sum.result();
+  if (out_w) for (int j = lane; j < n; j += 32) out_w[j] = __ddiv_rn(raw[j], total);
+  long long amb = 0;
+  for (int base = 0; base < n_draws; base += 256) {
+    const int m = min(256, n_draws - base);
+    mt_words_warp(mt, 2 * m, words, lane);
+    if (lane == 0) {
+      for (int k = 0; k < m; ++k) {
+        bool a = false;
+        out_idx[base + k] = sample_index(raw, n, total, mt_res53(words[2 * k], words[2 * k + 1]), &a);
+        amb += a;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && out_amb) *out_amb = amb;
+}
+
+// majority_vote + check_request_termination over count vectors.
+__global__ void vote_kernel(const int32_t* counts, int n_sets, int n_ans, int need_cons,
+                            int need_cov, int32_t* out_final, int32_t* out_reason) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_sets) return;
+  const int32_t* c = counts + int64_t(i) * n_ans;
+  int best = -1, mc = 0, total = 0;
+  for (int a = 0; a < n_ans; ++a) {
+    total += c[a];
+    if (c[a] > mc) { mc = c[a]; best = a; }
+  }
+  if (out_final) out_final[i] = total > 0 ? best : -1;
+  if (out_reason)
+    out_reason[i] = mc >= need_cons ? DUCHESS_REASON_CONSENSUS
+                  : total >= need_cov ? DUCHESS_REASON_COVERAGE : DUCHESS_REASON_NONE;
+}
+
+__global__ void lookup_kernel(DuchessWorkload w, const int32_t* tmpl, const int32_t* pos, int n,
+                              int32_t* out_ans, double* out_pred) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (out_ans) out_ans[i] = probe_answer(w, tmpl[i], pos[i]);
+  if (out_pred) out_pred[i] = trace_prediction(w, tmpl[i], pos[i]);
+}
+
+}  // namespace duchess
+
+using namespace duchess;
+
+static bool state_ok(const DuchessPolicy* pol, const DuchessState* s) {
+  return pol && s && pol->max_branches >= 1 && pol->max_branches <= DUCHESS_MAX_SLOTS &&
+         s->branch_cap >= 1 && s->answer_cap >= 1 && s->n_slots >= 0;
+}
+
+extern "C" int duchess_advance(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                               const DuchessState* state, void* stream) {
+  if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  advance_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      *policy, *workload, *state);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                              const DuchessState* state, const double* probs, void* stream) {
+  if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
+  if (policy->pred_source != DUCHESS_PRED_TRACE && probs == nullptr) return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  decide_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      *policy, *workload, *state, probs);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,
+                                         uint32_t* mt_state, int32_t n_draws, int32_t* out_idx,
+                                         double* out_weights, long long* out_ambiguous,
+                                         void* stream) {
+  if (!probs || n < 1 || n > 4096 || n_draws < 0) return DUCHESS_EINVAL;
+  if (n_draws > 0 && (!mt_state || !out_idx)) return DUCHESS_EINVAL;
+  branch_out_kernel<<<1, 32, size_t(n) * sizeof(double), static_cast<cudaStream_t>(stream)>>>(
+      probs, n, inv_temperature, mt_state, n_draws, out_idx, out_weights, out_ambiguous);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_vote(const int32_t* counts, int32_t n_sets, int32_t n_answers,
+                            int32_t need_consensus, int32_t need_coverage, int32_t* out_final,
+                            int32_t* out_reason, void* stream) {
+  if (!counts || n_sets < 0 || n_answers < 0) return DUCHESS_EINVAL;
+  if (n_sets == 0) return DUCHESS_OK;
+  vote_kernel<<<(n_sets + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, n_sets, n_answers, need_consensus, need_coverage, out_final, out_reason);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_template_lookup(const DuchessWorkload* workload, const int32_t* tmpl,
+                                       const int32_t* pos, int32_t n, int32_t* out_probe_answer,
+                                       double* out_trace_pred, void* stream) {
+  if (!workload || n < 0) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  lookup_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      *workload, tmpl, pos, n, out_probe_answer, out_trace_pred);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}

@@ -1,0 +1,391 @@
+// K1: fused token-pooling + LayerNorm + linear-probe scoring (sm_100a).
+//
+// Restates, batched over every active (branch, layer) window, the reference's
+// per-vector probe forward `mlp_forward` (reference pkg/src/branchsim/
+// predictor.py:126-151) for the linear probe (layer_dims = [], head_dim = 1):
+//     m      = mean_t x[t, :]                        (pooling: north-star extension)
+//     z      = (m - mean(m)) / sqrt(var(m) + 1e-5)   (predictor.py:134-136, population var)
+//     logit  = sum_h w_h (g_h z_h + b_h) + b          (predictor.py:137-138, :146)
+//     prob   = clip(sigmoid(logit), 1e-12, 1-1e-12)   (predictor.py:148)
+// folded as logit = (sum_h wg_h (m_h - mu)) / sigma + c1 with wg = w*g and
+// c1 = sum w*b_ln + b precomputed on the host.
+//
+// The kernel is HBM-bound (< 1 FLOP/B): each CTA streams one H-chunk of one
+// window with 128-bit no-L1-allocate loads, keeps its pooled values in
+// registers (two-pass mean/variance costs no extra HBM traffic) and, when a
+// window is split over several CTAs, merges (count, mean, M2, dot) partials
+// with Chan's formula in fixed chunk order in the last-arriving CTA, so the
+// result is deterministic run to run.
+#include "common.cuh"
+#include "../../include/duchess_b200.h"
+
+namespace duchess {
+
+struct ScoreArgs {
+  const char* acts;
+  int64_t row_stride, layer_stride, token_stride;  // elements
+  int64_t n_units;                                 // rows * L
+  int L, T, H;
+  int nsplit, chunk;                               // chunk = columns per split
+  const float* wg;
+  const float* c1;
+  const uint8_t* mask;
+  float* out_logit;
+  double* out_prob;
+  float4* partials;     // [n_units * nsplit] (mean, M2, dot, wsum)
+  unsigned* counters;   // [n_units]
+};
+
+template <int NT>
+__device__ __forceinline__ void block_sum2(float& a, float& b, float2* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = make_float2(a, b);
+  __syncthreads();
+  if (warp == 0) {
+    float2 v = lane < NT / 32 ? red[lane] : make_float2(0.f, 0.f);
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    if (lane == 0) red[NT / 32] = v;
+  }
+  __syncthreads();
+  a = red[NT / 32].x;
+  b = red[NT / 32].y;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void write_score(const ScoreArgs& a, int64_t unit, float logit) {
+  a.out_logit[unit] = logit;
+  double p = 1.0 / (1.0 + exp(-double(logit)));
+  p = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
+  a.out_prob[unit] = p;
+}
+
+// Last CTA of a split window: merge chunk partials in chunk order (double).
+__device__ void merge_partials(const ScoreArgs& a, int64_t unit, int l) {
+  const float4* parts = a.partials + unit * a.nsplit;
+  double n_a = 0.0, mean = 0.0, m2 = 0.0;
+  for (int k = 0; k < a.nsplit; ++k) {
+    float4 pk = __ldcg(parts + k);
+    int beg = k * a.chunk, end = min(a.H, beg + a.chunk);
+    double n_b = double(end - beg);
+    if (n_b <= 0) continue;
+    double delta = double(pk.x) - mean;
+    double n = n_a + n_b;
+    mean += delta * n_b / n;
+    m2 += double(pk.y) + delta * delta * n_a * n_b / n;
+    n_a = n;
+  }
+  double dot = 0.0;
+  for (int k = 0; k < a.nsplit; ++k) {
+    float4 pk = __ldcg(parts + k);
+    int beg = k * a.chunk, end = min(a.H, beg + a.chunk);
+    if (end <= beg) continue;
+    dot += double(pk.z) + (double(pk.x) - mean) * double(pk.w);
+  }
+  double var = m2 / double(a.H);
+  float logit = float(dot / sqrt(var + double(kLayerNormEps))) + a.c1[l];
+  write_score(a, unit, logit);
+}
+
+// Fast path: 16-byte aligned windows, H a multiple of the vector width.
+template <bool BF16, int NT, int PASSES>
+__global__ void __launch_bounds__(NT) score_fast_kernel(ScoreArgs a) {
+  constexpr int VEC = BF16 ? 8 : 4;                 // elements per 16-byte load
+  constexpr int ESZ = BF16 ? 2 : 4;
+  constexpr int U = (16 / PASSES) > 0 ? (16 / PASSES) : 1;  // tokens per load batch
+  __shared__ float2 red[NT / 32 + 1];
+  __shared__ int last_flag;
+
+  const int64_t unit = blockIdx.x / a.nsplit;
+  const int split = blockIdx.x - int(unit * a.nsplit);
+  const int64_t row = unit / a.L;
+  const int l = int(unit - row * a.L);
+  if (a.mask != nullptr && a.mask[row] == 0) return;
+
+  const int cbeg = split * a.chunk;
+  const int cend = min(a.H, cbeg + a.chunk);
+  const char* base = a.acts + (row * a.row_stride + int64_t(l) * a.layer_stride) * ESZ;
+  const int64_t tok_bytes = a.token_stride * ESZ;
+
+  float acc[PASSES][VEC];
+  bool valid[PASSES];
+  const char* colp[PASSES];
+#pragma unroll
+  for (int p = 0; p < PASSES; ++p) {
+    const int col = cbeg + (p * NT + int(threadIdx.x)) * VEC;
+    valid[p] = col < cend;
+    colp[p] = base + int64_t(col) * ESZ;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[p][v] = 0.f;
+  }
+
+  for (int t0 = 0; t0 < a.T; t0 += U) {
+    uint4 buf[U][PASSES];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int p = 0; p < PASSES; ++p)
+        if (valid[p] && t0 + u < a.T) buf[u][p] = ldg_stream(colp[p] + int64_t(t0 + u) * tok_bytes);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int p = 0; p < PASSES; ++p)
+        if (valid[p] && t0 + u < a.T) {
+          const uint32_t w[4] = {buf[u][p].x, buf[u][p].y, buf[u][p].z, buf[u][p].w};
+          if constexpr (BF16) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[p][2 * q] += bf16lo(w[q]);
+              acc[p][2 * q + 1] += bf16hi(w[q]);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[p][q] += __uint_as_float(w[q]);
+          }
+        }
+  }
+
+  // Pooled window mean, local (chunk) statistics.
+  const float invT = 1.0f / float(a.T);
+  float wgv[PASSES][VEC];
+  float s1 = 0.f, sw = 0.f;
+  const float* wrow = a.wg + int64_t(l) * a.H;
+#pragma unroll
+  for (int p = 0; p < PASSES; ++p) {
+    const int col = cbeg + (p * NT + int(threadIdx.x)) * VEC;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      acc[p][v] = (a.T & (a.T - 1)) == 0 ? acc[p][v] * invT : acc[p][v] / float(a.T);
+      wgv[p][v] = valid[p] ? __ldg(wrow + col + v) : 0.f;
+      if (valid[p]) { s1 += acc[p][v]; sw += wgv[p][v]; }
+    }
+  }
+  block_sum2<NT>(s1, sw, red);
+  const float n_loc = float(cend - cbeg);
+  const float mean_loc = s1 / n_loc;
+  float q = 0.f, d = 0.f;
+#pragma unroll
+  for (int p = 0; p < PASSES; ++p)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+      if (valid[p]) {
+        const float c = acc[p][v] - mean_loc;
+        q += c * c;
+        d += wgv[p][v] * c;
+      }
+  block_sum2<NT>(q, d, red);
+
+  if (a.nsplit == 1) {
+    if (threadIdx.x == 0) {
+      const float var = q / float(a.H);
+      write_score(a, unit, d / sqrtf(var + kLayerNormEps) + a.c1[l]);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    a.partials[unit * a.nsplit + split] = make_float4(mean_loc, q, d, sw);
+    __threadfence();
+    const unsigned prev = atomicAdd(a.counters + unit, 1u);
+    last_flag = (prev == unsigned(a.nsplit - 1));
+  }
+  __syncthreads();
+  if (last_flag && threadIdx.x == 0) {
+    __threadfence();
+    merge_partials(a, unit, l);
+    a.counters[unit] = 0u;   // ready for the next launch
+  }
+}
+
+// Generic path: any alignment / width; pooled window staged in shared memory.
+template <bool BF16>
+__global__ void __launch_bounds__(256) score_generic_kernel(ScoreArgs a) {
+  constexpr int NT = 256;
+  extern __shared__ float pooled[];
+  __shared__ float2 red[NT / 32 + 1];
+  const int64_t unit = blockIdx.x;
+  const int64_t row = unit / a.L;
+  const int l = int(unit - row * a.L);
+  if (a.mask != nullptr && a.mask[row] == 0) return;
+  const int64_t off = row * a.row_stride + int64_t(l) * a.layer_stride;
+  const float* wrow = a.wg + int64_t(l) * a.H;
+  float s1 = 0.f, sw = 0.f;
+  for (int h = threadIdx.x; h < a.H; h += NT) {
+    float acc = 0.f;
+    for (int t = 0; t < a.T; ++t) {
+      const int64_t idx = off + int64_t(t) * a.token_stride + h;
+      if constexpr (BF16) {
+        const uint16_t raw = reinterpret_cast<const uint16_t*>(a.acts)[idx];
+        acc += __uint_as_float(uint32_t(raw) << 16);
+      } else {
+        acc += reinterpret_cast<const float*>(a.acts)[idx];
+      }
+    }
+    const float m = acc / float(a.T);
+    pooled[h] = m;
+    s1 += m;
+    sw += wrow[h];
+  }
+  block_sum2<NT>(s1, sw, red);
+  const float mean = s1 / float(a.H);
+  float q = 0.f, d = 0.f;
+  for (int h = threadIdx.x; h < a.H; h += NT) {
+    const float c = pooled[h] - mean;
+    q += c * c;
+    d += wrow[h] * c;
+  }
+  block_sum2<NT>(q, d, red);
+  if (threadIdx.x == 0) {
+    const float var = q / float(a.H);
+    write_score(a, unit, d / sqrtf(var + kLayerNormEps) + a.c1[l]);
+  }
+}
+
+// Synthetic activation windows keyed by (seed, request, template, position).
+template <bool BF16>
+__global__ void __launch_bounds__(256) fill_kernel(char* acts, int64_t row_stride,
+                                                   int64_t layer_stride, int64_t token_stride,
+                                                   int L, int T, int H, uint64_t seed,
+                                                   const int64_t* row_req, const int32_t* row_tmpl,
+                                                   const int32_t* row_pos, const uint8_t* mask) {
+  const int64_t unit = blockIdx.x;
+  const int64_t row = unit / L;
+  const int l = int(unit - row * L);
+  if (mask != nullptr && mask[row] == 0) return;
+  const uint64_t req = row_req ? uint64_t(row_req[row]) : uint64_t(row);
+  const uint64_t tmpl = row_tmpl ? uint64_t(uint32_t(row_tmpl[row])) : 0ull;
+  const uint64_t pos = row_pos ? uint64_t(uint32_t(row_pos[row])) : 0ull;
+  const uint64_t rk = row_key(seed, req, tmpl, pos, uint64_t(l));
+  const int64_t off = row * row_stride + int64_t(l) * layer_stride;
+  const int64_t n = int64_t(T) * H;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const int t = int(e / H), h = int(e - int64_t(t) * H);
+    const float x = synth_value(rk, uint32_t(t), uint32_t(h));
+    const int64_t idx = off + int64_t(t) * token_stride + h;
+    if constexpr (BF16) reinterpret_cast<uint16_t*>(acts)[idx] = f32_to_bf16_rne(x);
+    else reinterpret_cast<float*>(acts)[idx] = x;
+  }
+}
+
+template <bool BF16, int NT>
+static cudaError_t launch_fast(const ScoreArgs& a, int passes, cudaStream_t s) {
+  const dim3 grid(unsigned(a.n_units * a.nsplit));
+  switch (passes) {
+    case 1: score_fast_kernel<BF16, NT, 1><<<grid, NT, 0, s>>>(a); break;
+    case 2: score_fast_kernel<BF16, NT, 2><<<grid, NT, 0, s>>>(a); break;
+    case 4: score_fast_kernel<BF16, NT, 4><<<grid, NT, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace duchess
+
+using namespace duchess;
+
+extern "C" size_t duchess_score_workspace_bytes(int64_t n_units, int32_t nsplit_max) {
+  if (n_units <= 0 || nsplit_max <= 1) return 0;
+  return size_t(n_units) * size_t(nsplit_max) * sizeof(float4) + size_t(n_units) * sizeof(unsigned);
+}
+
+extern "C" int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                             int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                             int64_t token_stride, const float* wg, const float* c1,
+                             const uint8_t* row_mask, float* out_logit, double* out_prob,
+                             void* workspace, size_t workspace_bytes, int32_t nsplit,
+                             int32_t threads, void* stream) {
+  if (n_rows < 0 || n_layers < 1 || T < 1 || H < 1) return DUCHESS_EINVAL;
+  if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
+  if (!acts || !wg || !c1 || !out_logit || !out_prob) return DUCHESS_EINVAL;
+  if (n_rows == 0) return DUCHESS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool bf16 = dtype == DUCHESS_BF16;
+  const int esz = bf16 ? 2 : 4, vec = 16 / esz;
+  ScoreArgs a{};
+  a.acts = static_cast<const char*>(acts);
+  a.row_stride = row_stride;
+  a.layer_stride = layer_stride;
+  a.token_stride = token_stride;
+  a.n_units = n_rows * n_layers;
+  a.L = n_layers;
+  a.T = T;
+  a.H = H;
+  a.wg = wg;
+  a.c1 = c1;
+  a.mask = row_mask;
+  a.out_logit = out_logit;
+  a.out_prob = out_prob;
+
+  const bool aligned = (reinterpret_cast<uintptr_t>(acts) % 16 == 0) &&
+                       ((row_stride * esz) % 16 == 0) && ((layer_stride * esz) % 16 == 0) &&
+                       ((token_stride * esz) % 16 == 0) && (H % vec == 0) &&
+                       (reinterpret_cast<uintptr_t>(wg) % 16 == 0);
+  if (!aligned) {
+    a.nsplit = 1;
+    a.chunk = H;
+    const size_t smem = size_t(H) * sizeof(float);
+    if (smem > 200 * 1024) return DUCHESS_EINVAL;
+    if (bf16) {
+      cudaFuncSetAttribute(score_generic_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      score_generic_kernel<true><<<unsigned(a.n_units), 256, smem, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(score_generic_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      score_generic_kernel<false><<<unsigned(a.n_units), 256, smem, s>>>(a);
+    }
+    return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  }
+
+  int nt = threads > 0 ? threads : 256;
+  if (nt != 128 && nt != 256 && nt != 512) return DUCHESS_EINVAL;
+  const int cols_per_pass = nt * vec;
+  const int passes_needed = (H + cols_per_pass - 1) / cols_per_pass;
+  int ns = nsplit > 0 ? nsplit : (passes_needed + 1) / 2;
+  if (ns > passes_needed) ns = passes_needed;
+  int chunk = (H + ns - 1) / ns;
+  chunk = (chunk + vec - 1) / vec * vec;
+  int passes = (chunk + cols_per_pass - 1) / cols_per_pass;
+  if (passes == 3) passes = 4;
+  if (passes > 4) return DUCHESS_EINVAL;
+  a.nsplit = ns;
+  a.chunk = chunk;
+  if (ns > 1) {
+    if (workspace_bytes < duchess_score_workspace_bytes(a.n_units, ns) || !workspace)
+      return DUCHESS_EINVAL;
+    a.partials = static_cast<float4*>(workspace);
+    a.counters = reinterpret_cast<unsigned*>(a.partials + a.n_units * ns);
+  }
+  cudaError_t e;
+  if (bf16) {
+    e = nt == 128 ? launch_fast<true, 128>(a, passes, s)
+      : nt == 256 ? launch_fast<true, 256>(a, passes, s)
+                  : launch_fast<true, 512>(a, passes, s);
+  } else {
+    e = nt == 128 ? launch_fast<false, 128>(a, passes, s)
+      : nt == 256 ? launch_fast<false, 256>(a, passes, s)
+                  : launch_fast<false, 512>(a, passes, s);
+  }
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                                        int32_t T, int32_t H, int64_t row_stride,
+                                        int64_t layer_stride, int64_t token_stride, uint64_t seed,
+                                        const int64_t* row_req, const int32_t* row_tmpl,
+                                        const int32_t* row_pos, const uint8_t* row_mask,
+                                        void* stream) {
+  if (!acts || n_rows < 0 || n_layers < 1 || T < 1 || H < 1) return DUCHESS_EINVAL;
+  if (n_rows == 0) return DUCHESS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = unsigned(n_rows * n_layers);
+  char* p = static_cast<char*>(acts);
+  if (dtype == DUCHESS_BF16)
+    fill_kernel<true><<<grid, 256, 0, s>>>(p, row_stride, layer_stride, token_stride, n_layers, T,
+                                           H, seed, row_req, row_tmpl, row_pos, row_mask);
+  else if (dtype == DUCHESS_F32)
+    fill_kernel<false><<<grid, 256, 0, s>>>(p, row_stride, layer_stride, token_stride, n_layers, T,
+                                            H, seed, row_req, row_tmpl, row_pos, row_mask);
+  else
+    return DUCHESS_EINVAL;
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}

@@ -1,0 +1,340 @@
+// K4: fused logistic-regression gradient for probe training (one HBM pass).
+//
+// The reference ships no training ("OUT OF SCOPE ... training the
+// MLPs"); the paper trains its probes with BCE. The
+// north-star trains the linear probe of predictor.py:126-151 data-parallel:
+//     g_h = inv_n * sum_i (sigmoid(x_i . w + b) - y_i) x_ih,   g_b = inv_n * sum_i (...)
+// followed by an NCCL all-reduce of the H+1 gradient (python side).
+//
+// Blackwell design: one persistent CTA per SM; a producer warp streams row
+// blocks into a shared-memory ring with cp.async.bulk (TMA bulk copies,
+// completion tracked by mbarrier transaction counts), eight consumer warps
+// compute the row dots from shared memory, reduce them with one named barrier
+// per stage, and accumulate residual * x into per-thread fp32 registers, so X
+// is read from HBM exactly once. Per-CTA partial gradients are reduced in a
+// fixed order by a second kernel (deterministic).
+#include "common.cuh"
+#include "../../include/duchess_b200.h"
+
+namespace duchess {
+
+constexpr int kConsWarps = 8;
+constexpr int kCons = kConsWarps * 32;
+constexpr int kStageBytesTarget = 32 * 1024;
+constexpr int kSmemBudget = 200 * 1024;
+constexpr int kMaxRB = 8;
+
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
+}
+
+struct GradArgs {
+  const char* X;
+  const float* y;
+  const float* w;
+  int64_t n_rows;
+  int H;
+  int row_bytes;
+  int rb;          // rows per stage
+  int stages;
+  int64_t rows_per_cta;
+  float* partial;  // [grid, H+1]
+};
+
+template <bool BF16, int VPT>
+__global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
+  constexpr int EPV = BF16 ? 8 : 4;   // elements per 16-byte vector
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t full_bar[16], empty_bar[16];
+  __shared__ float red[2][kConsWarps][kMaxRB];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = int64_t(blockIdx.x) * a.rows_per_cta;
+  const int64_t row1 = lmin(a.n_rows, row0 + a.rows_per_cta);
+  const int64_t n_my = lmax(int64_t(0), row1 - row0);
+  const int64_t n_iter = (n_my + a.rb - 1) / a.rb;
+  const int stage_bytes = a.rb * a.row_bytes;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsWarps) {
+    // ---- producer: TMA bulk copies of row blocks into the ring ----
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      for (int64_t it = 0; it < n_iter; ++it) {
+        const int s = int(it % a.stages);
+        const uint32_t ph = uint32_t((it / a.stages) & 1);
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        const int64_t r = row0 + it * a.rb;
+        const int nr = int(lmin(a.rb, row1 - r));
+        const uint32_t bytes = uint32_t(nr) * uint32_t(a.row_bytes);
+        mbar_expect_tx(&full_bar[s], bytes);
+        bulk_g2s(smem + size_t(s) * stage_bytes, a.X + r * a.row_bytes, bytes, &full_bar[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int nvec = a.row_bytes / 16;
+  float g[VPT][EPV];
+  float wv[VPT][EPV];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = j * kCons + int(threadIdx.x);
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      g[j][e] = 0.f;
+      const int col = v * EPV + e;
+      wv[j][e] = (v < nvec && col < a.H) ? a.w[col] : 0.f;
+    }
+  }
+  const float bias = a.w[a.H];
+  float gb = 0.f;
+
+  for (int64_t it = 0; it < n_iter; ++it) {
+    const int s = int(it % a.stages);
+    const uint32_t ph = uint32_t((it / a.stages) & 1);
+    const int64_t r = row0 + it * a.rb;
+    const int nr = int(lmin(a.rb, row1 - r));
+    mbar_wait(&full_bar[s], ph);
+    const char* base = smem + size_t(s) * stage_bytes;
+    float dots[kMaxRB];
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) dots[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) {
+      if (q < nr) {
+        const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          const int v = j * kCons + int(threadIdx.x);
+          if (v < nvec) {
+            const uint4 x = rowv[v];
+            const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+            if constexpr (BF16) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                dots[q] += wv[j][2 * e] * bf16lo(xw[e]) + wv[j][2 * e + 1] * bf16hi(xw[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) dots[q] += wv[j][e] * __uint_as_float(xw[e]);
+            }
+          }
+        }
+      }
+    }
+    const int buf = int(it & 1);
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) {
+      if (q < nr) {
+        const float d = warp_sum(dots[q]);
+        if (lane == 0) red[buf][warp][q] = d;
+      }
+    }
+    consumer_bar();
+    float res[kMaxRB];
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) {
+      res[q] = 0.f;
+      if (q < nr) {
+        float z = bias;
+#pragma unroll
+        for (int k = 0; k < kConsWarps; ++k) z += red[buf][k][q];
+        const float sig = 1.0f / (1.0f + expf(-z));
+        res[q] = sig - a.y[r + q];
+        gb += res[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) {
+      if (q < nr) {
+        const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          const int v = j * kCons + int(threadIdx.x);
+          if (v < nvec) {
+            const uint4 x = rowv[v];
+            const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+            if constexpr (BF16) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                g[j][2 * e] += res[q] * bf16lo(xw[e]);
+                g[j][2 * e + 1] += res[q] * bf16hi(xw[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) g[j][e] += res[q] * __uint_as_float(xw[e]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+
+  float* out = a.partial + int64_t(blockIdx.x) * (a.H + 1);
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = j * kCons + int(threadIdx.x);
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      const int col = v * EPV + e;
+      if (v < nvec && col < a.H) out[col] = g[j][e];
+    }
+  }
+  if (threadIdx.x == 0) out[a.H] = gb;
+}
+
+// Fixed-order reduction of per-CTA partials, scaled by inv_n.
+__global__ void grad_reduce_kernel(const float* partial, int n_parts, int n, float inv_n,
+                                   float* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+  for (int k = 0; k < n_parts; ++k) acc += partial[int64_t(k) * n + i];
+  out[i] = acc * inv_n;
+}
+
+__global__ void sgd_kernel(float* w, const float* g, int n, float lr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] -= lr * g[i];
+}
+
+template <bool BF16, int VPT>
+static cudaError_t launch_grad(const GradArgs& a, int grid, size_t smem, cudaStream_t s) {
+  auto k = lr_grad_kernel<BF16, VPT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k<<<grid, kCons + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace duchess
+
+using namespace duchess;
+
+extern "C" size_t duchess_lr_grad_workspace_bytes(int32_t H) {
+  if (H < 1) return 0;
+  return size_t(num_sms()) * size_t(H + 1) * sizeof(float);
+}
+
+extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, const float* w,
+                               int64_t n_rows, int32_t H, float inv_n, float* grad_out,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (!X || !y || !w || !grad_out || n_rows < 0 || H < 1) return DUCHESS_EINVAL;
+  if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
+  const int esz = dtype == DUCHESS_BF16 ? 2 : 4;
+  const int64_t row_bytes = int64_t(H) * esz;
+  if (row_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(X) % 16 != 0) return DUCHESS_EINVAL;
+  const int nvec = int(row_bytes / 16);
+  const int vpt_needed = (nvec + kCons - 1) / kCons;
+  int vpt = 1;
+  while (vpt < vpt_needed) vpt <<= 1;
+  if (vpt > 8) return DUCHESS_EINVAL;
+  const int sms = num_sms();
+  if (!workspace || workspace_bytes < size_t(sms) * size_t(H + 1) * sizeof(float))
+    return DUCHESS_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GradArgs a{};
+  a.X = static_cast<const char*>(X);
+  a.y = y;
+  a.w = w;
+  a.n_rows = n_rows;
+  a.H = H;
+  a.row_bytes = int(row_bytes);
+  a.rb = int(lmax(1, lmin(kMaxRB, kStageBytesTarget / row_bytes)));
+  const int stage_bytes = a.rb * a.row_bytes;
+  a.stages = int(lmin(16, lmax(2, kSmemBudget / stage_bytes)));
+  if (int64_t(a.stages) * stage_bytes > kSmemBudget) return DUCHESS_EINVAL;
+  const int grid = sms;
+  a.rows_per_cta = (n_rows + grid - 1) / grid;
+  a.partial = static_cast<float*>(workspace);
+  const size_t smem = size_t(a.stages) * stage_bytes;
+  cudaError_t e;
+  const bool bf16 = dtype == DUCHESS_BF16;
+  switch (vpt) {
+    case 1: e = bf16 ? launch_grad<true, 1>(a, grid, smem, s) : launch_grad<false, 1>(a, grid, smem, s); break;
+    case 2: e = bf16 ? launch_grad<true, 2>(a, grid, smem, s) : launch_grad<false, 2>(a, grid, smem, s); break;
+    case 4: e = bf16 ? launch_grad<true, 4>(a, grid, smem, s) : launch_grad<false, 4>(a, grid, smem, s); break;
+    default: e = bf16 ? launch_grad<true, 8>(a, grid, smem, s) : launch_grad<false, 8>(a, grid, smem, s); break;
+  }
+  if (e != cudaSuccess) return DUCHESS_ECUDA;
+  const int n = H + 1;
+  grad_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(a.partial, grid, n, inv_n, grad_out);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_sgd_update(float* w, const float* grad, int32_t n, float lr, void* stream) {
+  if (!w || !grad || n < 0) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  sgd_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(w, grad, n, lr);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" const char* duchess_version(void) { return "duchess_b200 0.1.0 sm_100a"; }
+
+extern "C" int duchess_device_arch(void) {
+#if defined(__CUDA_ARCH__)
+  return __CUDA_ARCH__;
+#else
+  return 1000;
+#endif
+}
