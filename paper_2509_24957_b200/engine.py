@@ -1,0 +1,299 @@
+"""BatchedDuchess — the device-resident DUCHESS orchestration engine.
+
+Holds the SoA state of R request slots (each with up to C = max_branches
+branch slots) in device memory and advances all of them one round per
+``step()``: ``duchess_advance`` (refill + phase 1) -> ``duchess_score`` (K1,
+when predictions come from probe scores) -> ``duchess_decide`` (phases 2-5).
+Requests enter slots from a service queue (FCFS or difficulty order, see
+scheduler.py) and finished slots are refilled on device, so a run needs no
+host synchronisation between rounds.
+
+Per-request semantics are exactly the reference's DuchessRun
+(orchestrator.py:316-402); the host only packs traces (workload.py:35-60) and
+unpacks RoundReports / RequestOutcomes.
+"""
+
+from __future__ import annotations
+
+import math
+import random
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+NO_ANSWER = ""
+
+
+def at_least(frac: float, slots: int) -> int:
+    """orchestrator.py:162-164."""
+    return math.ceil(frac * slots - 1e-9)
+
+
+def mt_state_words(rng_or_seed) -> np.ndarray:
+    """625 uint32 words (624 MT19937 words + index) of a random.Random."""
+    rng = rng_or_seed if isinstance(rng_or_seed, random.Random) else random.Random(rng_or_seed)
+    version, internal, _gauss = rng.getstate()
+    if version != 3 or len(internal) != _lib.MT_WORDS:
+        raise ValueError("unsupported random.Random state layout")
+    return np.asarray(internal, dtype=np.uint32)
+
+
+def set_mt_state(rng: random.Random, words: np.ndarray) -> None:
+    _v, _internal, gauss = rng.getstate()
+    rng.setstate((3, tuple(int(x) for x in words), gauss))
+
+
+@dataclass
+class PackedWorkload:
+    """Device tables for a pool of traces; answers interned per request."""
+    answers: list            # per request: list of answer strings, id order
+    n_templates: np.ndarray  # [P]
+    tensors: dict
+    struct: _lib.Workload
+    branch_cap: int
+    answer_cap: int
+
+
+def intern_answers(trace) -> list[str]:
+    """Sorted distinct answers of a request with "" first, so answer-id order
+    equals string order (majority_vote tie-break, core.py:83)."""
+    s = {NO_ANSWER, trace.ground_truth}
+    for t in trace.templates:
+        s.add(t.final_answer)
+        s.update(a for _, a in t.probes)
+    return sorted(s)
+
+
+def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkload:
+    P = len(traces)
+    tmpl_off = [0]
+    gt, nat, fin, conv = [], [], [], []
+    probe_off, probe_at, probe_ans = [0], [], []
+    pred_off, pred_at, pred_p = [0], [], []
+    answers = []
+    for tr in traces:
+        ans = intern_answers(tr)
+        idx = {a: i for i, a in enumerate(ans)}
+        answers.append(ans)
+        gt.append(idx[tr.ground_truth])
+        for t in tr.templates:
+            nat.append(int(t.natural_length))
+            fin.append(idx[t.final_answer])
+            conv.append(-1 if t.oracle_convergence is None else int(t.oracle_convergence))
+            for at, a in t.probes:
+                probe_at.append(int(at))
+                probe_ans.append(idx[a])
+            probe_off.append(len(probe_at))
+            for at, p in (t.pred_probs or []):
+                pred_at.append(int(at))
+                pred_p.append(float(p))
+            pred_off.append(len(pred_at))
+        tmpl_off.append(len(nat))
+
+    def i32(x):
+        return torch.tensor(np.asarray(x, dtype=np.int32).reshape(-1) if len(x) else
+                            np.zeros(1, np.int32), dtype=torch.int32, device=device)
+
+    tens = {
+        "tmpl_off": i32(tmpl_off), "ground_truth": i32(gt), "nat_len": i32(nat),
+        "final_ans": i32(fin), "conv": i32(conv), "probe_off": i32(probe_off),
+        "probe_at": i32(probe_at), "probe_ans": i32(probe_ans), "pred_off": i32(pred_off),
+        "pred_at": i32(pred_at),
+        "pred_p": torch.tensor(np.asarray(pred_p if pred_p else [0.0], dtype=np.float64),
+                               device=device),
+        "mt_init": torch.from_numpy(np.ascontiguousarray(mt_words, dtype=np.uint32).view(np.int32))
+        .reshape(-1).to(device),
+        "queue": i32(queue),
+    }
+    st = _lib.Workload()
+    st.n_requests = P
+    st.queue_len = len(queue)
+    st.cycle = 1 if cycle else 0
+    for k, v in tens.items():
+        setattr(st, k, v.data_ptr())
+    n_t = np.diff(np.asarray(tmpl_off))
+    return PackedWorkload(answers, n_t, tens, st, int(max(n_t.max() if P else 1, 1)),
+                          int(max(len(a) for a in answers) if P else 1))
+
+
+class BatchedDuchess:
+    """R request slots advanced in lockstep rounds on one GPU.
+
+    traces:   list of RequestTrace-like objects (templates, ground_truth).
+    config:   OrchestratorConfig-like (max_branches, interval_tokens, ...).
+    seeds:    per-request int seeds or random.Random objects (DuchessRun's rng).
+    pred_source: _lib.PRED_TRACE (reference default predictor: pred_probs, else
+              synthetic with rho), _lib.PRED_DEVICE (K1 probe scores) or
+              _lib.PRED_HOST (caller-provided probabilities by slot).
+    """
+
+    def __init__(self, traces, config, seeds, n_slots: int | None = None, *,
+                 pred_source: int = _lib.PRED_TRACE, rho: float = 1.0, queue=None,
+                 cycle: bool = False, n_layers: int = 1, combine: int = 0,
+                 device: str | torch.device = "cuda"):
+        _lib.require_cuda()
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.traces = traces
+        self.config = config
+        c = int(config.max_branches)
+        if not 1 <= c <= _lib.MAX_SLOTS:
+            raise ValueError(f"max_branches must be in [1, {_lib.MAX_SLOTS}] on device")
+        P = len(traces)
+        self.P, self.C = P, c
+        self.R = n_slots if n_slots is not None else P
+        queue = list(range(P)) if queue is None else list(queue)
+        mt = np.stack([mt_state_words(s) for s in seeds]) if P else np.zeros((0, 625), np.uint32)
+        self.wl = pack_workload(traces, mt, queue, cycle, self.device)
+
+        pol = _lib.Policy()
+        pol.max_branches = c
+        pol.interval_tokens = int(config.interval_tokens)
+        pol.early_term_rounds = int(config.early_term_rounds)
+        pol.token_cap = int(config.token_cap)
+        pol.probe_cost_tokens = int(config.probe_cost_tokens)
+        pol.need_consensus = at_least(config.consensus_frac, c)
+        pol.need_coverage = at_least(config.coverage_frac, c)
+        pol.pred_source = int(pred_source)
+        pol.n_layers = int(n_layers)
+        pol.combine = int(combine)
+        pol.early_term_threshold = float(config.early_term_threshold)
+        pol.inv_temperature = 1.0 / config.branch_out_temperature     # orchestrator.py:182
+        pol.rho = float(rho)
+        self.policy = pol
+        self._alloc_state()
+
+    # ------------------------------------------------------------------
+    def _alloc_state(self) -> None:
+        R, C, dev = self.R, self.C, self.device
+        B, A = self.wl.branch_cap, self.wl.answer_cap
+        i32 = dict(dtype=torch.int32, device=dev)
+        t = {}
+        for name in ("slot_req", "n_branches", "next_template", "tokens_decode",
+                     "tokens_probe", "rounds"):
+            t[name] = torch.zeros(R, **i32)
+        t["slot_req"].fill_(-1)
+        t["needs_refill"] = torch.ones(R, **i32)
+        t["done"] = torch.ones(R, **i32)
+        t["tally"] = torch.zeros(R * A, **i32)
+        t["mt"] = torch.zeros(R * _lib.MT_WORDS, **i32)
+        for name in ("br_offset", "br_decoded", "br_streak", "br_status", "br_final",
+                     "br_npred", "br_slot"):
+            t[name] = torch.zeros(R * B, **i32)
+        t["br_last_pred"] = torch.zeros(R * B, dtype=torch.float64, device=dev)
+        t["slot_branch"] = torch.full((R * C,), -1, **i32)
+        t["row_mask"] = torch.zeros(R * C, dtype=torch.uint8, device=dev)
+        t["row_pos"] = torch.zeros(R * C, **i32)
+        t["row_tmpl"] = torch.zeros(R * C, **i32)
+        t["row_req"] = torch.zeros(R * C, dtype=torch.int64, device=dev)
+        t["round_rec"] = torch.zeros(R * _lib.REC_WORDS, **i32)
+        t["actions"] = torch.zeros(R * 2 * C * 3, **i32)
+        t["forks"] = torch.zeros(R * C * 4, **i32)
+        t["step_pred"] = torch.zeros(R * C, dtype=torch.float64, device=dev)
+        t["queue_head"] = torch.zeros(2, **i32)
+        P = max(self.P, 1)
+        for name in ("out_final", "out_reason", "out_tokens_decode", "out_tokens_probe",
+                     "out_rounds", "out_error"):
+            t[name] = torch.full((P,), -1, **i32)
+        t["out_tally"] = torch.zeros(P * A, **i32)
+        t["counters"] = torch.zeros(_lib.N_COUNTERS, dtype=torch.int64, device=dev)
+        self.t = t
+        st = _lib.State()
+        st.n_slots, st.branch_cap, st.answer_cap = R, B, A
+        for name in _lib.STATE_PTR_FIELDS:
+            setattr(st, name, t[name].data_ptr())
+        self.state = st
+        self.probs = torch.zeros(R * C * max(self.policy.n_layers, 1), dtype=torch.float64,
+                                 device=dev)
+
+    # ------------------------------------------------------------------
+    def advance(self, stream=None) -> None:
+        """Refill finished slots, then phase 1 (orchestrator.py:344-355)."""
+        _lib.check(self.lib.duchess_advance(self.policy, self.wl.struct, self.state,
+                                            _lib.stream_handle(stream)), "duchess_advance")
+
+    def decide(self, probs: torch.Tensor | None = None, stream=None) -> None:
+        """Phases 2-5 (orchestrator.py:357-402). probs: [R*C*L] fp64 by slot,
+        required for PRED_DEVICE / PRED_HOST."""
+        p = probs if probs is not None else self.probs
+        _lib.check(self.lib.duchess_decide(self.policy, self.wl.struct, self.state,
+                                           p.data_ptr(), _lib.stream_handle(stream)),
+                   "duchess_decide")
+
+    def step(self, score_fn=None, stream=None) -> None:
+        """One round for every occupied slot. score_fn(engine) must fill
+        self.probs for the survivors flagged in t['row_mask'] when the
+        prediction source is PRED_DEVICE (e.g. fill + K1)."""
+        self.advance(stream)
+        if self.policy.pred_source != _lib.PRED_TRACE:
+            if score_fn is None:
+                raise ValueError("this prediction source needs a score_fn")
+            score_fn(self)
+        self.decide(stream=stream)
+
+    # ------------------------------------------------------------------
+    def counters(self) -> np.ndarray:
+        return self.t["counters"].cpu().numpy()
+
+    def all_done(self) -> bool:
+        done = self.t["done"].cpu().numpy()
+        head = int(self.t["queue_head"][0])
+        return bool(done.all()) and head >= self.wl.struct.queue_len
+
+    def round_reports(self):
+        """Per-slot (pool index, RoundReport-tuple) of the latest round:
+        (round_index, decoding, max_chunk, decode_tokens, probes,
+        [(kind, branch_id, source_or_None)], done)."""
+        rec = self.t["round_rec"].view(self.R, _lib.REC_WORDS).cpu().numpy()
+        acts = self.t["actions"].view(self.R, 2 * self.C, 3).cpu().numpy()
+        kinds = {_lib.ACT_CONTINUE: "continue", _lib.ACT_TERMINATE: "terminate",
+                 _lib.ACT_BRANCH_OUT: "branch_out"}
+        out = []
+        for r in range(self.R):
+            rr = rec[r]
+            if rr[_lib.REC_ROUND] == 0:
+                continue
+            n = int(rr[_lib.REC_NACTIONS])
+            actions = [(kinds[int(a[0])], int(a[1]), None if a[2] < 0 else int(a[2]))
+                       for a in acts[r, :n]]
+            out.append((int(rr[_lib.REC_REQ]),
+                        (int(rr[_lib.REC_ROUND]), int(rr[_lib.REC_DECODING]),
+                         int(rr[_lib.REC_MAX_CHUNK]), int(rr[_lib.REC_DECODE]),
+                         int(rr[_lib.REC_PROBES]), actions, bool(rr[_lib.REC_DONE]))))
+        return out
+
+    def outcomes(self):
+        """Per pool index: None (unfinished) or dict(tally, final, reason,
+        tokens_decode, tokens_probe, rounds, error)."""
+        t = {k: self.t[k].cpu().numpy() for k in
+             ("out_final", "out_reason", "out_tokens_decode", "out_tokens_probe",
+              "out_rounds", "out_error")}
+        tally = self.t["out_tally"].view(max(self.P, 1), self.wl.answer_cap).cpu().numpy()
+        reasons = {1: "consensus", 2: "coverage", 3: "exhausted"}
+        res = []
+        for p in range(self.P):
+            if t["out_reason"][p] < 0:
+                res.append(None)
+                continue
+            ans = self.wl.answers[p]
+            counts = {ans[a]: int(n) for a, n in enumerate(tally[p][:len(ans)]) if n}
+            fin = int(t["out_final"][p])
+            res.append(dict(tally=counts, final=None if fin < 0 else ans[fin],
+                            reason=reasons[int(t["out_reason"][p])],
+                            tokens_decode=int(t["out_tokens_decode"][p]),
+                            tokens_probe=int(t["out_tokens_probe"][p]),
+                            rounds=int(t["out_rounds"][p]), error=int(t["out_error"][p])))
+        return res
+
+    def branch_snapshot(self, slot: int):
+        """Host copy of one slot's branch table (for facades / tests)."""
+        B = self.wl.branch_cap
+        sl = slice(slot * B, (slot + 1) * B)
+        g = {k: self.t[k][sl].cpu().numpy() for k in
+             ("br_offset", "br_decoded", "br_streak", "br_status", "br_final", "br_npred",
+              "br_last_pred", "br_slot")}
+        n = int(self.t["n_branches"][slot])
+        return {k: v[:n] for k, v in g.items()}

@@ -1,0 +1,68 @@
+"""CPU checks of the C-ABI boundary: the in-tree sm_100a library loads and
+exports every function declared in include/duchess_b200.h, and the ctypes
+struct layouts match the header's field lists."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "duchess_b200.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(duchess_\w+)\s*\(", text, flags=re.M)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SYMBOLS, f"{name} missing from the ctypes binding"
+    assert lib.duchess_version().decode().startswith("duchess_b200")
+
+
+def _struct_fields(name):
+    text = HEADER.read_text()
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), text, flags=re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body)
+    return re.findall(r"\b(\w+)\s*;", body)
+
+
+@pytest.mark.parametrize("cname,pyname", [("DuchessPolicy", "Policy"),
+                                          ("DuchessWorkload", "Workload"),
+                                          ("DuchessState", "State")])
+def test_struct_layouts_match_header(cname, pyname):
+    from paper_2509_24957_b200 import _lib
+    py = getattr(_lib, pyname)
+    assert [f[0] for f in py._fields_] == _struct_fields(cname)
+
+
+def test_workspace_queries_need_no_gpu():
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    assert lib.duchess_score_workspace_bytes(4096, 1) == 0
+    assert lib.duchess_score_workspace_bytes(4096, 2) == 4096 * 2 * 16 + 4096 * 4
+    assert lib.duchess_fork_workspace_bytes(4, 8) == (4 + 1 + 2 * 32 + 4) * 4
+
+
+def test_invalid_arguments_are_rejected_before_launch():
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    # null pointers / bad sizes return DUCHESS_EINVAL (1) without touching a device
+    assert lib.duchess_score(None, 1, 4, 1, 1, 16, 16, 16, 16, None, None, None, None, None,
+                             None, 0, 0, 0, None) == 1
+    assert lib.duchess_sort_difficulty(None, None, 1, None, None) == 1
+    assert lib.duchess_lr_grad(None, 1, None, None, 8, 16, 1.0, None, None, 0, None) == 1
+    assert lib.duchess_branch_out_sample(None, 0, 1.0, None, 0, None, None, None, None) == 1
+    pol = _lib.Policy()
+    pol.max_branches = 0
+    assert lib.duchess_advance(ctypes.byref(pol), ctypes.byref(_lib.Workload()),
+                               ctypes.byref(_lib.State()), None) == 1
