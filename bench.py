@@ -1,0 +1,445 @@
+"""Benchmark: branch-steps/s scored + decided (DUCHESS probe + orchestration).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c1|c3]
+
+One step = one orchestration round over every request slot on the GPU:
+duchess_advance (refill + decode phase) -> duchess_score (K1: pooled LN +
+linear probe over each survivor's activation window, read from HBM) ->
+duchess_decide (predict / early-terminate / branch-out / request termination).
+A branch-step is one survivor scored and decided (one `self._predict` call in
+reference orchestrator.py:358-362).
+
+Default workload (BASELINE.json configs[1], "C2"): 256 request slots x 16
+branch slots, hidden 4096, bf16 activations, 32-token pooling window, one
+probe layer, math-like knobs with max_branches=16 (presets.py:55-59), a
+cycling pool of 2048 synthetic requests (64 templates each) admitted in
+easiest-first order. Activations: 4 rotating 1 GiB slabs (4x the 126 MB L2,
+so every step streams from HBM). Under torchrun each rank runs its own
+request shard (weak scaling, no data-path collective).
+
+--impl reference times the CPU restatement of the reference (oracle/port.py:
+the reference's DuchessRun with a predictor= that pools + LayerNorms + dots
+the same windows in numpy) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "branch-steps/sec scored+decided (HBM GB/s % of peak) at 1/2/4/8 B200 vs CPU"
+UNIT = "branch-steps/s"
+
+CONFIGS = {
+    # name: (R slots, c, L, T, H, dtype, preset, pool)
+    "c2": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048),
+    "c1": dict(R=8, c=8, L=1, T=1, H=4096, dtype="f32", preset="gsm8k-like", pool=128),
+    "c3": dict(R=1024, c=32, L=4, T=32, H=5120, dtype="bf16", preset="math-like", pool=4096),
+}
+
+PRESET_KNOBS = {   # presets.py:30-68 (knobs) — max_branches overridden per config
+    "gsm8k-like": dict(interval_tokens=16, early_term_threshold=0.70, early_term_rounds=2,
+                       branch_out_temperature=1.0, consensus_frac=0.6, coverage_frac=0.8),
+    "math-like": dict(interval_tokens=80, early_term_threshold=0.80, early_term_rounds=2,
+                      branch_out_temperature=0.8, consensus_frac=0.6, coverage_frac=0.8),
+}
+PRESET_GEN = {
+    "gsm8k-like": dict(level_median_tokens=(180, 220, 260, 300, 350),
+                       level_correct_prob=(0.92, 0.88, 0.84, 0.80, 0.75), probe_stride=16),
+    "math-like": dict(level_median_tokens=(340, 460, 640, 840, 1180),
+                      level_correct_prob=(0.85, 0.78, 0.70, 0.62, 0.52),
+                      distractor_count=10, probe_stride=40),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload (host-side packing; identical for the GPU arm and the CPU arm)
+
+def make_workload(cfg, seed):
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    from paper_2509_24957_b200.orchestrator import OrchestratorConfig
+    params = SyntheticParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]])
+    traces = generate_synthetic(params, cfg["pool"], seed=seed).requests
+    knobs = OrchestratorConfig(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+    master = random.Random(seed + 1)
+    seeds = [master.getrandbits(64) for _ in traces]
+    return traces, knobs, seeds
+
+
+def make_probe(H, L, seed=0):
+    rng = np.random.default_rng(seed)
+    w = rng.normal(0.0, 1.5 / np.sqrt(H), size=(L, H))
+    g = rng.uniform(0.5, 1.5, size=(L, H))
+    beta = rng.uniform(-0.1, 0.1, size=(L, H))
+    return w, np.zeros(L), g, beta
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait(timeout=10)
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def run_gpu(args, cfg, rank, world, local_rank):
+    import torch
+
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
+    from paper_2509_24957_b200.scheduler import difficulty_queue
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R, C, L, T, H = cfg["R"], cfg["c"], cfg["L"], cfg["T"], cfg["H"]
+    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    esz = 2 if cfg["dtype"] == "bf16" else 4
+    traces, knobs, seeds = make_workload(cfg, seed=1000 + 17 * rank)
+    queue = difficulty_queue([t.difficulty for t in traces], device=dev)
+    eng = BatchedDuchess(traces, knobs, seeds, n_slots=R, pred_source=_lib.PRED_DEVICE,
+                         queue=queue, cycle=True, n_layers=L, combine=1 if L > 1 else 0,
+                         device=dev)
+    w, b, g, beta = make_probe(H, L)
+    bank = ProbeBank.from_linear(w, b, g, beta, device=dev)
+    scorer = Scorer(bank, R * C * L, nsplit=args.nsplit, threads=args.threads)
+    rows = R * C
+    n_slabs = max(2, min(4, int((4 << 30) // (rows * L * T * H * esz)) or 2))
+    if rows * L * T * H * esz < (256 << 20):
+        n_slabs = 4
+    slabs = [torch.empty((rows, L, T, H), dtype=tdtype, device=dev) for _ in range(n_slabs)]
+    for i, s in enumerate(slabs):
+        fill_windows(s, 7000 + 31 * rank + i)
+    logit = torch.empty((rows, L), dtype=torch.float32, device=dev)
+    probs = eng.probs.view(rows, L)
+    stream = torch.cuda.current_stream(dev)
+    k1_ev = []
+
+    def one_step(i, timed):
+        eng.advance()
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        scorer(slabs[i % n_slabs], logit, probs, row_mask=eng.t["row_mask"])
+        if timed:
+            e1.record(stream)
+            k1_ev.append((e0, e1))
+        eng.decide()
+
+    for i in range(args.warmup):
+        one_step(i, False)
+    torch.cuda.synchronize(dev)
+    c0 = eng.t["counters"].clone()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        one_step(args.warmup + i, True)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    if world > 1:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1)
+    cnt = (eng.t["counters"] - c0).cpu().numpy()
+    branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
+    k1_ms = sum(a.elapsed_time(b) for a, b in k1_ev)
+    stats = torch.tensor([ms, float(branch_steps), k1_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = stats[:1].clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tot = stats[1:2].clone()
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        ms_all, bs_all = float(tmax[0]), float(tot[0])
+    else:
+        ms_all, bs_all = ms, float(branch_steps)
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world)
+
+    if rank != 0:
+        return None
+    bytes_per_bs = T * H * esz * L
+    k1_avg_s = k1_ms / args.steps / 1e3
+    bytes_per_launch = branch_steps / args.steps * bytes_per_bs
+    peak, peak_kind = load_peaks()
+    achieved = bytes_per_launch / k1_avg_s / 1e9
+    out = {
+        "metric": METRIC, "value": bs_all / (ms_all / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg["dtype"], "data": "synthetic (counter-hashed N(0,1) activations with "
+        "outlier channels; generate_synthetic workload, random-init probe)",
+        "config": {"workload": f"{args.config.upper()}: {R} request slots x {C} branches, "
+                   f"hidden {H}, {L} probe layer(s), T={T} pooling window, {cfg['dtype']}, "
+                   f"{cfg['preset']} knobs, cycling pool of {cfg['pool']} requests "
+                   f"(easiest-first), {n_slabs} rotating activation slabs "
+                   f"({rows * L * T * H * esz / 2**30:.2f} GiB each, > L2)",
+                   "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
+                   "l2": "inputs larger than L2 (rotating slabs)",
+                   "parallelism": f"request-sharded x{world}"},
+        "branch_steps_per_step": branch_steps / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "kernel": "duchess_score (K1)", "bytes_per_launch": bytes_per_launch,
+                     "k1_us_per_launch": k1_avg_s * 1e6,
+                     "k1_share_of_step": k1_ms / ms,
+                     "traffic": None},
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk,
+        "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
+                     "finished_requests": int(cnt[_lib.CNT_FINISHED]),
+                     "forks": int(cnt[_lib.CNT_FORKS])},
+    }
+    return out
+
+
+def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world):
+    """Same step through the public API with the activations in pinned HOST
+    memory: per step H2D of the activation window slab, the three kernels,
+    and a D2H read of the round records (RoundReports)."""
+    import torch
+    steps = max(2, min(args.e2e_steps, args.steps))
+    host = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
+    host.copy_(torch.zeros(1, dtype=tdtype).expand_as(host))
+    dslab = torch.empty_like(host, device=dev)
+    rec_host = torch.empty(eng.t["round_rec"].numel(), dtype=torch.int32, pin_memory=True)
+    act_host = torch.empty(eng.t["actions"].numel(), dtype=torch.int32, pin_memory=True)
+    from paper_2509_24957_b200 import _lib
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        dslab.copy_(host, non_blocking=True)
+        eng.advance()
+        scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
+        eng.decide()
+        rec_host.copy_(eng.t["round_rec"], non_blocking=True)
+        act_host.copy_(eng.t["actions"], non_blocking=True)
+        stream.synchronize()
+
+    step()
+    c0 = eng.t["counters"].clone()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    bs = int((eng.t["counters"] - c0)[_lib.CNT_BRANCH_STEPS])
+    st = torch.tensor([dt, float(bs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        a = st[:1].clone()
+        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
+        b = st[1:].clone()
+        torch.distributed.all_reduce(b, op=torch.distributed.ReduceOp.SUM)
+        dt, bs = float(a[0]), float(b[0])
+    return {"value": bs / dt, "unit": UNIT,
+            "h2d_bytes_per_step": host.numel() * host.element_size(),
+            "d2h_bytes_per_step": (rec_host.numel() + act_host.numel()) * 4,
+            "steps": steps, "timing": "host wall clock, stream-synchronised each step"}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) — only here and in tests may oracle/ run.
+
+_CPU = {}
+
+
+def _cpu_init(cfg_name, n_req, seed):
+    import oracle.activations as oact
+    from oracle import port
+    cfg = CONFIGS[cfg_name]
+    H, T, L = cfg["H"], cfg["T"], cfg["L"]
+    params = port.GenParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]])
+    traces = port.generate(params, n_req, seed)
+    knobs = port.Knobs(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+    master = random.Random(seed + 1)
+    seeds = [master.getrandbits(64) for _ in traces]
+    w, b, g, beta = make_probe(H, L)
+    windows = [[oact.synth_window(7000 + k, k, 0, 0, l, T, H, cfg["dtype"] == "bf16")
+                for l in range(L)] for k in range(16)]
+    _CPU.update(traces=traces, knobs=knobs, seeds=seeds, w=w, b=b, g=g, beta=beta,
+                windows=windows, L=L, next=0)
+
+
+def _cpu_run(budget_s):
+    from oracle import port
+    st = _CPU
+    count = [0]
+
+    def predictor(tmpl, position, _rng):
+        count[0] += 1
+        win = st["windows"][(position * 31 + tmpl.natural_length) % len(st["windows"])]
+        ps = [port.pooled_linear_probe(win[l], st["w"][l], st["b"][l], st["g"][l],
+                                       st["beta"][l])[1] for l in range(st["L"])]
+        return ps[0] if len(ps) == 1 else sum(ps) / len(ps)
+
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        i = st["next"] % len(st["traces"])
+        st["next"] += 1
+        req = port.DuchessRequest(st["traces"][i], st["knobs"], random.Random(st["seeds"][i]),
+                                  predictor=predictor)
+        while not req.done and time.perf_counter() - t0 < budget_s:
+            req.step()
+    return count[0], time.perf_counter() - t0
+
+
+def cpu_measure(cfg_name, steps, budget_s, procs):
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_cpu_init, initargs=(cfg_name, 64, 4242)) as pool:
+        pool.map(_cpu_run, [0.2] * procs)            # warm
+        total_bs, total_t = 0, 0.0
+        per_step = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_run, [budget_s] * procs)
+            dt = time.perf_counter() - t0
+            bs = sum(r[0] for r in res)
+            total_bs += bs
+            total_t += dt
+            per_step.append(bs / dt)
+    return total_bs / total_t, per_step
+
+
+def cpu_baseline_entry(cfg_name, budget_total=12.0):
+    procs = os.cpu_count() or 1
+    steps = 3
+    val, _ = cpu_measure(cfg_name, steps, budget_total / steps, procs)
+    cfg = CONFIGS[cfg_name]
+    return {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"oracle/port.py DuchessRun restatement + numpy pooled LN probe "
+                      f"(T={cfg['T']}, H={cfg['H']}, L={cfg['L']}) on {cfg['preset']} requests "
+                      f"(c={cfg['c']}), {procs} processes x {steps} x {budget_total/steps:.1f} s"}
+
+
+def run_reference(args, cfg):
+    procs = os.cpu_count() or 1
+    total = args.steps + args.warmup
+    budget = max(0.5, min(5.0, 120.0 / max(total, 1)))
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_cpu_init, initargs=(args.config, 64, 4242)) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_run, [budget] * procs)
+        total_bs, total_t = 0, 0.0
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_run, [budget] * procs)
+            total_t += time.perf_counter() - t0
+            total_bs += sum(r[0] for r in res)
+    val = total_bs / total_t
+    return {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config.upper()} (CPU port)",
+                                        "requests": cfg["R"], "branches": cfg["c"],
+                                        "hidden": cfg["H"], "layers": cfg["L"],
+                                        "window": cfg["T"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} processes x {budget:.2f} s per step of "
+                                   f"oracle/port.py DuchessRun + numpy pooled probe"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--nsplit", type=int, default=2)
+    ap.add_argument("--threads", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    out = run_gpu(args, cfg, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_entry(args.config)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

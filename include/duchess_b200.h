@@ -205,6 +205,30 @@ int duchess_template_lookup(const DuchessWorkload* workload, const int32_t* tmpl
                             const int32_t* pos, int32_t n, int32_t* out_probe_answer,
                             double* out_trace_pred, void* stream);
 
+/* synthetic_predict (predictor.py:328-335): n sequential draws from one
+ * MT19937 stream (mt_state[625], updated in place). */
+int duchess_synthetic_predict(uint32_t* mt_state, int32_t n, const int32_t* converged, double rho,
+                              double* out, void* stream);
+/* sample_confused_level (predictor.py:376-386); matrix is 5x5 row-major fp64. */
+int duchess_confused_level(uint32_t* mt_state, int32_t n, const int32_t* true_level,
+                           const double* matrix, int32_t* out, void* stream);
+/* check_early_termination (orchestrator.py:167-174) over CSR prediction histories. */
+int duchess_early_termination(const double* history, const int32_t* offsets, int32_t n_sets,
+                              double threshold, int32_t rounds, int32_t* out, void* stream);
+
+/* ---- frozen MLP forward (predictor.py:126-151), fp64, any depth ----------
+ * Packed parameters (fp64): [ln_gain H, ln_bias H] if has_ln, then per hidden
+ * layer k: W_k [d_{k+1} x d_k] row-major, b_k, and if has_bn: mean, var,
+ * gain, bias; then head W [head x d_last], b [head]. act[k]: 0 relu, 1 gelu.
+ * Output per row: logits[head], probs[head] (clipped sigmoid if head == 1,
+ * softmax otherwise). One CTA per input row. dims (n_hidden + 1 entries:
+ * input and hidden widths) and act (n_hidden) are HOST arrays, passed by value;
+ * params, x, logits, probs are device memory. */
+int duchess_mlp_forward(const double* params, const int32_t* dims, int32_t n_hidden,
+                        int32_t head_dim, const int32_t* act, int32_t has_ln, int32_t has_bn,
+                        const double* x, int64_t n_rows, double* logits, double* probs,
+                        void* stream);
+
 /* ---- difficulty ordering (scheduler.py:60-96) --------------------------- */
 int duchess_sort_difficulty(const uint64_t* keys, const int32_t* seg_offsets, int32_t n_segs,
                             int32_t* out_perm, void* stream);

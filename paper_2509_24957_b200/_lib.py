@@ -110,6 +110,15 @@ SYMBOLS = {
                                   C.c_void_p]),
     "duchess_sgd_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_float,
                                      C.c_void_p]),
+    "duchess_synthetic_predict": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_double,
+                                            C.c_void_p, C.c_void_p]),
+    "duchess_confused_level": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p]),
+    "duchess_early_termination": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                                            C.c_int32, C.c_void_p, C.c_void_p]),
+    "duchess_mlp_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_void_p,
+                                      C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "duchess_version": (C.c_char_p, []),
     "duchess_device_arch": (C.c_int, []),
 }

@@ -599,6 +599,60 @@ __global__ void lookup_kernel(DuchessWorkload w, const int32_t* tmpl, const int3
   if (out_pred) out_pred[i] = trace_prediction(w, tmpl[i], pos[i]);
 }
 
+// synthetic_predict (predictor.py:328-335) for n calls drawing from one stream.
+__global__ void synthetic_kernel(uint32_t* mt, int n, const int32_t* converged, double rho,
+                                 double* out) {
+  __shared__ uint32_t words[2 * 256];
+  const int lane = threadIdx.x;
+  for (int base = 0; base < n; base += 256) {
+    const int m = min(256, n - base);
+    mt_words_warp(mt, 2 * m, words, lane);
+    for (int k = lane; k < m; k += 32) {
+      const double u = mt_res53(words[2 * k], words[2 * k + 1]);
+      const double oracle = converged[base + k] ? 1.0 : 0.0;
+      const double v = __dadd_rn(__dmul_rn(rho, oracle), __dmul_rn(__dsub_rn(1.0, rho), u));
+      out[base + k] = fmin(fmax(v, 0.0), 1.0);
+    }
+    __syncwarp();
+  }
+}
+
+// sample_confused_level (predictor.py:376-386): row-wise CDF walk, one draw per call.
+__global__ void confusion_kernel(uint32_t* mt, int n, const int32_t* true_level,
+                                 const double* matrix, int32_t* out) {
+  __shared__ uint32_t words[2 * 256];
+  const int lane = threadIdx.x;
+  for (int base = 0; base < n; base += 256) {
+    const int m = min(256, n - base);
+    mt_words_warp(mt, 2 * m, words, lane);
+    if (lane == 0) {
+      for (int k = 0; k < m; ++k) {
+        const double u = mt_res53(words[2 * k], words[2 * k + 1]);
+        const double* row = matrix + (true_level[base + k] - 1) * 5;
+        double acc = 0.0;
+        int lvl = 5;
+        for (int j = 0; j < 5; ++j) {
+          acc = __dadd_rn(acc, row[j]);
+          if (u < acc) { lvl = j + 1; break; }
+        }
+        out[base + k] = lvl;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// check_early_termination (orchestrator.py:167-174): last `rounds` strictly > threshold.
+__global__ void streak_kernel(const double* hist, const int32_t* off, int n_sets, double thr,
+                              int rounds, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_sets) return;
+  const int lo = off[i], hi = off[i + 1];
+  int ok = hi - lo >= rounds;
+  for (int j = hi - rounds; ok && j < hi; ++j) ok = hist[j] > thr;
+  out[i] = ok;
+}
+
 }  // namespace duchess
 
 using namespace duchess;
@@ -657,5 +711,31 @@ extern "C" int duchess_template_lookup(const DuchessWorkload* workload, const in
   if (n == 0) return DUCHESS_OK;
   lookup_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       *workload, tmpl, pos, n, out_probe_answer, out_trace_pred);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_synthetic_predict(uint32_t* mt_state, int32_t n, const int32_t* converged,
+                                         double rho, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!mt_state || !converged || !out))) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  synthetic_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(mt_state, n, converged, rho, out);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_confused_level(uint32_t* mt_state, int32_t n, const int32_t* true_level,
+                                      const double* matrix, int32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!mt_state || !true_level || !matrix || !out))) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  confusion_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(mt_state, n, true_level, matrix, out);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_early_termination(const double* history, const int32_t* offsets,
+                                         int32_t n_sets, double threshold, int32_t rounds,
+                                         int32_t* out, void* stream) {
+  if (n_sets < 0 || rounds < 1 || (n_sets > 0 && (!history || !offsets || !out))) return DUCHESS_EINVAL;
+  if (n_sets == 0) return DUCHESS_OK;
+  streak_kernel<<<(n_sets + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      history, offsets, n_sets, threshold, rounds, out);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

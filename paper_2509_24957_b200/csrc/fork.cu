@@ -172,6 +172,10 @@ segsort_kernel(const uint64_t* keys, const int32_t* seg_off, int32_t* out_perm) 
   __shared__ int32_t v[kSortMax];
   const int seg = blockIdx.x;
   const int lo = seg_off[seg], n = seg_off[seg + 1] - lo;
+  if (n > kSortMax) {   // segment too large for one CTA: flag every entry
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out_perm[lo + i] = -1;
+    return;
+  }
   int m = 1;
   while (m < n) m <<= 1;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {

@@ -1,0 +1,134 @@
+"""Inter-request scheduling (mirrors reference scheduler.py).
+
+Difficulty ordering is the device segmented sort ``duchess_sort_difficulty``
+over 64-bit keys ``level << 61 | arrival << 21 | order``. The keys are unique,
+so sorting one queue snapshot gives exactly the sequence of repeated
+``next_request`` pops (scheduler.py:60-96); ``next_request`` itself is that
+sort over the eligible entries, popping the first.
+"""
+
+from __future__ import annotations
+
+import heapq
+import random
+from dataclasses import dataclass
+
+import numpy as np
+
+from .workload import RequestTrace
+
+FCFS = "fcfs"
+EASIEST_ACTUAL = "easiest-actual"
+EASIEST_PREDICTED = "easiest-predicted"
+SCHEDULES = (FCFS, EASIEST_ACTUAL, EASIEST_PREDICTED)
+
+SEGMENT_MAX = 4096          # keys per device segment (one CTA, shared memory)
+_ARRIVAL_BITS, _ORDER_BITS = 40, 21
+
+
+@dataclass(frozen=True)
+class ArrivalConfig:
+    rate_qpm: float
+    n_requests: int
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        if self.rate_qpm <= 0:
+            raise ValueError("rate_qpm must be > 0")
+        if self.n_requests < 1:
+            raise ValueError("n_requests must be >= 1")
+
+
+def gen_arrivals(config: ArrivalConfig) -> list:
+    """Strictly increasing Poisson arrival times in ms (scheduler.py:35-48)."""
+    rng = random.Random(config.seed)
+    gap = 60000.0 / config.rate_qpm
+    out, t, prev = [], 0.0, -1
+    for _ in range(config.n_requests):
+        t += rng.expovariate(1.0 / gap)
+        prev = max(int(round(t)), prev + 1)
+        out.append(prev)
+    return out
+
+
+@dataclass
+class QueueEntry:
+    trace: RequestTrace
+    arrival: int
+    order: int
+    prefill_done: int | None = None
+    predicted_difficulty: int | None = None
+
+
+def pack_keys(levels, arrivals, orders) -> np.ndarray:
+    lv = np.asarray(levels, dtype=np.uint64)
+    ar = np.asarray(arrivals, dtype=np.uint64)
+    od = np.asarray(orders, dtype=np.uint64)
+    if (ar >= (1 << _ARRIVAL_BITS)).any() or (od >= (1 << _ORDER_BITS)).any() or (lv > 7).any():
+        raise ValueError("key field out of range (level < 8, arrival < 2^40 ms, order < 2^21)")
+    return (lv << np.uint64(61)) | (ar << np.uint64(_ORDER_BITS)) | od
+
+
+def device_sort(keys: np.ndarray, device="cuda") -> list:
+    """Permutation sorting unique uint64 keys ascending, on the GPU (segments
+    of <= SEGMENT_MAX keys sorted on device, merged on the host)."""
+    import torch
+
+    from . import _lib
+    n = len(keys)
+    if n == 0:
+        return []
+    lib = _lib.load()
+    _lib.require_cuda()
+    segs = list(range(0, n, SEGMENT_MAX)) + [n]
+    k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(device)
+    off = torch.tensor(segs, dtype=torch.int32, device=device)
+    perm = torch.empty(n, dtype=torch.int32, device=device)
+    _lib.check(lib.duchess_sort_difficulty(k.data_ptr(), off.data_ptr(), len(segs) - 1,
+                                           perm.data_ptr(), _lib.stream_handle()),
+               "duchess_sort_difficulty")
+    p = perm.cpu().numpy()
+    if len(segs) == 2:
+        return [int(x) for x in p]
+    runs = [[(int(keys[j]), int(j)) for j in p[a:b]] for a, b in zip(segs[:-1], segs[1:])]
+    return [j for _, j in heapq.merge(*runs)]
+
+
+def difficulty_queue(levels, arrivals=None, device="cuda") -> list:
+    """Easiest-first service order of a queue snapshot (level, arrival, order)."""
+    n = len(levels)
+    arrivals = list(range(n)) if arrivals is None else arrivals
+    return device_sort(pack_keys([1 if lv is None else lv for lv in levels], arrivals,
+                                 range(n)), device=device)
+
+
+def next_request(queue: list, policy: str, now: int) -> QueueEntry:
+    """Pop the next request to serve (scheduler.py:60-96)."""
+    if policy not in SCHEDULES:
+        raise ValueError(f"unknown schedule policy {policy!r}")
+    idx, lv, ar, od = [], [], [], []
+    for i, e in enumerate(queue):
+        if e.arrival > now:
+            continue
+        if policy == FCFS:
+            level = 0
+        elif policy == EASIEST_ACTUAL:
+            if e.trace.difficulty is None:
+                raise ValueError(f"request {e.trace.id!r} has no difficulty label; "
+                                 f"easiest-actual needs labeled traces")
+            level = e.trace.difficulty
+        else:
+            if e.prefill_done is None or e.prefill_done > now:
+                continue
+            if e.predicted_difficulty is None:
+                raise ValueError(f"request {e.trace.id!r} has no predicted difficulty; "
+                                 f"prefill must run before easiest-predicted selection")
+            level = e.predicted_difficulty
+        idx.append(i)
+        lv.append(level)
+        ar.append(e.arrival)
+        od.append(e.order)
+    if not idx:
+        raise ValueError("no eligible request")
+    first = device_sort(pack_keys(lv, ar, od))[0]
+    return queue.pop(idx[first])
