@@ -166,7 +166,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                          device=dev)
     w, b, g, beta = make_probe(H, L)
     bank = ProbeBank.from_linear(w, b, g, beta, device=dev)
-    scorer = Scorer(bank, R * C * L, nsplit=args.nsplit, threads=args.threads)
+    if args.k1 == "ldg":
+        scorer = Scorer(bank, R * C * L, nsplit=args.nsplit, threads=args.threads)
+    else:
+        scorer = Scorer(bank, R * C * L)          # persistent TMA-bulk kernel
     rows = R * C
     n_slabs = max(2, min(4, int((4 << 30) // (rows * L * T * H * esz)) or 2))
     if rows * L * T * H * esz < (256 << 20):
@@ -184,7 +187,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        scorer(slabs[i % n_slabs], logit, probs, row_mask=eng.t["row_mask"])
+        if args.k1 == "list":
+            scorer.score_list(slabs[i % n_slabs], logit, probs, eng.t["active_rows"],
+                              eng.t["active_count"])
+        else:
+            scorer(slabs[i % n_slabs], logit, probs, row_mask=eng.t["row_mask"])
         if timed:
             e1.record(stream)
             k1_ev.append((e0, e1))
@@ -248,7 +255,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "branch_steps_per_step": branch_steps / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
-                     "kernel": "duchess_score (K1)", "bytes_per_launch": bytes_per_launch,
+                     "kernel": f"duchess_score (K1, {args.k1})", "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_share_of_step": k1_ms / ms,
                      "traffic": None},
@@ -279,7 +286,8 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world):
     def step():
         dslab.copy_(host, non_blocking=True)
         eng.advance()
-        scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
+        scorer.score_list(dslab, logit, probs, eng.t["active_rows"], eng.t["active_count"]) \
+            if args.k1 == "list" else scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
         eng.decide()
         rec_host.copy_(eng.t["round_rec"], non_blocking=True)
         act_host.copy_(eng.t["actions"], non_blocking=True)
@@ -421,6 +429,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
+                    help="K1 variant: persistent TMA over the compacted survivor list "
+                         "(default), TMA over the row mask, or the per-window LDG kernel")
     ap.add_argument("--nsplit", type=int, default=2)
     ap.add_argument("--threads", type=int, default=128)
     ap.add_argument("--e2e-steps", type=int, default=10)

@@ -164,6 +164,8 @@ typedef struct DuchessState {
   int32_t* forks;      /* [R*C*4]  (child, source, table_root, prefix_tokens) */
   double* step_pred;   /* [R*C] prediction used for each survivor, by slot */
   int32_t* queue_head; /* [2] */
+  int32_t* active_rows;  /* [R*C] compacted survivor rows (r*C + slot) for K1, or NULL */
+  int32_t* active_count; /* [1] entries in active_rows; reset by duchess_decide */
   /* outcomes by pool index [P] */
   int32_t* out_final;
   int32_t* out_reason;
@@ -182,6 +184,14 @@ int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_lay
                   const float* wg, const float* c1, const uint8_t* row_mask, float* out_logit,
                   double* out_prob, void* workspace, size_t workspace_bytes, int32_t nsplit,
                   int32_t threads, void* stream);
+/* Same computation over a compacted device list of rows (row_list[0..*row_count),
+ * e.g. DuchessState.active_rows written by duchess_advance): persistent,
+ * TMA-bulk-staged kernel, one CTA per SM; n_rows bounds the row indices. */
+int duchess_score_list(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                       int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                       int64_t token_stride, const float* wg, const float* c1,
+                       const int32_t* row_list, const int32_t* row_count, float* out_logit,
+                       double* out_prob, void* stream);
 int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
                              int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
                              int64_t token_stride, uint64_t seed, const int64_t* row_req,

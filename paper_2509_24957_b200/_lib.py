@@ -63,7 +63,7 @@ STATE_PTR_FIELDS = [
     "br_offset", "br_decoded", "br_streak", "br_status", "br_final", "br_npred", "br_slot",
     "br_last_pred",
     "slot_branch", "row_mask", "row_pos", "row_tmpl", "row_req",
-    "round_rec", "actions", "forks", "step_pred", "queue_head",
+    "round_rec", "actions", "forks", "step_pred", "queue_head", "active_rows", "active_count",
     "out_final", "out_reason", "out_tokens_decode", "out_tokens_probe", "out_rounds",
     "out_error", "out_tally", "counters",
 ]
@@ -82,6 +82,10 @@ SYMBOLS = {
                                 C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_size_t, C.c_int32, C.c_int32, C.c_void_p]),
+    "duchess_score_list": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]),
     "duchess_fill_activations": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                            C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                            C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p,

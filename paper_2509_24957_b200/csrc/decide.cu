@@ -160,120 +160,209 @@ __device__ int sample_index(const double* raw, int n, double total, double u, bo
 }
 
 // ---------------------------------------------------------------------------
+// Per-warp shared-memory cache of one request slot. Active branches are exactly
+// the occupied branch slots (a slot is released whenever its branch leaves
+// ACTIVE), so a round only touches <= C branches: they are gathered once with
+// independent loads, processed in shared memory, and every state change is
+// stored straight back (stores are off the critical path).
 
-struct WarpScratch {
-  uint32_t words[4 * kMaxC];
-  double draws[2 * kMaxC];
+struct SlotCache {
+  int bid[kMaxC];        // branch id occupying slot j, -1 = free
+  int off[kMaxC], dec[kMaxC], streak[kMaxC], status[kMaxC], npred[kMaxC];
+  double lp[kMaxC];
+  int rank[kMaxC];       // creation-order rank of slot j among occupied slots
+  int order[kMaxC];      // occupied slots in creation (branch id) order
+  int need[kMaxC];       // survivor needs a synthetic draw
+  int free_slots[kMaxC];
+  int nat_child[kMaxC];
+  int alive_slot[kMaxC];
+  int alive_root[kMaxC];
+  int src_idx[kMaxC];
   double raw[kMaxC];
-  int alive[kMaxC];
-  int root[kMaxC];
+  double draws[kMaxC];
+  uint32_t words[2 * kMaxC];
+  uint32_t mt[kMtN + 1];
 };
 
-__device__ __forceinline__ int warp_count_lt(const int32_t* flags, int n, int upto, int lane) {
+__device__ __forceinline__ int warp_count_flags(const int32_t* flags, int upto, int lane) {
   int cnt = 0;
-  for (int base = 0; base < upto; base += 32) {
-    const int j = base + lane;
-    const bool f = j < upto && j < n && flags[j] != 0;
-    cnt += __popc(__ballot_sync(0xffffffffu, f));
+  for (int base = 0; base < upto; base += 128) {
+    int f[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = base + q * 32 + lane;
+      f[q] = j < upto ? flags[j] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cnt += __popc(__ballot_sync(0xffffffffu, f[q] != 0));
   }
   return cnt;
 }
 
+__device__ __forceinline__ void load_slot(const DuchessState& s, int64_t rC, int64_t rB, int C,
+                                          SlotCache& c, int lane) {
+  for (int j = lane; j < C; j += 32) {
+    const int b = s.slot_branch[rC + j];
+    c.bid[j] = b;
+    if (b >= 0) {
+      const int64_t bi = rB + b;
+      c.off[j] = s.br_offset[bi];
+      c.dec[j] = s.br_decoded[bi];
+      c.streak[j] = s.br_streak[bi];
+      c.status[j] = s.br_status[bi];
+      c.npred[j] = s.br_npred[bi];
+      c.lp[j] = s.br_last_pred[bi];
+    }
+  }
+  __syncwarp();
+}
+
+// Creation-order ranks of occupied slots; returns the number occupied.
+__device__ __forceinline__ int order_slots(SlotCache& c, int C, int lane) {
+  int n = 0;
+  for (int base = 0; base < C; base += 32) {
+    const int j = base + lane;
+    const bool occ = j < C && c.bid[j] >= 0;
+    if (occ) {
+      const int b = c.bid[j];
+      int rk = 0;
+      for (int k = 0; k < C; ++k) rk += (c.bid[k] >= 0 && c.bid[k] < b);
+      c.rank[j] = rk;
+      c.order[rk] = j;
+    }
+    n += __popc(__ballot_sync(0xffffffffu, occ));
+  }
+  __syncwarp();
+  return n;
+}
+
+__device__ __forceinline__ void load_mt(const uint32_t* g, uint32_t* sm, int lane) {
+  for (int j = lane; j <= kMtN; j += 32) sm[j] = g[j];
+  __syncwarp();
+}
+__device__ __forceinline__ void store_mt(uint32_t* g, const uint32_t* sm, int lane) {
+  __syncwarp();
+  for (int j = lane; j <= kMtN; j += 32) g[j] = sm[j];
+}
+
+// Refill slot r with pool request p: RequestRun.__init__ (:242-248).
+__device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
+                            const DuchessState& s, int r, int p, SlotCache& c, int lane) {
+  const int C = pol.max_branches;
+  const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
+  const int n_tmpl = w.tmpl_off[p + 1] - w.tmpl_off[p];
+  const int seeded = min(C, n_tmpl);
+  for (int j = lane; j < C; j += 32) {
+    const bool live = j < seeded;
+    c.bid[j] = live ? j : -1;
+    c.off[j] = 0; c.dec[j] = 0; c.streak[j] = 0; c.status[j] = DUCHESS_ACTIVE;
+    c.npred[j] = 0; c.lp[j] = 0.5;
+    s.slot_branch[rC + j] = live ? j : -1;
+    if (live) {
+      const int64_t bi = rB + j;
+      s.br_offset[bi] = 0; s.br_decoded[bi] = 0; s.br_streak[bi] = 0;
+      s.br_status[bi] = DUCHESS_ACTIVE; s.br_final[bi] = -1; s.br_npred[bi] = 0;
+      s.br_slot[bi] = j; s.br_last_pred[bi] = 0.5;
+    }
+  }
+  for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
+  const uint32_t* src = w.mt_init + int64_t(p) * DUCHESS_MT_WORDS;
+  uint32_t* dst = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
+  for (int j = lane; j < DUCHESS_MT_WORDS; j += 32) dst[j] = src[j];
+  if (lane == 0) {
+    s.slot_req[r] = p;
+    s.n_branches[r] = seeded;
+    s.next_template[r] = seeded;
+    s.tokens_decode[r] = 0;
+    s.tokens_probe[r] = 0;
+    s.rounds[r] = 0;
+    s.done[r] = 0;
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= s.n_slots) return;
+  SlotCache& c = cache[threadIdx.x >> 5];
   const int C = pol.max_branches;
-  const int64_t rC = int64_t(r) * C;
-  const int64_t rB = int64_t(r) * s.branch_cap;
+  const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
-
   for (int j = lane; j < C; j += 32) s.row_mask[rC + j] = 0;
   if (lane < DUCHESS_REC_WORDS) rec[lane] = 0;
-  __syncwarp();
 
-  // ---- refill: the k-th empty slot (slot order) takes queue[head + k] ----
+  // ---- refill: the k-th slot needing one (slot order) takes queue[head + k] ----
   const int head = s.queue_head[0];
   if (r == 0) {
-    const int total = warp_count_lt(s.needs_refill, s.n_slots, s.n_slots, lane);
+    const int total = warp_count_flags(s.needs_refill, s.n_slots, lane);
     const int avail = w.cycle ? total : max(0, min(total, w.queue_len - head));
     if (lane == 0) s.queue_head[1] = head + avail;
   }
+  int p;
   if (s.needs_refill[r]) {
-    const int rank = warp_count_lt(s.needs_refill, s.n_slots, r, lane);
-    int q = head + rank;
-    int p = -1;
+    const int q = head + warp_count_flags(s.needs_refill, r, lane);
+    p = -1;
     if (w.queue_len > 0) {
       if (w.cycle) p = w.queue[q % w.queue_len];
       else if (q < w.queue_len) p = w.queue[q];
     }
-    if (lane == 0) s.slot_req[r] = p;
     if (p < 0) {
-      if (lane == 0) s.done[r] = 1;
+      if (lane == 0) { s.slot_req[r] = -1; s.done[r] = 1; }
       return;
     }
-    const int n_tmpl = w.tmpl_off[p + 1] - w.tmpl_off[p];
-    const int seeded = min(C, n_tmpl);   // RequestRun.__init__ :242-248
-    for (int b = lane; b < s.branch_cap; b += 32) {
-      const bool live = b < seeded;
-      s.br_offset[rB + b] = 0;
-      s.br_decoded[rB + b] = 0;
-      s.br_streak[rB + b] = 0;
-      s.br_status[rB + b] = live ? DUCHESS_ACTIVE : DUCHESS_CANCELLED;
-      s.br_final[rB + b] = -1;
-      s.br_npred[rB + b] = 0;
-      s.br_slot[rB + b] = live ? b : -1;
-      s.br_last_pred[rB + b] = 0.5;
-    }
-    for (int j = lane; j < C; j += 32) s.slot_branch[rC + j] = j < seeded ? j : -1;
-    for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
-    const uint32_t* src = w.mt_init + int64_t(p) * DUCHESS_MT_WORDS;
-    uint32_t* dst = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
-    for (int j = lane; j < DUCHESS_MT_WORDS; j += 32) dst[j] = src[j];
-    if (lane == 0) {
-      s.n_branches[r] = seeded;
-      s.next_template[r] = seeded;
-      s.tokens_decode[r] = 0;
-      s.tokens_probe[r] = 0;
-      s.rounds[r] = 0;
-      s.done[r] = 0;
-    }
-    __syncwarp();
+    refill_slot(pol, w, s, r, p, c, lane);
+  } else {
+    if (s.done[r]) return;
+    p = s.slot_req[r];
+    if (p < 0) return;
+    load_slot(s, rC, rB, C, c, lane);
   }
-  if (s.done[r] || s.slot_req[r] < 0) return;
 
   // ---- phase 1: decode one interval per active branch (:344-355) ----
-  const int p = s.slot_req[r];
   const int t0 = w.tmpl_off[p];
-  const int nb = s.n_branches[r];
   int decoding = 0, max_chunk = 0, dtok = 0, probes = 0;
-  for (int b = lane; b < nb; b += 32) {
-    const int64_t bi = rB + b;
-    if (s.br_status[bi] != DUCHESS_ACTIVE) continue;
-    const int t = t0 + b;                      // branch_id == template_index (:260-266)
-    const int nat = w.nat_len[t];
-    int pos = s.br_offset[bi] + s.br_decoded[bi];
-    const int room = min(nat, pol.token_cap) - pos;            // _decode_chunk :273-279
-    const int chunk = max(0, min(pol.interval_tokens, room));
-    s.br_decoded[bi] += chunk;
-    pos += chunk;
-    if (chunk > 0) { decoding++; max_chunk = max(max_chunk, chunk); dtok += chunk; }
-    int ans = -1, status = DUCHESS_ACTIVE;
-    if (pos >= nat) { ans = w.final_ans[t]; status = DUCHESS_NATURAL_END; }
-    else if (pos >= pol.token_cap) { ans = probe_answer(w, t, pos); status = DUCHESS_CAPPED; probes++; }
-    const int slot = s.br_slot[bi];
-    if (status != DUCHESS_ACTIVE) {
-      s.br_status[bi] = status;
-      s.br_final[bi] = ans;
-      atomicAdd(&s.tally[int64_t(r) * s.answer_cap + ans], 1);
-      if (slot >= 0) s.slot_branch[rC + slot] = -1;
-      s.br_slot[bi] = -1;
-    } else {
-      s.row_mask[rC + slot] = 1;
-      s.row_pos[rC + slot] = pos;
-      s.row_tmpl[rC + slot] = b;
-      s.row_req[rC + slot] = p;
+  for (int base = 0; base < C; base += 32) {
+    const int j = base + lane;
+    const int b = j < C ? c.bid[j] : -1;
+    bool surv = false;
+    if (b >= 0) {
+      const int64_t bi = rB + b;
+      const int t = t0 + b;                           // branch_id == template_index (:260-266)
+      const int nat = w.nat_len[t];
+      int pos = c.off[j] + c.dec[j];
+      const int room = min(nat, pol.token_cap) - pos;            // _decode_chunk :273-279
+      const int chunk = max(0, min(pol.interval_tokens, room));
+      c.dec[j] += chunk;
+      pos += chunk;
+      if (chunk > 0) { decoding++; max_chunk = max(max_chunk, chunk); dtok += chunk; }
+      s.br_decoded[bi] = c.dec[j];
+      int ans = -1, status = DUCHESS_ACTIVE;
+      if (pos >= nat) { ans = w.final_ans[t]; status = DUCHESS_NATURAL_END; }
+      else if (pos >= pol.token_cap) { ans = probe_answer(w, t, pos); status = DUCHESS_CAPPED; probes++; }
+      if (status != DUCHESS_ACTIVE) {                 // _collect (:287-290), slot released
+        s.br_status[bi] = status;
+        s.br_final[bi] = ans;
+        s.br_slot[bi] = -1;
+        atomicAdd(&s.tally[int64_t(r) * s.answer_cap + ans], 1);
+        s.slot_branch[rC + j] = -1;
+      } else {
+        surv = true;
+        s.row_mask[rC + j] = 1;
+        s.row_pos[rC + j] = pos;
+        s.row_tmpl[rC + j] = b;
+        s.row_req[rC + j] = p;
+      }
+    }
+    // compacted list of windows for the persistent scorer (order irrelevant)
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    if (m && s.active_rows) {
+      int basei = 0;
+      if (lane == 0) basei = atomicAdd(s.active_count, __popc(m));
+      basei = __shfl_sync(0xffffffffu, basei, 0);
+      if (surv) s.active_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
     }
   }
 #pragma unroll
@@ -284,10 +373,11 @@ advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
     max_chunk = max(max_chunk, __shfl_xor_sync(0xffffffffu, max_chunk, o));
   }
   if (lane == 0) {
-    s.rounds[r] += 1;
+    const int rounds = s.rounds[r] + 1;
+    s.rounds[r] = rounds;
     s.tokens_decode[r] += dtok;
     s.tokens_probe[r] += probes * pol.probe_cost_tokens;
-    rec[DUCHESS_REC_ROUND] = s.rounds[r];
+    rec[DUCHESS_REC_ROUND] = rounds;
     rec[DUCHESS_REC_DECODING] = decoding;
     rec[DUCHESS_REC_MAX_CHUNK] = max_chunk;
     rec[DUCHESS_REC_DECODE] = dtok;
@@ -298,195 +388,208 @@ advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
-  __shared__ WarpScratch scratch[kWarpsPerBlock];
+  __shared__ SlotCache cache[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int wi = threadIdx.x >> 5;
   const int r = blockIdx.x * kWarpsPerBlock + wi;
-  if (blockIdx.x == 0 && threadIdx.x == 0) s.queue_head[0] = s.queue_head[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.queue_head[0] = s.queue_head[1];
+    if (s.active_count) *s.active_count = 0;     // consumed by the scorer this round
+  }
   if (r >= s.n_slots) return;
-  WarpScratch& sc = scratch[wi];
+  SlotCache& c = cache[wi];
   const int C = pol.max_branches;
-  const int64_t rC = int64_t(r) * C;
-  const int64_t rB = int64_t(r) * s.branch_cap;
+  const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   const int64_t rA = int64_t(r) * s.answer_cap;
   int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
   if (rec[DUCHESS_REC_ROUND] == 0) return;   // slot idle or finished
   const int p = s.slot_req[r];
   const int t0 = w.tmpl_off[p];
   const int n_tmpl = w.tmpl_off[p + 1] - t0;
-  int nb = s.n_branches[r];
-  uint32_t* mt = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
+  const int nb = s.n_branches[r];
+  const int next_t = s.next_template[r];
+  uint32_t* mt_g = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
   int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
+  load_slot(s, rC, rB, C, c, lane);
+  const int n_surv = order_slots(c, C, lane);
+  bool mt_loaded = false;
 
-  // ---- phase 2: predictions for survivors, creation order (:357-363) ----
-  // Synthetic draws happen in survivor order for templates without pred_probs.
+  // ---- phase 2: predictions, creation order (:357-363) ----
   int n_need = 0;
   if (pol.pred_source == DUCHESS_PRED_TRACE) {
-    for (int base = 0; base < nb; base += 32) {
-      const int b = base + lane;
-      bool need = false;
-      if (b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE) {
-        const int t = t0 + b;
-        need = w.pred_off[t + 1] <= w.pred_off[t];
+    for (int base = 0; base < C; base += 32) {
+      const int j = base + lane;
+      bool nd = false;
+      if (j < C && c.bid[j] >= 0) {
+        const int t = t0 + c.bid[j];
+        nd = w.pred_off[t + 1] <= w.pred_off[t];
+        c.need[j] = nd;
       }
-      n_need += __popc(__ballot_sync(0xffffffffu, need));
+      n_need += __popc(__ballot_sync(0xffffffffu, nd));
     }
+    __syncwarp();
     if (n_need > 0) {
-      mt_words_warp(mt, 2 * n_need, sc.words, lane);
-      for (int k = lane; k < n_need; k += 32) sc.draws[k] = mt_res53(sc.words[2 * k], sc.words[2 * k + 1]);
+      load_mt(mt_g, c.mt, lane);
+      mt_loaded = true;
+      mt_words_warp(c.mt, 2 * n_need, c.words, lane);
+      for (int k = lane; k < n_need; k += 32) c.draws[k] = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
       __syncwarp();
     }
   }
-  int need_rank = 0, surv_rank = 0, n_term = 0;
   const double tau = pol.early_term_threshold;
-  for (int base = 0; base < nb; base += 32) {
-    const int b = base + lane;
-    const bool surv = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
-    const unsigned sm = __ballot_sync(0xffffffffu, surv);
-    bool need = false;
-    if (surv && pol.pred_source == DUCHESS_PRED_TRACE) {
-      const int t = t0 + b;
-      need = w.pred_off[t + 1] <= w.pred_off[t];
-    }
-    const unsigned nm = __ballot_sync(0xffffffffu, need);
-    const unsigned lower = (1u << lane) - 1u;
+  int n_term = 0;
+  for (int base = 0; base < C; base += 32) {
+    const int j = base + lane;
+    const int b = j < C ? c.bid[j] : -1;
     bool term = false;
-    if (surv) {
+    if (b >= 0) {
       const int64_t bi = rB + b;
-      const int slot = s.br_slot[bi];
-      const int pos = s.br_offset[bi] + s.br_decoded[bi];
       const int t = t0 + b;
+      const int pos = c.off[j] + c.dec[j];
       double pr;
       if (pol.pred_source == DUCHESS_PRED_TRACE) {
-        if (!need) {
+        if (!c.need[j]) {
           pr = trace_prediction(w, t, pos);
         } else {
-          const double u = sc.draws[need_rank + __popc(nm & lower)];
+          int k = 0;                                     // rank among draw-needing survivors
+          for (int q = 0; q < C; ++q) k += (c.bid[q] >= 0 && c.bid[q] < b && c.need[q]);
+          const double u = c.draws[k];
           // synthetic_predict (predictor.py:328-335) on probe_answer == ground truth
           const double oracle = probe_answer(w, t, pos) == w.ground_truth[p] ? 1.0 : 0.0;
           const double v = __dadd_rn(__dmul_rn(pol.rho, oracle), __dmul_rn(__dsub_rn(1.0, pol.rho), u));
           pr = fmin(fmax(v, 0.0), 1.0);
         }
       } else if (pol.pred_source == DUCHESS_PRED_HOST || pol.n_layers == 1 || pol.combine == 0) {
-        pr = probs[(rC + slot) * pol.n_layers];
+        pr = probs[(rC + j) * pol.n_layers];
       } else {
         double acc = 0.0;
-        for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, probs[(rC + slot) * pol.n_layers + l]);
+        for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, probs[(rC + j) * pol.n_layers + l]);
         pr = __ddiv_rn(acc, double(pol.n_layers));
       }
-      s.step_pred[rC + slot] = pr;
+      const int streak = pr > tau ? c.streak[j] + 1 : 0;   // strict > (:363)
+      c.lp[j] = pr;
+      c.npred[j] += 1;
+      c.streak[j] = streak;
+      s.step_pred[rC + j] = pr;
       s.br_last_pred[bi] = pr;
-      s.br_npred[bi] += 1;
-      const int streak = pr > tau ? s.br_streak[bi] + 1 : 0;   // strict > (:363)
+      s.br_npred[bi] = c.npred[j];
       s.br_streak[bi] = streak;
       // ---- phase 3: early termination (:365-373) ----
       term = streak >= pol.early_term_rounds;
-      const int k = surv_rank + __popc(sm & lower);
+      const int k = c.rank[j];
       act[k * 3 + 0] = term ? DUCHESS_ACT_TERMINATE : DUCHESS_ACT_CONTINUE;
       act[k * 3 + 1] = b;
       act[k * 3 + 2] = -1;
       if (term) {
         const int ans = probe_answer(w, t, pos);
+        c.status[j] = DUCHESS_EARLY_TERMINATED;
         s.br_status[bi] = DUCHESS_EARLY_TERMINATED;
         s.br_final[bi] = ans;
-        atomicAdd(&s.tally[rA + ans], 1);
-        s.slot_branch[rC + slot] = -1;
         s.br_slot[bi] = -1;
+        atomicAdd(&s.tally[rA + ans], 1);
       }
     }
     n_term += __popc(__ballot_sync(0xffffffffu, term));
-    need_rank += __popc(nm);
-    surv_rank += __popc(sm);
   }
-  const int n_surv = surv_rank;
   __syncwarp();
 
   // ---- phase 4: branch-out refill of freed slots (:375-388) ----
-  int n_alive = 0;
-  for (int base = 0; base < nb; base += 32) {
-    const int b = base + lane;
-    const bool alive = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
+  // alive = survivors still ACTIVE, in creation order; free slots ascending.
+  int n_alive = 0, n_free = 0;
+  for (int base = 0; base < C; base += 32) {
+    const int i = base + lane;
+    bool alive = false;
+    int j = -1;
+    if (i < n_surv) {
+      j = c.order[i];
+      alive = c.status[j] == DUCHESS_ACTIVE;
+    }
     const unsigned am = __ballot_sync(0xffffffffu, alive);
     if (alive) {
       const int k = n_alive + __popc(am & ((1u << lane) - 1u));
-      sc.alive[k] = b;
-      sc.root[k] = b;
-      sc.raw[k] = branch_raw(s.br_last_pred[rB + b], pol.inv_temperature);
+      c.alive_slot[k] = j;
+      c.alive_root[k] = c.bid[j];
+      c.raw[k] = branch_raw(c.lp[j], pol.inv_temperature);
     }
     n_alive += __popc(am);
+    const int sj = base + lane;
+    const bool fr = sj < C && (c.bid[sj] < 0 || c.status[sj] != DUCHESS_ACTIVE);
+    const unsigned fm = __ballot_sync(0xffffffffu, fr);
+    if (fr) c.free_slots[n_free + __popc(fm & ((1u << lane) - 1u))] = sj;
+    n_free += __popc(fm);
   }
-  __syncwarp();
-  const int next_t = s.next_template[r];
   const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
+  for (int k = lane; k < n_forks; k += 32) c.nat_child[k] = w.nat_len[t0 + next_t + k];
+  __syncwarp();
   if (n_forks > 0) {
-    mt_words_warp(mt, 2 * n_forks, sc.words, lane);
+    if (!mt_loaded) { load_mt(mt_g, c.mt, lane); mt_loaded = true; }
+    mt_words_warp(c.mt, 2 * n_forks, c.words, lane);
     if (lane == 0) {
       NeumaierSum sum;
-      for (int j = 0; j < n_alive; ++j) sum.add(sc.raw[j]);
-      int n = n_alive;
-      int amb = 0;
+      for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
+      int n = n_alive, amb = 0;
       for (int k = 0; k < n_forks; ++k) {
-        const double u = mt_res53(sc.words[2 * k], sc.words[2 * k + 1]);
+        const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
         bool ambiguous = false;
-        const int idx = sample_index(sc.raw, n, sum.result(), u, &ambiguous);
+        const int idx = sample_index(c.raw, n, sum.result(), u, &ambiguous);
         amb += ambiguous;
-        sc.alive[n] = nb + k;                  // child branch id
-        sc.root[n] = sc.root[idx];
-        sc.raw[n] = sc.raw[idx];               // child inherits last_prediction (:264)
-        sum.add(sc.raw[idx]);
-        // stash source alive-index for the lane-parallel spawn below
-        sc.words[2 * kMaxC + k] = uint32_t(idx);
+        const int src_slot = c.alive_slot[idx];
+        const int child_slot = c.free_slots[k];
+        const int child = nb + k;
+        const int ob = min(c.off[src_slot] + c.dec[src_slot], c.nat_child[k]);   // _spawn (:263)
+        c.bid[child_slot] = child;
+        c.off[child_slot] = ob;
+        c.dec[child_slot] = 0;
+        c.streak[child_slot] = 0;
+        c.status[child_slot] = DUCHESS_ACTIVE;
+        c.npred[child_slot] = 0;
+        c.lp[child_slot] = c.lp[src_slot];           // inherits last_prediction (:264)
+        c.alive_slot[n] = child_slot;
+        c.alive_root[n] = c.alive_root[idx];
+        c.raw[n] = c.raw[idx];
+        c.src_idx[k] = idx;
+        sum.add(c.raw[idx]);
         ++n;
       }
       if (amb) add_counter(&s.counters[DUCHESS_CNT_AMBIGUOUS], (long long)(amb));
-    }
-    __syncwarp();
-    // Free slots in ascending order go to children in fork order. Chains of
-    // forks (a child forked from a child of this round) resolve serially.
-    if (lane == 0) {
-      int free_slot = 0;
-      for (int k = 0; k < n_forks; ++k) {
-        const int idx = int(sc.words[2 * kMaxC + k]);
-        const int src = sc.alive[idx];
-        const int child = nb + k;
-        const int t = t0 + next_t + k;
-        const int64_t ci = rB + child, si = rB + src;
-        const int src_pos = s.br_offset[si] + s.br_decoded[si];
-        const int ob = min(src_pos, w.nat_len[t]);     // _spawn clamp (:263)
-        while (free_slot < C && s.slot_branch[rC + free_slot] >= 0) ++free_slot;
-        s.br_offset[ci] = ob;
-        s.br_decoded[ci] = 0;
-        s.br_streak[ci] = 0;
-        s.br_status[ci] = DUCHESS_ACTIVE;
-        s.br_final[ci] = -1;
-        s.br_npred[ci] = 0;
-        s.br_last_pred[ci] = s.br_last_pred[si];
-        s.br_slot[ci] = free_slot;
-        s.slot_branch[rC + free_slot] = child;
-        const int a = n_surv + k;
-        act[a * 3 + 0] = DUCHESS_ACT_BRANCH_OUT;
-        act[a * 3 + 1] = child;
-        act[a * 3 + 2] = src;
-        int32_t* f = s.forks + (rC + k) * 4;
-        f[0] = child;
-        f[1] = src;
-        f[2] = sc.root[idx];
-        f[3] = ob;
-      }
+      add_counter(&s.counters[DUCHESS_CNT_FORKS], (long long)(n_forks));
       s.n_branches[r] = nb + n_forks;
       s.next_template[r] = next_t + n_forks;
-      add_counter(&s.counters[DUCHESS_CNT_FORKS], (long long)(n_forks));
     }
     __syncwarp();
-    nb += n_forks;
+    for (int k = lane; k < n_forks; k += 32) {
+      const int cs = c.free_slots[k];
+      const int child = nb + k;
+      const int idx = c.src_idx[k];
+      const int src = c.bid[c.alive_slot[idx]];
+      const int64_t ci = rB + child;
+      s.br_offset[ci] = c.off[cs];
+      s.br_decoded[ci] = 0;
+      s.br_streak[ci] = 0;
+      s.br_status[ci] = DUCHESS_ACTIVE;
+      s.br_final[ci] = -1;
+      s.br_npred[ci] = 0;
+      s.br_last_pred[ci] = c.lp[cs];
+      s.br_slot[ci] = cs;
+      const int a = n_surv + k;
+      act[a * 3 + 0] = DUCHESS_ACT_BRANCH_OUT;
+      act[a * 3 + 1] = child;
+      act[a * 3 + 2] = src;
+      int32_t* f = s.forks + (rC + k) * 4;
+      f[0] = child;
+      f[1] = src;
+      f[2] = c.alive_root[n_alive + k];
+      f[3] = c.off[cs];
+    }
   }
+  __syncwarp();
 
   // ---- phase 5: request termination (:390-399) ----
   int max_count = 0, total = 0, best = 0x7fffffff;
   for (int a = lane; a < s.answer_cap; a += 32) {
-    const int c = __ldcg(&s.tally[rA + a]);
-    total += c;
-    if (c > max_count) { max_count = c; best = a; }
+    const int cnt = __ldcg(&s.tally[rA + a]);
+    total += cnt;
+    if (cnt > max_count) { max_count = cnt; best = a; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -499,18 +602,20 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
   if (max_count >= pol.need_consensus) reason = DUCHESS_REASON_CONSENSUS;
   else if (total >= pol.need_coverage) reason = DUCHESS_REASON_COVERAGE;
   bool any_active = false;
-  for (int base = 0; base < nb; base += 32) {
-    const int b = base + lane;
-    const bool a = b < nb && s.br_status[rB + b] == DUCHESS_ACTIVE;
+  for (int base = 0; base < C; base += 32) {
+    const int j = base + lane;
+    bool a = j < C && c.bid[j] >= 0 && c.status[j] == DUCHESS_ACTIVE;
     if (a && reason != DUCHESS_REASON_NONE) {        // _cancel_active (:292-294)
-      s.br_status[rB + b] = DUCHESS_CANCELLED;
-      const int slot = s.br_slot[rB + b];
-      if (slot >= 0) s.slot_branch[rC + slot] = -1;
-      s.br_slot[rB + b] = -1;
+      s.br_status[rB + c.bid[j]] = DUCHESS_CANCELLED;
+      s.br_slot[rB + c.bid[j]] = -1;
+      c.bid[j] = -1;
     }
+    if (j < C && (c.bid[j] < 0 || c.status[j] != DUCHESS_ACTIVE)) c.bid[j] = -1;
+    if (j < C) s.slot_branch[rC + j] = c.bid[j];
     any_active |= __any_sync(0xffffffffu, a);
   }
   if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
+  if (mt_loaded) store_mt(mt_g, c.mt, lane);
   const bool done = reason != DUCHESS_REASON_NONE;
   if (done) {
     for (int a = lane; a < s.answer_cap; a += 32)

@@ -242,6 +242,214 @@ __global__ void __launch_bounds__(256) score_generic_kernel(ScoreArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent warp-specialised variant: one CTA per SM, a producer warp streams
+// each window's token rows into a shared-memory ring with cp.async.bulk
+// (mbarrier transaction counts), 8 consumer warps pool from shared memory and
+// finish the window (two-pass LN stats + dot) while the producer already
+// streams the next one. Keeps up to ~190 KB in flight per SM regardless of
+// register pressure. Windows come from a compacted row list (written by
+// duchess_advance) or from all rows filtered by the mask.
+constexpr int kTmaConsWarps = 8;
+constexpr int kTmaCons = kTmaConsWarps * 32;
+constexpr int kTmaStageTarget = 16 * 1024;
+constexpr int kTmaSmemBudget = 196 * 1024;
+
+struct TmaArgs {
+  const int32_t* row_list;   // nullable
+  const int32_t* row_count;  // device count when row_list != nullptr
+  int tokens_per_stage;
+  int stages;
+  int row_bytes;             // H * esz
+  int contiguous;            // token_stride == H
+};
+
+__device__ __forceinline__ bool tma_unit(const ScoreArgs& a, const TmaArgs& t, int64_t u,
+                                         int64_t& row, int& l) {
+  const int64_t r = u / a.L;
+  l = int(u - r * a.L);
+  if (t.row_list) {
+    row = t.row_list[r];
+    return true;
+  }
+  row = r;
+  return a.mask == nullptr || a.mask[r] != 0;
+}
+
+__device__ __forceinline__ void cons_sum2(float& x, float& y, float2 (*red)[kTmaConsWarps], int& k) {
+  x = warp_sum(x);
+  y = warp_sum(y);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[k & 1][warp] = make_float2(x, y);
+  asm volatile("bar.sync 1, %0;" ::"n"(kTmaCons) : "memory");
+  float sx = 0.f, sy = 0.f;
+#pragma unroll
+  for (int w = 0; w < kTmaConsWarps; ++w) {
+    sx += red[k & 1][w].x;
+    sy += red[k & 1][w].y;
+  }
+  x = sx;
+  y = sy;
+  ++k;
+}
+
+template <bool BF16, int VPT>
+__global__ void __launch_bounds__(kTmaCons + 32, 1) score_tma_kernel(ScoreArgs a, TmaArgs t) {
+  constexpr int VEC = BF16 ? 8 : 4;
+  constexpr int ESZ = BF16 ? 2 : 4;
+  extern __shared__ __align__(128) char ring[];
+  __shared__ uint64_t full_bar[32], empty_bar[32];
+  __shared__ float2 red[2][kTmaConsWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
+  const int stage_bytes = t.tokens_per_stage * t.row_bytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < t.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kTmaConsWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kTmaConsWarps) {   // ---- producer ----
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int64_t row;
+        int l;
+        if (!tma_unit(a, t, u, row, l)) continue;
+        const char* base = a.acts + (row * a.row_stride + int64_t(l) * a.layer_stride) * ESZ;
+        for (int t0 = 0; t0 < a.T; t0 += t.tokens_per_stage) {
+          const int nt = min(t.tokens_per_stage, a.T - t0);
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          mbar_expect_tx(&full_bar[s], uint32_t(nt * t.row_bytes));
+          char* dst = ring + size_t(s) * stage_bytes;
+          if (t.contiguous) {
+            bulk_g2s(dst, base + int64_t(t0) * t.row_bytes, uint32_t(nt * t.row_bytes),
+                     &full_bar[s], pol);
+          } else {
+            for (int k = 0; k < nt; ++k)
+              bulk_g2s(dst + k * t.row_bytes, base + int64_t(t0 + k) * a.token_stride * ESZ,
+                       uint32_t(t.row_bytes), &full_bar[s], pol);
+          }
+          if (++s == t.stages) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int nvec = t.row_bytes / 16;
+  int s = 0, k = 0;
+  uint32_t ph = 0;
+  const float invT = 1.0f / float(a.T);
+  const bool pow2T = (a.T & (a.T - 1)) == 0;
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    int64_t row;
+    int l;
+    if (!tma_unit(a, t, u, row, l)) continue;
+    float acc[VPT][VEC];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[j][v] = 0.f;
+    for (int t0 = 0; t0 < a.T; t0 += t.tokens_per_stage) {
+      const int nt = min(t.tokens_per_stage, a.T - t0);
+      mbar_wait(&full_bar[s], ph);
+      const char* st = ring + size_t(s) * stage_bytes;
+      for (int q = 0; q < nt; ++q) {
+        const uint4* rowv = reinterpret_cast<const uint4*>(st + q * t.row_bytes);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          const int v = j * kTmaCons + int(threadIdx.x);
+          if (v < nvec) {
+            const uint4 x = rowv[v];
+            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+            if constexpr (BF16) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                acc[j][2 * e] += bf16lo(w4[e]);
+                acc[j][2 * e + 1] += bf16hi(w4[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[j][e] += __uint_as_float(w4[e]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      if (++s == t.stages) { s = 0; ph ^= 1u; }
+    }
+    const float* wrow = a.wg + int64_t(l) * a.H;
+    float wgv[VPT][VEC];
+    float s1 = 0.f, sw = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int v = j * kTmaCons + int(threadIdx.x);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const bool ok = v < nvec;
+        acc[j][e] = pow2T ? acc[j][e] * invT : acc[j][e] / float(a.T);
+        wgv[j][e] = ok ? __ldg(wrow + v * VEC + e) : 0.f;
+        if (ok) { s1 += acc[j][e]; sw += wgv[j][e]; }
+      }
+    }
+    cons_sum2(s1, sw, red, k);
+    const float mean = s1 / float(a.H);
+    float qq = 0.f, d = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      if (j * kTmaCons + int(threadIdx.x) < nvec) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const float c = acc[j][e] - mean;
+          qq += c * c;
+          d += wgv[j][e] * c;
+        }
+      }
+    }
+    cons_sum2(qq, d, red, k);
+    if (threadIdx.x == 0) {
+      const float var = qq / float(a.H);
+      write_score(a, row * a.L + l, d / sqrtf(var + kLayerNormEps) + a.c1[l]);
+    }
+  }
+}
+
+template <bool BF16>
+static cudaError_t launch_tma(const ScoreArgs& a, const TmaArgs& t, int vpt, int grid, cudaStream_t s) {
+  const size_t smem = size_t(t.stages) * t.tokens_per_stage * t.row_bytes;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, kTmaCons + 32, smem, s>>>(a, t);
+  };
+  switch (vpt) {
+    case 1: go(score_tma_kernel<BF16, 1>); break;
+    case 2: go(score_tma_kernel<BF16, 2>); break;
+    case 4: go(score_tma_kernel<BF16, 4>); break;
+    case 8: go(score_tma_kernel<BF16, 8>); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 // Synthetic activation windows keyed by (seed, request, template, position).
 template <bool BF16>
 __global__ void __launch_bounds__(256) fill_kernel(char* acts, int64_t row_stride,
@@ -289,12 +497,12 @@ extern "C" size_t duchess_score_workspace_bytes(int64_t n_units, int32_t nsplit_
   return size_t(n_units) * size_t(nsplit_max) * sizeof(float4) + size_t(n_units) * sizeof(unsigned);
 }
 
-extern "C" int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
-                             int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
-                             int64_t token_stride, const float* wg, const float* c1,
-                             const uint8_t* row_mask, float* out_logit, double* out_prob,
-                             void* workspace, size_t workspace_bytes, int32_t nsplit,
-                             int32_t threads, void* stream) {
+static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                      int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                      int64_t token_stride, const float* wg, const float* c1,
+                      const uint8_t* row_mask, const int32_t* row_list, const int32_t* row_count,
+                      float* out_logit, double* out_prob, void* workspace, size_t workspace_bytes,
+                      int32_t nsplit, int32_t threads, void* stream) {
   if (n_rows < 0 || n_layers < 1 || T < 1 || H < 1) return DUCHESS_EINVAL;
   if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
   if (!acts || !wg || !c1 || !out_logit || !out_prob) return DUCHESS_EINVAL;
@@ -336,6 +544,33 @@ extern "C" int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, in
     return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
   }
 
+  const int64_t row_bytes = int64_t(H) * esz;
+  const bool tma_ok = row_bytes <= kTmaStageTarget * 4 && (row_bytes % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(acts) % 16 == 0);
+  if (row_list && !(tma_ok && nsplit == 0 && threads == 0)) return DUCHESS_EINVAL;
+  if (nsplit == 0 && threads == 0 && tma_ok) {
+    TmaArgs t{};
+    t.row_list = row_list;
+    t.row_count = row_count;
+    t.row_bytes = int(row_bytes);
+    t.contiguous = token_stride == H;
+    t.tokens_per_stage = int(row_bytes >= kTmaStageTarget ? 1 : kTmaStageTarget / row_bytes);
+    if (t.tokens_per_stage > T) t.tokens_per_stage = T;
+    const int stage_bytes = t.tokens_per_stage * t.row_bytes;
+    t.stages = kTmaSmemBudget / stage_bytes;
+    if (t.stages > 32) t.stages = 32;
+    if (t.stages < 2) return DUCHESS_EINVAL;
+    const int nvec = int(row_bytes / 16);
+    int vpt = 1;
+    while (vpt * kTmaCons < nvec) vpt <<= 1;
+    if (vpt > 8) return DUCHESS_EINVAL;
+    a.nsplit = 1;
+    a.chunk = H;
+    int grid = sm_count();
+    if (int64_t(grid) > a.n_units) grid = int(a.n_units);
+    const cudaError_t e = bf16 ? launch_tma<true>(a, t, vpt, grid, s) : launch_tma<false>(a, t, vpt, grid, s);
+    return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  }
   int nt = threads > 0 ? threads : 256;
   if (nt != 128 && nt != 256 && nt != 512) return DUCHESS_EINVAL;
   const int cols_per_pass = nt * vec;
@@ -366,6 +601,29 @@ extern "C" int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, in
                   : launch_fast<false, 512>(a, passes, s);
   }
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_score(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                             int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                             int64_t token_stride, const float* wg, const float* c1,
+                             const uint8_t* row_mask, float* out_logit, double* out_prob,
+                             void* workspace, size_t workspace_bytes, int32_t nsplit,
+                             int32_t threads, void* stream) {
+  return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
+                    wg, c1, row_mask, nullptr, nullptr, out_logit, out_prob, workspace,
+                    workspace_bytes, nsplit, threads, stream);
+}
+
+extern "C" int duchess_score_list(const void* acts, int32_t dtype, int64_t n_rows,
+                                  int32_t n_layers, int32_t T, int32_t H, int64_t row_stride,
+                                  int64_t layer_stride, int64_t token_stride, const float* wg,
+                                  const float* c1, const int32_t* row_list,
+                                  const int32_t* row_count, float* out_logit, double* out_prob,
+                                  void* stream) {
+  if (!row_list || !row_count) return DUCHESS_EINVAL;
+  return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
+                    wg, c1, nullptr, row_list, row_count, out_logit, out_prob, nullptr, 0, 0, 0,
+                    stream);
 }
 
 extern "C" int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,

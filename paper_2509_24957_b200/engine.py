@@ -194,6 +194,8 @@ class BatchedDuchess:
         t["forks"] = torch.zeros(R * C * 4, **i32)
         t["step_pred"] = torch.zeros(R * C, dtype=torch.float64, device=dev)
         t["queue_head"] = torch.zeros(2, **i32)
+        t["active_rows"] = torch.zeros(R * C, **i32)
+        t["active_count"] = torch.zeros(1, **i32)
         P = max(self.P, 1)
         for name in ("out_final", "out_reason", "out_tokens_decode", "out_tokens_probe",
                      "out_rounds", "out_error"):

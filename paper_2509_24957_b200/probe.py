@@ -100,6 +100,24 @@ class Scorer:
             "duchess_score")
 
 
+    def score_list(self, acts: torch.Tensor, out_logit: torch.Tensor, out_prob: torch.Tensor,
+                   row_list: torch.Tensor, row_count: torch.Tensor, stream=None) -> None:
+        """Score only the rows in the device list row_list[:row_count[0]]
+        (DuchessState.active_rows from duchess_advance); persistent TMA kernel."""
+        _lib.require_cuda(acts)
+        rows, L, T, H = acts.shape
+        if L != self.bank.L or H != self.bank.H:
+            raise ValueError(f"activation shape (L={L}, H={H}) does not match probe bank "
+                             f"(L={self.bank.L}, H={self.bank.H})")
+        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}[acts.dtype]
+        st = acts.stride()
+        _lib.check(self.lib.duchess_score_list(
+            acts.data_ptr(), dtype, rows, L, T, H, st[0], st[1], st[2],
+            self.bank.wg.data_ptr(), self.bank.c1.data_ptr(), row_list.data_ptr(),
+            row_count.data_ptr(), out_logit.data_ptr(), out_prob.data_ptr(),
+            _lib.stream_handle(stream)), "duchess_score_list")
+
+
 def fill_windows(acts: torch.Tensor, seed: int, row_req=None, row_tmpl=None, row_pos=None,
                  row_mask=None, stream=None) -> None:
     """Write counter-hashed synthetic activations (oracle/activations.py
