@@ -159,6 +159,21 @@ __device__ int sample_index(const double* raw, int n, double total, double u, bo
   return pick;
 }
 
+// Sequential CDF walk over precomputed weights (orchestrator.py:192-197).
+__device__ __forceinline__ int cdf_pick(const double* w, int n, double u, bool* ambiguous) {
+  double acc = 0.0, prev = 0.0;
+  int pick = n - 1;
+  for (int j = 0; j < n; ++j) {
+    prev = acc;
+    acc = __dadd_rn(acc, w[j]);
+    if (u < acc) { pick = j; break; }
+  }
+  const double tol = 4.0 * 2.220446049250313e-16;
+  *ambiguous = fabs(u - acc) <= tol * fmax(acc, 1e-300) ||
+               (pick > 0 && fabs(u - prev) <= tol * fmax(prev, 1e-300));
+  return pick;
+}
+
 // ---------------------------------------------------------------------------
 // Per-warp shared-memory cache of one request slot. Active branches are exactly
 // the occupied branch slots (a slot is released whenever its branch leaves
@@ -179,6 +194,7 @@ struct SlotCache {
   int alive_root[kMaxC];
   int src_idx[kMaxC];
   double raw[kMaxC];
+  double wts[kMaxC];
   double draws[kMaxC];
   uint32_t words[2 * kMaxC];
   uint32_t mt[kMtN + 1];
@@ -236,13 +252,39 @@ __device__ __forceinline__ int order_slots(SlotCache& c, int C, int lane) {
   return n;
 }
 
-__device__ __forceinline__ void load_mt(const uint32_t* g, uint32_t* sm, int lane) {
-  for (int j = lane; j <= kMtN; j += 32) sm[j] = g[j];
+constexpr int kMtPerLane = (kMtN + 1 + 31) / 32;   // 20
+
+// Batched copy of the 625-word state: all loads issued before any store.
+__device__ __forceinline__ void copy_mt(const uint32_t* src, uint32_t* dst, int lane) {
+  uint32_t v[kMtPerLane];
+#pragma unroll
+  for (int q = 0; q < kMtPerLane; ++q) {
+    const int j = q * 32 + lane;
+    v[q] = j <= kMtN ? src[j] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < kMtPerLane; ++q) {
+    const int j = q * 32 + lane;
+    if (j <= kMtN) dst[j] = v[q];
+  }
   __syncwarp();
 }
-__device__ __forceinline__ void store_mt(uint32_t* g, const uint32_t* sm, int lane) {
-  __syncwarp();
-  for (int j = lane; j <= kMtN; j += 32) g[j] = sm[j];
+
+// n tempered words from a global-memory stream. Common case (no twist due):
+// read just mt[idx, idx+n) and bump the index. Otherwise stage the state in
+// shared memory, run the warp-parallel twist there, and write it back.
+__device__ void mt_words_global(uint32_t* mt_g, uint32_t* mt_s, int n, uint32_t* out, int lane) {
+  const int idx = int(mt_g[kMtN]);
+  if (idx + n <= kMtN) {
+    for (int k = lane; k < n; k += 32) out[k] = mt_temper(mt_g[idx + k]);
+    __syncwarp();
+    if (lane == 0) mt_g[kMtN] = uint32_t(idx + n);
+    __syncwarp();
+    return;
+  }
+  copy_mt(mt_g, mt_s, lane);
+  mt_words_warp(mt_s, n, out, lane);
+  copy_mt(mt_s, mt_g, lane);
 }
 
 // Refill slot r with pool request p: RequestRun.__init__ (:242-248).
@@ -266,9 +308,7 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
   }
   for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
-  const uint32_t* src = w.mt_init + int64_t(p) * DUCHESS_MT_WORDS;
-  uint32_t* dst = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
-  for (int j = lane; j < DUCHESS_MT_WORDS; j += 32) dst[j] = src[j];
+  copy_mt(w.mt_init + int64_t(p) * DUCHESS_MT_WORDS, s.mt + int64_t(r) * DUCHESS_MT_WORDS, lane);
   if (lane == 0) {
     s.slot_req[r] = p;
     s.n_branches[r] = seeded;
@@ -412,7 +452,6 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
   int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
   load_slot(s, rC, rB, C, c, lane);
   const int n_surv = order_slots(c, C, lane);
-  bool mt_loaded = false;
 
   // ---- phase 2: predictions, creation order (:357-363) ----
   int n_need = 0;
@@ -429,9 +468,7 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
     }
     __syncwarp();
     if (n_need > 0) {
-      load_mt(mt_g, c.mt, lane);
-      mt_loaded = true;
-      mt_words_warp(c.mt, 2 * n_need, c.words, lane);
+      mt_words_global(mt_g, c.mt, 2 * n_need, c.words, lane);
       for (int k = lane; k < n_need; k += 32) c.draws[k] = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
       __syncwarp();
     }
@@ -522,22 +559,26 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
   for (int k = lane; k < n_forks; k += 32) c.nat_child[k] = w.nat_len[t0 + next_t + k];
   __syncwarp();
   if (n_forks > 0) {
-    if (!mt_loaded) { load_mt(mt_g, c.mt, lane); mt_loaded = true; }
-    mt_words_warp(c.mt, 2 * n_forks, c.words, lane);
-    if (lane == 0) {
-      NeumaierSum sum;
-      for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
-      int n = n_alive, amb = 0;
-      for (int k = 0; k < n_forks; ++k) {
+    mt_words_global(mt_g, c.mt, 2 * n_forks, c.words, lane);
+    // Every lane replays the same compensated sum; the n quotients raw/total are
+    // computed lane-parallel and lane 0 runs the sequential CDF walk.
+    NeumaierSum sum;
+    for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
+    int n = n_alive, amb = 0;
+    for (int k = 0; k < n_forks; ++k) {
+      const double total = sum.result();
+      for (int q = lane; q < n; q += 32) c.wts[q] = __ddiv_rn(c.raw[q], total);
+      __syncwarp();
+      int idx = 0;
+      if (lane == 0) {
         const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
         bool ambiguous = false;
-        const int idx = sample_index(c.raw, n, sum.result(), u, &ambiguous);
+        idx = cdf_pick(c.wts, n, u, &ambiguous);
         amb += ambiguous;
         const int src_slot = c.alive_slot[idx];
         const int child_slot = c.free_slots[k];
-        const int child = nb + k;
         const int ob = min(c.off[src_slot] + c.dec[src_slot], c.nat_child[k]);   // _spawn (:263)
-        c.bid[child_slot] = child;
+        c.bid[child_slot] = nb + k;
         c.off[child_slot] = ob;
         c.dec[child_slot] = 0;
         c.streak[child_slot] = 0;
@@ -548,9 +589,13 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
         c.alive_root[n] = c.alive_root[idx];
         c.raw[n] = c.raw[idx];
         c.src_idx[k] = idx;
-        sum.add(c.raw[idx]);
-        ++n;
       }
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      __syncwarp();
+      sum.add(c.raw[idx]);
+      ++n;
+    }
+    if (lane == 0) {
       if (amb) add_counter(&s.counters[DUCHESS_CNT_AMBIGUOUS], (long long)(amb));
       add_counter(&s.counters[DUCHESS_CNT_FORKS], (long long)(n_forks));
       s.n_branches[r] = nb + n_forks;
@@ -615,7 +660,6 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
     any_active |= __any_sync(0xffffffffu, a);
   }
   if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
-  if (mt_loaded) store_mt(mt_g, c.mt, lane);
   const bool done = reason != DUCHESS_REASON_NONE;
   if (done) {
     for (int a = lane; a < s.answer_cap; a += 32)

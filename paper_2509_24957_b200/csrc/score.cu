@@ -16,6 +16,8 @@
 // window is split over several CTAs, merges (count, mean, M2, dot) partials
 // with Chan's formula in fixed chunk order in the last-arriving CTA, so the
 // result is deterministic run to run.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
 
@@ -294,7 +296,7 @@ __device__ __forceinline__ void cons_sum2(float& x, float& y, float2 (*red)[kTma
 }
 
 template <bool BF16, int VPT>
-__global__ void __launch_bounds__(kTmaCons + 32, 1) score_tma_kernel(ScoreArgs a, TmaArgs t) {
+__global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, TmaArgs t) {
   constexpr int VEC = BF16 ? 8 : 4;
   constexpr int ESZ = BF16 ? 2 : 4;
   extern __shared__ __align__(128) char ring[];
@@ -554,10 +556,13 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     t.row_count = row_count;
     t.row_bytes = int(row_bytes);
     t.contiguous = token_stride == H;
-    t.tokens_per_stage = int(row_bytes >= kTmaStageTarget ? 1 : kTmaStageTarget / row_bytes);
+    // Tunables (env, for sweeps): CTAs per SM and stage size target.
+    static const int cps = [] { const char* e = getenv("DUCHESS_K1_CPS"); int v = e ? atoi(e) : 1; return v < 1 ? 1 : (v > 4 ? 4 : v); }();
+    static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kTmaStageTarget; return v < 4096 ? 4096 : v; }();
+    t.tokens_per_stage = int(row_bytes >= stage_target ? 1 : stage_target / row_bytes);
     if (t.tokens_per_stage > T) t.tokens_per_stage = T;
     const int stage_bytes = t.tokens_per_stage * t.row_bytes;
-    t.stages = kTmaSmemBudget / stage_bytes;
+    t.stages = (kTmaSmemBudget / cps) / stage_bytes;
     if (t.stages > 32) t.stages = 32;
     if (t.stages < 2) return DUCHESS_EINVAL;
     const int nvec = int(row_bytes / 16);
@@ -566,8 +571,8 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     if (vpt > 8) return DUCHESS_EINVAL;
     a.nsplit = 1;
     a.chunk = H;
-    int grid = sm_count();
-    if (int64_t(grid) > a.n_units) grid = int(a.n_units);
+    int grid = sm_count() * cps;
+    if (!row_list && int64_t(grid) > a.n_units) grid = int(a.n_units);
     const cudaError_t e = bf16 ? launch_tma<true>(a, t, vpt, grid, s) : launch_tma<false>(a, t, vpt, grid, s);
     return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
   }
