@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) score_generic_kernel(ScoreArgs a) {
 // duchess_advance) or from all rows filtered by the mask.
 constexpr int kTmaConsWarps = 8;
 constexpr int kTmaCons = kTmaConsWarps * 32;
-constexpr int kTmaStageTarget = 16 * 1024;
+constexpr int kTmaStageTarget = 8 * 1024;
 constexpr int kTmaSmemBudget = 196 * 1024;
 
 struct TmaArgs {
@@ -557,7 +557,7 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     t.row_bytes = int(row_bytes);
     t.contiguous = token_stride == H;
     // Tunables (env, for sweeps): CTAs per SM and stage size target.
-    static const int cps = [] { const char* e = getenv("DUCHESS_K1_CPS"); int v = e ? atoi(e) : 1; return v < 1 ? 1 : (v > 4 ? 4 : v); }();
+    static const int cps = [] { const char* e = getenv("DUCHESS_K1_CPS"); int v = e ? atoi(e) : 2; return v < 1 ? 1 : (v > 4 ? 4 : v); }();
     static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kTmaStageTarget; return v < 4096 ? 4096 : v; }();
     t.tokens_per_stage = int(row_bytes >= stage_target ? 1 : stage_target / row_bytes);
     if (t.tokens_per_stage > T) t.tokens_per_stage = T;
