@@ -183,7 +183,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     k1_ev = []
 
     def one_step(i, timed):
-        eng.advance()
+        # round k: K1 scores the survivors flagged by the previous launch, then
+        # duchess_round decides round k and advances every slot into round k+1
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -195,8 +196,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if timed:
             e1.record(stream)
             k1_ev.append((e0, e1))
-        eng.decide()
+        eng.round()
 
+    eng.advance()                      # round 0: refill every slot + phase 1
     for i in range(args.warmup):
         one_step(i, False)
     torch.cuda.synchronize(dev)
@@ -260,7 +262,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                      "k1_share_of_step": k1_ms / ms,
                      "traffic": None},
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 2 * args.steps,
         "clocks": clk,
         "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
                      "finished_requests": int(cnt[_lib.CNT_FINISHED]),

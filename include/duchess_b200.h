@@ -159,7 +159,8 @@ typedef struct DuchessState {
   int32_t* row_tmpl;
   int64_t* row_req;
   /* latest round */
-  int32_t* round_rec;  /* [R*DUCHESS_REC_WORDS] */
+  int32_t* p1_rec;     /* [R*8] phase-1 record of the round in flight (internal) */
+  int32_t* round_rec;  /* [R*DUCHESS_REC_WORDS] latest completed round */
   int32_t* actions;    /* [R*2C*3] (kind, branch_id, source_branch_id or -1) */
   int32_t* forks;      /* [R*C*4]  (child, source, table_root, prefix_tokens) */
   double* step_pred;   /* [R*C] prediction used for each survivor, by slot */
@@ -203,6 +204,13 @@ int duchess_advance(const DuchessPolicy* policy, const DuchessWorkload* workload
                     const DuchessState* state, void* stream);
 int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
                    const DuchessState* state, const double* probs, void* stream);
+
+/* Fused round boundary: duchess_decide for the round in flight, then
+ * duchess_advance for the next one, in one cooperative launch (grid-wide
+ * barrier between the halves keeps refill order deterministic). Equivalent to
+ * calling decide then advance; round_rec holds the round just decided. */
+int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                  const DuchessState* state, const double* probs, void* stream);
 
 /* Rule primitives (orchestrator.py:177-197, :200-208; core.py:76-83). */
 int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,

@@ -63,7 +63,7 @@ STATE_PTR_FIELDS = [
     "br_offset", "br_decoded", "br_streak", "br_status", "br_final", "br_npred", "br_slot",
     "br_last_pred",
     "slot_branch", "row_mask", "row_pos", "row_tmpl", "row_req",
-    "round_rec", "actions", "forks", "step_pred", "queue_head", "active_rows", "active_count",
+    "p1_rec", "round_rec", "actions", "forks", "step_pred", "queue_head", "active_rows", "active_count",
     "out_final", "out_reason", "out_tokens_decode", "out_tokens_probe", "out_rounds",
     "out_error", "out_tally", "counters",
 ]
@@ -94,6 +94,8 @@ SYMBOLS = {
                                   C.c_void_p]),
     "duchess_decide": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                  C.c_void_p, C.c_void_p]),
+    "duchess_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
+                                C.c_void_p, C.c_void_p]),
     "duchess_branch_out_sample": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
                                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p]),

@@ -15,8 +15,12 @@
 // otherwise be contracted; random draws replay CPython's MT19937
 // genrand_res53; the branch-out normaliser replays CPython >= 3.12's
 // compensated (Neumaier) builtin sum().
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
+
+namespace cg = cooperative_groups;
 
 namespace duchess {
 
@@ -321,46 +325,51 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (r >= s.n_slots) return;
-  SlotCache& c = cache[threadIdx.x >> 5];
+// Phase-1 record of the round in flight: round, decoding, max_chunk,
+// decode_tokens, probes, pool request (round 0 = no round started).
+constexpr int kP1Words = 8;
+
+// Refill-or-load prologue of a round (RequestRun.__init__ on refill).
+// Returns the pool request in slot r, or -1 if the slot stays idle.
+__device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
+                             const DuchessState& s, int r, SlotCache& c, int lane,
+                             bool cache_valid) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
-  int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
-  for (int j = lane; j < C; j += 32) s.row_mask[rC + j] = 0;
-  if (lane < DUCHESS_REC_WORDS) rec[lane] = 0;
-
-  // ---- refill: the k-th slot needing one (slot order) takes queue[head + k] ----
+  // the k-th slot needing a refill (slot order) takes queue[head + k]
   const int head = s.queue_head[0];
   if (r == 0) {
     const int total = warp_count_flags(s.needs_refill, s.n_slots, lane);
     const int avail = w.cycle ? total : max(0, min(total, w.queue_len - head));
     if (lane == 0) s.queue_head[1] = head + avail;
   }
-  int p;
   if (s.needs_refill[r]) {
     const int q = head + warp_count_flags(s.needs_refill, r, lane);
-    p = -1;
+    int p = -1;
     if (w.queue_len > 0) {
       if (w.cycle) p = w.queue[q % w.queue_len];
       else if (q < w.queue_len) p = w.queue[q];
     }
     if (p < 0) {
       if (lane == 0) { s.slot_req[r] = -1; s.done[r] = 1; }
-      return;
+      __syncwarp();
+      return -1;
     }
     refill_slot(pol, w, s, r, p, c, lane);
-  } else {
-    if (s.done[r]) return;
-    p = s.slot_req[r];
-    if (p < 0) return;
-    load_slot(s, rC, rB, C, c, lane);
+    return p;
   }
+  if (s.done[r]) return -1;
+  const int p = s.slot_req[r];
+  if (p < 0) return -1;
+  if (!cache_valid) load_slot(s, rC, rB, C, c, lane);
+  return p;
+}
 
+__device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
+                            const DuchessState& s, int r, int p, SlotCache& c, int lane) {
+  const int C = pol.max_branches;
+  const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
+  int32_t* p1 = s.p1_rec + int64_t(r) * kP1Words;
   // ---- phase 1: decode one interval per active branch (:344-355) ----
   const int t0 = w.tmpl_off[p];
   int decoding = 0, max_chunk = 0, dtok = 0, probes = 0;
@@ -417,33 +426,36 @@ advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
     s.rounds[r] = rounds;
     s.tokens_decode[r] += dtok;
     s.tokens_probe[r] += probes * pol.probe_cost_tokens;
-    rec[DUCHESS_REC_ROUND] = rounds;
-    rec[DUCHESS_REC_DECODING] = decoding;
-    rec[DUCHESS_REC_MAX_CHUNK] = max_chunk;
-    rec[DUCHESS_REC_DECODE] = dtok;
-    rec[DUCHESS_REC_PROBES] = probes;
-    rec[DUCHESS_REC_REQ] = p;
+    p1[0] = rounds;
+    p1[1] = decoding;
+    p1[2] = max_chunk;
+    p1[3] = dtok;
+    p1[4] = probes;
+    p1[5] = p;
   }
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  const int wi = threadIdx.x >> 5;
-  const int r = blockIdx.x * kWarpsPerBlock + wi;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    s.queue_head[0] = s.queue_head[1];
-    if (s.active_count) *s.active_count = 0;     // consumed by the scorer this round
-  }
-  if (r >= s.n_slots) return;
-  SlotCache& c = cache[wi];
+__device__ void clear_round_inputs(const DuchessPolicy& pol, const DuchessState& s, int r, int lane) {
+  const int C = pol.max_branches;
+  for (int j = lane; j < C; j += 32) s.row_mask[int64_t(r) * C + j] = 0;
+  if (lane < kP1Words) s.p1_rec[int64_t(r) * kP1Words + lane] = 0;
+  __syncwarp();
+}
+
+// Phases 2-5 for slot r whose phase-1 record is live (cache not yet loaded
+// unless cache_loaded). Completes round_rec.
+__device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
+                            const DuchessState& s, int r, SlotCache& c, int lane,
+                            const double* probs) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   const int64_t rA = int64_t(r) * s.answer_cap;
   int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
-  if (rec[DUCHESS_REC_ROUND] == 0) return;   // slot idle or finished
-  const int p = s.slot_req[r];
+  const int32_t* p1 = s.p1_rec + int64_t(r) * kP1Words;
+  if (lane < DUCHESS_REC_WORDS)
+    rec[lane] = lane < DUCHESS_REC_NACTIONS ? p1[lane] : (lane == DUCHESS_REC_REQ ? p1[5] : 0);
+  __syncwarp();
+  const int p = p1[5];
   const int t0 = w.tmpl_off[p];
   const int n_tmpl = w.tmpl_off[p + 1] - t0;
   const int nb = s.n_branches[r];
@@ -667,7 +679,7 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
   }
   if (lane == 0) {
     s.tokens_probe[r] += n_term * pol.probe_cost_tokens;
-    rec[DUCHESS_REC_PROBES] += n_term;
+    rec[DUCHESS_REC_PROBES] = p1[4] + n_term;
     rec[DUCHESS_REC_NACTIONS] = n_surv + n_forks;
     rec[DUCHESS_REC_NFORKS] = n_forks;
     rec[DUCHESS_REC_NSURV] = n_surv;
@@ -690,6 +702,64 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
     } else {
       s.needs_refill[r] = 0;
     }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= s.n_slots) return;
+  SlotCache& c = cache[threadIdx.x >> 5];
+  clear_round_inputs(pol, s, r, lane);
+  const int p = slot_prologue(pol, w, s, r, c, lane, false);
+  if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane);
+}
+
+__device__ __forceinline__ void decide_prologue(const DuchessState& s) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.queue_head[0] = s.queue_head[1];
+    if (s.active_count) *s.active_count = 0;     // consumed by the scorer this round
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  decide_prologue(s);
+  if (r >= s.n_slots) return;
+  if (s.p1_rec[int64_t(r) * kP1Words] == 0) {     // slot idle or finished: no round
+    if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
+    return;
+  }
+  decide_slot(pol, w, s, r, cache[threadIdx.x >> 5], lane, probs);
+}
+
+// Fused round boundary: decide round k for every slot, grid-wide barrier (so
+// refill ranks see every slot's completion), then refill + phase 1 of round
+// k+1 reusing the shared-memory slot cache. Launched cooperatively.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  SlotCache& c = cache[threadIdx.x >> 5];
+  decide_prologue(s);
+  bool had_round = false;
+  if (r < s.n_slots) {
+    had_round = s.p1_rec[int64_t(r) * kP1Words] != 0;
+    if (had_round) decide_slot(pol, w, s, r, c, lane, probs);
+    else if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  if (r < s.n_slots) {
+    clear_round_inputs(pol, s, r, lane);
+    const int p = slot_prologue(pol, w, s, r, c, lane, had_round);
+    if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane);
   }
 }
 
@@ -830,6 +900,22 @@ extern "C" int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload
   decide_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
       *policy, *workload, *state, probs);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                             const DuchessState* state, const double* probs, void* stream) {
+  if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
+  if (policy->pred_source != DUCHESS_PRED_TRACE && probs == nullptr) return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  DuchessPolicy pol = *policy;
+  DuchessWorkload w = *workload;
+  DuchessState st = *state;
+  void* args[] = {&pol, &w, &st, &probs};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(round_kernel), dim3(grid),
+                                                    dim3(32 * kWarpsPerBlock), args, 0,
+                                                    static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
 extern "C" int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,

@@ -189,6 +189,7 @@ class BatchedDuchess:
         t["row_pos"] = torch.zeros(R * C, **i32)
         t["row_tmpl"] = torch.zeros(R * C, **i32)
         t["row_req"] = torch.zeros(R * C, dtype=torch.int64, device=dev)
+        t["p1_rec"] = torch.zeros(R * 8, **i32)
         t["round_rec"] = torch.zeros(R * _lib.REC_WORDS, **i32)
         t["actions"] = torch.zeros(R * 2 * C * 3, **i32)
         t["forks"] = torch.zeros(R * C * 4, **i32)
@@ -224,6 +225,15 @@ class BatchedDuchess:
         _lib.check(self.lib.duchess_decide(self.policy, self.wl.struct, self.state,
                                            p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_decide")
+
+    def round(self, probs: torch.Tensor | None = None, stream=None) -> None:
+        """Fused decide(k) + advance(k+1) (duchess_round, one cooperative
+        launch). After it, round_reports() describe round k and the row mask /
+        active list describe the survivors of round k+1."""
+        p = probs if probs is not None else self.probs
+        _lib.check(self.lib.duchess_round(self.policy, self.wl.struct, self.state,
+                                          p.data_ptr(), _lib.stream_handle(stream)),
+                   "duchess_round")
 
     def step(self, score_fn=None, stream=None) -> None:
         """One round for every occupied slot. score_fn(engine) must fill

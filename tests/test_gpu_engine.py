@@ -69,6 +69,32 @@ def test_engine_matches_reference_golden(case, slots, reverse):
         assert branches[p] == want, f"request {p} branch states"
 
 
+@pytest.mark.parametrize("case", load("decisions.json"), ids=lambda c: c["name"])
+def test_fused_round_kernel_matches_reference_golden(case):
+    """duchess_round (decide k + advance k+1 in one cooperative launch) must
+    give the same RoundReports and outcomes as the split kernels."""
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    traces = case_traces(case)
+    seeds = [int(r["seed"]) for r in case["requests"]]
+    eng = BatchedDuchess(traces, case_knobs(case), seeds, n_slots=min(7, len(traces)),
+                         pred_source=_lib.PRED_TRACE, rho=case["rho"])
+    eng.advance()
+    reports = {}
+    for _ in range(100000):
+        eng.round()
+        for p, rep in eng.round_reports():
+            reports.setdefault(p, []).append(rep)
+        if eng.all_done():
+            break
+    outcomes = eng.outcomes()
+    for p, ref in enumerate(case["requests"]):
+        assert reports[p] == [report_tuple(r) for r in ref["reports"]], f"request {p}"
+        assert outcomes[p]["final"] == ref["outcome"]["final"]
+        assert outcomes[p]["tally"] == ref["outcome"]["tally"]
+        assert outcomes[p]["tokens_decode"] == ref["outcome"]["tokens_decode"]
+
+
 def _c1_setup(n_req=24, templates=64, c=8, temperature=1.0):
     knobs = port.Knobs(max_branches=c, interval_tokens=16, early_term_threshold=0.70,
                        early_term_rounds=2, branch_out_temperature=temperature,
