@@ -176,6 +176,7 @@ typedef struct DuchessState {
   int32_t* out_error;
   int32_t* out_tally;  /* [P*A] */
   long long* counters; /* [DUCHESS_N_COUNTERS] */
+  long long* trace;    /* [R*8] optional per-slot decide phase timestamps (ns), or NULL */
 } DuchessState;
 
 /* ---- K1: pooled LayerNorm + linear-probe scoring ------------------------ */

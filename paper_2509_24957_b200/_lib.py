@@ -65,7 +65,7 @@ STATE_PTR_FIELDS = [
     "slot_branch", "row_mask", "row_pos", "row_tmpl", "row_req",
     "p1_rec", "round_rec", "actions", "forks", "step_pred", "queue_head", "active_rows", "active_count",
     "out_final", "out_reason", "out_tokens_decode", "out_tokens_probe", "out_rounds",
-    "out_error", "out_tally", "counters",
+    "out_error", "out_tally", "counters", "trace",
 ]
 
 

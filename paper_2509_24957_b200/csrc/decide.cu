@@ -325,6 +325,15 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   __syncwarp();
 }
 
+// Optional per-slot phase timestamps (DuchessState.trace, 8 x int64 per slot).
+__device__ __forceinline__ void trace_mark(const DuchessState& s, int r, int k, int lane) {
+  if (s.trace && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    s.trace[int64_t(r) * 8 + k] = (long long)t;
+  }
+}
+
 // Phase-1 record of the round in flight: round, decoding, max_chunk,
 // decode_tokens, probes, pool request (round 0 = no round started).
 constexpr int kP1Words = 8;
@@ -462,8 +471,10 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const int next_t = s.next_template[r];
   uint32_t* mt_g = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
   int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
+  trace_mark(s, r, 0, lane);
   load_slot(s, rC, rB, C, c, lane);
   const int n_surv = order_slots(c, C, lane);
+  trace_mark(s, r, 1, lane);
 
   // ---- phase 2: predictions, creation order (:357-363) ----
   int n_need = 0;
@@ -542,6 +553,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   __syncwarp();
 
+  trace_mark(s, r, 2, lane);
   // ---- phase 4: branch-out refill of freed slots (:375-388) ----
   // alive = survivors still ACTIVE, in creation order; free slots ascending.
   int n_alive = 0, n_free = 0;
@@ -570,6 +582,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
   for (int k = lane; k < n_forks; k += 32) c.nat_child[k] = w.nat_len[t0 + next_t + k];
   __syncwarp();
+  trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
     mt_words_global(mt_g, c.mt, 2 * n_forks, c.words, lane);
     // Every lane replays the same compensated sum; the n quotients raw/total are
@@ -641,6 +654,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   __syncwarp();
 
+  trace_mark(s, r, 4, lane);
   // ---- phase 5: request termination (:390-399) ----
   int max_count = 0, total = 0, best = 0x7fffffff;
   for (int a = lane; a < s.answer_cap; a += 32) {
@@ -673,6 +687,8 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
   const bool done = reason != DUCHESS_REASON_NONE;
+  trace_mark(s, r, 5, lane);
+  if (s.trace && lane == 0) { s.trace[int64_t(r) * 8 + 6] = n_forks; s.trace[int64_t(r) * 8 + 7] = n_term; }
   if (done) {
     for (int a = lane; a < s.answer_cap; a += 32)
       s.out_tally[int64_t(p) * s.answer_cap + a] = __ldcg(&s.tally[rA + a]);

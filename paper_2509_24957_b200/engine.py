@@ -207,12 +207,19 @@ class BatchedDuchess:
         st = _lib.State()
         st.n_slots, st.branch_cap, st.answer_cap = R, B, A
         for name in _lib.STATE_PTR_FIELDS:
-            setattr(st, name, t[name].data_ptr())
+            if name in t:
+                setattr(st, name, t[name].data_ptr())
         self.state = st
         self.probs = torch.zeros(R * C * max(self.policy.n_layers, 1), dtype=torch.float64,
                                  device=dev)
 
     # ------------------------------------------------------------------
+    def enable_trace(self) -> torch.Tensor:
+        """Per-slot decide phase timestamps (globaltimer ns) for profiling."""
+        self.t["trace"] = torch.zeros(self.R * 8, dtype=torch.int64, device=self.device)
+        self.state.trace = self.t["trace"].data_ptr()
+        return self.t["trace"]
+
     def advance(self, stream=None) -> None:
         """Refill finished slots, then phase 1 (orchestrator.py:344-355)."""
         _lib.check(self.lib.duchess_advance(self.policy, self.wl.struct, self.state,
