@@ -61,6 +61,11 @@ extern "C" {
 #define DUCHESS_PRED_TRACE 1  /* make_correctness_predictor: pred_probs else synthetic */
 #define DUCHESS_PRED_HOST 2   /* caller-supplied probabilities by slot (predictor= callable) */
 
+/* Policy flags. EXACT_CDF: always walk the branch-out CDF sequentially (the
+ * default decides from a warp prefix sum unless u is within the rounding
+ * margin of a boundary; both give identical picks — the flag exists to test that). */
+#define DUCHESS_FLAG_EXACT_CDF 1
+
 #define DUCHESS_MT_WORDS 625 /* 624 MT19937 words + index, as random.Random.getstate() */
 #define DUCHESS_MAX_SLOTS 64 /* max_branches limit of the warp-per-request kernel */
 #define DUCHESS_REC_WORDS 12
@@ -98,6 +103,8 @@ typedef struct DuchessPolicy {
   int32_t pred_source;       /* DUCHESS_PRED_* */
   int32_t n_layers;          /* probability columns per slot in `probs` */
   int32_t combine;           /* 0 = layer 0, 1 = mean over layers */
+  int32_t flags;             /* DUCHESS_FLAG_* */
+  int32_t _pad;
   double early_term_threshold; /* tau, :68; +inf disables (:58-59) */
   double inv_temperature;      /* 1.0 / branch_out_temperature, computed by the host (:182) */
   double rho;                  /* SyntheticPredictorConfig.rho, predictor.py:321 */

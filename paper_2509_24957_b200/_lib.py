@@ -20,6 +20,7 @@ ACTIVE, EARLY_TERMINATED, NATURAL_END, CAPPED, CANCELLED = range(5)
 REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
 PRED_DEVICE, PRED_TRACE, PRED_HOST = 0, 1, 2
+FLAG_EXACT_CDF = 1
 MT_WORDS = 625
 MAX_SLOTS = 64
 REC_WORDS = 12
@@ -40,6 +41,7 @@ class Policy(C.Structure):
         ("probe_cost_tokens", C.c_int32), ("need_consensus", C.c_int32),
         ("need_coverage", C.c_int32), ("pred_source", C.c_int32),
         ("n_layers", C.c_int32), ("combine", C.c_int32),
+        ("flags", C.c_int32), ("_pad", C.c_int32),
         ("early_term_threshold", C.c_double), ("inv_temperature", C.c_double),
         ("rho", C.c_double),
     ]

@@ -117,6 +117,42 @@ __device__ __forceinline__ int probe_answer(const DuchessWorkload& w, int t, int
   return 0;
 }
 
+// Same lookup with independent loads per level: conv / CSR bounds / final in
+// one round trip, then an 8-ary search over probe_at (8 loads per level).
+// Invariant: probe_at[i] <= pos for i in [L, lo), probe_at[i] > pos for i in [hi, H).
+__device__ __forceinline__ int probe_answer_fast(const DuchessWorkload& w, int t, int pos) {
+  const int conv = w.conv[t];
+  const int L = w.probe_off[t];
+  const int H = w.probe_off[t + 1];
+  const int fin = w.final_ans[t];
+  if (conv >= 0 && pos >= conv) return fin;
+  int lo = L, hi = H;
+  while (hi - lo > 8) {
+    const int span = hi - lo;
+    int idx[8], at[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) idx[q] = lo + (span * (q + 1)) / 9;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) at[q] = w.probe_at[idx[q]];
+    int nlo = lo, nhi = hi;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (at[q] <= pos) nlo = idx[q] + 1;
+      else nhi = min(nhi, idx[q]);
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+  int at8[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) at8[q] = (lo + q < hi) ? w.probe_at[lo + q] : 0x7fffffff;
+  int k = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) k += at8[q] <= pos;
+  const int ans = lo + k - 1;
+  return ans >= L ? w.probe_ans[ans] : 0;
+}
+
 // trace_prediction (workload.py:97-106).
 __device__ __forceinline__ double trace_prediction(const DuchessWorkload& w, int t, int pos) {
   const int lo = w.pred_off[t], hi = w.pred_off[t + 1];
@@ -277,18 +313,29 @@ __device__ __forceinline__ void copy_mt(const uint32_t* src, uint32_t* dst, int 
 // n tempered words from a global-memory stream. Common case (no twist due):
 // read just mt[idx, idx+n) and bump the index. Otherwise stage the state in
 // shared memory, run the warp-parallel twist there, and write it back.
-__device__ void mt_words_global(uint32_t* mt_g, uint32_t* mt_s, int n, uint32_t* out, int lane) {
-  const int idx = int(mt_g[kMtN]);
+__device__ int mt_words_global(uint32_t* mt_g, uint32_t* mt_s, int idx, int n, uint32_t* out,
+                                int lane) {
   if (idx + n <= kMtN) {
     for (int k = lane; k < n; k += 32) out[k] = mt_temper(mt_g[idx + k]);
     __syncwarp();
     if (lane == 0) mt_g[kMtN] = uint32_t(idx + n);
     __syncwarp();
-    return;
+    return idx + n;
   }
   copy_mt(mt_g, mt_s, lane);
   mt_words_warp(mt_s, n, out, lane);
+  const int nidx = int(mt_s[kMtN]);
   copy_mt(mt_s, mt_g, lane);
+  return nidx;
+}
+
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
 }
 
 // Refill slot r with pool request p: RequestRun.__init__ (:242-248).
@@ -399,7 +446,7 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       s.br_decoded[bi] = c.dec[j];
       int ans = -1, status = DUCHESS_ACTIVE;
       if (pos >= nat) { ans = w.final_ans[t]; status = DUCHESS_NATURAL_END; }
-      else if (pos >= pol.token_cap) { ans = probe_answer(w, t, pos); status = DUCHESS_CAPPED; probes++; }
+      else if (pos >= pol.token_cap) { ans = probe_answer_fast(w, t, pos); status = DUCHESS_CAPPED; probes++; }
       if (status != DUCHESS_ACTIVE) {                 // _collect (:287-290), slot released
         s.br_status[bi] = status;
         s.br_final[bi] = ans;
@@ -472,6 +519,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   uint32_t* mt_g = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
   int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
   trace_mark(s, r, 0, lane);
+  int mt_idx = int(mt_g[kMtN]);                       // prefetched: stream position
+  for (int k = lane; k < C && next_t + k < n_tmpl; k += 32)
+    c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
   load_slot(s, rC, rB, C, c, lane);
   const int n_surv = order_slots(c, C, lane);
   trace_mark(s, r, 1, lane);
@@ -491,7 +541,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
     __syncwarp();
     if (n_need > 0) {
-      mt_words_global(mt_g, c.mt, 2 * n_need, c.words, lane);
+      mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_need, c.words, lane);
       for (int k = lane; k < n_need; k += 32) c.draws[k] = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
       __syncwarp();
     }
@@ -515,7 +565,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
           for (int q = 0; q < C; ++q) k += (c.bid[q] >= 0 && c.bid[q] < b && c.need[q]);
           const double u = c.draws[k];
           // synthetic_predict (predictor.py:328-335) on probe_answer == ground truth
-          const double oracle = probe_answer(w, t, pos) == w.ground_truth[p] ? 1.0 : 0.0;
+          const double oracle = probe_answer_fast(w, t, pos) == w.ground_truth[p] ? 1.0 : 0.0;
           const double v = __dadd_rn(__dmul_rn(pol.rho, oracle), __dmul_rn(__dsub_rn(1.0, pol.rho), u));
           pr = fmin(fmax(v, 0.0), 1.0);
         }
@@ -541,7 +591,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       act[k * 3 + 1] = b;
       act[k * 3 + 2] = -1;
       if (term) {
-        const int ans = probe_answer(w, t, pos);
+        const int ans = probe_answer_fast(w, t, pos);
         c.status[j] = DUCHESS_EARLY_TERMINATED;
         s.br_status[bi] = DUCHESS_EARLY_TERMINATED;
         s.br_final[bi] = ans;
@@ -580,26 +630,46 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     n_free += __popc(fm);
   }
   const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
-  for (int k = lane; k < n_forks; k += 32) c.nat_child[k] = w.nat_len[t0 + next_t + k];
   __syncwarp();
   trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
-    mt_words_global(mt_g, c.mt, 2 * n_forks, c.words, lane);
-    // Every lane replays the same compensated sum; the n quotients raw/total are
-    // computed lane-parallel and lane 0 runs the sequential CDF walk.
+    mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
+    // Every lane replays the same compensated sum (CPython sum(), :184).
     NeumaierSum sum;
     for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
     int n = n_alive, amb = 0;
     for (int k = 0; k < n_forks; ++k) {
       const double total = sum.result();
-      for (int q = lane; q < n; q += 32) c.wts[q] = __ddiv_rn(c.raw[q], total);
-      __syncwarp();
-      int idx = 0;
+      // Exact quotients (lane-parallel), then a tree-order warp prefix sum. The
+      // reference's sequential running sum differs from it by at most
+      // (n + 7) ulp of ~1, so unless u lies within that margin of a prefix the
+      // pick is decided here; otherwise lane 0 replays the exact sequential walk.
+      const double w0 = lane < n ? __ddiv_rn(c.raw[lane], total) : 0.0;
+      const double w1 = lane + 32 < n ? __ddiv_rn(c.raw[lane + 32], total) : 0.0;
+      const double p0 = warp_incl_scan(w0, lane);
+      const double p1 = warp_incl_scan(w1, lane) + __shfl_sync(0xffffffffu, p0, 31);
+      const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
+      const double margin = 2.0 * double(n + 8) * 1.1102230246251565e-16;
+      const bool near = (lane < n && fabs(u - p0) <= margin) ||
+                        (lane + 32 < n && fabs(u - p1) <= margin);
+      int idx;
+      if (!(pol.flags & DUCHESS_FLAG_EXACT_CDF) && !__any_sync(0xffffffffu, near)) {
+        const unsigned b0 = __ballot_sync(0xffffffffu, lane < n && u < p0);
+        const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < n && u < p1);
+        idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
+      } else {
+        if (lane < n) c.wts[lane] = w0;
+        if (lane + 32 < n) c.wts[lane + 32] = w1;
+        __syncwarp();
+        idx = 0;
+        if (lane == 0) {
+          bool ambiguous = false;
+          idx = cdf_pick(c.wts, n, u, &ambiguous);
+          amb += ambiguous;
+        }
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+      }
       if (lane == 0) {
-        const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
-        bool ambiguous = false;
-        idx = cdf_pick(c.wts, n, u, &ambiguous);
-        amb += ambiguous;
         const int src_slot = c.alive_slot[idx];
         const int child_slot = c.free_slots[k];
         const int ob = min(c.off[src_slot] + c.dec[src_slot], c.nat_child[k]);   // _spawn (:263)
@@ -830,7 +900,7 @@ __global__ void lookup_kernel(DuchessWorkload w, const int32_t* tmpl, const int3
                               int32_t* out_ans, double* out_pred) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (out_ans) out_ans[i] = probe_answer(w, tmpl[i], pos[i]);
+  if (out_ans) out_ans[i] = probe_answer_fast(w, tmpl[i], pos[i]);
   if (out_pred) out_pred[i] = trace_prediction(w, tmpl[i], pos[i]);
 }
 

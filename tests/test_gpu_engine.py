@@ -70,7 +70,8 @@ def test_engine_matches_reference_golden(case, slots, reverse):
 
 
 @pytest.mark.parametrize("case", load("decisions.json"), ids=lambda c: c["name"])
-def test_fused_round_kernel_matches_reference_golden(case):
+@pytest.mark.parametrize("exact_cdf", [False, True])
+def test_fused_round_kernel_matches_reference_golden(case, exact_cdf):
     """duchess_round (decide k + advance k+1 in one cooperative launch) must
     give the same RoundReports and outcomes as the split kernels."""
     from paper_2509_24957_b200 import _lib
@@ -79,6 +80,8 @@ def test_fused_round_kernel_matches_reference_golden(case):
     seeds = [int(r["seed"]) for r in case["requests"]]
     eng = BatchedDuchess(traces, case_knobs(case), seeds, n_slots=min(7, len(traces)),
                          pred_source=_lib.PRED_TRACE, rho=case["rho"])
+    if exact_cdf:
+        eng.policy.flags |= _lib.FLAG_EXACT_CDF
     eng.advance()
     reports = {}
     for _ in range(100000):
@@ -181,3 +184,41 @@ def test_scores_to_decisions_composition(dtype, T, temperature):
         o = req.outcome
         assert outcomes[p]["final"] == o.final and outcomes[p]["reason"] == o.termination_reason
         assert outcomes[p]["tally"] == o.tally
+
+
+def test_probe_lookup_long_probe_lists():
+    """8-ary probe_answer search vs the oracle's bisect on templates with up to
+    600 probes, convergence points, and positions on/around every boundary."""
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import pack_workload
+    rng = random.Random(12)
+    traces, queries = [], []
+    for i in range(40):
+        n_probes = rng.choice([0, 1, 2, 7, 8, 9, 17, 64, 65, 200, 600])
+        ats = sorted(rng.sample(range(1, 5000), n_probes))
+        length = (ats[-1] if ats else 10) + rng.randint(0, 50)
+        conv = rng.choice([None, rng.randint(0, length)])
+        probes = [(a, str(rng.randint(0, 30))) for a in ats]
+        if conv is not None:
+            probes = [(a, "f" if a >= conv else x) for a, x in probes]
+        t = port.Tmpl(length, "f", probes, conv)
+        traces.append(port.Trace(f"q{i}", "f", 0, [t]))
+        pts = {0, length, length + 3}
+        for a in ats[:50] + ats[-50:]:
+            pts.update({a - 1, a, a + 1})
+        queries.append(sorted(p for p in pts if p >= 0))
+    wl = pack_workload(traces, [[0] * _lib.MT_WORDS] * len(traces), list(range(len(traces))),
+                       False, torch.device("cuda"))
+    tm, ps, want = [], [], []
+    for i, (tr, qs) in enumerate(zip(traces, queries)):
+        for q in qs:
+            tm.append(i)
+            ps.append(q)
+            want.append(wl.answers[i].index(port.probe_answer(tr.templates[0], q)))
+    lib = _lib.load()
+    t_ = torch.tensor(tm, dtype=torch.int32, device="cuda")
+    p_ = torch.tensor(ps, dtype=torch.int32, device="cuda")
+    out = torch.empty(len(tm), dtype=torch.int32, device="cuda")
+    _lib.check(lib.duchess_template_lookup(wl.struct, t_.data_ptr(), p_.data_ptr(), len(tm),
+                                           out.data_ptr(), None, _lib.stream_handle()), "lookup")
+    assert out.cpu().tolist() == want
