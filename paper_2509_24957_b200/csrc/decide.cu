@@ -605,7 +605,8 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
 
   trace_mark(s, r, 2, lane);
   // ---- phase 4: branch-out refill of freed slots (:375-388) ----
-  // alive = survivors still ACTIVE, in creation order; free slots ascending.
+  // alive = survivors still ACTIVE in creation order; entry j is held in
+  // registers by lane j % 32 (set j / 32, C <= 64). Free slots ascending.
   int n_alive = 0, n_free = 0;
   for (int base = 0; base < C; base += 32) {
     const int i = base + lane;
@@ -616,12 +617,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       alive = c.status[j] == DUCHESS_ACTIVE;
     }
     const unsigned am = __ballot_sync(0xffffffffu, alive);
-    if (alive) {
-      const int k = n_alive + __popc(am & ((1u << lane) - 1u));
-      c.alive_slot[k] = j;
-      c.alive_root[k] = c.bid[j];
-      c.raw[k] = branch_raw(c.lp[j], pol.inv_temperature);
-    }
+    if (alive) c.alive_slot[n_alive + __popc(am & ((1u << lane) - 1u))] = j;
     n_alive += __popc(am);
     const int sj = base + lane;
     const bool fr = sj < C && (c.bid[sj] < 0 || c.status[sj] != DUCHESS_ACTIVE);
@@ -629,37 +625,51 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     if (fr) c.free_slots[n_free + __popc(fm & ((1u << lane) - 1u))] = sj;
     n_free += __popc(fm);
   }
+  __syncwarp();
+  int sl0 = -1, sl1 = -1, rt0 = -1, rt1 = -1, ps0 = 0, ps1 = 0;
+  double lp0 = 0.0, lp1 = 0.0, rw0 = 0.0, rw1 = 0.0;
+  if (lane < n_alive) {
+    sl0 = c.alive_slot[lane]; rt0 = c.bid[sl0]; ps0 = c.off[sl0] + c.dec[sl0]; lp0 = c.lp[sl0];
+    rw0 = branch_raw(lp0, pol.inv_temperature);
+    c.raw[lane] = rw0;
+  }
+  if (lane + 32 < n_alive) {
+    sl1 = c.alive_slot[lane + 32]; rt1 = c.bid[sl1]; ps1 = c.off[sl1] + c.dec[sl1]; lp1 = c.lp[sl1];
+    rw1 = branch_raw(lp1, pol.inv_temperature);
+    c.raw[lane + 32] = rw1;
+  }
   const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
   __syncwarp();
   trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
     mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
-    // Every lane replays the same compensated sum (CPython sum(), :184).
+    // The reference's normaliser is CPython's compensated sum() (:184); every
+    // lane replays it over the raws in creation order.
     NeumaierSum sum;
     for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
+    // Tree-order prefix sums of the raws, extended by one entry per fork.
+    double P0 = warp_incl_scan(rw0, lane);
+    double P1 = warp_incl_scan(rw1, lane) + __shfl_sync(0xffffffffu, P0, 31);
     int n = n_alive, amb = 0;
     for (int k = 0; k < n_forks; ++k) {
       const double total = sum.result();
-      // Exact quotients (lane-parallel), then a tree-order warp prefix sum. The
-      // reference's sequential running sum differs from it by at most
-      // (n + 7) ulp of ~1, so unless u lies within that margin of a prefix the
-      // pick is decided here; otherwise lane 0 replays the exact sequential walk.
-      const double w0 = lane < n ? __ddiv_rn(c.raw[lane], total) : 0.0;
-      const double w1 = lane + 32 < n ? __ddiv_rn(c.raw[lane + 32], total) : 0.0;
-      const double p0 = warp_incl_scan(w0, lane);
-      const double p1 = warp_incl_scan(w1, lane) + __shfl_sync(0xffffffffu, p0, 31);
       const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
-      const double margin = 2.0 * double(n + 8) * 1.1102230246251565e-16;
-      const bool near = (lane < n && fabs(u - p0) <= margin) ||
-                        (lane + 32 < n && fabs(u - p1) <= margin);
+      // The reference picks the first j with u < acc_j, acc_j the sequential
+      // sum of fl(raw_i / total). acc_j and P_j / total differ by less than
+      // (2n + 9) ulp, so away from that margin the decision is read off the
+      // prefixes; otherwise lane 0 replays the exact sequential walk.
+      const double thr = __dmul_rn(u, total);
+      const double margin = 4.0 * double(n + 9) * 1.1102230246251565e-16 * total;
+      const bool v0 = lane < n, v1 = lane + 32 < n;
+      const bool near = (v0 && fabs(thr - P0) <= margin) || (v1 && fabs(thr - P1) <= margin);
       int idx;
       if (!(pol.flags & DUCHESS_FLAG_EXACT_CDF) && !__any_sync(0xffffffffu, near)) {
-        const unsigned b0 = __ballot_sync(0xffffffffu, lane < n && u < p0);
-        const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < n && u < p1);
+        const unsigned b0 = __ballot_sync(0xffffffffu, v0 && thr < P0);
+        const unsigned b1 = __ballot_sync(0xffffffffu, v1 && thr < P1);
         idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
       } else {
-        if (lane < n) c.wts[lane] = w0;
-        if (lane + 32 < n) c.wts[lane + 32] = w1;
+        if (v0) c.wts[lane] = __ddiv_rn(rw0, total);
+        if (v1) c.wts[lane + 32] = __ddiv_rn(rw1, total);
         __syncwarp();
         idx = 0;
         if (lane == 0) {
@@ -669,25 +679,33 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         }
         idx = __shfl_sync(0xffffffffu, idx, 0);
       }
+      // source of the fork, broadcast from the lane holding entry idx
+      const int own = idx & 31;
+      const bool hi = idx >= 32;
+      const int src_slot = __shfl_sync(0xffffffffu, hi ? sl1 : sl0, own);
+      const int src_root = __shfl_sync(0xffffffffu, hi ? rt1 : rt0, own);
+      const int src_pos = __shfl_sync(0xffffffffu, hi ? ps1 : ps0, own);
+      const double src_lp = __shfl_sync(0xffffffffu, hi ? lp1 : lp0, own);
+      const double src_raw = __shfl_sync(0xffffffffu, hi ? rw1 : rw0, own);
+      const double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
+      const int child_slot = c.free_slots[k];
+      const int ob = min(src_pos, c.nat_child[k]);          // _spawn clamp (:263)
+      if (lane == (n & 31)) {                               // append child as entry n
+        if (n < 32) { sl0 = child_slot; rt0 = src_root; ps0 = ob; lp0 = src_lp; rw0 = src_raw; P0 = p_last + src_raw; }
+        else        { sl1 = child_slot; rt1 = src_root; ps1 = ob; lp1 = src_lp; rw1 = src_raw; P1 = p_last + src_raw; }
+      }
       if (lane == 0) {
-        const int src_slot = c.alive_slot[idx];
-        const int child_slot = c.free_slots[k];
-        const int ob = min(c.off[src_slot] + c.dec[src_slot], c.nat_child[k]);   // _spawn (:263)
         c.bid[child_slot] = nb + k;
         c.off[child_slot] = ob;
         c.dec[child_slot] = 0;
         c.streak[child_slot] = 0;
         c.status[child_slot] = DUCHESS_ACTIVE;
         c.npred[child_slot] = 0;
-        c.lp[child_slot] = c.lp[src_slot];           // inherits last_prediction (:264)
-        c.alive_slot[n] = child_slot;
-        c.alive_root[n] = c.alive_root[idx];
-        c.raw[n] = c.raw[idx];
-        c.src_idx[k] = idx;
+        c.lp[child_slot] = src_lp;                         // inherits last_prediction (:264)
+        c.src_idx[k] = src_slot;
+        c.alive_root[k] = src_root;
       }
-      idx = __shfl_sync(0xffffffffu, idx, 0);
-      __syncwarp();
-      sum.add(c.raw[idx]);
+      sum.add(src_raw);
       ++n;
     }
     if (lane == 0) {
@@ -700,8 +718,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     for (int k = lane; k < n_forks; k += 32) {
       const int cs = c.free_slots[k];
       const int child = nb + k;
-      const int idx = c.src_idx[k];
-      const int src = c.bid[c.alive_slot[idx]];
+      const int src = c.bid[c.src_idx[k]];
       const int64_t ci = rB + child;
       s.br_offset[ci] = c.off[cs];
       s.br_decoded[ci] = 0;
@@ -718,7 +735,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       int32_t* f = s.forks + (rC + k) * 4;
       f[0] = child;
       f[1] = src;
-      f[2] = c.alive_root[n_alive + k];
+      f[2] = c.alive_root[k];
       f[3] = c.off[cs];
     }
   }
