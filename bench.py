@@ -318,6 +318,163 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world):
 
 
 # ---------------------------------------------------------------------------
+# C4: branch-out-heavy copy-on-write trace; C5: probe-training step
+
+def make_fork_trace(R, roots, forks_per_req, bt, max_blocks, seed):
+    """Synthetic C4 trace: `roots` live branches per request at positions
+    U[16, 2048]; forks sampled like branch_out_sample (p^(1/0.8) weights over
+    the alive set incl. children created earlier, chains resolved to roots)."""
+    rng = np.random.default_rng(seed)
+    pos = rng.integers(16, 2049, size=(R, roots))
+    probs = rng.random((R, roots + forks_per_req))
+    forks = np.zeros((R, forks_per_req, 4), dtype=np.int32)
+    for r in range(R):
+        alive_pos = list(pos[r])
+        alive_root = list(range(roots))
+        for k in range(forks_per_req):
+            n = len(alive_pos)
+            wts = np.maximum(probs[r, :n], 1e-6) ** 1.25
+            src = int(rng.choice(n, p=wts / wts.sum()))
+            forks[r, k] = (roots + k, src, alive_root[src], alive_pos[src])
+            alive_pos.append(alive_pos[src])
+            alive_root.append(alive_root[src])
+    return pos, forks
+
+
+def run_fork_bench(args, rank, world, local_rank):
+    import torch
+    from paper_2509_24957_b200.kvfork import BlockTable
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R, roots, nf, bt, max_blocks, kvb = 512, 16, 48, 16, 256, 4096
+    pos, forks = make_fork_trace(R, roots, nf, bt, max_blocks, seed=31 + rank)
+    rows_per = roots + nf
+    nblk_root = -(-pos // bt)
+    n_root_blocks = int(nblk_root.sum())
+    n_tail = int(((forks[:, :, 3] % bt) != 0).sum())
+    n_blocks = n_root_blocks + n_tail
+    table = np.full((R * rows_per, max_blocks), -1, dtype=np.int32)
+    nxt = 0
+    for r in range(R):
+        for b in range(roots):
+            table[r * rows_per + b, :nblk_root[r, b]] = np.arange(nxt, nxt + nblk_root[r, b])
+            nxt += nblk_root[r, b]
+    t = BlockTable(R * rows_per, max_blocks, n_blocks, bt, kvb, device=dev)
+    t.table.copy_(torch.from_numpy(table))
+    t.refcount[:n_root_blocks] = 1
+    t.free_list = torch.arange(n_root_blocks, n_blocks, dtype=torch.int32, device=dev)
+    fk = torch.from_numpy(forks).to(dev)
+    n_full = forks[:, :, 3] // bt
+    tail = forks[:, :, 3] % bt
+    bytes_per_step = int((n_full * 4 * 3).sum() + R * nf * (max_blocks * 4 + 16)
+                         + (2 * tail * kvb).sum())
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        t.cursor.zero_()
+        t.fork(fk, None, 1, rows_per)
+    torch.cuda.synchronize(dev)
+    evs = []
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_all0.record(stream)
+    for _ in range(args.steps):
+        t.cursor.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        t.fork(fk, None, 1, rows_per)
+        b.record(stream)
+        evs.append((a, b))
+    e_all1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    k3_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    step_ms = e_all0.elapsed_time(e_all1) / args.steps
+    peak, kind = load_peaks()
+    achieved = bytes_per_step / (k3_ms / 1e3) / 1e9
+    return {"metric": "copy-on-write forks/s (C4 branch-out-heavy trace)",
+            "value": R * nf * world / (step_ms / 1e3), "unit": "forks/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32+u8",
+            "data": "synthetic fork trace", "config": {
+                "workload": f"C4: {R} requests x {roots} root branches at U[16,2048] tokens, "
+                            f"{nf} forks/request (24576), 16-token blocks, {kvb} B/token KV",
+                "n_blocks": n_blocks},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": kind,
+                         "kernel": "duchess_fork_cow (plan + exec)",
+                         "bytes_per_launch": bytes_per_step, "k3_us_per_launch": k3_ms * 1e3,
+                         "traffic": None},
+            "gpu_launches": 2 * args.steps, "clocks": clk}
+
+
+def run_train_bench(args, rank, world, local_rank):
+    import torch
+    from paper_2509_24957_b200.probe import fill_windows
+    from paper_2509_24957_b200.train import LogisticProbeTrainer
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    H = 8192
+    n_total = 4194304
+    n_local = n_total // 8          # the per-GPU shard of the 8-GPU configuration
+    X = torch.empty((n_local, 1, 1, H), dtype=torch.bfloat16, device=dev)
+    fill_windows(X, 5000 + rank)
+    X = X.view(n_local, H)
+    g = torch.Generator(device=dev).manual_seed(5)
+    w_true = torch.randn(H, generator=g, device=dev) / np.sqrt(H)
+    y = torch.empty(n_local, device=dev)
+    for lo in range(0, n_local, 65536):
+        z = X[lo:lo + 65536].float() @ w_true
+        y[lo:lo + 65536] = (torch.rand(z.shape[0], generator=g, device=dev)
+                            < torch.sigmoid(z)).float()
+    tr = LogisticProbeTrainer(H, device=dev, lr=0.5)
+    n_global = n_local * world
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        tr.step(X, y, n_global)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    evs = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tr.local_grad(X, y, 1.0 / n_global)
+        b.record(stream)
+        evs.append((a, b))
+        from paper_2509_24957_b200.distributed import allreduce_sum
+        allreduce_sum(tr.grad)
+        tr.lib.duchess_sgd_update(tr.w.data_ptr(), tr.grad.data_ptr(), H + 1, 0.5,
+                                  stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    st = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
+    ms = float(st[0])
+    k4_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    peak, kind = load_peaks()
+    bytes_launch = n_local * (H * 2 + 4)
+    achieved = bytes_launch / (k4_ms / 1e3) / 1e9
+    return {"metric": "probe-training rows/s (C5 logistic regression, full-batch step)",
+            "value": n_local * world / (ms / 1e3), "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) activations, labels ~ Bernoulli(sigmoid(X w*))",
+            "config": {"workload": f"C5: {n_local} rows x {H} per GPU (8 GiB, the 8-GPU shard "
+                                   f"of 4M rows), grad + NCCL all-reduce (8193 f32) + SGD"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": kind,
+                         "kernel": "duchess_lr_grad (K4)", "bytes_per_launch": bytes_launch,
+                         "k4_us_per_launch": k4_ms * 1e3, "traffic": None},
+            "gpu_launches": 3 * args.steps, "clocks": clk}
+
+
+# ---------------------------------------------------------------------------
 # CPU reference (oracle port) — only here and in tests may oracle/ run.
 
 _CPU = {}
@@ -392,7 +549,66 @@ def cpu_baseline_entry(cfg_name, budget_total=12.0):
                       f"(c={cfg['c']}), {procs} processes x {steps} x {budget_total/steps:.1f} s"}
 
 
+def cpu_fork_or_train(args):
+    """CPU references for C4 (serial CoW restatement) and C5 (numpy fp32 BLAS
+    gradient on all threads), each step a bounded sample."""
+    from oracle import extensions as ext
+    procs = os.cpu_count() or 1
+    if args.config == "c4":
+        R, roots, nf, bt, kvb = 24, 16, 48, 16, 4096
+        pos, forks = make_fork_trace(R, roots, nf, bt, 256, seed=31)
+        rows_per = roots + nf
+        nblk = -(-pos // bt)
+        table = np.full((R * rows_per, 256), -1, dtype=np.int32)
+        nxt = 0
+        for r in range(R):
+            for b in range(roots):
+                table[r * rows_per + b, :nblk[r, b]] = np.arange(nxt, nxt + nblk[r, b])
+                nxt += nblk[r, b]
+        n_blocks = nxt + R * nf
+        ref = np.ones(n_blocks, dtype=np.int32)
+        free = np.arange(nxt, n_blocks, dtype=np.int32)
+        kv = np.zeros(n_blocks * bt * kvb, dtype=np.uint8)
+        times = []
+        for _ in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            ext.cow_fork_ref(forks, None, table, ref, free, 0, kv, kvb, bt, rows_per)
+            times.append(time.perf_counter() - t0)
+        dt = sum(times[args.warmup:])
+        val, unit, sample = R * nf * args.steps / dt, "forks/s", \
+            f"oracle/extensions.cow_fork_ref over {R} requests x {nf} forks, 1 core"
+        cores = 1
+    else:
+        H, n = 8192, 65536
+        rng = np.random.default_rng(0)
+        X = rng.standard_normal((n, H), dtype=np.float32)
+        y = (rng.random(n) < 0.5).astype(np.float32)
+        w = (rng.standard_normal(H + 1) / 90).astype(np.float32)
+        times = []
+        for _ in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            z = X @ w[:-1] + w[-1]
+            r = 1.0 / (1.0 + np.exp(-z)) - y
+            _g = np.concatenate([X.T @ r, [r.sum()]]) / n
+            times.append(time.perf_counter() - t0)
+        dt = sum(times[args.warmup:])
+        val, unit, sample = n * args.steps / dt, "rows/s", \
+            f"numpy fp32 BLAS gradient on {n} x {H} rows, all threads"
+        cores = procs
+    return {"impl": "reference", "metric": f"{args.config} CPU reference", "value": val,
+            "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32" if args.config == "c4" else "f32",
+            "data": "synthetic", "config": {"workload": args.config.upper() + " (CPU)"},
+            "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
 def run_reference(args, cfg):
+    if cfg is None:
+        return cpu_fork_or_train(args)
     procs = os.cpu_count() or 1
     total = args.steps + args.warmup
     budget = max(0.5, min(5.0, 120.0 / max(total, 1)))
@@ -430,7 +646,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
@@ -439,7 +655,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS.get(args.config)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -451,9 +667,14 @@ def main():
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl")
-    out = run_gpu(args, cfg, rank, world, local_rank)
+    if args.config == "c4":
+        out = run_fork_bench(args, rank, world, local_rank)
+    elif args.config == "c5":
+        out = run_train_bench(args, rank, world, local_rank)
+    else:
+        out = run_gpu(args, cfg, rank, world, local_rank)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and cfg is not None:
             out["cpu_baseline"] = cpu_baseline_entry(args.config)
         print(json.dumps(out), flush=True)
     if world > 1:

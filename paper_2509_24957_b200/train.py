@@ -51,17 +51,4 @@ class LogisticProbeTrainer:
         return g
 
 
-def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
-    """Sum a per-rank partial gradient across the data-parallel group (NCCL on
-    GPUs, gloo on CPU tensors); a no-op without an initialised process group."""
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t
-
-
-def shard_rows(n_rows: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous row range [lo, hi) of this rank (the last ranks get one less)."""
-    base, extra = divmod(n_rows, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+from .distributed import allreduce_sum, shard_range as shard_rows  # noqa: E402,F401
