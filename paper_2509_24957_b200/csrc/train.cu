@@ -21,7 +21,7 @@ namespace duchess {
 constexpr int kConsWarps = 8;
 constexpr int kCons = kConsWarps * 32;
 constexpr int kStageBytesTarget = 32 * 1024;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 100 * 1024;   // per CTA; 2 CTAs per SM
 constexpr int kMaxRB = 8;
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -45,7 +45,7 @@ struct GradArgs {
 };
 
 template <bool BF16, int VPT>
-__global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
+__global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
   constexpr int EPV = BF16 ? 8 : 4;   // elements per 16-byte vector
   extern __shared__ __align__(128) char smem[];
   __shared__ uint64_t full_bar[16], empty_bar[16];
@@ -107,11 +107,14 @@ __global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
     const uint32_t ph = uint32_t((it / a.stages) & 1);
     const int64_t r = row0 + it * a.rb;
     const int nr = int(lmin(a.rb, row1 - r));
+    float yv[kMaxRB];                       // labels prefetched before the stage wait
+#pragma unroll
+    for (int q = 0; q < kMaxRB; ++q) yv[q] = q < nr ? __ldg(a.y + r + q) : 0.f;
     mbar_wait(&full_bar[s], ph);
     const char* base = smem + size_t(s) * stage_bytes;
-    float dots[kMaxRB];
+    float dots[kMaxRB], dots2[kMaxRB];
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) dots[q] = 0.f;
+    for (int q = 0; q < kMaxRB; ++q) { dots[q] = 0.f; dots2[q] = 0.f; }
 #pragma unroll
     for (int q = 0; q < kMaxRB; ++q) {
       if (q < nr) {
@@ -124,11 +127,16 @@ __global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
             const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
             if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                dots[q] += wv[j][2 * e] * bf16lo(xw[e]) + wv[j][2 * e + 1] * bf16hi(xw[e]);
+              for (int e = 0; e < 4; ++e) {
+                dots[q] = fmaf(wv[j][2 * e], bf16lo(xw[e]), dots[q]);
+                dots2[q] = fmaf(wv[j][2 * e + 1], bf16hi(xw[e]), dots2[q]);
+              }
             } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) dots[q] += wv[j][e] * __uint_as_float(xw[e]);
+              for (int e = 0; e < 4; e += 2) {
+                dots[q] = fmaf(wv[j][e], __uint_as_float(xw[e]), dots[q]);
+                dots2[q] = fmaf(wv[j][e + 1], __uint_as_float(xw[e + 1]), dots2[q]);
+              }
             }
           }
         }
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
 #pragma unroll
     for (int q = 0; q < kMaxRB; ++q) {
       if (q < nr) {
-        const float d = warp_sum(dots[q]);
+        const float d = warp_sum(dots[q] + dots2[q]);
         if (lane == 0) red[buf][warp][q] = d;
       }
     }
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(kCons + 32, 1) lr_grad_kernel(GradArgs a) {
 #pragma unroll
         for (int k = 0; k < kConsWarps; ++k) z += red[buf][k][q];
         const float sig = 1.0f / (1.0f + expf(-z));
-        res[q] = sig - a.y[r + q];
+        res[q] = sig - yv[q];
         gb += res[q];
       }
     }
@@ -237,7 +245,7 @@ using namespace duchess;
 
 extern "C" size_t duchess_lr_grad_workspace_bytes(int32_t H) {
   if (H < 1) return 0;
-  return size_t(num_sms()) * size_t(H + 1) * sizeof(float);
+  return size_t(2 * num_sms()) * size_t(H + 1) * sizeof(float);
 }
 
 extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, const float* w,
@@ -253,8 +261,8 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   int vpt = 1;
   while (vpt < vpt_needed) vpt <<= 1;
   if (vpt > 8) return DUCHESS_EINVAL;
-  const int sms = num_sms();
-  if (!workspace || workspace_bytes < size_t(sms) * size_t(H + 1) * sizeof(float))
+  const int ctas = 2 * num_sms();
+  if (!workspace || workspace_bytes < size_t(ctas) * size_t(H + 1) * sizeof(float))
     return DUCHESS_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GradArgs a{};
@@ -268,7 +276,7 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   const int stage_bytes = a.rb * a.row_bytes;
   a.stages = int(lmin(16, lmax(2, kSmemBudget / stage_bytes)));
   if (int64_t(a.stages) * stage_bytes > kSmemBudget) return DUCHESS_EINVAL;
-  const int grid = sms;
+  const int grid = ctas;
   a.rows_per_cta = (n_rows + grid - 1) / grid;
   a.partial = static_cast<float*>(workspace);
   const size_t smem = size_t(a.stages) * stage_bytes;
