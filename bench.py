@@ -63,6 +63,18 @@ PRESET_GEN = {
 }
 
 
+def k1_traffic_ratio():
+    """DRAM bytes / algorithmic bytes of K1 from the committed ncu --set full
+    capture (tools/profile_all.sh -> profiles/<round>/k1_traffic.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k1_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return d["dram_bytes"] / d["algorithmic_bytes"], os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -260,7 +272,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                      "kernel": f"duchess_score (K1, {args.k1})", "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_share_of_step": k1_ms / ms,
-                     "traffic": None},
+                     "traffic": (None if k1_traffic_ratio()[0] is None
+                                 else k1_traffic_ratio()[0] * bytes_per_launch),
+                     "traffic_source": k1_traffic_ratio()[1]},
         "e2e": e2e,
         "gpu_launches": 2 * args.steps,
         "clocks": clk,
@@ -363,6 +377,11 @@ def run_fork_bench(args, rank, world, local_rank):
     t.table.copy_(torch.from_numpy(table))
     t.refcount[:n_root_blocks] = 1
     t.free_list = torch.arange(n_root_blocks, n_blocks, dtype=torch.int32, device=dev)
+    g = torch.Generator(device=dev).manual_seed(3)
+    for lo in range(0, t.kv.numel(), 1 << 30):      # incompressible KV contents
+        hi = min(t.kv.numel(), lo + (1 << 30))
+        t.kv[lo:hi] = torch.randint(0, 256, (hi - lo,), dtype=torch.uint8, device=dev,
+                                    generator=g)
     fk = torch.from_numpy(forks).to(dev)
     n_full = forks[:, :, 3] // bt
     tail = forks[:, :, 3] % bt

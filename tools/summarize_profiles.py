@@ -1,0 +1,73 @@
+"""Summarise a profile pass (tools/profile_all.sh) into profiles/<tag>/ text files."""
+import csv
+import collections
+import json
+import os
+import subprocess
+import sys
+
+tag = sys.argv[1]
+src = f"gpurun_out/prof_{tag}"
+dst = f"profiles/{tag}"
+os.makedirs(dst, exist_ok=True)
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__occupancy_limit_registers",
+        "lts__t_sector_hit_rate.pct", "sm__cycles_active.avg", "gpc__cycles_elapsed.max"]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units, vals = rows[0], rows[1], rows[2]
+    return {n: (vals[i], units[i]) for i, n in enumerate(h)}
+
+
+summary = {}
+for name in ("k1_full", "round_full", "k3_full", "k4_full"):
+    rep = f"{src}/{name}.ncu-rep"
+    if not os.path.exists(rep):
+        continue
+    r = raw(rep)
+    pick = {k: r[k] for k in KEYS if k in r}
+    summary[name] = {"kernel": r.get("Kernel Name", ("?", ""))[0], **{k: f"{v} {u}" for k, (v, u) in pick.items()}}
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    with open(f"{dst}/{name}_details.txt", "w") as f:
+        f.write(det)
+    lines = subprocess.run([sys.executable, "tools/ncu_lines.py", rep, "25"], capture_output=True,
+                           text=True).stdout
+    with open(f"{dst}/{name}_hot_lines.txt", "w") as f:
+        f.write(lines)
+with open(f"{dst}/ncu_full_summary.json", "w") as f:
+    json.dump(summary, f, indent=1)
+
+# launch list of the default bench (C2)
+rows = list(csv.reader(open(f"{src}/launches_c2.csv")))
+hdr, data = None, collections.defaultdict(dict)
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        d = dict(zip(hdr, r))
+        data[(int(d["ID"]), d["Kernel Name"])][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+agg = collections.defaultdict(list)
+for (i, k), m in sorted(data.items()):
+    agg[k.split("(")[0]].append(m)
+with open(f"{dst}/launches_c2_summary.txt", "w") as f:
+    f.write("ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+            "--clock-control none  python bench.py --steps 8 --warmup 3 (cold-cache, serialised)\n")
+    f.write(f"{'kernel':55s} {'n':>4s} {'mean_us':>9s} {'min_us':>8s} {'max_us':>8s} {'rd_MB':>9s} {'wr_MB':>8s}\n")
+    for k, ms in agg.items():
+        t = [m["gpu__time_duration.sum"] / 1e3 for m in ms]
+        rd = [m.get("dram__bytes_read.sum", 0) / 1e6 for m in ms]
+        wr = [m.get("dram__bytes_write.sum", 0) / 1e6 for m in ms]
+        f.write(f"{k[:55]:55s} {len(t):4d} {sum(t)/len(t):9.2f} {min(t):8.2f} {max(t):8.2f} "
+                f"{sum(rd)/len(rd):9.2f} {sum(wr)/len(wr):8.2f}\n")
+os.system(f"cp {src}/launches_c2.csv {dst}/launches_c2.csv")
+print(open(f"{dst}/launches_c2_summary.txt").read())
+print(json.dumps(summary, indent=1))
