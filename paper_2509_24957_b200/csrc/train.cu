@@ -44,12 +44,12 @@ struct GradArgs {
   float* partial;  // [grid, H+1]
 };
 
-template <bool BF16, int VPT>
+template <bool BF16, int VPT, int RB>
 __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
   constexpr int EPV = BF16 ? 8 : 4;   // elements per 16-byte vector
   extern __shared__ __align__(128) char smem[];
   __shared__ uint64_t full_bar[16], empty_bar[16];
-  __shared__ float red[2][kConsWarps][kMaxRB];
+  __shared__ float red[2][kConsWarps][RB];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = int64_t(blockIdx.x) * a.rows_per_cta;
@@ -107,16 +107,16 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
     const uint32_t ph = uint32_t((it / a.stages) & 1);
     const int64_t r = row0 + it * a.rb;
     const int nr = int(lmin(a.rb, row1 - r));
-    float yv[kMaxRB];                       // labels prefetched before the stage wait
+    float yv[RB];                       // labels prefetched before the stage wait
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) yv[q] = q < nr ? __ldg(a.y + r + q) : 0.f;
+    for (int q = 0; q < RB; ++q) yv[q] = q < nr ? __ldg(a.y + r + q) : 0.f;
     mbar_wait(&full_bar[s], ph);
     const char* base = smem + size_t(s) * stage_bytes;
-    float dots[kMaxRB], dots2[kMaxRB];
+    float dots[RB], dots2[RB];
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) { dots[q] = 0.f; dots2[q] = 0.f; }
+    for (int q = 0; q < RB; ++q) { dots[q] = 0.f; dots2[q] = 0.f; }
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) {
+    for (int q = 0; q < RB; ++q) {
       if (q < nr) {
         const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
 #pragma unroll
@@ -144,16 +144,16 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
     }
     const int buf = int(it & 1);
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) {
+    for (int q = 0; q < RB; ++q) {
       if (q < nr) {
         const float d = warp_sum(dots[q] + dots2[q]);
         if (lane == 0) red[buf][warp][q] = d;
       }
     }
     consumer_bar();
-    float res[kMaxRB];
+    float res[RB];
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) {
+    for (int q = 0; q < RB; ++q) {
       res[q] = 0.f;
       if (q < nr) {
         float z = bias;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
       }
     }
 #pragma unroll
-    for (int q = 0; q < kMaxRB; ++q) {
+    for (int q = 0; q < RB; ++q) {
       if (q < nr) {
         const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
 #pragma unroll
@@ -220,12 +220,22 @@ __global__ void sgd_kernel(float* w, const float* g, int n, float lr) {
   if (i < n) w[i] -= lr * g[i];
 }
 
-template <bool BF16, int VPT>
-static cudaError_t launch_grad(const GradArgs& a, int grid, size_t smem, cudaStream_t s) {
-  auto k = lr_grad_kernel<BF16, VPT>;
+template <bool BF16, int VPT, int RB>
+static cudaError_t launch_grad_rb(const GradArgs& a, int grid, size_t smem, cudaStream_t s) {
+  auto k = lr_grad_kernel<BF16, VPT, RB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<grid, kCons + 32, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <bool BF16, int VPT>
+static cudaError_t launch_grad(const GradArgs& a, int grid, size_t smem, cudaStream_t s) {
+  switch (a.rb) {
+    case 1: return launch_grad_rb<BF16, VPT, 1>(a, grid, smem, s);
+    case 2: return launch_grad_rb<BF16, VPT, 2>(a, grid, smem, s);
+    case 4: return launch_grad_rb<BF16, VPT, 4>(a, grid, smem, s);
+    default: return launch_grad_rb<BF16, VPT, 8>(a, grid, smem, s);
+  }
 }
 
 static int num_sms() {
@@ -272,7 +282,10 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   a.n_rows = n_rows;
   a.H = H;
   a.row_bytes = int(row_bytes);
-  a.rb = int(lmax(1, lmin(kMaxRB, kStageBytesTarget / row_bytes)));
+  {
+    int rb = int(lmax(1, lmin(kMaxRB, kStageBytesTarget / row_bytes)));
+    a.rb = rb >= 8 ? 8 : rb >= 4 ? 4 : rb >= 2 ? 2 : 1;   // compile-time rows per stage
+  }
   const int stage_bytes = a.rb * a.row_bytes;
   a.stages = int(lmin(16, lmax(2, kSmemBudget / stage_bytes)));
   if (int64_t(a.stages) * stage_bytes > kSmemBudget) return DUCHESS_EINVAL;
