@@ -66,6 +66,13 @@ extern "C" {
  * margin of a boundary; both give identical picks — the flag exists to test that). */
 #define DUCHESS_FLAG_EXACT_CDF 1
 
+/* Policies (orchestrator.py:47-52). DUCHESS runs through advance / decide /
+ * round; the baselines through duchess_baseline_round. */
+#define DUCHESS_POLICY_DUCHESS 0
+#define DUCHESS_POLICY_DEFAULT_SC 1
+#define DUCHESS_POLICY_SHORT_MK 2
+#define DUCHESS_POLICY_DYNASOR 3
+
 #define DUCHESS_MT_WORDS 625 /* 624 MT19937 words + index, as random.Random.getstate() */
 #define DUCHESS_MAX_SLOTS 64 /* max_branches limit of the warp-per-request kernel */
 #define DUCHESS_REC_WORDS 12
@@ -104,7 +111,10 @@ typedef struct DuchessPolicy {
   int32_t n_layers;          /* probability columns per slot in `probs` */
   int32_t combine;           /* 0 = layer 0, 1 = mean over layers */
   int32_t flags;             /* DUCHESS_FLAG_* */
-  int32_t _pad;
+  int32_t policy_kind;       /* DUCHESS_POLICY_* (orchestrator.py:47-52) */
+  int32_t short_m;           /* short-m@k m, :76 */
+  int32_t dynasor_window;    /* dynasor D, :75 */
+  int32_t _pad2[2];
   double early_term_threshold; /* tau, :68; +inf disables (:58-59) */
   double inv_temperature;      /* 1.0 / branch_out_temperature, computed by the host (:182) */
   double rho;                  /* SyntheticPredictorConfig.rho, predictor.py:321 */
@@ -159,6 +169,9 @@ typedef struct DuchessState {
   int32_t* br_npred;
   int32_t* br_slot;
   double* br_last_pred;
+  int32_t* br_probe_last; /* dynasor: last probed answer id (-1 none) */
+  int32_t* br_probe_run;  /* dynasor: trailing run of identical probe answers */
+  int32_t* slot_aux;      /* [R] short-m@k: finishers counted so far */
   /* per branch slot [R*C] */
   int32_t* slot_branch;
   uint8_t* row_mask;   /* survivors to score this round */
@@ -219,6 +232,12 @@ int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
  * calling decide then advance; round_rec holds the round just decided. */
 int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                   const DuchessState* state, const double* probs, void* stream);
+
+/* One round of a baseline policy for every slot (DefaultScRun.step
+ * orchestrator.py:408-435, ShortMkRun.step :466-516, DynasorRun.step
+ * :529-561), refill included; cooperative launch. No predictions, no forks. */
+int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                           const DuchessState* state, void* stream);
 
 /* Rule primitives (orchestrator.py:177-197, :200-208; core.py:76-83). */
 int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,

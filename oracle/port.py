@@ -333,6 +333,144 @@ class DuchessRequest:
 
 
 # ---------------------------------------------------------------------------
+# orchestrator.py:405-561 — baseline policies (restated on the same request base)
+
+class _Baseline(DuchessRequest):
+    def __init__(self, trace, knobs: Knobs):
+        super().__init__(trace, knobs, rng=None, predictor=lambda *a: 0.0)
+
+    def _round_start(self):
+        if self.done:
+            raise RuntimeError("request already terminated")
+        self.rounds += 1
+
+    def _advance(self, b: Branch):
+        k = self.k
+        room = min(b.template.natural_length, k.token_cap) - b.position
+        n = max(0, min(k.interval_tokens, room))
+        b.tokens_decoded += n
+        self.tokens_decode += n
+        return n
+
+
+class DefaultScRequest(_Baseline):
+    """orchestrator.py:405-435 — every branch runs to its end (or the cap)."""
+
+    def step(self) -> Round:
+        self._round_start()
+        acts, probes, dec, mc, dt = [], 0, 0, 0, 0
+        for b in self.active():
+            n = self._advance(b)
+            if n:
+                dec, mc, dt = dec + 1, max(mc, n), dt + n
+            if b.position >= b.template.natural_length:
+                self._vote(b, NATURAL_END, b.template.final_answer)
+            elif b.position >= self.k.token_cap:
+                probes += 1
+                self._vote(b, CAPPED, self._probe(b))
+            else:
+                acts.append(("continue", b.branch_id, None))
+        if not self.active():
+            self._close("exhausted")
+        return Round(self.rounds, dec, mc, dt, probes, acts, self.done)
+
+
+class ShortMkRequest(_Baseline):
+    """orchestrator.py:438-516 — stop at the m-th finisher (lockstep cut)."""
+
+    def __init__(self, trace, knobs: Knobs):
+        if knobs.short_m > knobs.max_branches:
+            raise ValueError(f"short_m ({knobs.short_m}) must not exceed max_branches "
+                             f"({knobs.max_branches})")
+        super().__init__(trace, knobs)
+        self.finished = 0
+        self.target = min(knobs.short_m, len(self.branches))
+
+    def _finish_branch(self, b: Branch) -> int:
+        if b.position >= b.template.natural_length:
+            self._vote(b, NATURAL_END, b.template.final_answer)
+            return 0
+        self._vote(b, CAPPED, self._probe(b))
+        return 1
+
+    def step(self) -> Round:
+        self._round_start()
+        k = self.k
+        plan = []
+        for b in self.active():
+            room = min(b.template.natural_length, k.token_cap) - b.position
+            n = min(k.interval_tokens, room)
+            plan.append((b, n, n == room))
+        fins = sorted((n, b.branch_id, b) for b, n, f in plan if f)
+        cut = None
+        if self.finished + len(fins) >= self.target:
+            cut = fins[self.target - self.finished - 1][0]
+        probes = dec = mc = dt = 0
+        for b, n, _f in plan:
+            take = n if cut is None else min(n, cut)
+            b.tokens_decoded += take
+            self.tokens_decode += take
+            if take > 0:
+                dec, mc, dt = dec + 1, max(mc, take), dt + take
+        if cut is None:
+            for b, _n, f in plan:
+                if f:
+                    probes += self._finish_branch(b)
+                    self.finished += 1
+        else:
+            done_n = self.finished
+            for n, _bid, b in fins:
+                if done_n < self.target and n <= cut:
+                    probes += self._finish_branch(b)
+                    done_n += 1
+            self.finished = done_n
+            for b in self.active():
+                b.status = CANCELLED
+            self._close("exhausted")
+        if not self.done and not self.active():
+            self._close("exhausted")
+        return Round(self.rounds, dec, mc, dt, probes, [], self.done)
+
+
+class DynasorRequest(_Baseline):
+    """orchestrator.py:519-561 — probe every round, stop a branch once its last
+    `dynasor_window` probe answers agree."""
+
+    def __init__(self, trace, knobs: Knobs):
+        if knobs.dynasor_window < 2:
+            raise ValueError("dynasor_window must be >= 2")
+        super().__init__(trace, knobs)
+
+    def step(self) -> Round:
+        self._round_start()
+        win = self.k.dynasor_window
+        probes = dec = mc = dt = 0
+        for b in self.active():
+            n = self._advance(b)
+            if n:
+                dec, mc, dt = dec + 1, max(mc, n), dt + n
+            if b.position >= b.template.natural_length:
+                self._vote(b, NATURAL_END, b.template.final_answer)
+                continue
+            if b.position >= self.k.token_cap:
+                probes += 1
+                self._vote(b, CAPPED, self._probe(b))
+                continue
+            ans = self._probe(b)
+            probes += 1
+            last = [a for _p, a in b.probe_history[-win:]]
+            if len(last) == win and len(set(last)) == 1:
+                self._vote(b, EARLY_TERMINATED, ans)
+        if not self.active():
+            self._close("exhausted")
+        return Round(self.rounds, dec, mc, dt, probes, [], self.done)
+
+
+BASELINES = {"default-sc": DefaultScRequest, "short-mk": ShortMkRequest,
+             "dynasor": DynasorRequest}
+
+
+# ---------------------------------------------------------------------------
 # predictor.py — frozen MLP forward (restated; numpy f64)
 
 def _gelu(x: np.ndarray) -> np.ndarray:

@@ -21,6 +21,7 @@ REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
 PRED_DEVICE, PRED_TRACE, PRED_HOST = 0, 1, 2
 FLAG_EXACT_CDF = 1
+POLICY_DUCHESS, POLICY_DEFAULT_SC, POLICY_SHORT_MK, POLICY_DYNASOR = 0, 1, 2, 3
 MT_WORDS = 625
 MAX_SLOTS = 64
 REC_WORDS = 12
@@ -41,7 +42,8 @@ class Policy(C.Structure):
         ("probe_cost_tokens", C.c_int32), ("need_consensus", C.c_int32),
         ("need_coverage", C.c_int32), ("pred_source", C.c_int32),
         ("n_layers", C.c_int32), ("combine", C.c_int32),
-        ("flags", C.c_int32), ("_pad", C.c_int32),
+        ("flags", C.c_int32), ("policy_kind", C.c_int32), ("short_m", C.c_int32),
+        ("dynasor_window", C.c_int32), ("_pad2", C.c_int32 * 2),
         ("early_term_threshold", C.c_double), ("inv_temperature", C.c_double),
         ("rho", C.c_double),
     ]
@@ -63,7 +65,7 @@ STATE_PTR_FIELDS = [
     "slot_req", "needs_refill", "n_branches", "next_template", "tokens_decode",
     "tokens_probe", "rounds", "done", "tally", "mt",
     "br_offset", "br_decoded", "br_streak", "br_status", "br_final", "br_npred", "br_slot",
-    "br_last_pred",
+    "br_last_pred", "br_probe_last", "br_probe_run", "slot_aux",
     "slot_branch", "row_mask", "row_pos", "row_tmpl", "row_req",
     "p1_rec", "round_rec", "actions", "forks", "step_pred", "queue_head", "active_rows", "active_count",
     "out_final", "out_reason", "out_tokens_decode", "out_tokens_probe", "out_rounds",
@@ -98,6 +100,8 @@ SYMBOLS = {
                                  C.c_void_p, C.c_void_p]),
     "duchess_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                 C.c_void_p, C.c_void_p]),
+    "duchess_baseline_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload),
+                                         C.POINTER(State), C.c_void_p]),
     "duchess_branch_out_sample": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
                                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p]),

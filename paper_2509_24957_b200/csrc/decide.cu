@@ -356,12 +356,14 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       s.br_offset[bi] = 0; s.br_decoded[bi] = 0; s.br_streak[bi] = 0;
       s.br_status[bi] = DUCHESS_ACTIVE; s.br_final[bi] = -1; s.br_npred[bi] = 0;
       s.br_slot[bi] = j; s.br_last_pred[bi] = 0.5;
+      if (s.br_probe_last) { s.br_probe_last[bi] = -1; s.br_probe_run[bi] = 0; }
     }
   }
   for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
   copy_mt(w.mt_init + int64_t(p) * DUCHESS_MT_WORDS, s.mt + int64_t(r) * DUCHESS_MT_WORDS, lane);
   if (lane == 0) {
     s.slot_req[r] = p;
+    if (s.slot_aux) s.slot_aux[r] = 0;
     s.n_branches[r] = seeded;
     s.next_template[r] = seeded;
     s.tokens_decode[r] = 0;
@@ -867,6 +869,223 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
 }
 
 // ---------------------------------------------------------------------------
+// Baseline policies (orchestrator.py:405-561) on the same slot machinery.
+
+// _finish (:296-304) for the baselines: tally -> majority vote, outcome record.
+__device__ void close_slot(const DuchessState& s, int r, int p, int reason, int lane,
+                           int32_t* rec) {
+  const int64_t rA = int64_t(r) * s.answer_cap;
+  int max_count = 0, total = 0, best = 0x7fffffff;
+  for (int a = lane; a < s.answer_cap; a += 32) {
+    const int cnt = __ldcg(&s.tally[rA + a]);
+    total += cnt;
+    if (cnt > max_count) { max_count = cnt; best = a; }
+    s.out_tally[int64_t(p) * s.answer_cap + a] = cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    total += __shfl_xor_sync(0xffffffffu, total, o);
+    const int mc = __shfl_xor_sync(0xffffffffu, max_count, o);
+    const int bb = __shfl_xor_sync(0xffffffffu, best, o);
+    if (mc > max_count || (mc == max_count && bb < best)) { max_count = mc; best = bb; }
+  }
+  if (lane == 0) {
+    const bool empty = total == 0;
+    s.done[r] = 1;
+    s.needs_refill[r] = 1;
+    rec[DUCHESS_REC_DONE] = 1;
+    rec[DUCHESS_REC_REASON] = reason;
+    rec[DUCHESS_REC_FINAL] = empty ? -1 : best;
+    s.out_final[p] = empty ? -1 : best;
+    s.out_reason[p] = reason;
+    s.out_tokens_decode[p] = s.tokens_decode[r];
+    s.out_tokens_probe[p] = s.tokens_probe[r];
+    s.out_rounds[p] = s.rounds[r];
+    s.out_error[p] = empty ? 1 : 0;
+    add_counter(&s.counters[DUCHESS_CNT_FINISHED], 1ll);
+    if (empty) add_counter(&s.counters[DUCHESS_CNT_ERRORS], 1ll);
+  }
+}
+
+__device__ void baseline_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
+                              const DuchessState& s, int r, int p, SlotCache& c, int lane) {
+  const int C = pol.max_branches;
+  const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
+  const int64_t rA = int64_t(r) * s.answer_cap;
+  int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
+  int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
+  const int t0 = w.tmpl_off[p];
+  const int n_tmpl = w.tmpl_off[p + 1] - t0;
+  const int kind = pol.policy_kind;
+  // ShortMk bookkeeping (:454-455): m finishers end the request
+  const int target = min(pol.short_m, min(C, n_tmpl));
+  const int finished0 = (kind == DUCHESS_POLICY_SHORT_MK) ? s.slot_aux[r] : 0;
+  // per-slot plan in registers (slots j = lane, lane + 32)
+  int chunk[2] = {0, 0}, pos0[2] = {0, 0}, nat[2] = {0, 0}, tt[2] = {0, 0};
+  bool occ[2] = {false, false}, fin[2] = {false, false};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (j < C && c.bid[j] >= 0) {
+      occ[q] = true;
+      tt[q] = t0 + c.bid[j];
+      nat[q] = w.nat_len[tt[q]];
+      pos0[q] = c.off[j] + c.dec[j];
+      const int room = min(nat[q], pol.token_cap) - pos0[q];
+      chunk[q] = kind == DUCHESS_POLICY_SHORT_MK ? min(pol.interval_tokens, room)
+                                                  : max(0, min(pol.interval_tokens, room));
+      fin[q] = kind == DUCHESS_POLICY_SHORT_MK && chunk[q] == room;
+    }
+  }
+  // ShortMk: finishers ordered by (chunk, branch id); cut at the m-th (:480-484)
+  int cut = -1, n_fin = 0;
+  if (kind == DUCHESS_POLICY_SHORT_MK) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      if (j < C) c.need[j] = fin[q] ? chunk[q] : -1;      // reuse: finisher chunk or -1
+      n_fin += __popc(__ballot_sync(0xffffffffu, fin[q]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      if (fin[q]) {
+        int rk = 0;
+        for (int k = 0; k < C; ++k) {
+          const int ck = c.need[k];
+          if (ck >= 0 && (ck < chunk[q] || (ck == chunk[q] && c.bid[k] < c.bid[j]))) ++rk;
+        }
+        c.rank[j] = rk;
+        c.order[rk] = chunk[q];
+      }
+    }
+    __syncwarp();
+    if (finished0 + n_fin >= target) cut = c.order[target - finished0 - 1];
+  }
+  int decoding = 0, max_chunk = 0, dtok = 0, probes = 0, counted = 0;
+  bool cont[2] = {false, false};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (!occ[q]) continue;
+    const int b = c.bid[j];
+    const int64_t bi = rB + b;
+    const int take = (kind == DUCHESS_POLICY_SHORT_MK && cut >= 0) ? min(chunk[q], cut) : chunk[q];
+    const int pos = pos0[q] + take;
+    c.dec[j] += take;
+    s.br_decoded[bi] = c.dec[j];
+    if (take > 0) { decoding++; max_chunk = max(max_chunk, take); dtok += take; }
+    int status = DUCHESS_ACTIVE, ans = -1;
+    if (kind == DUCHESS_POLICY_SHORT_MK) {
+      // _finish_branch (:457-464) for counted finishers
+      const bool collect = fin[q] && (cut < 0 || (c.rank[j] < target - finished0 && chunk[q] <= cut));
+      if (collect) {
+        counted++;
+        if (pos >= nat[q]) { status = DUCHESS_NATURAL_END; ans = w.final_ans[tt[q]]; }
+        else { status = DUCHESS_CAPPED; ans = probe_answer_fast(w, tt[q], pos); probes++; }
+      }
+    } else if (pos >= nat[q]) {
+      status = DUCHESS_NATURAL_END; ans = w.final_ans[tt[q]];
+    } else if (pos >= pol.token_cap) {
+      status = DUCHESS_CAPPED; ans = probe_answer_fast(w, tt[q], pos); probes++;
+    } else if (kind == DUCHESS_POLICY_DYNASOR) {
+      ans = probe_answer_fast(w, tt[q], pos);                  // probe every round (:553-557)
+      probes++;
+      const int last = s.br_probe_last[bi];
+      const int run = (ans == last) ? s.br_probe_run[bi] + 1 : 1;
+      s.br_probe_last[bi] = ans;
+      s.br_probe_run[bi] = run;
+      if (run >= pol.dynasor_window) status = DUCHESS_EARLY_TERMINATED;
+      else ans = -1;
+    } else {
+      cont[q] = true;                                           // DefaultSc continue (:430-431)
+    }
+    if (status != DUCHESS_ACTIVE) {
+      c.status[j] = status;
+      s.br_status[bi] = status;
+      s.br_final[bi] = ans;
+      s.br_slot[bi] = -1;
+      atomicAdd(&s.tally[rA + ans], 1);
+      c.bid[j] = -1;
+    }
+  }
+  // continue actions in creation order (branch id == slot for DefaultSc: no forks)
+  int n_act = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    const unsigned m = __ballot_sync(0xffffffffu, cont[q]);
+    if (cont[q]) {
+      const int k = n_act + __popc(m & ((1u << lane) - 1u));
+      act[k * 3 + 0] = DUCHESS_ACT_CONTINUE;
+      act[k * 3 + 1] = c.bid[j];
+      act[k * 3 + 2] = -1;
+    }
+    n_act += __popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    decoding += __shfl_xor_sync(0xffffffffu, decoding, o);
+    dtok += __shfl_xor_sync(0xffffffffu, dtok, o);
+    probes += __shfl_xor_sync(0xffffffffu, probes, o);
+    counted += __shfl_xor_sync(0xffffffffu, counted, o);
+    max_chunk = max(max_chunk, __shfl_xor_sync(0xffffffffu, max_chunk, o));
+  }
+  __syncwarp();
+  bool cancel = kind == DUCHESS_POLICY_SHORT_MK && cut >= 0;
+  bool any_active = false;
+  for (int base = 0; base < C; base += 32) {
+    const int j = base + lane;
+    const bool a = j < C && c.bid[j] >= 0;
+    if (a && cancel) {                                          // _cancel_active (:292-294)
+      s.br_status[rB + c.bid[j]] = DUCHESS_CANCELLED;
+      s.br_slot[rB + c.bid[j]] = -1;
+      c.bid[j] = -1;
+    }
+    if (j < C) s.slot_branch[rC + j] = c.bid[j];
+    any_active |= __any_sync(0xffffffffu, a && !cancel);
+  }
+  if (lane == 0) {
+    const int rounds = s.rounds[r] + 1;
+    s.rounds[r] = rounds;
+    s.tokens_decode[r] += dtok;
+    s.tokens_probe[r] += probes * pol.probe_cost_tokens;
+    if (kind == DUCHESS_POLICY_SHORT_MK) s.slot_aux[r] = cancel ? target : finished0 + counted;
+    rec[DUCHESS_REC_ROUND] = rounds;
+    rec[DUCHESS_REC_DECODING] = decoding;
+    rec[DUCHESS_REC_MAX_CHUNK] = max_chunk;
+    rec[DUCHESS_REC_DECODE] = dtok;
+    rec[DUCHESS_REC_PROBES] = probes;
+    rec[DUCHESS_REC_NACTIONS] = n_act;
+    rec[DUCHESS_REC_NFORKS] = 0;
+    rec[DUCHESS_REC_NSURV] = 0;
+    rec[DUCHESS_REC_DONE] = 0;
+    rec[DUCHESS_REC_REQ] = p;
+    if (!cancel && any_active) s.needs_refill[r] = 0;
+  }
+  __syncwarp();
+  if (cancel || !any_active) close_slot(s, r, p, DUCHESS_REASON_EXHAUSTED, lane, rec);
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+baseline_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.queue_head[0] = s.queue_head[1];
+  __threadfence();
+  cg::this_grid().sync();
+  if (r >= s.n_slots) return;
+  SlotCache& c = cache[threadIdx.x >> 5];
+  const int32_t* rec0 = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
+  if (lane < DUCHESS_REC_WORDS) const_cast<int32_t*>(rec0)[lane] = 0;
+  __syncwarp();
+  const int p = slot_prologue(pol, w, s, r, c, lane, false);
+  if (p >= 0) baseline_slot(pol, w, s, r, p, c, lane);
+}
+
+// ---------------------------------------------------------------------------
 // Rule primitives, one warp (branch_out_weights / branch_out_sample).
 __global__ void branch_out_kernel(const double* probs, int n, double inv_temp, uint32_t* mt,
                                   int n_draws, int32_t* out_idx, double* out_w,
@@ -1018,6 +1237,28 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(round_kernel), dim3(grid),
                                                     dim3(32 * kWarpsPerBlock), args, 0,
                                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                                      const DuchessState* state, void* stream) {
+  if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
+  if (policy->policy_kind < DUCHESS_POLICY_DEFAULT_SC || policy->policy_kind > DUCHESS_POLICY_DYNASOR)
+    return DUCHESS_EINVAL;
+  if (policy->policy_kind == DUCHESS_POLICY_SHORT_MK && (!state->slot_aux || policy->short_m < 1))
+    return DUCHESS_EINVAL;
+  if (policy->policy_kind == DUCHESS_POLICY_DYNASOR &&
+      (!state->br_probe_last || !state->br_probe_run || policy->dynasor_window < 2))
+    return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  DuchessPolicy pol = *policy;
+  DuchessWorkload w = *workload;
+  DuchessState st = *state;
+  void* args[] = {&pol, &w, &st};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(baseline_kernel),
+                                                    dim3(grid), dim3(32 * kWarpsPerBlock), args,
+                                                    0, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 

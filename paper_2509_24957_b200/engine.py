@@ -133,7 +133,7 @@ class BatchedDuchess:
     def __init__(self, traces, config, seeds, n_slots: int | None = None, *,
                  pred_source: int = _lib.PRED_TRACE, rho: float = 1.0, queue=None,
                  cycle: bool = False, n_layers: int = 1, combine: int = 0,
-                 device: str | torch.device = "cuda"):
+                 policy: str = "duchess", device: str | torch.device = "cuda"):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.device = torch.device(device)
@@ -163,6 +163,14 @@ class BatchedDuchess:
         pol.early_term_threshold = float(config.early_term_threshold)
         pol.inv_temperature = 1.0 / config.branch_out_temperature     # orchestrator.py:182
         pol.rho = float(rho)
+        kinds = {"duchess": _lib.POLICY_DUCHESS, "default-sc": _lib.POLICY_DEFAULT_SC,
+                 "short-mk": _lib.POLICY_SHORT_MK, "dynasor": _lib.POLICY_DYNASOR}
+        if policy not in kinds:
+            raise ValueError(f"unknown policy {policy!r}")
+        pol.policy_kind = kinds[policy]
+        pol.short_m = int(getattr(config, "short_m", 5))
+        pol.dynasor_window = int(getattr(config, "dynasor_window", 3))
+        self.policy_name = policy
         self.policy = pol
         self._alloc_state()
 
@@ -184,6 +192,9 @@ class BatchedDuchess:
                      "br_npred", "br_slot"):
             t[name] = torch.zeros(R * B, **i32)
         t["br_last_pred"] = torch.zeros(R * B, dtype=torch.float64, device=dev)
+        t["br_probe_last"] = torch.full((R * B,), -1, **i32)
+        t["br_probe_run"] = torch.zeros(R * B, **i32)
+        t["slot_aux"] = torch.zeros(R, **i32)
         t["slot_branch"] = torch.full((R * C,), -1, **i32)
         t["row_mask"] = torch.zeros(R * C, dtype=torch.uint8, device=dev)
         t["row_pos"] = torch.zeros(R * C, **i32)
@@ -242,10 +253,19 @@ class BatchedDuchess:
                                           p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_round")
 
+    def baseline_round(self, stream=None) -> None:
+        """One round of a baseline policy (Default SC / Short-m@k / Dynasor)."""
+        _lib.check(self.lib.duchess_baseline_round(self.policy, self.wl.struct, self.state,
+                                                   _lib.stream_handle(stream)),
+                   "duchess_baseline_round")
+
     def step(self, score_fn=None, stream=None) -> None:
         """One round for every occupied slot. score_fn(engine) must fill
         self.probs for the survivors flagged in t['row_mask'] when the
         prediction source is PRED_DEVICE (e.g. fill + K1)."""
+        if self.policy.policy_kind != _lib.POLICY_DUCHESS:
+            self.baseline_round(stream)
+            return
         self.advance(stream)
         if self.policy.pred_source != _lib.PRED_TRACE:
             if score_fn is None:

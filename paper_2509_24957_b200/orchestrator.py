@@ -404,6 +404,53 @@ class DuchessRun(RequestRun):
                            int(rec[_lib.REC_PROBES]), actions, done)
 
 
+class _BaselineRun(RequestRun):
+    """Device-backed baseline policy (orchestrator.py:405-561): one
+    duchess_baseline_round per step, state mirrored like DuchessRun."""
+    _policy = ""
+
+    def __init__(self, trace: RequestTrace, config: OrchestratorConfig,
+                 rng: random.Random | None = None) -> None:
+        super().__init__(trace, config, rng)
+        from .engine import BatchedDuchess
+        self._engine = BatchedDuchess([trace], config, [random.Random(0)], n_slots=1,
+                                      policy=self._policy)
+
+    def step(self) -> RoundReport:
+        if self.done:
+            raise RuntimeError("request already terminated")
+        self._engine.baseline_round()
+        return DuchessRun._mirror_round(self)
+
+
+class DefaultScRun(_BaselineRun):
+    """Plain self-consistency (orchestrator.py:405-435)."""
+    _policy = POLICY_DEFAULT_SC
+
+
+class ShortMkRun(_BaselineRun):
+    """Stop at the m-th finisher (orchestrator.py:438-516)."""
+    _policy = POLICY_SHORT_MK
+
+    def __init__(self, trace: RequestTrace, config: OrchestratorConfig,
+                 rng: random.Random | None = None) -> None:
+        if config.short_m > config.max_branches:
+            raise ValueError(f"short_m ({config.short_m}) must not exceed max_branches "
+                             f"({config.max_branches})")
+        super().__init__(trace, config, rng)
+
+
+class DynasorRun(_BaselineRun):
+    """Probe every round; stop a branch on D identical answers (orchestrator.py:519-561)."""
+    _policy = POLICY_DYNASOR
+
+    def __init__(self, trace: RequestTrace, config: OrchestratorConfig,
+                 rng: random.Random | None = None) -> None:
+        if config.dynasor_window < 2:
+            raise ValueError("dynasor_window must be >= 2")
+        super().__init__(trace, config, rng)
+
+
 def make_request_run(policy: str, trace: RequestTrace, config: OrchestratorConfig,
                      rng: random.Random | None = None,
                      synthetic: SyntheticPredictorConfig | None = None) -> RequestRun:
@@ -411,12 +458,27 @@ def make_request_run(policy: str, trace: RequestTrace, config: OrchestratorConfi
         if rng is None:
             raise ValueError("the duchess policy needs an rng")
         return DuchessRun(trace, config, rng, synthetic=synthetic)
-    if policy in (POLICY_DEFAULT_SC, POLICY_SHORT_MK, POLICY_DYNASOR):
-        raise NotImplementedError(f"policy {policy!r} (a baseline, SURVEY §8f) is not on the "
-                                  f"device yet")
+    if policy == POLICY_DEFAULT_SC:
+        return DefaultScRun(trace, config)
+    if policy == POLICY_SHORT_MK:
+        return ShortMkRun(trace, config)
+    if policy == POLICY_DYNASOR:
+        return DynasorRun(trace, config)
     raise ValueError(f"unknown policy {policy!r}")
 
 
 def run_duchess(trace: RequestTrace, config: OrchestratorConfig, rng: random.Random,
                 synthetic: SyntheticPredictorConfig | None = None) -> RequestOutcome:
     return DuchessRun(trace, config, rng, synthetic=synthetic).run()
+
+
+def run_default_sc(trace: RequestTrace, config: OrchestratorConfig) -> RequestOutcome:
+    return DefaultScRun(trace, config).run()
+
+
+def run_short_mk(trace: RequestTrace, config: OrchestratorConfig) -> RequestOutcome:
+    return ShortMkRun(trace, config).run()
+
+
+def run_dynasor(trace: RequestTrace, config: OrchestratorConfig) -> RequestOutcome:
+    return DynasorRun(trace, config).run()

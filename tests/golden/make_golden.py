@@ -22,7 +22,8 @@ sys.path.insert(0, str(REF / "tests"))
 
 import numpy as np  # noqa: E402
 
-from branchsim.orchestrator import (DuchessRun, OrchestratorConfig,  # noqa: E402
+from branchsim.orchestrator import (DefaultScRun, DuchessRun, DynasorRun,  # noqa: E402
+                                    OrchestratorConfig, ShortMkRun,
                                     TERMINATION_DISABLED, branch_out_sample,
                                     branch_out_weights)
 from branchsim.predictor import (DEFAULT_CONFUSION, SyntheticPredictorConfig,  # noqa: E402
@@ -153,6 +154,60 @@ def decisions():
     return cases
 
 
+def run_baseline_case(name, policy, params, n, wseed, cfg):
+    requests = generate_synthetic(params, n, seed=wseed).requests
+    cls = {"default-sc": DefaultScRun, "short-mk": ShortMkRun, "dynasor": DynasorRun}[policy]
+    reqs = []
+    for trace in requests:
+        run = cls(trace, cfg)
+        reports = []
+        while not run.done:
+            rep = run.step()
+            reports.append([rep.round_index, rep.decoding_branches, rep.max_chunk,
+                            rep.decode_tokens, rep.probes,
+                            [[KIND[a.kind], a.branch_id,
+                              -1 if a.source_branch_id is None else a.source_branch_id]
+                             for a in rep.actions], int(rep.done)])
+        o = run.outcome
+        reqs.append({"reports": reports,
+                     "outcome": {"tally": dict(sorted(o.tally.counts.items())), "final": o.final,
+                                 "reason": o.termination_reason,
+                                 "tokens_decode": o.tokens_decode,
+                                 "tokens_probe": o.tokens_probe, "rounds": o.rounds},
+                     "branches": [[STATUS[b.status], b.final_answer, b.offset_base,
+                                   b.tokens_decoded] for b in run.branches]})
+    cfg_d = {k: getattr(cfg, k) for k in cfg.__dataclass_fields__}
+    cfg_d["early_term_threshold"] = float(cfg.early_term_threshold).hex()
+    return {"name": name, "policy": policy,
+            "params": {k: getattr(params, k) for k in params.__dataclass_fields__},
+            "n": n, "workload_seed": wseed, "config": cfg_d,
+            "digest": workload_digest(requests), "requests": reqs}
+
+
+def baselines():
+    gsm = PRESETS["gsm8k-like"].synthetic
+    math_ = PRESETS["math-like"]
+    base = replace(math_.orchestrator, max_branches=10)
+    return [
+        run_baseline_case("sc_math", "default-sc", math_.synthetic, 20, 21, base),
+        run_baseline_case("sc_capped", "default-sc", gsm, 20, 22,
+                          replace(base, token_cap=160, interval_tokens=32)),
+        run_baseline_case("sc_few_templates", "default-sc", replace(gsm, templates_per_request=6),
+                          12, 23, base),
+        run_baseline_case("mk_m5", "short-mk", math_.synthetic, 20, 24, replace(base, short_m=5)),
+        run_baseline_case("mk_m1", "short-mk", gsm, 20, 25, replace(base, short_m=1,
+                                                                      interval_tokens=16)),
+        run_baseline_case("mk_mk", "short-mk", gsm, 12, 26, replace(base, short_m=10)),
+        run_baseline_case("mk_capped", "short-mk", math_.synthetic, 16, 27,
+                          replace(base, short_m=4, token_cap=320)),
+        run_baseline_case("dyn_w3", "dynasor", math_.synthetic, 20, 28, base),
+        run_baseline_case("dyn_w2", "dynasor", gsm, 20, 29, replace(base, dynasor_window=2,
+                                                                      interval_tokens=16)),
+        run_baseline_case("dyn_capped", "dynasor", math_.synthetic, 16, 30,
+                          replace(base, dynasor_window=4, token_cap=400)),
+    ]
+
+
 def hexs(xs):
     return [float(x).hex() for x in xs]
 
@@ -262,6 +317,7 @@ def primitives():
 
 def main():
     (OUT / "decisions.json").write_text(json.dumps(decisions(), separators=(",", ":")))
+    (OUT / "baselines.json").write_text(json.dumps(baselines(), separators=(",", ":")))
     (OUT / "primitives.json").write_text(json.dumps(primitives(), separators=(",", ":")))
     for p in sorted(OUT.glob("*.json")):
         print(p.name, p.stat().st_size)

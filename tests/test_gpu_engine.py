@@ -222,3 +222,28 @@ def test_probe_lookup_long_probe_lists():
     _lib.check(lib.duchess_template_lookup(wl.struct, t_.data_ptr(), p_.data_ptr(), len(tm),
                                            out.data_ptr(), None, _lib.stream_handle()), "lookup")
     assert out.cpu().tolist() == want
+
+
+@pytest.mark.parametrize("case", load("baselines.json"), ids=lambda c: c["name"])
+def test_baseline_policies_match_reference_golden(case):
+    """Default SC / Short-m@k / Dynasor on the device engine (slot refill on)
+    vs the reference's own runs (tests/golden/baselines.json)."""
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    from tests.golden_util import gen_params
+    traces = port.generate(gen_params(case["params"]), case["n"], case["workload_seed"])
+    eng = BatchedDuchess(traces, case_knobs(case), [0] * len(traces), n_slots=6,
+                         policy=case["policy"])
+    reports = {}
+    for _ in range(100000):
+        eng.step()
+        for p, rep in eng.round_reports():
+            reports.setdefault(p, []).append(rep)
+        if eng.all_done():
+            break
+    outcomes = eng.outcomes()
+    for p, ref in enumerate(case["requests"]):
+        assert reports[p] == [report_tuple(r) for r in ref["reports"]], f"request {p}"
+        o = outcomes[p]
+        assert (o["tally"], o["final"], o["reason"], o["tokens_decode"], o["tokens_probe"],
+                o["rounds"]) == tuple(ref["outcome"][k] for k in (
+                    "tally", "final", "reason", "tokens_decode", "tokens_probe", "rounds"))

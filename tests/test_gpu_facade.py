@@ -373,3 +373,46 @@ def test_probe_answer_and_trace_prediction():
     assert [probe_answer(t, p) for p in (8, 16, 40, 90, 200)] == ["", "7", "13", "42", "42"]
     t = tmpl(100, "1", pred=[(16, 0.25), (32, 0.75)])
     assert [trace_prediction(t, p) for p in (10, 20, 32)] == [0.0, 0.25, 0.75]
+
+
+def test_baseline_facades_match_reference_behaviour():
+    """The reference's baseline tests (test_orchestrator.py:337-460,
+    test_acceptance.py crit 1 and 10) against the device-backed facades."""
+    from paper_2509_24957_b200.orchestrator import (CANCELLED, DefaultScRun, DynasorRun,
+                                                    OrchestratorConfig, TERMINATION_DISABLED,
+                                                    make_request_run, run_default_sc,
+                                                    run_duchess, run_short_mk)
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    tr = trace("a", [tmpl(100, "a"), tmpl(200, "b"), tmpl(300, "a")])
+    cfg = OrchestratorConfig(max_branches=3, interval_tokens=80)
+    o = run_default_sc(tr, cfg)
+    assert o.tokens_decode == 600 and o.final == "a" and o.termination_reason == "exhausted"
+    with pytest.raises(ValueError, match="short_m"):
+        make_request_run("short-mk", tr, OrchestratorConfig(max_branches=2, short_m=3))
+    with pytest.raises(ValueError, match="dynasor_window"):
+        DynasorRun(tr, OrchestratorConfig(dynasor_window=1))
+    # crit 1: termination disabled + full fractions == plain self-consistency
+    wl = generate_synthetic(SyntheticParams(templates_per_request=10), 12, seed=101)
+    cfg = OrchestratorConfig(max_branches=10, interval_tokens=80,
+                             early_term_threshold=TERMINATION_DISABLED, consensus_frac=1.0,
+                             coverage_frac=1.0)
+    for i, t in enumerate(wl.requests):
+        sc = run_default_sc(t, cfg)
+        du = run_duchess(t, cfg, random.Random(i))
+        assert (du.tokens_total, du.tally, du.final) == (sc.tokens_total, sc.tally, sc.final)
+    # crit 10: short-m@k == default SC at m = k; exactly m answers for m < k
+    rng = random.Random(31)
+    for trial in range(6):
+        k = rng.randint(2, 10)
+        t = trace("0", [tmpl(rng.randint(40, 500), str(rng.randint(0, 3))) for _ in range(k)])
+        full = OrchestratorConfig(max_branches=k, interval_tokens=16, short_m=k)
+        mk, sc = run_short_mk(t, full), run_default_sc(t, full)
+        assert (mk.tally, mk.final, mk.tokens_total) == (sc.tally, sc.final, sc.tokens_total)
+        m = rng.randint(1, k - 1)
+        cut = run_short_mk(t, OrchestratorConfig(max_branches=k, interval_tokens=16, short_m=m))
+        assert cut.tally.total == m
+    run = DefaultScRun(tr, OrchestratorConfig(max_branches=3, interval_tokens=80))
+    run.run()
+    with pytest.raises(RuntimeError, match="request already terminated"):
+        run.step()
+    del CANCELLED

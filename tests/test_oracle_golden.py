@@ -35,6 +35,27 @@ def test_port_replays_reference_decisions(case):
         assert got == want
 
 
+@pytest.mark.parametrize("case", load("baselines.json"), ids=lambda c: c["name"])
+def test_port_replays_reference_baselines(case):
+    traces = port.generate(gen_params(case["params"]), case["n"], case["workload_seed"])
+    assert workload_digest(traces) == case["digest"]
+    knobs = case_knobs(case)
+    for trace, ref in zip(traces, case["requests"]):
+        req = port.BASELINES[case["policy"]](trace, knobs)
+        reports = []
+        while not req.done:
+            reports.append(port_report_tuple(req.step()))
+        assert reports == [report_tuple(r) for r in ref["reports"]]
+        o = req.outcome
+        assert (o.tally, o.final, o.termination_reason, o.tokens_decode, o.tokens_probe,
+                o.rounds) == tuple(ref["outcome"][k] for k in ("tally", "final", "reason",
+                                                               "tokens_decode", "tokens_probe",
+                                                               "rounds"))
+        assert [[b.status, b.final_answer, b.offset_base, b.tokens_decoded]
+                for b in req.branches] == [[STATUS[s], fa, ob, td] for s, fa, ob, td
+                                           in ref["branches"]]
+
+
 def test_port_decision_fixture_covers_every_path():
     seen_status, seen_reason, seen_kind = set(), set(), set()
     for case in load("decisions.json"):
