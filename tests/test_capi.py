@@ -33,7 +33,7 @@ def _struct_fields(name):
     text = HEADER.read_text()
     body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), text, flags=re.S).group(1)
     body = re.sub(r"/\*.*?\*/", "", body)
-    return re.findall(r"\b(\w+)\s*;", body)
+    return re.findall(r"\b(\w+)\s*(?:\[\d+\])?\s*;", body)
 
 
 @pytest.mark.parametrize("cname,pyname", [("DuchessPolicy", "Policy"),
@@ -66,3 +66,28 @@ def test_invalid_arguments_are_rejected_before_launch():
     pol.max_branches = 0
     assert lib.duchess_advance(ctypes.byref(pol), ctypes.byref(_lib.Workload()),
                                ctypes.byref(_lib.State()), None) == 1
+
+
+@pytest.mark.parametrize("cname,pyname", [("DuchessPolicy", "Policy"),
+                                          ("DuchessWorkload", "Workload"),
+                                          ("DuchessState", "State")])
+def test_struct_offsets_match_c_compiler(cname, pyname, tmp_path):
+    """Field offsets and sizes of the ctypes mirrors == what a C compiler lays out."""
+    import shutil
+    import subprocess
+    from paper_2509_24957_b200 import _lib
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    py = getattr(_lib, pyname)
+    fields = [f[0] for f in py._fields_]
+    src = tmp_path / "off.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"duchess_b200.h\"\n"
+                   "int main(void){\n" + "".join(
+                       f'printf("%zu\\n", offsetof({cname}, {f}));\n' for f in fields)
+                   + f'printf("%zu\\n", sizeof({cname}));return 0;}}\n')
+    exe = tmp_path / "off"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [getattr(py, f).offset for f in fields] + [ctypes.sizeof(py)]
+    assert got == want
