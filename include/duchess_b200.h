@@ -274,6 +274,15 @@ int duchess_mlp_forward(const double* params, const int32_t* dims, int32_t n_hid
                         const double* x, int64_t n_rows, double* logits, double* probs,
                         void* stream);
 
+/* ---- tensor-core MLP probe (tcgen05 + TMEM + TMA) -------------------------
+ * logit_i = b2 + sum_j w2_j relu((X_i . W1g_j - mu_i s_j) / sigma_i + c_j):
+ * the paper's MLP probe (one ReLU hidden layer, LayerNorm folded) batched as a
+ * GEMM. X [M, K] bf16, W1g [NH, K] bf16 (K-major), s/c/w2 [NH] fp32;
+ * K % 64 == 0, NH % 256 == 0. out_logit fp32 [M], out_prob fp64 [M]. */
+int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, int32_t NH,
+                         const float* s, const float* c, const float* w2, float b2,
+                         float* out_logit, double* out_prob, void* stream);
+
 /* ---- difficulty ordering (scheduler.py:60-96) --------------------------- */
 int duchess_sort_difficulty(const uint64_t* keys, const int32_t* seg_offsets, int32_t n_segs,
                             int32_t* out_perm, void* stream);

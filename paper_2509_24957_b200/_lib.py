@@ -131,6 +131,9 @@ SYMBOLS = {
     "duchess_mlp_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
                                       C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_void_p,
                                       C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "duchess_mlp_probe_tc": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_float,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
     "duchess_version": (C.c_char_p, []),
     "duchess_device_arch": (C.c_int, []),
 }
