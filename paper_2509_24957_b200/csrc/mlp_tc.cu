@@ -19,6 +19,7 @@
 //              the epilogue: tcgen05.ld 32 columns at a time, LN fold, bias,
 //              ReLU, dot with w2 accumulated per row in registers.
 // The hidden activations never touch HBM.
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -43,6 +44,8 @@ struct TcArgs {
   float b2;
   float* out_logit;
   double* out_prob;
+  const uint16_t* X;   // debug: stats from global when debug_stats != 0
+  int debug_stats;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
@@ -202,6 +205,14 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
+    if (a.debug_stats) {
+      sx = 0.f; sxx = 0.f;
+      if (row < a.M)
+        for (int k = 0; k < a.K; ++k) {
+          const float x = __uint_as_float(uint32_t(a.X[row * a.K + k]) << 16);
+          sx += x; sxx = fmaf(x, x, sxx);
+        }
+    }
     const float mean = sx / float(a.K);
     const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
     const float rsig = rsqrtf(var + kLayerNormEps);
@@ -281,7 +292,8 @@ extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const v
   CUtensorMap ma, mb;
   if (!make_map(&ma, X, uint64_t(M), uint64_t(K), kTcBM)) return DUCHESS_ECUDA;
   if (!make_map(&mb, W1, uint64_t(NH), uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
-  TcArgs a{M, K, NH, s, c, w2, b2, out_logit, out_prob};
+  static const int dbg = [] { const char* e = getenv("DUCHESS_TC_DEBUG_STATS"); return e ? atoi(e) : 0; }();
+  TcArgs a{M, K, NH, s, c, w2, b2, out_logit, out_prob, static_cast<const uint16_t*>(X), dbg};
   cudaFuncSetAttribute(mlp_probe_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   const unsigned grid = unsigned((M + kTcBM - 1) / kTcBM);
   mlp_probe_tc_kernel<<<grid, kTcThreads, kTcSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
