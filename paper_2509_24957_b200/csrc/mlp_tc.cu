@@ -15,11 +15,10 @@
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
 //              (M=128, N=256, K=16, fp32 accumulators in TMEM, double buffered
 //              2 x 256 columns so the epilogue of tile j overlaps MMAs of j+1)
-//   warps 2-5  row statistics from the A tiles of the first hidden tile, then
-//              the epilogue: tcgen05.ld 32 columns at a time, LN fold, bias,
+//   warps 2-5  row statistics (read from global while the first tile's MMAs
+//              run), then the epilogue: tcgen05.ld 32 columns at a time, LN fold, bias,
 //              ReLU, dot with w2 accumulated per row in registers.
 // The hidden activations never touch HBM.
-#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -44,8 +43,7 @@ struct TcArgs {
   float b2;
   float* out_logit;
   double* out_prob;
-  const uint16_t* X;   // debug: stats from global when debug_stats != 0
-  int debug_stats;
+  const uint16_t* X;   // row statistics are read straight from global (L2-hot)
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
@@ -123,7 +121,7 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTcStages; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1 + 4);      // MMA commit + 4 statistics warps
+      mbar_init(&empty_bar[i], 1);          // MMA commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
@@ -175,7 +173,6 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int k = 0; k < kTcBK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
             umma_bf16(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
           umma_commit(&empty_bar[s]);
-          if (n > 0) mbar_arrive_cnt(&empty_bar[s], 4);   // statistics only on the first tile
         }
         umma_commit(&tmem_full[acc]);
       }
@@ -185,33 +182,28 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const int q = warp & 3;
     const int row_local = 32 * q + lane;
     const int64_t row = m0 + row_local;
+    // Row statistics while the first hidden tile's MMAs run: 16-byte loads of the
+    // row from global memory (the TMA producer streams the same rows, so they
+    // are L2-resident), fp32 sums.
     float sx = 0.f, sxx = 0.f;
-    for (int kb = 0; kb < k_blocks; ++kb) {            // it == kb for the first hidden tile
-      const int s = kb % kTcStages;
-      const uint32_t ph = (kb / kTcStages) & 1;
-      mbar_wait(&full_bar[s], ph);
-      const uint4* rp = reinterpret_cast<const uint4*>(smem + s * kTcStageBytes + row_local * 128);
+    if (row < a.M) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+      const int nv = a.K / 8;
+      for (int v0 = 0; v0 < nv; v0 += 8) {
+        uint4 buf[8];
 #pragma unroll
-      for (int cix = 0; cix < 8; ++cix) {              // whole 128 B row, swizzle irrelevant
-        const uint4 v = rp[cix];
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        for (int u = 0; u < 8; ++u) buf[u] = v0 + u < nv ? __ldg(rp + v0 + u) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-          sx += lo + hi;
-          sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t w4[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+            sx += lo + hi;
+            sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+          }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-    }
-    if (a.debug_stats) {
-      sx = 0.f; sxx = 0.f;
-      if (row < a.M)
-        for (int k = 0; k < a.K; ++k) {
-          const float x = __uint_as_float(uint32_t(a.X[row * a.K + k]) << 16);
-          sx += x; sxx = fmaf(x, x, sxx);
-        }
     }
     const float mean = sx / float(a.K);
     const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
@@ -292,8 +284,7 @@ extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const v
   CUtensorMap ma, mb;
   if (!make_map(&ma, X, uint64_t(M), uint64_t(K), kTcBM)) return DUCHESS_ECUDA;
   if (!make_map(&mb, W1, uint64_t(NH), uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
-  static const int dbg = [] { const char* e = getenv("DUCHESS_TC_DEBUG_STATS"); return e ? atoi(e) : 0; }();
-  TcArgs a{M, K, NH, s, c, w2, b2, out_logit, out_prob, static_cast<const uint16_t*>(X), dbg};
+  TcArgs a{M, K, NH, s, c, w2, b2, out_logit, out_prob, static_cast<const uint16_t*>(X)};
   cudaFuncSetAttribute(mlp_probe_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   const unsigned grid = unsigned((M + kTcBM - 1) / kTcBM);
   mlp_probe_tc_kernel<<<grid, kTcThreads, kTcSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
