@@ -429,6 +429,60 @@ def run_fork_bench(args, rank, world, local_rank):
             "gpu_launches": 2 * args.steps, "clocks": clk}
 
 
+def run_tc_bench(args, rank, world, local_rank):
+    """C3 tensor-core variant: the paper's MLP probe (hidden 2048, ReLU, LN
+    folded) at T=1 over 1024 requests x 32 branches of hidden 5120, as one
+    tcgen05 GEMM per step with the head fused into the epilogue."""
+    import torch
+    from paper_2509_24957_b200.mlp_probe import TensorCoreMlpProbe
+    from paper_2509_24957_b200.predictor import MlpWeights
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    M, K, NH = 1024 * 32, 5120, 2048
+    rng = np.random.default_rng(0)
+    w = MlpWeights(K, [NH], 1, ["relu"], [rng.normal(0, 1 / np.sqrt(K), (NH, K)),
+                                          rng.normal(0, 1 / np.sqrt(NH), (1, NH))],
+                   [rng.normal(0, 0.1, NH), np.array([0.0])], rng.uniform(0.5, 1.5, K),
+                   rng.uniform(-0.1, 0.1, K))
+    probe = TensorCoreMlpProbe(w, device=dev)
+    slabs = [torch.randn((M, K), device=dev).to(torch.bfloat16) for _ in range(2)]  # 2 x 335 MB
+    logit = torch.empty(M, device=dev)
+    prob = torch.empty(M, dtype=torch.float64, device=dev)
+    for i in range(args.warmup):
+        probe(slabs[i % 2], logit, prob)
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        probe(slabs[i % 2], logit, prob)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    flops = probe.flops(M)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        peak, kind = float(pk["bf16_tflops"]), "measured (burst)"
+    except Exception:  # noqa: BLE001
+        peak, kind = 1590.0, "fallback"
+    tflops = flops / (ms / 1e3) / 1e12
+    return {"metric": "MLP-probe branch-steps/s (C3 tensor-core variant, T=1)",
+            "value": M * world / (ms / 1e3), "unit": "branch-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) activations, random-init MLP probe",
+            "config": {"workload": f"C3-TC: {M} windows (1024 req x 32 br), hidden {K} -> "
+                                   f"{NH} ReLU -> 1, LN folded, 2 rotating inputs (> L2)"},
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak,
+                         "unit": "TFLOP/s", "frac": tflops / peak, "peak_kind": kind,
+                         "kernel": "mlp_probe_tc_kernel (tcgen05)", "flops_per_launch": flops,
+                         "traffic": None},
+            "gpu_launches": args.steps, "clocks": clk}
+
+
 def run_train_bench(args, rank, world, local_rank):
     import torch
     from paper_2509_24957_b200.probe import fill_windows
@@ -668,7 +722,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3tc", "c4", "c5"])
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
@@ -693,6 +747,8 @@ def main():
         out = run_fork_bench(args, rank, world, local_rank)
     elif args.config == "c5":
         out = run_train_bench(args, rank, world, local_rank)
+    elif args.config == "c3tc":
+        out = run_tc_bench(args, rank, world, local_rank)
     else:
         out = run_gpu(args, cfg, rank, world, local_rank)
     if rank == 0:
