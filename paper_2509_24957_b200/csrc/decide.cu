@@ -852,6 +852,7 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   SlotCache& c = cache[threadIdx.x >> 5];
+  pdl_wait();   // probabilities from the scorer launched just before
   decide_prologue(s);
   bool had_round = false;
   if (r < s.n_slots) {
@@ -1233,10 +1234,18 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   DuchessPolicy pol = *policy;
   DuchessWorkload w = *workload;
   DuchessState st = *state;
-  void* args[] = {&pol, &w, &st, &probs};
-  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(round_kernel), dim3(grid),
-                                                    dim3(32 * kWarpsPerBlock), args, 0,
-                                                    static_cast<cudaStream_t>(stream));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * kWarpsPerBlock);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, round_kernel, pol, w, st, probs);
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 

@@ -303,7 +303,6 @@ __global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, T
   __shared__ uint64_t full_bar[32], empty_bar[32];
   __shared__ float2 red[2][kTmaConsWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
   const int stage_bytes = t.tokens_per_stage * t.row_bytes;
   if (threadIdx.x == 0) {
     for (int s = 0; s < t.stages; ++s) {
@@ -313,6 +312,8 @@ __global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, T
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();   // setup above overlaps the previous kernel; inputs are read below
+  const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
 
   if (warp == kTmaConsWarps) {   // ---- producer ----
     if (lane == 0) {
@@ -429,7 +430,17 @@ static cudaError_t launch_tma(const ScoreArgs& a, const TmaArgs& t, int vpt, int
   const size_t smem = size_t(t.stages) * t.tokens_per_stage * t.row_bytes;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, kTmaCons + 32, smem, s>>>(a, t);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTmaCons + 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, t);
   };
   switch (vpt) {
     case 1: go(score_tma_kernel<BF16, 1>); break;
