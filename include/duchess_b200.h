@@ -196,7 +196,7 @@ typedef struct DuchessState {
   int32_t* out_error;
   int32_t* out_tally;  /* [P*A] */
   long long* counters; /* [DUCHESS_N_COUNTERS] */
-  long long* trace;    /* [R*8] optional per-slot decide phase timestamps (ns), or NULL */
+  long long* trace;    /* [R*16] optional per-slot phase timestamps (ns), or NULL */
 } DuchessState;
 
 /* ---- K1: pooled LayerNorm + linear-probe scoring ------------------------ */

@@ -379,7 +379,7 @@ __device__ __forceinline__ void trace_mark(const DuchessState& s, int r, int k, 
   if (s.trace && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    s.trace[int64_t(r) * 8 + k] = (long long)t;
+    s.trace[int64_t(r) * 16 + k] = (long long)t;
   }
 }
 
@@ -777,7 +777,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
   const bool done = reason != DUCHESS_REASON_NONE;
   trace_mark(s, r, 5, lane);
-  if (s.trace && lane == 0) { s.trace[int64_t(r) * 8 + 6] = n_forks; s.trace[int64_t(r) * 8 + 7] = n_term; }
+  if (s.trace && lane == 0) { s.trace[int64_t(r) * 16 + 6] = n_forks; s.trace[int64_t(r) * 16 + 7] = n_term; }
   if (done) {
     for (int a = lane; a < s.answer_cap; a += 32)
       s.out_tally[int64_t(p) * s.answer_cap + a] = __ldcg(&s.tally[rA + a]);
@@ -853,6 +853,7 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   SlotCache& c = cache[threadIdx.x >> 5];
   pdl_wait();   // probabilities from the scorer launched just before
+  if (r < s.n_slots) trace_mark(s, r, 12, lane);
   decide_prologue(s);
   bool had_round = false;
   if (r < s.n_slots) {
@@ -860,12 +861,16 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
     if (had_round) decide_slot(pol, w, s, r, c, lane, probs);
     else if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
   }
+  if (r < s.n_slots) trace_mark(s, r, 8, lane);
   __threadfence();
   cg::this_grid().sync();
   if (r < s.n_slots) {
+    trace_mark(s, r, 9, lane);
     clear_round_inputs(pol, s, r, lane);
     const int p = slot_prologue(pol, w, s, r, c, lane, had_round);
+    trace_mark(s, r, 10, lane);
     if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane);
+    trace_mark(s, r, 11, lane);
   }
 }
 

@@ -227,7 +227,7 @@ class BatchedDuchess:
     # ------------------------------------------------------------------
     def enable_trace(self) -> torch.Tensor:
         """Per-slot decide phase timestamps (globaltimer ns) for profiling."""
-        self.t["trace"] = torch.zeros(self.R * 8, dtype=torch.int64, device=self.device)
+        self.t["trace"] = torch.zeros(self.R * 16, dtype=torch.int64, device=self.device)
         self.state.trace = self.t["trace"].data_ptr()
         return self.t["trace"]
 
