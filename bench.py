@@ -196,7 +196,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     def one_step(i, timed):
         # round k: K1 scores the survivors flagged by the previous launch, then
-        # duchess_round decides round k and advances every slot into round k+1
+        # duchess_round decides round k and advances every slot into round k+1.
+        # K1 is bracketed by CUDA events on every `k1_every`-th timed step: an
+        # event record between two PDL-chained kernels breaks their overlap, so
+        # sampling keeps the measurement from inflating the step time.
+        timed = timed and (i % args.k1_every == 0)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -231,7 +235,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ms = ev0.elapsed_time(ev1)
     cnt = (eng.t["counters"] - c0).cpu().numpy()
     branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
-    k1_ms = sum(a.elapsed_time(b) for a, b in k1_ev)
+    k1_ms = sum(a.elapsed_time(b) for a, b in k1_ev) / max(len(k1_ev), 1) * args.steps
     stats = torch.tensor([ms, float(branch_steps), k1_ms], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = stats[:1].clone()
@@ -272,6 +276,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                      "kernel": f"duchess_score (K1, {args.k1})", "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_share_of_step": k1_ms / ms,
+                     "k1_launches_timed": len(k1_ev),
                      "traffic": (None if k1_traffic_ratio()[0] is None
                                  else k1_traffic_ratio()[0] * bytes_per_launch),
                      "traffic_source": k1_traffic_ratio()[1]},
@@ -726,6 +731,8 @@ def main():
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
+    ap.add_argument("--k1-every", type=int, default=4,
+                    help="bracket K1 with CUDA events on every N-th timed step")
     ap.add_argument("--nsplit", type=int, default=2)
     ap.add_argument("--threads", type=int, default=128)
     ap.add_argument("--e2e-steps", type=int, default=10)

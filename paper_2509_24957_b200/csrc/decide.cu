@@ -645,23 +645,25 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
     mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
-    // The reference's normaliser is CPython's compensated sum() (:184); every
-    // lane replays it over the raws in creation order.
-    NeumaierSum sum;
-    for (int q = 0; q < n_alive; ++q) sum.add(c.raw[q]);
+    // The reference's normaliser is CPython's compensated sum() (:184). The fast
+    // path only needs it to within a few ulp (the margin below absorbs that), so
+    // it tracks a plain running sum; the exact compensated sum is replayed from
+    // the raws (creation order) only on the rare fallback.
+    double run_sum = 0.0;
+    for (int q = 0; q < n_alive; ++q) run_sum = __dadd_rn(run_sum, c.raw[q]);
     // Tree-order prefix sums of the raws, extended by one entry per fork.
     double P0 = warp_incl_scan(rw0, lane);
     double P1 = warp_incl_scan(rw1, lane) + __shfl_sync(0xffffffffu, P0, 31);
     int n = n_alive, amb = 0;
     for (int k = 0; k < n_forks; ++k) {
-      const double total = sum.result();
       const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
       // The reference picks the first j with u < acc_j, acc_j the sequential
-      // sum of fl(raw_i / total). acc_j and P_j / total differ by less than
-      // (2n + 9) ulp, so away from that margin the decision is read off the
-      // prefixes; otherwise lane 0 replays the exact sequential walk.
-      const double thr = __dmul_rn(u, total);
-      const double margin = 4.0 * double(n + 9) * 1.1102230246251565e-16 * total;
+      // sum of fl(raw_i / total_c). acc_j, P_j / total and the running sum
+      // differ by less than (3n + 10) ulp of the total, so away from a
+      // 4 (2n + 9) ulp margin the pick is read off the prefixes; otherwise
+      // lane 0 replays the exact sequential walk with the compensated total.
+      const double thr = __dmul_rn(u, run_sum);
+      const double margin = 4.0 * double(2 * n + 9) * 1.1102230246251565e-16 * run_sum;
       const bool v0 = lane < n, v1 = lane + 32 < n;
       const bool near = (v0 && fabs(thr - P0) <= margin) || (v1 && fabs(thr - P1) <= margin);
       int idx;
@@ -670,6 +672,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         const unsigned b1 = __ballot_sync(0xffffffffu, v1 && thr < P1);
         idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
       } else {
+        NeumaierSum sum;
+        for (int q = 0; q < n; ++q) sum.add(c.raw[q]);
+        const double total = sum.result();
         if (v0) c.wts[lane] = __ddiv_rn(rw0, total);
         if (v1) c.wts[lane + 32] = __ddiv_rn(rw1, total);
         __syncwarp();
@@ -706,9 +711,11 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         c.lp[child_slot] = src_lp;                         // inherits last_prediction (:264)
         c.src_idx[k] = src_slot;
         c.alive_root[k] = src_root;
+        c.raw[n] = src_raw;
       }
-      sum.add(src_raw);
+      run_sum = __dadd_rn(run_sum, src_raw);
       ++n;
+      __syncwarp();
     }
     if (lane == 0) {
       if (amb) add_counter(&s.counters[DUCHESS_CNT_AMBIGUOUS], (long long)(amb));
