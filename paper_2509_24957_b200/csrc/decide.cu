@@ -153,6 +153,38 @@ __device__ __forceinline__ int probe_answer_fast(const DuchessWorkload& w, int t
   return ans >= L ? w.probe_ans[ans] : 0;
 }
 
+// probe_answer_fast with the template's (conv, probe CSR bounds, final)
+// already in registers: only the search levels touch memory.
+__device__ __forceinline__ int probe_answer_pref(const DuchessWorkload& w, int conv, int L, int H,
+                                                 int fin, int pos) {
+  if (conv >= 0 && pos >= conv) return fin;
+  int lo = L, hi = H;
+  while (hi - lo > 8) {
+    const int span = hi - lo;
+    int idx[8], at[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) idx[q] = lo + (span * (q + 1)) / 9;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) at[q] = w.probe_at[idx[q]];
+    int nlo = lo, nhi = hi;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (at[q] <= pos) nlo = idx[q] + 1;
+      else nhi = min(nhi, idx[q]);
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+  int at8[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) at8[q] = (lo + q < hi) ? w.probe_at[lo + q] : 0x7fffffff;
+  int k = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) k += at8[q] <= pos;
+  const int ans = lo + k - 1;
+  return ans >= L ? w.probe_ans[ans] : 0;
+}
+
 // trace_prediction (workload.py:97-106).
 __device__ __forceinline__ double trace_prediction(const DuchessWorkload& w, int t, int pos) {
   const int lo = w.pred_off[t], hi = w.pred_off[t + 1];
@@ -236,6 +268,7 @@ struct SlotCache {
   double raw[kMaxC];
   double wts[kMaxC];
   double draws[kMaxC];
+  int tally_delta[64];   // this round's terminations, per answer id (answer_cap <= 64)
   uint32_t words[2 * kMaxC];
   uint32_t mt[kMtN + 1];
 };
@@ -510,21 +543,81 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const int64_t rA = int64_t(r) * s.answer_cap;
   int32_t* rec = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
   const int32_t* p1 = s.p1_rec + int64_t(r) * kP1Words;
-  if (lane < DUCHESS_REC_WORDS)
-    rec[lane] = lane < DUCHESS_REC_NACTIONS ? p1[lane] : (lane == DUCHESS_REC_REQ ? p1[5] : 0);
-  __syncwarp();
-  const int p = p1[5];
-  const int t0 = w.tmpl_off[p];
-  const int n_tmpl = w.tmpl_off[p + 1] - t0;
-  const int nb = s.n_branches[r];
-  const int next_t = s.next_template[r];
   uint32_t* mt_g = s.mt + int64_t(r) * DUCHESS_MT_WORDS;
   int32_t* act = s.actions + int64_t(r) * 2 * C * 3;
+  const bool dev_probs = pol.pred_source != DUCHESS_PRED_TRACE;
+  const bool small_tally = s.answer_cap <= 64;
   trace_mark(s, r, 0, lane);
-  int mt_idx = int(mt_g[kMtN]);                       // prefetched: stream position
+  // ---- wave 1: everything addressed by the slot alone, issued together ----
+  const int p1v = lane < 6 ? p1[lane] : 0;
+  const int sb0 = lane < C ? s.slot_branch[rC + lane] : -1;
+  const int sb1 = lane + 32 < C ? s.slot_branch[rC + lane + 32] : -1;
+  double pr0 = 0.0, pr1 = 0.0;
+  if (dev_probs) {
+    if (lane < C) pr0 = probs[(rC + lane) * pol.n_layers];
+    if (lane + 32 < C) pr1 = probs[(rC + lane + 32) * pol.n_layers];
+  }
+  int tl0 = 0, tl1 = 0;
+  if (small_tally) {
+    if (lane < s.answer_cap) tl0 = s.tally[rA + lane];
+    if (lane + 32 < s.answer_cap) tl1 = s.tally[rA + lane + 32];
+  }
+  int mt_idx = int(mt_g[kMtN]);
+  const int nb = s.n_branches[r];
+  const int next_t = s.next_template[r];
+  const int p = __shfl_sync(0xffffffffu, p1v, 5);
+  if (lane < DUCHESS_REC_WORDS) {
+    const int v = __shfl_sync(0x00000fffu, p1v, lane < DUCHESS_REC_NACTIONS ? lane : 5);
+    rec[lane] = lane < DUCHESS_REC_NACTIONS ? v : (lane == DUCHESS_REC_REQ ? v : 0);
+  }
+  if (lane < 64) c.tally_delta[lane] = 0;
+  c.tally_delta[lane + 32 < 64 ? lane + 32 : 63] = 0;
+  // ---- wave 2: template base + branch fields ----
+  const int t0 = w.tmpl_off[p];
+  const int n_tmpl = w.tmpl_off[p + 1] - t0;
+  c.bid[lane] = -1;
+  if (lane + 32 < kMaxC) c.bid[lane + 32] = -1;
+  {
+    const int sbs[2] = {sb0, sb1};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      const int b = sbs[q];
+      if (j < C) c.bid[j] = b;
+      if (b >= 0) {
+        const int64_t bi = rB + b;
+        c.off[j] = s.br_offset[bi];
+        c.dec[j] = s.br_decoded[bi];
+        c.streak[j] = s.br_streak[bi];
+        c.status[j] = s.br_status[bi];
+        c.npred[j] = s.br_npred[bi];
+        c.lp[j] = s.br_last_pred[bi];
+      }
+    }
+  }
+  // ---- wave 3: per-survivor template headers (speculative: used only if the
+  // branch terminates), child template lengths, MT words a round can consume ----
+  int hconv[2], hlo[2], hhi[2], hfin[2];
+  {
+    const int sbs[2] = {sb0, sb1};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      hconv[q] = -1; hlo[q] = 0; hhi[q] = 0; hfin[q] = 0;
+      if (sbs[q] >= 0) {
+        const int t = t0 + sbs[q];
+        hconv[q] = w.conv[t];
+        hlo[q] = w.probe_off[t];
+        hhi[q] = w.probe_off[t + 1];
+        hfin[q] = w.final_ans[t];
+      }
+    }
+  }
   for (int k = lane; k < C && next_t + k < n_tmpl; k += 32)
     c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
-  load_slot(s, rC, rB, C, c, lane);
+  const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
+  if (words_ready)
+    for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(mt_g[mt_idx + k]);
+  __syncwarp();
   const int n_surv = order_slots(c, C, lane);
   trace_mark(s, r, 1, lane);
 
@@ -550,8 +643,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   const double tau = pol.early_term_threshold;
   int n_term = 0;
-  for (int base = 0; base < C; base += 32) {
-    const int j = base + lane;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
     const int b = j < C ? c.bid[j] : -1;
     bool term = false;
     if (b >= 0) {
@@ -564,15 +658,16 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
           pr = trace_prediction(w, t, pos);
         } else {
           int k = 0;                                     // rank among draw-needing survivors
-          for (int q = 0; q < C; ++q) k += (c.bid[q] >= 0 && c.bid[q] < b && c.need[q]);
+          for (int qq = 0; qq < C; ++qq) k += (c.bid[qq] >= 0 && c.bid[qq] < b && c.need[qq]);
           const double u = c.draws[k];
           // synthetic_predict (predictor.py:328-335) on probe_answer == ground truth
-          const double oracle = probe_answer_fast(w, t, pos) == w.ground_truth[p] ? 1.0 : 0.0;
+          const int pa = probe_answer_pref(w, hconv[q], hlo[q], hhi[q], hfin[q], pos);
+          const double oracle = pa == w.ground_truth[p] ? 1.0 : 0.0;
           const double v = __dadd_rn(__dmul_rn(pol.rho, oracle), __dmul_rn(__dsub_rn(1.0, pol.rho), u));
           pr = fmin(fmax(v, 0.0), 1.0);
         }
       } else if (pol.pred_source == DUCHESS_PRED_HOST || pol.n_layers == 1 || pol.combine == 0) {
-        pr = probs[(rC + j) * pol.n_layers];
+        pr = q == 0 ? pr0 : pr1;
       } else {
         double acc = 0.0;
         for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, probs[(rC + j) * pol.n_layers + l]);
@@ -593,12 +688,13 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       act[k * 3 + 1] = b;
       act[k * 3 + 2] = -1;
       if (term) {
-        const int ans = probe_answer_fast(w, t, pos);
+        const int ans = probe_answer_pref(w, hconv[q], hlo[q], hhi[q], hfin[q], pos);
         c.status[j] = DUCHESS_EARLY_TERMINATED;
         s.br_status[bi] = DUCHESS_EARLY_TERMINATED;
         s.br_final[bi] = ans;
         s.br_slot[bi] = -1;
         atomicAdd(&s.tally[rA + ans], 1);
+        if (small_tally) atomicAdd(&c.tally_delta[ans], 1);
       }
     }
     n_term += __popc(__ballot_sync(0xffffffffu, term));
@@ -644,7 +740,12 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   __syncwarp();
   trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
-    mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
+    if (words_ready) {                                 // words prefetched in wave 3
+      if (lane == 0) mt_g[kMtN] = uint32_t(mt_idx + 2 * n_forks);
+      mt_idx += 2 * n_forks;
+    } else {
+      mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
+    }
     // The reference's normaliser is CPython's compensated sum() (:184). The fast
     // path only needs it to within a few ulp (the margin below absorbs that), so
     // it tracks a plain running sum; the exact compensated sum is replayed from
@@ -753,10 +854,19 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   trace_mark(s, r, 4, lane);
   // ---- phase 5: request termination (:390-399) ----
   int max_count = 0, total = 0, best = 0x7fffffff;
-  for (int a = lane; a < s.answer_cap; a += 32) {
-    const int cnt = __ldcg(&s.tally[rA + a]);
-    total += cnt;
-    if (cnt > max_count) { max_count = cnt; best = a; }
+  int cnt0 = 0, cnt1 = 0;
+  if (small_tally) {                 // tally prefetched in wave 1 + this round's terminations
+    if (lane < s.answer_cap) cnt0 = tl0 + c.tally_delta[lane];
+    if (lane + 32 < s.answer_cap) cnt1 = tl1 + c.tally_delta[lane + 32];
+    total = cnt0 + cnt1;
+    if (cnt0 > 0) { max_count = cnt0; best = lane; }
+    if (cnt1 > max_count) { max_count = cnt1; best = lane + 32; }
+  } else {
+    for (int a = lane; a < s.answer_cap; a += 32) {
+      const int cnt = __ldcg(&s.tally[rA + a]);
+      total += cnt;
+      if (cnt > max_count) { max_count = cnt; best = a; }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -786,8 +896,13 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   trace_mark(s, r, 5, lane);
   if (s.trace && lane == 0) { s.trace[int64_t(r) * 16 + 6] = n_forks; s.trace[int64_t(r) * 16 + 7] = n_term; }
   if (done) {
-    for (int a = lane; a < s.answer_cap; a += 32)
-      s.out_tally[int64_t(p) * s.answer_cap + a] = __ldcg(&s.tally[rA + a]);
+    if (small_tally) {
+      if (lane < s.answer_cap) s.out_tally[int64_t(p) * s.answer_cap + lane] = cnt0;
+      if (lane + 32 < s.answer_cap) s.out_tally[int64_t(p) * s.answer_cap + lane + 32] = cnt1;
+    } else {
+      for (int a = lane; a < s.answer_cap; a += 32)
+        s.out_tally[int64_t(p) * s.answer_cap + a] = __ldcg(&s.tally[rA + a]);
+    }
   }
   if (lane == 0) {
     s.tokens_probe[r] += n_term * pol.probe_cost_tokens;
