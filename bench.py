@@ -194,16 +194,27 @@ def run_gpu(args, cfg, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     k1_ev = []
 
+    fused = args.mode == "fused"
+
     def one_step(i, timed):
-        # round k: K1 scores the survivors flagged by the previous launch, then
-        # duchess_round decides round k and advances every slot into round k+1.
-        # K1 is bracketed by CUDA events on every `k1_every`-th timed step: an
-        # event record between two PDL-chained kernels breaks their overlap, so
-        # sampling keeps the measurement from inflating the step time.
+        # fused (default): ONE persistent launch per round (duchess_step) —
+        # K1 streams the survivors' windows while a decision warp per CTA
+        # decides every request whose windows are scored and advances it into
+        # the next round. split: K1 launch, then duchess_round (decide k +
+        # advance k+1). The scoring kernel is bracketed by CUDA events on every
+        # `k1_every`-th timed step: an event record between two PDL-chained
+        # kernels breaks their overlap, so sampling keeps the measurement from
+        # inflating the step time.
         timed = timed and (i % args.k1_every == 0)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
+        if fused:
+            eng.step_fused(slabs[i % n_slabs], bank, logit.view(-1))
+            if timed:
+                e1.record(stream)
+                k1_ev.append((e0, e1))
+            return
         if args.k1 == "list":
             scorer.score_list(slabs[i % n_slabs], logit, probs, eng.t["active_rows"],
                               eng.t["active_count"])
@@ -214,7 +225,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             k1_ev.append((e0, e1))
         eng.round()
 
-    eng.advance()                      # round 0: refill every slot + phase 1
+    if fused:
+        eng.begin_fused()              # round 0: refill every slot + phase 1
+    else:
+        eng.advance()
     for i in range(args.warmup):
         one_step(i, False)
     torch.cuda.synchronize(dev)
@@ -247,7 +261,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         ms_all, bs_all = ms, float(branch_steps)
 
     # ---- end to end through the public API with host buffers ----
-    e2e = run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world)
+    e2e = run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank)
 
     if rank != 0:
         return None
@@ -273,7 +287,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "branch_steps_per_step": branch_steps / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
-                     "kernel": f"duchess_score (K1, {args.k1})", "bytes_per_launch": bytes_per_launch,
+                     "kernel": ("duchess_step (fused K1 scoring + decide + advance, one "
+                                "launch per round)" if fused else f"duchess_score (K1, {args.k1})"),
+                     "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_share_of_step": k1_ms / ms,
                      "k1_launches_timed": len(k1_ev),
@@ -281,7 +297,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                  else k1_traffic_ratio()[0] * bytes_per_launch),
                      "traffic_source": k1_traffic_ratio()[1]},
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": clk,
         "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
                      "finished_requests": int(cnt[_lib.CNT_FINISHED]),
@@ -290,10 +306,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     return out
 
 
-def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world):
+def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank=None):
     """Same step through the public API with the activations in pinned HOST
-    memory: per step H2D of the activation window slab, the three kernels,
-    and a D2H read of the round records (RoundReports)."""
+    memory: per step H2D of the activation window slab, the round (one fused
+    launch, or advance / K1 / decide when split), and a D2H read of the round
+    records and actions (RoundReports)."""
     import torch
     steps = max(2, min(args.e2e_steps, args.steps))
     host = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
@@ -306,6 +323,12 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world):
 
     def step():
         dslab.copy_(host, non_blocking=True)
+        if args.mode == "fused":
+            eng.step_fused(dslab, bank, logit.view(-1))
+            rec_host.copy_(eng.t["round_rec"], non_blocking=True)
+            act_host.copy_(eng.t["actions"], non_blocking=True)
+            stream.synchronize()
+            return
         eng.advance()
         scorer.score_list(dslab, logit, probs, eng.t["active_rows"], eng.t["active_count"]) \
             if args.k1 == "list" else scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
@@ -731,6 +754,9 @@ def main():
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
+    ap.add_argument("--mode", default="fused", choices=["fused", "split"],
+                    help="fused: one duchess_step launch per round (default); split: K1 "
+                         "launch + duchess_round launch")
     ap.add_argument("--k1-every", type=int, default=4,
                     help="bracket K1 with CUDA events on every N-th timed step")
     ap.add_argument("--nsplit", type=int, default=2)

@@ -79,6 +79,15 @@ class State(C.Structure):
         (name, C.c_void_p) for name in STATE_PTR_FIELDS]
 
 
+class StepCtl(C.Structure):
+    _fields_ = [("rows", C.c_void_p), ("ready", C.c_void_p), ("pending", C.c_void_p),
+                ("idle", C.c_void_p), ("ctl", C.c_void_p)]
+
+
+STEP_CTL_WORDS = 16
+STEP_CTL_TAG, STEP_CTL_POP, STEP_CTL_COUNT = 0, 2, 4
+
+
 SYMBOLS = {
     # name: (restype, argtypes)
     "duchess_score_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
@@ -100,6 +109,12 @@ SYMBOLS = {
                                  C.c_void_p, C.c_void_p]),
     "duchess_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                 C.c_void_p, C.c_void_p]),
+    "duchess_step_begin": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
+                                     C.POINTER(StepCtl), C.c_void_p]),
+    "duchess_step": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
+                               C.POINTER(StepCtl), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                               C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p, C.c_void_p]),
     "duchess_baseline_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload),
                                          C.POINTER(State), C.c_void_p]),
     "duchess_branch_out_sample": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,

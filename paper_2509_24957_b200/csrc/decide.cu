@@ -16,8 +16,10 @@
 // genrand_res53; the branch-out normaliser replays CPython >= 3.12's
 // compensated (Neumaier) builtin sum().
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
+#include "score_core.cuh"
 #include "../../include/duchess_b200.h"
 
 namespace cg = cooperative_groups;
@@ -456,8 +458,32 @@ __device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
   return p;
 }
 
+// Fused-step bookkeeping for phase 1 (duchess_step): survivors go to the
+// next round's list, the slot's pending-window count is armed, and a slot
+// with no survivor is ready for its decision at once.
+struct Phase1Out {
+  int32_t* rows;
+  int32_t* count;
+  int32_t* live;
+  int32_t* tail;
+  int64_t* ready;
+  int32_t* pending;
+  int tag;
+};
+
+__device__ __forceinline__ void publish_ready(int32_t* tail, int64_t* ready, int tag, int r) {
+  __threadfence();
+  const int t = atomicAdd(tail, 1);
+  atomicExch(reinterpret_cast<unsigned long long*>(ready + t),
+             (static_cast<unsigned long long>(uint32_t(tag)) << 32) | uint32_t(r));
+}
+
 __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
-                            const DuchessState& s, int r, int p, SlotCache& c, int lane) {
+                            const DuchessState& s, int r, int p, SlotCache& c, int lane,
+                            const Phase1Out* fo = nullptr) {
+  int32_t* list_rows = fo ? fo->rows : s.active_rows;
+  int32_t* list_count = fo ? fo->count : s.active_count;
+  int n_listed = 0;
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   int32_t* p1 = s.p1_rec + int64_t(r) * kP1Words;
@@ -498,12 +524,18 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
     // compacted list of windows for the persistent scorer (order irrelevant)
     const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (m && s.active_rows) {
+    n_listed += __popc(m);
+    if (m && list_rows) {
       int basei = 0;
-      if (lane == 0) basei = atomicAdd(s.active_count, __popc(m));
+      if (lane == 0) basei = atomicAdd(list_count, __popc(m));
       basei = __shfl_sync(0xffffffffu, basei, 0);
-      if (surv) s.active_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
+      if (surv) list_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
     }
+  }
+  if (fo && lane == 0) {
+    fo->pending[r] = n_listed * pol.n_layers;
+    atomicAdd(fo->live, 1);
+    if (n_listed == 0) publish_ready(fo->tail, fo->ready, fo->tag, r);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -554,8 +586,8 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const int sb1 = lane + 32 < C ? s.slot_branch[rC + lane + 32] : -1;
   double pr0 = 0.0, pr1 = 0.0;
   if (dev_probs) {
-    if (lane < C) pr0 = probs[(rC + lane) * pol.n_layers];
-    if (lane + 32 < C) pr1 = probs[(rC + lane + 32) * pol.n_layers];
+    if (lane < C) pr0 = __ldcg(probs + (rC + lane) * pol.n_layers);
+    if (lane + 32 < C) pr1 = __ldcg(probs + (rC + lane + 32) * pol.n_layers);
   }
   int tl0 = 0, tl1 = 0;
   if (small_tally) {
@@ -670,7 +702,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         pr = q == 0 ? pr0 : pr1;
       } else {
         double acc = 0.0;
-        for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, probs[(rC + j) * pol.n_layers + l]);
+        for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, __ldcg(probs + (rC + j) * pol.n_layers + l));
         pr = __ddiv_rn(acc, double(pol.n_layers));
       }
       const int streak = pr > tau ? c.streak[j] + 1 : 0;   // strict > (:363)
@@ -993,6 +1025,173 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
     trace_mark(s, r, 10, lane);
     if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane);
     trace_mark(s, r, 11, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused round (duchess_step): K1 scoring + decide + advance in one launch.
+//
+// ctl words: tag (index of the next step launch), exit counter, queue pops,
+// then per round parity: listed survivor rows, live slots, ready-queue tail,
+// ready-queue claims. Launch `tag` consumes parity tag & 1 (built by the
+// previous launch or duchess_step_begin) and builds parity (tag + 1) & 1; its
+// last CTA resets the consumed parity and bumps the tag.
+enum : int {
+  kCtlTag = DUCHESS_STEP_CTL_TAG, kCtlExit = 1, kCtlPop = DUCHESS_STEP_CTL_POP,
+  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlLive = 6, kCtlTail = 8, kCtlClaim = 10
+};
+
+__device__ __forceinline__ long long ld_acquire_s64(const int64_t* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ Phase1Out phase1_out(const DuchessStepCtl& x, int R, int C, int par,
+                                                int tag) {
+  Phase1Out o;
+  o.rows = x.rows + int64_t(par) * R * C;
+  o.count = x.ctl + kCtlCount + par;
+  o.live = x.ctl + kCtlLive + par;
+  o.tail = x.ctl + kCtlTail + par;
+  o.ready = x.ready + int64_t(par) * R;
+  o.pending = x.pending;
+  o.tag = tag;
+  return o;
+}
+
+// Refill-or-load prologue with the service queue popped atomically in
+// completion order (the fused step has no grid-wide barrier to rank slots).
+__device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorkload& w,
+                                   const DuchessState& s, int r, SlotCache& c, int lane,
+                                   bool cache_valid, int32_t* pop) {
+  const int C = pol.max_branches;
+  if (s.needs_refill[r]) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(pop, 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    int p = -1;
+    if (w.queue_len > 0) {
+      if (w.cycle) p = w.queue[q % w.queue_len];
+      else if (q < w.queue_len) p = w.queue[q];
+    }
+    if (p < 0) {
+      if (lane == 0) { s.slot_req[r] = -1; s.done[r] = 1; s.needs_refill[r] = 0; }
+      __syncwarp();
+      return -1;
+    }
+    refill_slot(pol, w, s, r, p, c, lane);
+    if (lane == 0) s.needs_refill[r] = 0;
+    __syncwarp();
+    return p;
+  }
+  if (s.done[r]) return -1;
+  const int p = s.slot_req[r];
+  if (p < 0) return -1;
+  if (!cache_valid) load_slot(s, int64_t(r) * C, int64_t(r) * s.branch_cap, C, c, lane);
+  return p;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+step_begin_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= s.n_slots) return;
+  SlotCache& c = cache[threadIdx.x >> 5];
+  const int tag = x.ctl[kCtlTag];
+  clear_round_inputs(pol, s, r, lane);
+  const int p = slot_prologue_fused(pol, w, s, r, c, lane, false, x.ctl + kCtlPop);
+  if (p >= 0) {
+    const Phase1Out fo = phase1_out(x, s.n_slots, pol.max_branches, tag & 1, tag);
+    phase1_slot(pol, w, s, r, p, c, lane, &fo);
+  } else if (lane == 0) {
+    x.idle[r] = 1;
+  }
+}
+
+constexpr int kStepThreads = kTmaCons + 64;   // 8 consumer warps, producer, decision warp
+
+template <bool BF16, int VPT>
+__global__ void __launch_bounds__(kStepThreads, 2)
+step_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x, ScoreArgs a,
+            TmaArgs t) {
+  constexpr int ESZ = BF16 ? 2 : 4;
+  extern __shared__ __align__(128) char ring[];
+  __shared__ uint64_t full_bar[32], empty_bar[32];
+  __shared__ float2 red[2][kTmaConsWarps];
+  __shared__ SlotCache cache;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TmaRing rg{ring, full_bar, empty_bar, t.tokens_per_stage * t.row_bytes};
+  tma_ring_init(t, rg);
+  __syncthreads();
+  pdl_wait();   // the previous round's lists, counters and state are complete
+  const int tag = x.ctl[kCtlTag];
+  const int par = tag & 1;
+  const int R = s.n_slots, C = pol.max_branches, L = pol.n_layers;
+  t.row_list = x.rows + int64_t(par) * R * C;
+  const int64_t n_units = int64_t(x.ctl[kCtlCount + par]) * L;
+  int64_t* ready = x.ready + int64_t(par) * R;
+
+  if (warp == kTmaConsWarps) {                       // ---- producer ----
+    if (lane == 0) tma_produce<ESZ>(a, t, rg, n_units);
+  } else if (warp == kTmaConsWarps + 1) {            // ---- decisions ----
+    for (int r = blockIdx.x * 32 + lane; r < R; r += gridDim.x * 32) {
+      if (x.idle[r]) {                               // slot ran no round this step
+        s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
+        x.idle[r] = 0;
+      }
+    }
+    const int live = x.ctl[kCtlLive + par];
+    const Phase1Out fo = phase1_out(x, R, C, par ^ 1, tag + 1);
+    while (true) {
+      int i = 0;
+      if (lane == 0) i = atomicAdd(x.ctl + kCtlClaim + par, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= live) break;
+      if (lane == 0) {
+        int ns = 32;
+        while ((ld_acquire_s64(ready + i) >> 32) != tag) {
+          __nanosleep(ns);
+          ns = ns < 256 ? 2 * ns : 256;
+        }
+      }
+      __syncwarp();
+      const int r = int(ld_acquire_s64(ready + i) & 0xffffffffll);   // acquire in every lane
+      trace_mark(s, r, 12, lane);
+      decide_slot(pol, w, s, r, cache, lane, a.out_prob);
+      trace_mark(s, r, 8, lane);
+      clear_round_inputs(pol, s, r, lane);
+      const int p = slot_prologue_fused(pol, w, s, r, cache, lane, true, x.ctl + kCtlPop);
+      trace_mark(s, r, 10, lane);
+      if (p >= 0) phase1_slot(pol, w, s, r, p, cache, lane, &fo);
+      else if (lane == 0) x.idle[r] = 1;
+      trace_mark(s, r, 11, lane);
+      __syncwarp();
+    }
+  } else {                                           // ---- consumers ----
+    tma_consume<BF16, VPT>(a, t, rg, n_units, red, [&](int64_t row, int, int64_t) {
+      const int r = int(row / C);
+      __threadfence();                               // this window's score before the count
+      if (atomicSub(x.pending + r, 1) == 1) publish_ready(x.ctl + kCtlTail + par, ready, tag, r);
+    });
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pdl_launch_dependents();
+    __threadfence();
+    if (atomicAdd(x.ctl + kCtlExit, 1) == int(gridDim.x) - 1) {
+      __threadfence();
+      x.ctl[kCtlCount + par] = 0;
+      x.ctl[kCtlLive + par] = 0;
+      x.ctl[kCtlTail + par] = 0;
+      x.ctl[kCtlClaim + par] = 0;
+      x.ctl[kCtlExit] = 0;
+      const int pops = x.ctl[kCtlPop];
+      s.queue_head[0] = pops;
+      s.queue_head[1] = pops;
+      x.ctl[kCtlTag] = tag + 1;
+    }
   }
 }
 
@@ -1373,6 +1572,120 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, round_kernel, pol, w, st, probs);
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+static bool step_ctl_ok(const DuchessStepCtl* x) {
+  return x && x->rows && x->ready && x->pending && x->idle && x->ctl;
+}
+
+extern "C" int duchess_step_begin(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                                  const DuchessState* state, const DuchessStepCtl* ctl,
+                                  void* stream) {
+  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl)) return DUCHESS_EINVAL;
+  if (policy->policy_kind != DUCHESS_POLICY_DUCHESS || policy->pred_source != DUCHESS_PRED_DEVICE)
+    return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  step_begin_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      *policy, *workload, *state, *ctl);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+template <bool BF16, int VPT>
+static cudaError_t launch_step(const DuchessPolicy& pol, const DuchessWorkload& w,
+                               const DuchessState& st, const DuchessStepCtl& x, const ScoreArgs& a,
+                               const TmaArgs& t, size_t smem, cudaStream_t stream) {
+  auto kern = step_kernel<BF16, VPT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Every CTA must be resident at once: decision warps wait on windows that
+  // any CTA of the grid may hold.
+  const int grid = sms * (per_sm < 2 ? per_sm : 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, pol, w, st, x, a, t);
+}
+
+extern "C" int duchess_step(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                            const DuchessState* state, const DuchessStepCtl* ctl, const void* acts,
+                            int32_t dtype, int32_t T, int32_t H, int64_t row_stride,
+                            int64_t layer_stride, int64_t token_stride, const float* wg,
+                            const float* c1, float* out_logit, double* out_prob, void* stream) {
+  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl)) return DUCHESS_EINVAL;
+  if (policy->policy_kind != DUCHESS_POLICY_DUCHESS || policy->pred_source != DUCHESS_PRED_DEVICE)
+    return DUCHESS_EINVAL;
+  if (!acts || !wg || !c1 || !out_logit || !out_prob || T < 1 || H < 1) return DUCHESS_EINVAL;
+  if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
+  if (policy->n_layers < 1) return DUCHESS_EINVAL;
+  if (state->n_slots == 0) return DUCHESS_OK;
+  const bool bf16 = dtype == DUCHESS_BF16;
+  const int esz = bf16 ? 2 : 4;
+  const int64_t row_bytes = int64_t(H) * esz;
+  // TMA bulk copies: 16-byte aligned token rows.
+  if ((reinterpret_cast<uintptr_t>(acts) % 16) || (row_bytes % 16) || ((row_stride * esz) % 16) ||
+      ((layer_stride * esz) % 16) || ((token_stride * esz) % 16) || row_bytes > 4 * kTmaStageTarget ||
+      (reinterpret_cast<uintptr_t>(wg) % 16))
+    return DUCHESS_EINVAL;
+  ScoreArgs a{};
+  a.acts = static_cast<const char*>(acts);
+  a.row_stride = row_stride;
+  a.layer_stride = layer_stride;
+  a.token_stride = token_stride;
+  a.n_units = int64_t(state->n_slots) * policy->max_branches * policy->n_layers;
+  a.L = policy->n_layers;
+  a.T = T;
+  a.H = H;
+  a.nsplit = 1;
+  a.chunk = H;
+  a.wg = wg;
+  a.c1 = c1;
+  a.out_logit = out_logit;
+  a.out_prob = out_prob;
+  TmaArgs t{};
+  t.row_bytes = int(row_bytes);
+  t.contiguous = token_stride == H;
+  t.tokens_per_stage = int(row_bytes >= kTmaStageTarget ? 1 : kTmaStageTarget / row_bytes);
+  if (t.tokens_per_stage > T) t.tokens_per_stage = T;
+  const int stage_bytes = t.tokens_per_stage * t.row_bytes;
+  // Two CTAs per SM: 2 x (ring + static shared (slot cache, barriers) + 1 KB
+  // reserved) within the 228 KB of an SM.
+  const int static_bytes = int(sizeof(SlotCache)) + 1024;
+  t.stages = (115712 - static_bytes) / stage_bytes;
+  if (t.stages > 32) t.stages = 32;
+  if (t.stages < 2) return DUCHESS_EINVAL;
+  const int nvec = int(row_bytes / 16);
+  int vpt = 1;
+  while (vpt * kTmaCons < nvec) vpt <<= 1;
+  if (vpt > 8) return DUCHESS_EINVAL;
+  const size_t smem = size_t(t.stages) * stage_bytes;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  auto go = [&](auto tag_bf16) -> cudaError_t {
+    constexpr bool B = decltype(tag_bf16)::value;
+    switch (vpt) {
+      case 1: return launch_step<B, 1>(*policy, *workload, *state, *ctl, a, t, smem, s);
+      case 2: return launch_step<B, 2>(*policy, *workload, *state, *ctl, a, t, smem, s);
+      case 4: return launch_step<B, 4>(*policy, *workload, *state, *ctl, a, t, smem, s);
+      default: return launch_step<B, 8>(*policy, *workload, *state, *ctl, a, t, smem, s);
+    }
+  };
+  e = bf16 ? go(std::true_type{}) : go(std::false_type{});
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 

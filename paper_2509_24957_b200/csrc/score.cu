@@ -19,24 +19,10 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "score_core.cuh"
 #include "../../include/duchess_b200.h"
 
 namespace duchess {
-
-struct ScoreArgs {
-  const char* acts;
-  int64_t row_stride, layer_stride, token_stride;  // elements
-  int64_t n_units;                                 // rows * L
-  int L, T, H;
-  int nsplit, chunk;                               // chunk = columns per split
-  const float* wg;
-  const float* c1;
-  const uint8_t* mask;
-  float* out_logit;
-  double* out_prob;
-  float4* partials;     // [n_units * nsplit] (mean, M2, dot, wsum)
-  unsigned* counters;   // [n_units]
-};
 
 template <int NT>
 __device__ __forceinline__ void block_sum2(float& a, float& b, float2* red) {
@@ -55,13 +41,6 @@ __device__ __forceinline__ void block_sum2(float& a, float& b, float2* red) {
   a = red[NT / 32].x;
   b = red[NT / 32].y;
   __syncthreads();
-}
-
-__device__ __forceinline__ void write_score(const ScoreArgs& a, int64_t unit, float logit) {
-  a.out_logit[unit] = logit;
-  double p = 1.0 / (1.0 + exp(-double(logit)));
-  p = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
-  a.out_prob[unit] = p;
 }
 
 // Last CTA of a split window: merge chunk partials in chunk order (double).
@@ -245,184 +224,27 @@ __global__ void __launch_bounds__(256) score_generic_kernel(ScoreArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Persistent warp-specialised variant: one CTA per SM, a producer warp streams
-// each window's token rows into a shared-memory ring with cp.async.bulk
-// (mbarrier transaction counts), 8 consumer warps pool from shared memory and
-// finish the window (two-pass LN stats + dot) while the producer already
-// streams the next one. Keeps up to ~190 KB in flight per SM regardless of
-// register pressure. Windows come from a compacted row list (written by
-// duchess_advance) or from all rows filtered by the mask.
-constexpr int kTmaConsWarps = 8;
-constexpr int kTmaCons = kTmaConsWarps * 32;
-constexpr int kTmaStageTarget = 8 * 1024;
-constexpr int kTmaSmemBudget = 196 * 1024;
-
-struct TmaArgs {
-  const int32_t* row_list;   // nullable
-  const int32_t* row_count;  // device count when row_list != nullptr
-  int tokens_per_stage;
-  int stages;
-  int row_bytes;             // H * esz
-  int contiguous;            // token_stride == H
-};
-
-__device__ __forceinline__ bool tma_unit(const ScoreArgs& a, const TmaArgs& t, int64_t u,
-                                         int64_t& row, int& l) {
-  const int64_t r = u / a.L;
-  l = int(u - r * a.L);
-  if (t.row_list) {
-    row = t.row_list[r];
-    return true;
-  }
-  row = r;
-  return a.mask == nullptr || a.mask[r] != 0;
-}
-
-__device__ __forceinline__ void cons_sum2(float& x, float& y, float2 (*red)[kTmaConsWarps], int& k) {
-  x = warp_sum(x);
-  y = warp_sum(y);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) red[k & 1][warp] = make_float2(x, y);
-  asm volatile("bar.sync 1, %0;" ::"n"(kTmaCons) : "memory");
-  float sx = 0.f, sy = 0.f;
-#pragma unroll
-  for (int w = 0; w < kTmaConsWarps; ++w) {
-    sx += red[k & 1][w].x;
-    sy += red[k & 1][w].y;
-  }
-  x = sx;
-  y = sy;
-  ++k;
-}
-
+// Persistent warp-specialised variant (score_core.cuh): one producer warp
+// streams windows into a shared-memory ring with cp.async.bulk, 8 consumer
+// warps pool + LayerNorm + dot. Windows come from a compacted row list
+// (written by duchess_advance) or from all rows filtered by the mask.
 template <bool BF16, int VPT>
 __global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, TmaArgs t) {
-  constexpr int VEC = BF16 ? 8 : 4;
   constexpr int ESZ = BF16 ? 2 : 4;
   extern __shared__ __align__(128) char ring[];
   __shared__ uint64_t full_bar[32], empty_bar[32];
   __shared__ float2 red[2][kTmaConsWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int stage_bytes = t.tokens_per_stage * t.row_bytes;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < t.stages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kTmaConsWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  TmaRing rg{ring, full_bar, empty_bar, t.tokens_per_stage * t.row_bytes};
+  tma_ring_init(t, rg);
   __syncthreads();
   pdl_wait();   // setup above overlaps the previous kernel; inputs are read below
   const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
-
-  if (warp == kTmaConsWarps) {   // ---- producer ----
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int64_t row;
-        int l;
-        if (!tma_unit(a, t, u, row, l)) continue;
-        const char* base = a.acts + (row * a.row_stride + int64_t(l) * a.layer_stride) * ESZ;
-        for (int t0 = 0; t0 < a.T; t0 += t.tokens_per_stage) {
-          const int nt = min(t.tokens_per_stage, a.T - t0);
-          mbar_wait(&empty_bar[s], ph ^ 1u);
-          mbar_expect_tx(&full_bar[s], uint32_t(nt * t.row_bytes));
-          char* dst = ring + size_t(s) * stage_bytes;
-          if (t.contiguous) {
-            bulk_g2s(dst, base + int64_t(t0) * t.row_bytes, uint32_t(nt * t.row_bytes),
-                     &full_bar[s], pol);
-          } else {
-            for (int k = 0; k < nt; ++k)
-              bulk_g2s(dst + k * t.row_bytes, base + int64_t(t0 + k) * a.token_stride * ESZ,
-                       uint32_t(t.row_bytes), &full_bar[s], pol);
-          }
-          if (++s == t.stages) { s = 0; ph ^= 1u; }
-        }
-      }
-    }
+  if (warp == kTmaConsWarps) {
+    if (lane == 0) tma_produce<ESZ>(a, t, rg, n_units);
     return;
   }
-
-  // ---- consumers ----
-  const int nvec = t.row_bytes / 16;
-  int s = 0, k = 0;
-  uint32_t ph = 0;
-  const float invT = 1.0f / float(a.T);
-  const bool pow2T = (a.T & (a.T - 1)) == 0;
-  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-    int64_t row;
-    int l;
-    if (!tma_unit(a, t, u, row, l)) continue;
-    float acc[VPT][VEC];
-#pragma unroll
-    for (int j = 0; j < VPT; ++j)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[j][v] = 0.f;
-    for (int t0 = 0; t0 < a.T; t0 += t.tokens_per_stage) {
-      const int nt = min(t.tokens_per_stage, a.T - t0);
-      mbar_wait(&full_bar[s], ph);
-      const char* st = ring + size_t(s) * stage_bytes;
-      for (int q = 0; q < nt; ++q) {
-        const uint4* rowv = reinterpret_cast<const uint4*>(st + q * t.row_bytes);
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-          const int v = j * kTmaCons + int(threadIdx.x);
-          if (v < nvec) {
-            const uint4 x = rowv[v];
-            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-            if constexpr (BF16) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                acc[j][2 * e] += bf16lo(w4[e]);
-                acc[j][2 * e + 1] += bf16hi(w4[e]);
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) acc[j][e] += __uint_as_float(w4[e]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-      if (++s == t.stages) { s = 0; ph ^= 1u; }
-    }
-    const float* wrow = a.wg + int64_t(l) * a.H;
-    float wgv[VPT][VEC];
-    float s1 = 0.f, sw = 0.f;
-#pragma unroll
-    for (int j = 0; j < VPT; ++j) {
-      const int v = j * kTmaCons + int(threadIdx.x);
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const bool ok = v < nvec;
-        acc[j][e] = pow2T ? acc[j][e] * invT : acc[j][e] / float(a.T);
-        wgv[j][e] = ok ? __ldg(wrow + v * VEC + e) : 0.f;
-        if (ok) { s1 += acc[j][e]; sw += wgv[j][e]; }
-      }
-    }
-    cons_sum2(s1, sw, red, k);
-    const float mean = s1 / float(a.H);
-    float qq = 0.f, d = 0.f;
-#pragma unroll
-    for (int j = 0; j < VPT; ++j) {
-      if (j * kTmaCons + int(threadIdx.x) < nvec) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const float c = acc[j][e] - mean;
-          qq += c * c;
-          d += wgv[j][e] * c;
-        }
-      }
-    }
-    cons_sum2(qq, d, red, k);
-    if (threadIdx.x == 0) {
-      const float var = qq / float(a.H);
-      write_score(a, row * a.L + l, d / sqrtf(var + kLayerNormEps) + a.c1[l]);
-    }
-  }
+  tma_consume<BF16, VPT>(a, t, rg, n_units, red, [](int64_t, int, int64_t) {});
 }
 
 template <bool BF16>

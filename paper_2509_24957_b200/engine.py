@@ -253,6 +253,62 @@ class BatchedDuchess:
                                           p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_round")
 
+    # ------------------------------------------------------------------
+    # Fused round: K1 scoring + decide + advance in one persistent launch.
+    def begin_fused(self, stream=None) -> None:
+        """Allocate the fused-round lists / ready queues and run refill +
+        phase 1 of the first round (duchess_step_begin). Only for
+        pred_source == PRED_DEVICE; call once, then step_fused() per round."""
+        if self.policy.pred_source != _lib.PRED_DEVICE or self.policy_name != "duchess":
+            raise ValueError("the fused round needs the DUCHESS policy with device probabilities")
+        R, C, dev = self.R, self.C, self.device
+        x = {"rows": torch.zeros(2 * R * C, dtype=torch.int32, device=dev),
+             "ready": torch.full((2 * max(R, 1),), -1, dtype=torch.int64, device=dev),
+             "pending": torch.zeros(max(R, 1), dtype=torch.int32, device=dev),
+             "idle": torch.zeros(max(R, 1), dtype=torch.int32, device=dev),
+             "ctl": torch.zeros(_lib.STEP_CTL_WORDS, dtype=torch.int32, device=dev)}
+        sc = _lib.StepCtl()
+        for k, v in x.items():
+            setattr(sc, k, v.data_ptr())
+        self.fx, self.step_ctl = x, sc
+        _lib.check(self.lib.duchess_step_begin(self.policy, self.wl.struct, self.state, sc,
+                                               _lib.stream_handle(stream)), "duchess_step_begin")
+
+    def step_fused(self, acts: torch.Tensor, bank, out_logit: torch.Tensor, stream=None) -> None:
+        """One fused round (duchess_step). acts: [R*C, L, T, H] bf16/fp32
+        activation windows by branch slot (row r*C + slot); bank: ProbeBank
+        with L probes of width H; out_logit: [R*C*L] fp32. Probabilities land
+        in self.probs; round_reports() then describe the round just decided."""
+        if not hasattr(self, "step_ctl"):
+            raise RuntimeError("call begin_fused() first")
+        _lib.require_cuda(acts)
+        if acts.dim() != 4 or acts.shape[0] != self.R * self.C:
+            raise ValueError("acts must be [R*C, L, T, H]")
+        rows, L, T, H = acts.shape
+        if L != self.policy.n_layers or L != bank.L or H != bank.H:
+            raise ValueError(f"activation shape (L={L}, H={H}) does not match the probe bank "
+                             f"(L={bank.L}, H={bank.H}) / engine layers ({self.policy.n_layers})")
+        if acts.stride(3) != 1:
+            raise ValueError("hidden dimension must be contiguous")
+        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}.get(acts.dtype)
+        if dtype is None:
+            raise ValueError("activations must be bf16 or fp32")
+        if out_logit.numel() < rows * L or out_logit.dtype != torch.float32:
+            raise ValueError("out_logit must be fp32 with R*C*L entries")
+        st = acts.stride()
+        _lib.check(self.lib.duchess_step(
+            self.policy, self.wl.struct, self.state, self.step_ctl, acts.data_ptr(), dtype, T, H,
+            st[0], st[1], st[2], bank.wg.data_ptr(), bank.c1.data_ptr(), out_logit.data_ptr(),
+            self.probs.data_ptr(), _lib.stream_handle(stream)), "duchess_step")
+
+    def fused_rows(self):
+        """(row list, count) of the survivors the next step_fused() will score."""
+        tag = int(self.fx["ctl"][_lib.STEP_CTL_TAG])
+        par = tag & 1
+        n = int(self.fx["ctl"][_lib.STEP_CTL_COUNT + par])
+        RC = self.R * self.C
+        return self.fx["rows"][par * RC: par * RC + n], n
+
     def baseline_round(self, stream=None) -> None:
         """One round of a baseline policy (Default SC / Short-m@k / Dynasor)."""
         _lib.check(self.lib.duchess_baseline_round(self.policy, self.wl.struct, self.state,
