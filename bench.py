@@ -197,10 +197,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     fused = args.mode == "fused"
 
     def one_step(i, timed):
-        # fused (default): ONE persistent launch per round (duchess_step) —
+        # fused: ONE persistent launch per round (duchess_step) —
         # K1 streams the survivors' windows while a decision warp per CTA
         # decides every request whose windows are scored and advances it into
-        # the next round. split: K1 launch, then duchess_round (decide k +
+        # the next round. split (default): K1 launch, then duchess_round (decide k +
         # advance k+1). The scoring kernel is bracketed by CUDA events on every
         # `k1_every`-th timed step: an event record between two PDL-chained
         # kernels breaks their overlap, so sampling keeps the measurement from
@@ -754,9 +754,9 @@ def main():
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
-    ap.add_argument("--mode", default="fused", choices=["fused", "split"],
-                    help="fused: one duchess_step launch per round (default); split: K1 "
-                         "launch + duchess_round launch")
+    ap.add_argument("--mode", default="split", choices=["fused", "split"],
+                    help="split (default): K1 launch + duchess_round launch per round; "
+                         "fused: one duchess_step launch per round (see DESIGN.md 7)")
     ap.add_argument("--k1-every", type=int, default=4,
                     help="bracket K1 with CUDA events on every N-th timed step")
     ap.add_argument("--nsplit", type=int, default=2)

@@ -65,6 +65,8 @@ extern "C" {
  * default decides from a warp prefix sum unless u is within the rounding
  * margin of a boundary; both give identical picks — the flag exists to test that). */
 #define DUCHESS_FLAG_EXACT_CDF 1
+/* Profiling only: duchess_step skips the decision warps (scoring alone). */
+#define DUCHESS_FLAG_PROFILE_NO_DECIDE 2
 
 /* Policies (orchestrator.py:47-52). DUCHESS runs through advance / decide /
  * round; the baselines through duchess_baseline_round. */
@@ -238,8 +240,8 @@ int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
  * predictor seam (:358-363) served by the pooled linear probe (K1,
  * predictor.py:126-151). While the producer/consumer warps of each CTA
  * stream survivor windows from HBM, a decision warp per CTA takes every
- * request slot whose windows are all scored (per-slot pending counter ->
- * ready queue) and runs phases 2-5 for it, then refill + phase 1 of the next
+ * request slot whose windows are all scored (each score store replaces a
+ * sentinel the decision warp polls) and runs phases 2-5 for it, then refill + phase 1 of the next
  * round, appending its survivors to the next round's list. Decisions overlap
  * the streaming of other requests' windows; per-request results are those of
  * duchess_advance / duchess_score / duchess_decide. Refills pop the service
@@ -247,21 +249,23 @@ int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
  * same; only their slot placement may differ from duchess_round).
  * Requires pred_source == DUCHESS_PRED_DEVICE and the DUCHESS policy. */
 typedef struct DuchessStepCtl {
-  int32_t* rows;    /* [2 * R * C] survivor rows (r*C + slot) per round parity */
-  int64_t* ready;   /* [2 * R] ready-queue entries ((round tag << 32) | slot) */
-  int32_t* pending; /* [R] windows of the slot still unscored this round */
-  int32_t* idle;    /* [R] slot went idle last step: clear its round record */
-  int32_t* ctl;     /* [DUCHESS_STEP_CTL_WORDS] counters, zero-initialised */
+  int32_t* rows; /* [2 * R * C] survivor rows (r*C + slot) per round parity */
+  int32_t* reqs; /* [2 * R] request slots with a round, per round parity */
+  int32_t* idle; /* [R] slot went idle last step: clear its round record */
+  int32_t* ctl;  /* [DUCHESS_STEP_CTL_WORDS] counters, zero-initialised */
 } DuchessStepCtl;
 #define DUCHESS_STEP_CTL_WORDS 16
 #define DUCHESS_STEP_CTL_TAG 0   /* index of the next duchess_step launch */
 #define DUCHESS_STEP_CTL_POP 2   /* service-queue entries popped so far */
 #define DUCHESS_STEP_CTL_COUNT 4 /* +parity: survivor rows listed for the round */
+#define DUCHESS_STEP_CTL_NREQ 6  /* +parity: request slots listed for the round */
 
 /* Refill every slot and run phase 1 of the first round (call once on a fresh,
- * zeroed DuchessStepCtl). */
+ * zeroed DuchessStepCtl). probs [R*C*L] fp64 is the array later passed to
+ * duchess_step as out_prob (the survivors' entries are armed). */
 int duchess_step_begin(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                       const DuchessState* state, const DuchessStepCtl* ctl, void* stream);
+                       const DuchessState* state, const DuchessStepCtl* ctl, double* probs,
+                       void* stream);
 /* One fused round. acts: [R*C rows, L, T, H] (row index r*C + slot), bf16 or
  * fp32, hidden contiguous, 16-byte aligned rows; L = policy->n_layers.
  * out_prob [R*C*L] fp64 doubles as the decisions' probability input. */

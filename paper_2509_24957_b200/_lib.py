@@ -21,6 +21,7 @@ REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
 PRED_DEVICE, PRED_TRACE, PRED_HOST = 0, 1, 2
 FLAG_EXACT_CDF = 1
+FLAG_PROFILE_NO_DECIDE = 2
 POLICY_DUCHESS, POLICY_DEFAULT_SC, POLICY_SHORT_MK, POLICY_DYNASOR = 0, 1, 2, 3
 MT_WORDS = 625
 MAX_SLOTS = 64
@@ -80,12 +81,12 @@ class State(C.Structure):
 
 
 class StepCtl(C.Structure):
-    _fields_ = [("rows", C.c_void_p), ("ready", C.c_void_p), ("pending", C.c_void_p),
-                ("idle", C.c_void_p), ("ctl", C.c_void_p)]
+    _fields_ = [("rows", C.c_void_p), ("reqs", C.c_void_p), ("idle", C.c_void_p),
+                ("ctl", C.c_void_p)]
 
 
 STEP_CTL_WORDS = 16
-STEP_CTL_TAG, STEP_CTL_POP, STEP_CTL_COUNT = 0, 2, 4
+STEP_CTL_TAG, STEP_CTL_POP, STEP_CTL_COUNT, STEP_CTL_NREQ = 0, 2, 4, 6
 
 
 SYMBOLS = {
@@ -110,7 +111,7 @@ SYMBOLS = {
     "duchess_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                 C.c_void_p, C.c_void_p]),
     "duchess_step_begin": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
-                                     C.POINTER(StepCtl), C.c_void_p]),
+                                     C.POINTER(StepCtl), C.c_void_p, C.c_void_p]),
     "duchess_step": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                C.POINTER(StepCtl), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,

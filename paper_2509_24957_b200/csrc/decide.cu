@@ -16,6 +16,7 @@
 // genrand_res53; the branch-out normaliser replays CPython >= 3.12's
 // compensated (Neumaier) builtin sum().
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -26,7 +27,10 @@ namespace cg = cooperative_groups;
 
 namespace duchess {
 
-constexpr int kWarpsPerBlock = 4;
+#ifndef DUCHESS_K2_WARPS
+#define DUCHESS_K2_WARPS 4
+#endif
+constexpr int kWarpsPerBlock = DUCHESS_K2_WARPS;
 constexpr int kMaxC = DUCHESS_MAX_SLOTS;
 constexpr int kMtN = 624, kMtM = 397;
 constexpr double kProbFloor = 1e-6;   // orchestrator.py:56 BRANCH_PROB_FLOOR
@@ -459,24 +463,19 @@ __device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
 }
 
 // Fused-step bookkeeping for phase 1 (duchess_step): survivors go to the
-// next round's list, the slot's pending-window count is armed, and a slot
-// with no survivor is ready for its decision at once.
+// next round's window list, the slot to the next round's request list, and
+// the survivors' probability entries are armed with a sentinel (-1; scores
+// are clipped to [1e-12, 1 - 1e-12], predictor.py:148) that the scorer's
+// store replaces, so a decision warp knows a window is scored by reading the
+// score itself: no fence or atomic on the streaming path.
 struct Phase1Out {
   int32_t* rows;
   int32_t* count;
-  int32_t* live;
-  int32_t* tail;
-  int64_t* ready;
-  int32_t* pending;
-  int tag;
+  int32_t* reqs;
+  int32_t* nreq;
+  double* probs;
 };
-
-__device__ __forceinline__ void publish_ready(int32_t* tail, int64_t* ready, int tag, int r) {
-  __threadfence();
-  const int t = atomicAdd(tail, 1);
-  atomicExch(reinterpret_cast<unsigned long long*>(ready + t),
-             (static_cast<unsigned long long>(uint32_t(tag)) << 32) | uint32_t(r));
-}
+constexpr double kUnscored = -1.0;
 
 __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, int p, SlotCache& c, int lane,
@@ -532,10 +531,11 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       if (surv) list_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
     }
   }
-  if (fo && lane == 0) {
-    fo->pending[r] = n_listed * pol.n_layers;
-    atomicAdd(fo->live, 1);
-    if (n_listed == 0) publish_ready(fo->tail, fo->ready, fo->tag, r);
+  if (fo) {
+    for (int j = lane; j < C; j += 32)
+      if (s.row_mask[rC + j])
+        for (int l = 0; l < pol.n_layers; ++l) fo->probs[(rC + j) * pol.n_layers + l] = kUnscored;
+    if (lane == 0) fo->reqs[atomicAdd(fo->nreq, 1)] = r;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1032,31 +1032,23 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
 // Fused round (duchess_step): K1 scoring + decide + advance in one launch.
 //
 // ctl words: tag (index of the next step launch), exit counter, queue pops,
-// then per round parity: listed survivor rows, live slots, ready-queue tail,
-// ready-queue claims. Launch `tag` consumes parity tag & 1 (built by the
+// then per round parity: listed survivor windows, listed request slots,
+// decision claims. Launch `tag` consumes parity tag & 1 (built by the
 // previous launch or duchess_step_begin) and builds parity (tag + 1) & 1; its
 // last CTA resets the consumed parity and bumps the tag.
 enum : int {
   kCtlTag = DUCHESS_STEP_CTL_TAG, kCtlExit = 1, kCtlPop = DUCHESS_STEP_CTL_POP,
-  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlLive = 6, kCtlTail = 8, kCtlClaim = 10
+  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlNReq = DUCHESS_STEP_CTL_NREQ, kCtlClaim = 10
 };
 
-__device__ __forceinline__ long long ld_acquire_s64(const int64_t* p) {
-  long long v;
-  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ Phase1Out phase1_out(const DuchessStepCtl& x, int R, int C, int par,
-                                                int tag) {
+                                                double* probs) {
   Phase1Out o;
   o.rows = x.rows + int64_t(par) * R * C;
   o.count = x.ctl + kCtlCount + par;
-  o.live = x.ctl + kCtlLive + par;
-  o.tail = x.ctl + kCtlTail + par;
-  o.ready = x.ready + int64_t(par) * R;
-  o.pending = x.pending;
-  o.tag = tag;
+  o.reqs = x.reqs + int64_t(par) * R;
+  o.nreq = x.ctl + kCtlNReq + par;
+  o.probs = probs;
   return o;
 }
 
@@ -1093,7 +1085,8 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-step_begin_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x) {
+step_begin_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x,
+                  double* probs) {
   __shared__ SlotCache cache[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -1103,7 +1096,7 @@ step_begin_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessS
   clear_round_inputs(pol, s, r, lane);
   const int p = slot_prologue_fused(pol, w, s, r, c, lane, false, x.ctl + kCtlPop);
   if (p >= 0) {
-    const Phase1Out fo = phase1_out(x, s.n_slots, pol.max_branches, tag & 1, tag);
+    const Phase1Out fo = phase1_out(x, s.n_slots, pol.max_branches, tag & 1, probs);
     phase1_slot(pol, w, s, r, p, c, lane, &fo);
   } else if (lane == 0) {
     x.idle[r] = 1;
@@ -1131,33 +1124,56 @@ step_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl
   const int R = s.n_slots, C = pol.max_branches, L = pol.n_layers;
   t.row_list = x.rows + int64_t(par) * R * C;
   const int64_t n_units = int64_t(x.ctl[kCtlCount + par]) * L;
-  int64_t* ready = x.ready + int64_t(par) * R;
+  if (s.trace && blockIdx.x == 0 && threadIdx.x == 0) {   // profiling: kernel start
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    s.trace[13] = (long long)t0;
+  }
 
   if (warp == kTmaConsWarps) {                       // ---- producer ----
     if (lane == 0) tma_produce<ESZ>(a, t, rg, n_units);
   } else if (warp == kTmaConsWarps + 1) {            // ---- decisions ----
+    if (pol.flags & DUCHESS_FLAG_PROFILE_NO_DECIDE) {  // profiling: re-list, no decisions
+      const int nreq = x.ctl[kCtlNReq + par];
+      const Phase1Out fo = phase1_out(x, R, C, par ^ 1, a.out_prob);
+      for (int i = blockIdx.x; i < nreq; i += gridDim.x) {
+        const int r = x.reqs[int64_t(par) * R + i];
+        for (int j = lane; j < C; j += 32)
+          if (s.row_mask[int64_t(r) * C + j]) fo.rows[atomicAdd(fo.count, 1)] = int32_t(int64_t(r) * C + j);
+        if (lane == 0) fo.reqs[atomicAdd(fo.nreq, 1)] = r;
+      }
+      goto done;
+    }
     for (int r = blockIdx.x * 32 + lane; r < R; r += gridDim.x * 32) {
       if (x.idle[r]) {                               // slot ran no round this step
         s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
         x.idle[r] = 0;
       }
     }
-    const int live = x.ctl[kCtlLive + par];
-    const Phase1Out fo = phase1_out(x, R, C, par ^ 1, tag + 1);
+    const int nreq = x.ctl[kCtlNReq + par];
+    const int32_t* reqs = x.reqs + int64_t(par) * R;
+    const Phase1Out fo = phase1_out(x, R, C, par ^ 1, a.out_prob);
     while (true) {
       int i = 0;
       if (lane == 0) i = atomicAdd(x.ctl + kCtlClaim + par, 1);
       i = __shfl_sync(0xffffffffu, i, 0);
-      if (i >= live) break;
-      if (lane == 0) {
-        int ns = 32;
-        while ((ld_acquire_s64(ready + i) >> 32) != tag) {
-          __nanosleep(ns);
-          ns = ns < 256 ? 2 * ns : 256;
+      if (i >= nreq) break;
+      const int r = reqs[i];
+      const int64_t rC = int64_t(r) * C;
+      trace_mark(s, r, 9, lane);
+      // wait until every listed window of the slot is scored (its sentinel replaced)
+      for (int j = lane; j < C; j += 32) {
+        if (!s.row_mask[rC + j]) continue;
+        for (int l = 0; l < L; ++l) {
+          const double* pp = a.out_prob + (rC + j) * L + l;
+          int ns = 64;
+          while (__ldcv(pp) == kUnscored) {
+            __nanosleep(ns);
+            ns = ns < 512 ? 2 * ns : 512;
+          }
         }
       }
       __syncwarp();
-      const int r = int(ld_acquire_s64(ready + i) & 0xffffffffll);   // acquire in every lane
       trace_mark(s, r, 12, lane);
       decide_slot(pol, w, s, r, cache, lane, a.out_prob);
       trace_mark(s, r, 8, lane);
@@ -1170,12 +1186,14 @@ step_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl
       __syncwarp();
     }
   } else {                                           // ---- consumers ----
-    tma_consume<BF16, VPT>(a, t, rg, n_units, red, [&](int64_t row, int, int64_t) {
-      const int r = int(row / C);
-      __threadfence();                               // this window's score before the count
-      if (atomicSub(x.pending + r, 1) == 1) publish_ready(x.ctl + kCtlTail + par, ready, tag, r);
-    });
+    tma_consume<BF16, VPT>(a, t, rg, n_units, red, [](int64_t, int, int64_t) {});
+    if (s.trace && threadIdx.x == 0) {                // profiling: this CTA's last window
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      atomicMax(reinterpret_cast<unsigned long long*>(s.trace + 14), t1);
+    }
   }
+done:
   __syncthreads();
   if (threadIdx.x == 0) {
     pdl_launch_dependents();
@@ -1183,8 +1201,7 @@ step_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl
     if (atomicAdd(x.ctl + kCtlExit, 1) == int(gridDim.x) - 1) {
       __threadfence();
       x.ctl[kCtlCount + par] = 0;
-      x.ctl[kCtlLive + par] = 0;
-      x.ctl[kCtlTail + par] = 0;
+      x.ctl[kCtlNReq + par] = 0;
       x.ctl[kCtlClaim + par] = 0;
       x.ctl[kCtlExit] = 0;
       const int pops = x.ctl[kCtlPop];
@@ -1576,19 +1593,19 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
 }
 
 static bool step_ctl_ok(const DuchessStepCtl* x) {
-  return x && x->rows && x->ready && x->pending && x->idle && x->ctl;
+  return x && x->rows && x->reqs && x->idle && x->ctl;
 }
 
 extern "C" int duchess_step_begin(const DuchessPolicy* policy, const DuchessWorkload* workload,
                                   const DuchessState* state, const DuchessStepCtl* ctl,
-                                  void* stream) {
-  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl)) return DUCHESS_EINVAL;
+                                  double* probs, void* stream) {
+  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl) || !probs) return DUCHESS_EINVAL;
   if (policy->policy_kind != DUCHESS_POLICY_DUCHESS || policy->pred_source != DUCHESS_PRED_DEVICE)
     return DUCHESS_EINVAL;
   if (state->n_slots == 0) return DUCHESS_OK;
   const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
   step_begin_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      *policy, *workload, *state, *ctl);
+      *policy, *workload, *state, *ctl, probs);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
@@ -1597,18 +1614,29 @@ static cudaError_t launch_step(const DuchessPolicy& pol, const DuchessWorkload& 
                                const DuchessState& st, const DuchessStepCtl& x, const ScoreArgs& a,
                                const TmaArgs& t, size_t smem, cudaStream_t stream) {
   auto kern = step_kernel<BF16, VPT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int dev = 0, sms = 0;
+  // Grid = co-resident CTAs (decision warps wait on windows any CTA of the
+  // grid may hold, so every CTA must be resident at once). Cached per
+  // (device, instantiation, smem): the occupancy query costs host time.
+  static int cached_dev[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
+  static size_t cached_smem[2][4];
+  static int cached_grid[2][4];
+  const int vi = VPT == 1 ? 0 : VPT == 2 ? 1 : VPT == 4 ? 2 : 3;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // Every CTA must be resident at once: decision warps wait on windows that
-  // any CTA of the grid may hold.
-  const int grid = sms * (per_sm < 2 ? per_sm : 2);
+  int& cd = cached_dev[BF16][vi];
+  if (cd != dev || cached_smem[BF16][vi] != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cached_grid[BF16][vi] = sms * (per_sm < 2 ? per_sm : 2);
+    cached_smem[BF16][vi] = smem;
+    cd = dev;
+  }
+  const int grid = cached_grid[BF16][vi];
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kStepThreads);
@@ -1667,6 +1695,7 @@ extern "C" int duchess_step(const DuchessPolicy* policy, const DuchessWorkload* 
   // reserved) within the 228 KB of an SM.
   const int static_bytes = int(sizeof(SlotCache)) + 1024;
   t.stages = (115712 - static_bytes) / stage_bytes;
+  if (const char* e = getenv("DUCHESS_STEP_STAGES")) { const int v = atoi(e); if (v >= 2 && v < t.stages) t.stages = v; }
   if (t.stages > 32) t.stages = 32;
   if (t.stages < 2) return DUCHESS_EINVAL;
   const int nvec = int(row_bytes / 16);

@@ -263,8 +263,7 @@ class BatchedDuchess:
             raise ValueError("the fused round needs the DUCHESS policy with device probabilities")
         R, C, dev = self.R, self.C, self.device
         x = {"rows": torch.zeros(2 * R * C, dtype=torch.int32, device=dev),
-             "ready": torch.full((2 * max(R, 1),), -1, dtype=torch.int64, device=dev),
-             "pending": torch.zeros(max(R, 1), dtype=torch.int32, device=dev),
+             "reqs": torch.zeros(2 * max(R, 1), dtype=torch.int32, device=dev),
              "idle": torch.zeros(max(R, 1), dtype=torch.int32, device=dev),
              "ctl": torch.zeros(_lib.STEP_CTL_WORDS, dtype=torch.int32, device=dev)}
         sc = _lib.StepCtl()
@@ -272,7 +271,8 @@ class BatchedDuchess:
             setattr(sc, k, v.data_ptr())
         self.fx, self.step_ctl = x, sc
         _lib.check(self.lib.duchess_step_begin(self.policy, self.wl.struct, self.state, sc,
-                                               _lib.stream_handle(stream)), "duchess_step_begin")
+                                               self.probs.data_ptr(), _lib.stream_handle(stream)),
+                   "duchess_step_begin")
 
     def step_fused(self, acts: torch.Tensor, bank, out_logit: torch.Tensor, stream=None) -> None:
         """One fused round (duchess_step). acts: [R*C, L, T, H] bf16/fp32

@@ -72,16 +72,21 @@ def test_fused_step_matches_oracle(dtype, T, H, L, c, R, temperature):
         rows, n = eng.fused_rows()
         assert sorted(rows.cpu().tolist()) == list(np.nonzero(mask)[0])
         eng.step_fused(acts, bank, logit)
-        pr = eng.probs.view(R * C, L).cpu().numpy()
+        # the prediction each survivor was decided with (eng.probs already
+        # holds the next round's unscored sentinels)
+        pr = eng.t["step_pred"].cpu().numpy()
         lg = logit.view(R * C, L).cpu().numpy()
         for row in np.nonzero(mask)[0]:
             key = (int(req[row]), int(tm[row]), int(pos[row]))
-            seen[key] = float(pr[row].sum() / L) if L > 1 else float(pr[row, 0])
+            seen[key] = float(pr[row])
             if checked < 120 and row % 3 == 0:
+                ps = []
                 for l in range(L):
                     win = oact.synth_window(seed, *key, l, T, H, dtype == torch.bfloat16)
-                    ref, _ = port.pooled_linear_probe(win, w[l], 0.0, g[l], beta[l])
+                    ref, pref = port.pooled_linear_probe(win, w[l], 0.0, g[l], beta[l])
                     assert abs(float(lg[row, l]) - ref) <= 1e-4 * max(abs(ref), 1.0)
+                    ps.append(pref)
+                assert abs(seen[key] - sum(ps) / L) <= 1e-4
                 checked += 1
         for p, rep in eng.round_reports():
             reports.setdefault(p, []).append(rep)

@@ -34,6 +34,7 @@ for step in range(40):
         t = tr.view(-1, 16).cpu().numpy().astype(np.float64)
         t0 = t[:, 12].min()
         rel = lambda k: (t[:, k] - t0) / 1e3  # noqa: E731
+        np.save(f"gpurun_out/trace_round{step}.npy", t)
         print(f"step {step}: event {e0.elapsed_time(e1)*1e3:.1f}us | start max {rel(12).max():.2f} "
               f"decide_end max {rel(5).max():.2f} pre-sync max {rel(8).max():.2f} "
               f"post-sync min {rel(9).min():.2f} max {rel(9).max():.2f} prologue max {rel(10).max():.2f} "
