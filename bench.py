@@ -216,8 +216,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 k1_ev.append((e0, e1))
             return
         if args.k1 == "list":
-            scorer.score_list(slabs[i % n_slabs], logit, probs, eng.t["active_rows"],
-                              eng.t["active_count"])
+            scorer.score_active(slabs[i % n_slabs], logit, probs, eng)
         else:
             scorer(slabs[i % n_slabs], logit, probs, row_mask=eng.t["row_mask"])
         if timed:
@@ -330,7 +329,7 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, 
             stream.synchronize()
             return
         eng.advance()
-        scorer.score_list(dslab, logit, probs, eng.t["active_rows"], eng.t["active_count"]) \
+        scorer.score_active(dslab, logit, probs, eng) \
             if args.k1 == "list" else scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
         eng.decide()
         rec_host.copy_(eng.t["round_rec"], non_blocking=True)

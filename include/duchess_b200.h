@@ -187,8 +187,10 @@ typedef struct DuchessState {
   int32_t* forks;      /* [R*C*4]  (child, source, table_root, prefix_tokens) */
   double* step_pred;   /* [R*C] prediction used for each survivor, by slot */
   int32_t* queue_head; /* [2] */
-  int32_t* active_rows;  /* [R*C] compacted survivor rows (r*C + slot) for K1, or NULL */
-  int32_t* active_count; /* [1] entries in active_rows; reset by duchess_decide */
+  int32_t* active_rows;  /* [2*R*C] compacted survivor rows (r*C + slot) for K1 per list
+                            parity, or NULL */
+  int32_t* active_count; /* [4]: rows listed per parity [0..1], parity of the list the next
+                            scorer reads [2], duchess_round exit counter [3] */
   /* outcomes by pool index [P] */
   int32_t* out_final;
   int32_t* out_reason;
@@ -216,6 +218,14 @@ int duchess_score_list(const void* acts, int32_t dtype, int64_t n_rows, int32_t 
                        int64_t token_stride, const float* wg, const float* c1,
                        const int32_t* row_list, const int32_t* row_count, float* out_logit,
                        double* out_prob, void* stream);
+/* Score the survivors of an engine's round in flight: the list duchess_advance
+ * / duchess_round left in DuchessState.active_rows / active_count (double
+ * buffered; the parity word is read on the device). n_rows = R*C. */
+int duchess_score_active(const void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
+                         int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
+                         int64_t token_stride, const float* wg, const float* c1,
+                         const int32_t* active_rows, const int32_t* active_count,
+                         float* out_logit, double* out_prob, void* stream);
 int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
                              int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
                              int64_t token_stride, uint64_t seed, const int64_t* row_req,
@@ -228,10 +238,13 @@ int duchess_advance(const DuchessPolicy* policy, const DuchessWorkload* workload
 int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
                    const DuchessState* state, const double* probs, void* stream);
 
-/* Fused round boundary: duchess_decide for the round in flight, then
- * duchess_advance for the next one, in one cooperative launch (grid-wide
- * barrier between the halves keeps refill order deterministic). Equivalent to
- * calling decide then advance; round_rec holds the round just decided. */
+/* Round boundary: duchess_decide for the round in flight, then
+ * duchess_advance for the next one, in one launch with no grid-wide barrier:
+ * each slot is decided, refilled if it finished (the service queue is popped
+ * atomically, so the requests admitted per round are those of decide +
+ * advance; only their slot placement follows completion order) and advanced;
+ * its survivors go to the other parity's active list, and the parity flips.
+ * round_rec holds the round just decided. Needs active_rows / active_count. */
 int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                   const DuchessState* state, const double* probs, void* stream);
 

@@ -33,6 +33,10 @@ namespace duchess {
 constexpr int kWarpsPerBlock = DUCHESS_K2_WARPS;
 constexpr int kMaxC = DUCHESS_MAX_SLOTS;
 constexpr int kMtN = 624, kMtM = 397;
+// DuchessState.active_count words: [0], [1] survivor rows listed per parity,
+// [2] parity of the list the next scorer launch reads, [3] duchess_round exit
+// counter.
+enum : int { kListPar = 2, kListExit = 3 };
 constexpr double kProbFloor = 1e-6;   // orchestrator.py:56 BRANCH_PROB_FLOOR
 
 // ---------------------------------------------------------------------------
@@ -349,22 +353,35 @@ __device__ __forceinline__ void copy_mt(const uint32_t* src, uint32_t* dst, int 
   __syncwarp();
 }
 
-// n tempered words from a global-memory stream. Common case (no twist due):
-// read just mt[idx, idx+n) and bump the index. Otherwise stage the state in
-// shared memory, run the warp-parallel twist there, and write it back.
-__device__ int mt_words_global(uint32_t* mt_g, uint32_t* mt_s, int idx, int n, uint32_t* out,
-                                int lane) {
+// Slot MT states are copy-on-write: a refill stores only the index word with
+// kMtPristine set, and the words are read from the pool's initial state
+// (DuchessWorkload.mt_init[p], which the host stores already twisted, index
+// 0) until the first twist writes a private copy. So a refill copies nothing
+// and a fresh request's first draws need no twist.
+constexpr uint32_t kMtPristine = 0x80000000u;
+
+// n tempered words from a global-memory stream whose words live at `src`
+// (mt_g itself, or the pool's initial state while `flag` == kMtPristine).
+// Common case (no twist due): read src[idx, idx+n) and bump the index.
+// Otherwise stage the state in shared memory, run the warp-parallel twist
+// there, and write the (now private) state back to mt_g.
+__device__ int mt_words_global(uint32_t* mt_g, const uint32_t*& src, uint32_t& flag,
+                               uint32_t* mt_s, int idx, int n, uint32_t* out, int lane) {
   if (idx + n <= kMtN) {
-    for (int k = lane; k < n; k += 32) out[k] = mt_temper(mt_g[idx + k]);
+    for (int k = lane; k < n; k += 32) out[k] = mt_temper(src[idx + k]);
     __syncwarp();
-    if (lane == 0) mt_g[kMtN] = uint32_t(idx + n);
+    if (lane == 0) mt_g[kMtN] = uint32_t(idx + n) | flag;
     __syncwarp();
     return idx + n;
   }
-  copy_mt(mt_g, mt_s, lane);
+  copy_mt(src, mt_s, lane);
+  if (lane == 0) mt_s[kMtN] = uint32_t(idx);
+  __syncwarp();
   mt_words_warp(mt_s, n, out, lane);
   const int nidx = int(mt_s[kMtN]);
   copy_mt(mt_s, mt_g, lane);
+  src = mt_g;
+  flag = 0u;
   return nidx;
 }
 
@@ -399,8 +416,9 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
   }
   for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
-  copy_mt(w.mt_init + int64_t(p) * DUCHESS_MT_WORDS, s.mt + int64_t(r) * DUCHESS_MT_WORDS, lane);
   if (lane == 0) {
+    s.mt[int64_t(r) * DUCHESS_MT_WORDS + kMtN] =
+        kMtPristine | w.mt_init[int64_t(p) * DUCHESS_MT_WORDS + kMtN];   // copy-on-write
     s.slot_req[r] = p;
     if (s.slot_aux) s.slot_aux[r] = 0;
     s.n_branches[r] = seeded;
@@ -482,6 +500,11 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const Phase1Out* fo = nullptr) {
   int32_t* list_rows = fo ? fo->rows : s.active_rows;
   int32_t* list_count = fo ? fo->count : s.active_count;
+  if (!fo && s.active_rows) {                      // split launches: the current parity
+    const int par = s.active_count[kListPar];
+    list_rows += int64_t(par) * s.n_slots * pol.max_branches;
+    list_count += par;
+  }
   int n_listed = 0;
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
@@ -531,7 +554,7 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       if (surv) list_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
     }
   }
-  if (fo) {
+  if (fo && fo->reqs) {
     for (int j = lane; j < C; j += 32)
       if (s.row_mask[rC + j])
         for (int l = 0; l < pol.n_layers; ++l) fo->probs[(rC + j) * pol.n_layers + l] = kUnscored;
@@ -594,7 +617,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     if (lane < s.answer_cap) tl0 = s.tally[rA + lane];
     if (lane + 32 < s.answer_cap) tl1 = s.tally[rA + lane + 32];
   }
-  int mt_idx = int(mt_g[kMtN]);
+  const uint32_t mt_iw = mt_g[kMtN];
+  uint32_t mt_flag = mt_iw & kMtPristine;
+  int mt_idx = int(mt_iw & ~kMtPristine);
   const int nb = s.n_branches[r];
   const int next_t = s.next_template[r];
   const int p = __shfl_sync(0xffffffffu, p1v, 5);
@@ -606,6 +631,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   c.tally_delta[lane + 32 < 64 ? lane + 32 : 63] = 0;
   // ---- wave 2: template base + branch fields ----
   const int t0 = w.tmpl_off[p];
+  const uint32_t* mt_src = mt_flag ? w.mt_init + int64_t(p) * DUCHESS_MT_WORDS : mt_g;
   const int n_tmpl = w.tmpl_off[p + 1] - t0;
   c.bid[lane] = -1;
   if (lane + 32 < kMaxC) c.bid[lane + 32] = -1;
@@ -648,7 +674,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
   const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
   if (words_ready)
-    for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(mt_g[mt_idx + k]);
+    for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(mt_src[mt_idx + k]);
   __syncwarp();
   const int n_surv = order_slots(c, C, lane);
   trace_mark(s, r, 1, lane);
@@ -668,7 +694,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
     __syncwarp();
     if (n_need > 0) {
-      mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_need, c.words, lane);
+      mt_idx = mt_words_global(mt_g, mt_src, mt_flag, c.mt, mt_idx, 2 * n_need, c.words, lane);
       for (int k = lane; k < n_need; k += 32) c.draws[k] = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
       __syncwarp();
     }
@@ -773,10 +799,10 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   trace_mark(s, r, 3, lane);
   if (n_forks > 0) {
     if (words_ready) {                                 // words prefetched in wave 3
-      if (lane == 0) mt_g[kMtN] = uint32_t(mt_idx + 2 * n_forks);
+      if (lane == 0) mt_g[kMtN] = uint32_t(mt_idx + 2 * n_forks) | mt_flag;
       mt_idx += 2 * n_forks;
     } else {
-      mt_idx = mt_words_global(mt_g, c.mt, mt_idx, 2 * n_forks, c.words, lane);
+      mt_idx = mt_words_global(mt_g, mt_src, mt_flag, c.mt, mt_idx, 2 * n_forks, c.words, lane);
     }
     // The reference's normaliser is CPython's compensated sum() (:184). The fast
     // path only needs it to within a few ulp (the margin below absorbs that), so
@@ -787,9 +813,17 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     // Tree-order prefix sums of the raws, extended by one entry per fork.
     double P0 = warp_incl_scan(rw0, lane);
     double P1 = warp_incl_scan(rw1, lane) + __shfl_sync(0xffffffffu, P0, 31);
-    int n = n_alive, amb = 0;
+    // u of fork k, held by lane k % 32 (set k / 32), all drawn up front
+    double u0 = 0.0, u1 = 0.0;
+    if (lane < n_forks) u0 = mt_res53(c.words[2 * lane], c.words[2 * lane + 1]);
+    if (lane + 32 < n_forks) u1 = mt_res53(c.words[2 * lane + 64], c.words[2 * lane + 65]);
+    // The serial part: fork k picks entry idx_k of the list alive + children
+    // 0..k-1 (each child repeats its source's raw); lane k % 32 records idx_k.
+    // Child fields are resolved after the loop.
+    int pick0 = -1, pick1 = -1, n = n_alive, amb = 0;
     for (int k = 0; k < n_forks; ++k) {
-      const double u = mt_res53(c.words[2 * k], c.words[2 * k + 1]);
+      const double u = __shfl_sync(0xffffffffu, k < 32 ? u0 : u1, k & 31);
+      const double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
       // The reference picks the first j with u < acc_j, acc_j the sequential
       // sum of fl(raw_i / total_c). acc_j, P_j / total and the running sum
       // differ by less than (3n + 10) ulp of the total, so away from a
@@ -819,35 +853,77 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         }
         idx = __shfl_sync(0xffffffffu, idx, 0);
       }
-      // source of the fork, broadcast from the lane holding entry idx
-      const int own = idx & 31;
-      const bool hi = idx >= 32;
-      const int src_slot = __shfl_sync(0xffffffffu, hi ? sl1 : sl0, own);
-      const int src_root = __shfl_sync(0xffffffffu, hi ? rt1 : rt0, own);
-      const int src_pos = __shfl_sync(0xffffffffu, hi ? ps1 : ps0, own);
-      const double src_lp = __shfl_sync(0xffffffffu, hi ? lp1 : lp0, own);
-      const double src_raw = __shfl_sync(0xffffffffu, hi ? rw1 : rw0, own);
-      const double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
-      const int child_slot = c.free_slots[k];
-      const int ob = min(src_pos, c.nat_child[k]);          // _spawn clamp (:263)
-      if (lane == (n & 31)) {                               // append child as entry n
-        if (n < 32) { sl0 = child_slot; rt0 = src_root; ps0 = ob; lp0 = src_lp; rw0 = src_raw; P0 = p_last + src_raw; }
-        else        { sl1 = child_slot; rt1 = src_root; ps1 = ob; lp1 = src_lp; rw1 = src_raw; P1 = p_last + src_raw; }
+      const double src_raw = __shfl_sync(0xffffffffu, idx >= 32 ? rw1 : rw0, idx & 31);
+      if (lane == (n & 31)) {                               // append child k as entry n
+        if (n < 32) { rw0 = src_raw; P0 = p_last + src_raw; }
+        else        { rw1 = src_raw; P1 = p_last + src_raw; }
       }
-      if (lane == 0) {
-        c.bid[child_slot] = nb + k;
-        c.off[child_slot] = ob;
-        c.dec[child_slot] = 0;
-        c.streak[child_slot] = 0;
-        c.status[child_slot] = DUCHESS_ACTIVE;
-        c.npred[child_slot] = 0;
-        c.lp[child_slot] = src_lp;                         // inherits last_prediction (:264)
-        c.src_idx[k] = src_slot;
-        c.alive_root[k] = src_root;
-        c.raw[n] = src_raw;
+      if (lane == (k & 31)) {
+        if (k < 32) pick0 = idx; else pick1 = idx;
       }
+      if (lane == 0) c.raw[n] = src_raw;                    // for the exact fallback
       run_sum = __dadd_rn(run_sum, src_raw);
       ++n;
+      __syncwarp();
+    }
+    // Resolve children by pointer jumping over the pick chains: a child's
+    // source is an alive entry or an earlier child. Root / last_prediction
+    // come from the alive entry at the chain's end; the offset is the
+    // source's position clamped by each child's template length along the
+    // chain (_spawn clamp, :263).
+    {
+      const int na = n_alive;
+      int ptr0 = pick0, ptr1 = pick1;
+      int m0 = lane < n_forks ? c.nat_child[lane] : 0x7fffffff;
+      int m1 = lane + 32 < n_forks ? c.nat_child[lane + 32] : 0x7fffffff;
+      // value of entry j held as (v0, v1) by lane j % 32 (set j / 32); j is
+      // per-lane, so both sets are shuffled and the reader selects
+      auto fetch_i = [&](int v0, int v1, int j) {
+        const int a = __shfl_sync(0xffffffffu, v0, j & 31);
+        const int b = __shfl_sync(0xffffffffu, v1, j & 31);
+        return j >= 32 ? b : a;
+      };
+      auto fetch_d = [&](double v0, double v1, int j) {
+        const double a = __shfl_sync(0xffffffffu, v0, j & 31);
+        const double b = __shfl_sync(0xffffffffu, v1, j & 31);
+        return j >= 32 ? b : a;
+      };
+      const int C_hi = n_forks > 32;                         // any child in set 1
+#pragma unroll 1
+      for (int it = 0; (1 << it) < n_forks; ++it) {
+        const int q0 = ptr0 >= na ? ptr0 - na : 0, q1 = ptr1 >= na ? ptr1 - na : 0;
+        const int pj0 = fetch_i(ptr0, ptr1, q0), mj0 = fetch_i(m0, m1, q0);
+        int pj1 = 0, mj1 = 0;
+        if (C_hi) { pj1 = fetch_i(ptr0, ptr1, q1); mj1 = fetch_i(m0, m1, q1); }
+        if (lane < n_forks && ptr0 >= na) { m0 = min(m0, mj0); ptr0 = pj0; }
+        if (lane + 32 < n_forks && ptr1 >= na) { m1 = min(m1, mj1); ptr1 = pj1; }
+      }
+      // ptr now names an alive entry: fetch its slot / root / position / lp
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = lane + 32 * q;
+        const int ptr = q == 0 ? ptr0 : ptr1;
+        const int pick = q == 0 ? pick0 : pick1;
+        const int mm = q == 0 ? m0 : m1;
+        if (q == 1 && !C_hi) break;
+        const int e = max(ptr, 0);
+        const int a_root = fetch_i(rt0, rt1, e);
+        const int a_pos = fetch_i(ps0, ps1, e);
+        const double a_lp = fetch_d(lp0, lp1, e);
+        if (k < n_forks) {
+          const int child_slot = c.free_slots[k];
+          c.bid[child_slot] = nb + k;
+          c.off[child_slot] = min(a_pos, mm);
+          c.dec[child_slot] = 0;
+          c.streak[child_slot] = 0;
+          c.status[child_slot] = DUCHESS_ACTIVE;
+          c.npred[child_slot] = 0;
+          c.lp[child_slot] = a_lp;                         // inherits last_prediction (:264)
+          // source: an alive entry's slot, or the slot of an earlier child
+          c.src_idx[k] = pick < na ? -1 - c.alive_slot[pick] : pick - na;
+          c.alive_root[k] = a_root;
+        }
+      }
       __syncwarp();
     }
     if (lane == 0) {
@@ -860,7 +936,8 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     for (int k = lane; k < n_forks; k += 32) {
       const int cs = c.free_slots[k];
       const int child = nb + k;
-      const int src = c.bid[c.src_idx[k]];
+      const int si = c.src_idx[k];
+      const int src = si < 0 ? c.bid[-1 - si] : nb + si;   // source branch id
       const int64_t ci = rB + child;
       s.br_offset[ci] = c.off[cs];
       s.br_decoded[ci] = 0;
@@ -979,7 +1056,7 @@ advance_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
 __device__ __forceinline__ void decide_prologue(const DuchessState& s) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.queue_head[0] = s.queue_head[1];
-    if (s.active_count) *s.active_count = 0;     // consumed by the scorer this round
+    if (s.active_count) s.active_count[s.active_count[kListPar]] = 0;   // consumed by the scorer
   }
 }
 
@@ -995,61 +1072,6 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
     return;
   }
   decide_slot(pol, w, s, r, cache[threadIdx.x >> 5], lane, probs);
-}
-
-// Fused round boundary: decide round k for every slot, grid-wide barrier (so
-// refill ranks see every slot's completion), then refill + phase 1 of round
-// k+1 reusing the shared-memory slot cache. Launched cooperatively.
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  SlotCache& c = cache[threadIdx.x >> 5];
-  pdl_wait();   // probabilities from the scorer launched just before
-  if (r < s.n_slots) trace_mark(s, r, 12, lane);
-  decide_prologue(s);
-  bool had_round = false;
-  if (r < s.n_slots) {
-    had_round = s.p1_rec[int64_t(r) * kP1Words] != 0;
-    if (had_round) decide_slot(pol, w, s, r, c, lane, probs);
-    else if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
-  }
-  if (r < s.n_slots) trace_mark(s, r, 8, lane);
-  __threadfence();
-  cg::this_grid().sync();
-  if (r < s.n_slots) {
-    trace_mark(s, r, 9, lane);
-    clear_round_inputs(pol, s, r, lane);
-    const int p = slot_prologue(pol, w, s, r, c, lane, had_round);
-    trace_mark(s, r, 10, lane);
-    if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane);
-    trace_mark(s, r, 11, lane);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Fused round (duchess_step): K1 scoring + decide + advance in one launch.
-//
-// ctl words: tag (index of the next step launch), exit counter, queue pops,
-// then per round parity: listed survivor windows, listed request slots,
-// decision claims. Launch `tag` consumes parity tag & 1 (built by the
-// previous launch or duchess_step_begin) and builds parity (tag + 1) & 1; its
-// last CTA resets the consumed parity and bumps the tag.
-enum : int {
-  kCtlTag = DUCHESS_STEP_CTL_TAG, kCtlExit = 1, kCtlPop = DUCHESS_STEP_CTL_POP,
-  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlNReq = DUCHESS_STEP_CTL_NREQ, kCtlClaim = 10
-};
-
-__device__ __forceinline__ Phase1Out phase1_out(const DuchessStepCtl& x, int R, int C, int par,
-                                                double* probs) {
-  Phase1Out o;
-  o.rows = x.rows + int64_t(par) * R * C;
-  o.count = x.ctl + kCtlCount + par;
-  o.reqs = x.reqs + int64_t(par) * R;
-  o.nreq = x.ctl + kCtlNReq + par;
-  o.probs = probs;
-  return o;
 }
 
 // Refill-or-load prologue with the service queue popped atomically in
@@ -1082,6 +1104,72 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
   if (p < 0) return -1;
   if (!cache_valid) load_slot(s, int64_t(r) * C, int64_t(r) * s.branch_cap, C, c, lane);
   return p;
+}
+
+// Round boundary: decide round k, then refill + phase 1 of round k+1, per
+// slot with no grid-wide barrier: a finished slot pops the service queue
+// atomically (the requests admitted per round are the same as with ranked
+// refills; only their slot placement follows completion order), and phase 1
+// appends the slot's survivors to the other parity's list. The last warp
+// resets the consumed list and flips the parity.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  SlotCache& c = cache[threadIdx.x >> 5];
+  pdl_wait();   // probabilities from the scorer launched just before
+  if (r >= s.n_slots) return;
+  trace_mark(s, r, 12, lane);
+  const int par = s.active_count[kListPar];
+  const bool had_round = s.p1_rec[int64_t(r) * kP1Words] != 0;
+  if (had_round) decide_slot(pol, w, s, r, c, lane, probs);
+  else if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
+  trace_mark(s, r, 8, lane);
+  clear_round_inputs(pol, s, r, lane);
+  const int p = slot_prologue_fused(pol, w, s, r, c, lane, had_round, s.queue_head + 1);
+  trace_mark(s, r, 10, lane);
+  if (p >= 0) {
+    Phase1Out fo{};
+    fo.rows = s.active_rows + int64_t(par ^ 1) * s.n_slots * pol.max_branches;
+    fo.count = s.active_count + (par ^ 1);
+    phase1_slot(pol, w, s, r, p, c, lane, &fo);
+  }
+  trace_mark(s, r, 11, lane);
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(s.active_count + kListExit, 1) == s.n_slots - 1) {
+      __threadfence();
+      s.active_count[par] = 0;                   // consumed by the scorer this round
+      s.active_count[kListPar] = par ^ 1;
+      s.active_count[kListExit] = 0;
+      s.queue_head[0] = s.queue_head[1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused round (duchess_step): K1 scoring + decide + advance in one launch.
+//
+// ctl words: tag (index of the next step launch), exit counter, queue pops,
+// then per round parity: listed survivor windows, listed request slots,
+// decision claims. Launch `tag` consumes parity tag & 1 (built by the
+// previous launch or duchess_step_begin) and builds parity (tag + 1) & 1; its
+// last CTA resets the consumed parity and bumps the tag.
+enum : int {
+  kCtlTag = DUCHESS_STEP_CTL_TAG, kCtlExit = 1, kCtlPop = DUCHESS_STEP_CTL_POP,
+  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlNReq = DUCHESS_STEP_CTL_NREQ, kCtlClaim = 10
+};
+
+__device__ __forceinline__ Phase1Out phase1_out(const DuchessStepCtl& x, int R, int C, int par,
+                                                double* probs) {
+  Phase1Out o;
+  o.rows = x.rows + int64_t(par) * R * C;
+  o.count = x.ctl + kCtlCount + par;
+  o.reqs = x.reqs + int64_t(par) * R;
+  o.nreq = x.ctl + kCtlNReq + par;
+  o.probs = probs;
+  return o;
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
@@ -1571,6 +1659,7 @@ extern "C" int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload
 extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                              const DuchessState* state, const double* probs, void* stream) {
   if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
+  if (!state->active_rows || !state->active_count) return DUCHESS_EINVAL;
   if (policy->pred_source != DUCHESS_PRED_TRACE && probs == nullptr) return DUCHESS_EINVAL;
   if (state->n_slots == 0) return DUCHESS_OK;
   const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
@@ -1581,13 +1670,11 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32 * kWarpsPerBlock);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, round_kernel, pol, w, st, probs);
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

@@ -239,6 +239,11 @@ __global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, T
   tma_ring_init(t, rg);
   __syncthreads();
   pdl_wait();   // setup above overlaps the previous kernel; inputs are read below
+  if (t.row_par) {                     // engine list: the parity duchess_round left
+    const int par = *t.row_par;
+    t.row_list += par * t.list_stride;
+    t.row_count += par;
+  }
   const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
   if (warp == kTmaConsWarps) {
     if (lane == 0) tma_produce<ESZ>(a, t, rg, n_units);
@@ -337,7 +342,8 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
                       int64_t token_stride, const float* wg, const float* c1,
                       const uint8_t* row_mask, const int32_t* row_list, const int32_t* row_count,
                       float* out_logit, double* out_prob, void* workspace, size_t workspace_bytes,
-                      int32_t nsplit, int32_t threads, void* stream) {
+                      int32_t nsplit, int32_t threads, void* stream,
+                      const int32_t* row_par = nullptr, int64_t list_stride = 0) {
   if (n_rows < 0 || n_layers < 1 || T < 1 || H < 1) return DUCHESS_EINVAL;
   if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
   if (!acts || !wg || !c1 || !out_logit || !out_prob) return DUCHESS_EINVAL;
@@ -387,6 +393,8 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     TmaArgs t{};
     t.row_list = row_list;
     t.row_count = row_count;
+    t.row_par = row_par;
+    t.list_stride = list_stride;
     t.row_bytes = int(row_bytes);
     t.contiguous = token_stride == H;
     // Tunables (env, for sweeps): CTAs per SM and stage size target.
@@ -484,4 +492,17 @@ extern "C" int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_row
   else
     return DUCHESS_EINVAL;
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_score_active(const void* acts, int32_t dtype, int64_t n_rows,
+                                    int32_t n_layers, int32_t T, int32_t H, int64_t row_stride,
+                                    int64_t layer_stride, int64_t token_stride, const float* wg,
+                                    const float* c1, const int32_t* active_rows,
+                                    const int32_t* active_count, float* out_logit,
+                                    double* out_prob, void* stream) {
+  if (!active_rows || !active_count) return DUCHESS_EINVAL;
+  // DuchessState.active_count: [0..1] per-parity counts, [2] current parity
+  return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
+                    wg, c1, nullptr, active_rows, active_count, out_logit, out_prob, nullptr, 0, 0,
+                    0, stream, active_count + 2, n_rows);
 }

@@ -55,6 +55,8 @@ constexpr int kTmaSmemBudget = 196 * 1024;
 struct TmaArgs {
   const int32_t* row_list;   // nullable
   const int32_t* row_count;  // device count when row_list != nullptr
+  const int32_t* row_par;    // nullable: double-buffered list, parity word
+  int64_t list_stride;       // entries per parity buffer (with row_par)
   int tokens_per_stage;
   int stages;
   int row_bytes;             // H * esz

@@ -41,6 +41,24 @@ def mt_state_words(rng_or_seed) -> np.ndarray:
     return np.asarray(internal, dtype=np.uint32)
 
 
+MT_PRISTINE = 0x80000000   # slot MT index flag: words still live in the pool's mt_init
+
+
+def pretwist(words: np.ndarray) -> np.ndarray:
+    """The same MT19937 stream with its pending twist done: a freshly seeded
+    state (index 624) becomes the regenerated words with index 0, so the
+    device draws a fresh request's first words without a twist."""
+    words = np.asarray(words, dtype=np.uint32)
+    if int(words[-1]) < _lib.MT_WORDS - 1:
+        return words
+    r = random.Random()
+    r.setstate((3, tuple(int(x) for x in words), None))
+    r.getrandbits(32)                       # runs the twist, consumes word 0
+    out = np.asarray(r.getstate()[1], dtype=np.uint32)
+    out[-1] = 0
+    return out
+
+
 def set_mt_state(rng: random.Random, words: np.ndarray) -> None:
     _v, _internal, gauss = rng.getstate()
     rng.setstate((3, tuple(int(x) for x in words), gauss))
@@ -146,7 +164,8 @@ class BatchedDuchess:
         self.P, self.C = P, c
         self.R = n_slots if n_slots is not None else P
         queue = list(range(P)) if queue is None else list(queue)
-        mt = np.stack([mt_state_words(s) for s in seeds]) if P else np.zeros((0, 625), np.uint32)
+        mt = (np.stack([pretwist(mt_state_words(s)) for s in seeds]) if P
+              else np.zeros((0, 625), np.uint32))
         self.wl = pack_workload(traces, mt, queue, cycle, self.device)
 
         pol = _lib.Policy()
@@ -206,8 +225,8 @@ class BatchedDuchess:
         t["forks"] = torch.zeros(R * C * 4, **i32)
         t["step_pred"] = torch.zeros(R * C, dtype=torch.float64, device=dev)
         t["queue_head"] = torch.zeros(2, **i32)
-        t["active_rows"] = torch.zeros(R * C, **i32)
-        t["active_count"] = torch.zeros(1, **i32)
+        t["active_rows"] = torch.zeros(2 * R * C, **i32)
+        t["active_count"] = torch.zeros(4, **i32)
         P = max(self.P, 1)
         for name in ("out_final", "out_reason", "out_tokens_decode", "out_tokens_probe",
                      "out_rounds", "out_error"):
@@ -309,6 +328,12 @@ class BatchedDuchess:
         RC = self.R * self.C
         return self.fx["rows"][par * RC: par * RC + n], n
 
+    def active_list(self):
+        """(rows, count) device views of the survivor list the next scorer
+        launch reads (duchess_score_list): the parity duchess_round flips
+        lives on the device, so the views are chosen on the device too."""
+        return self.t["active_rows"], self.t["active_count"]
+
     def baseline_round(self, stream=None) -> None:
         """One round of a baseline policy (Default SC / Short-m@k / Dynasor)."""
         _lib.check(self.lib.duchess_baseline_round(self.policy, self.wl.struct, self.state,
@@ -382,6 +407,18 @@ class BatchedDuchess:
                             tokens_probe=int(t["out_tokens_probe"][p]),
                             rounds=int(t["out_rounds"][p]), error=int(t["out_error"][p])))
         return res
+
+    def slot_mt_state(self, slot: int) -> np.ndarray:
+        """625-word MT19937 state (words + index) of a slot's request,
+        resolving the copy-on-write pool state (MT_PRISTINE)."""
+        W = _lib.MT_WORDS
+        st = self.t["mt"][slot * W:(slot + 1) * W].cpu().numpy().view(np.uint32).copy()
+        if int(st[-1]) & MT_PRISTINE:
+            p = int(self.t["slot_req"][slot])
+            init = self.wl.tensors["mt_init"][p * W:(p + 1) * W].cpu().numpy().view(np.uint32)
+            st[:-1] = init[:-1]
+            st[-1] = int(st[-1]) & ~MT_PRISTINE
+        return st
 
     def branch_snapshot(self, slot: int):
         """Host copy of one slot's branch table (for facades / tests)."""

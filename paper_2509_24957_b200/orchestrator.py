@@ -306,20 +306,25 @@ class DuchessRun(RequestRun):
     def _sync_rng_to_device(self) -> None:
         import torch
 
-        from .engine import mt_state_words
+        from .engine import mt_state_words, pretwist
         if self.rng is None:
             return
-        w = torch.from_numpy(mt_state_words(self.rng).view(np.int32).copy()).to(
-            self._engine.device)
-        if self.rounds == 0:
-            self._engine.wl.tensors["mt_init"].copy_(w)
+        words = mt_state_words(self.rng)
+        if self.rounds == 0:      # the refill reads the pool state (pre-twisted)
+            w = torch.from_numpy(pretwist(words).view(np.int32).copy())
+            self._engine.wl.tensors["mt_init"].copy_(w.to(self._engine.device))
         else:
-            self._engine.t["mt"].copy_(w)
+            self._engine.t["mt"].copy_(torch.from_numpy(words.view(np.int32).copy()))
 
     def _sync_rng_from_device(self) -> None:
         from .engine import set_mt_state
-        if self.rng is not None:
-            set_mt_state(self.rng, self._engine.t["mt"].cpu().numpy().view(np.uint32))
+        if self.rng is None:
+            return
+        st = self._engine.slot_mt_state(0)
+        # index 0 only occurs in the pre-twisted initial state: nothing was
+        # drawn, and the caller's rng already holds the equivalent state
+        if int(st[-1]) != 0:
+            set_mt_state(self.rng, st)
 
     def step(self) -> RoundReport:
         if self.done:

@@ -118,6 +118,27 @@ class Scorer:
             _lib.stream_handle(stream)), "duchess_score_list")
 
 
+    def score_active(self, acts: torch.Tensor, out_logit: torch.Tensor, out_prob: torch.Tensor,
+                     engine, stream=None) -> None:
+        """Score the survivors of the engine's round in flight (the active list
+        duchess_advance / duchess_round left; parity chosen on the device).
+        acts: [R*C, L, T, H] by branch slot."""
+        _lib.require_cuda(acts)
+        rows, L, T, H = acts.shape
+        if L != self.bank.L or H != self.bank.H:
+            raise ValueError(f"activation shape (L={L}, H={H}) does not match probe bank "
+                             f"(L={self.bank.L}, H={self.bank.H})")
+        if rows != engine.R * engine.C:
+            raise ValueError("acts must have R*C rows (one per branch slot)")
+        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}[acts.dtype]
+        st = acts.stride()
+        _lib.check(self.lib.duchess_score_active(
+            acts.data_ptr(), dtype, rows, L, T, H, st[0], st[1], st[2],
+            self.bank.wg.data_ptr(), self.bank.c1.data_ptr(), engine.t["active_rows"].data_ptr(),
+            engine.t["active_count"].data_ptr(), out_logit.data_ptr(), out_prob.data_ptr(),
+            _lib.stream_handle(stream)), "duchess_score_active")
+
+
 def fill_windows(acts: torch.Tensor, seed: int, row_req=None, row_tmpl=None, row_pos=None,
                  row_mask=None, stream=None) -> None:
     """Write counter-hashed synthetic activations (oracle/activations.py

@@ -136,8 +136,7 @@ def test_fused_step_steady_state_matches_split_kernels():
     b.begin_fused()
     for step in range(60):
         fill_windows(acts, 9, a.t["row_req"], a.t["row_tmpl"], a.t["row_pos"], a.t["row_mask"])
-        scorer.score_list(acts, logit.view(R * C, L), a.probs.view(R * C, L),
-                          a.t["active_rows"], a.t["active_count"])
+        scorer.score_active(acts, logit.view(R * C, L), a.probs.view(R * C, L), a)
         a.round()
         fill_windows(acts, 9, b.t["row_req"], b.t["row_tmpl"], b.t["row_pos"], b.t["row_mask"])
         b.step_fused(acts, bank, logit)

@@ -18,6 +18,6 @@ else:
     probs = eng.probs.view(rows, 1)
     eng.advance()
     for i in range(12):
-        sc.score_list(slabs[i % 4], logit, probs, eng.t["active_rows"], eng.t["active_count"])
+        sc.score_active(slabs[i % 4], logit, probs, eng)
         eng.round()
 torch.cuda.synchronize()

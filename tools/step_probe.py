@@ -55,12 +55,12 @@ for mode in (modes if __name__ == "__main__" else []):
     else:
         eng.advance()
         for i in range(20):
-            sc.score_list(slabs[i % 4], logit, probs, eng.t["active_rows"], eng.t["active_count"])
+            sc.score_active(slabs[i % 4], logit, probs, eng)
             eng.round()
 
         def f(i):
             if mode != "roundonly":
-                sc.score_list(slabs[i % 4], logit, probs, eng.t["active_rows"], eng.t["active_count"])
+                sc.score_active(slabs[i % 4], logit, probs, eng)
             if mode != "k1only":
                 eng.round()
         us = timeit(f)

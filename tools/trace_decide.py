@@ -23,7 +23,7 @@ fill_windows(slab, 5)
 logit = torch.empty((rows, 1), device="cuda")
 eng.advance()
 for step in range(40):
-    sc.score_list(slab, logit, eng.probs.view(rows, 1), eng.t["active_rows"], eng.t["active_count"])
+    sc.score_active(slab, logit, eng.probs.view(rows, 1), eng)
     tr.zero_()
     eng.decide()
     torch.cuda.synchronize()

@@ -22,7 +22,7 @@ fill_windows(slab, 3)
 logit = torch.empty((rows, 1), device="cuda")
 eng.advance()
 for step in range(40):
-    sc.score_list(slab, logit, eng.probs.view(rows, 1), eng.t["active_rows"], eng.t["active_count"])
+    sc.score_active(slab, logit, eng.probs.view(rows, 1), eng)
     torch.cuda.synchronize()
     tr.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
