@@ -592,7 +592,7 @@ __device__ void clear_round_inputs(const DuchessPolicy& pol, const DuchessState&
 // unless cache_loaded). Completes round_rec.
 __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, SlotCache& c, int lane,
-                            const double* probs) {
+                            const double* probs, bool wait_inputs = false) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   const int64_t rA = int64_t(r) * s.answer_cap;
@@ -603,25 +603,24 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const bool dev_probs = pol.pred_source != DUCHESS_PRED_TRACE;
   const bool small_tally = s.answer_cap <= 64;
   trace_mark(s, r, 0, lane);
+  // Waves 1-3 read only state finished by the previous round and read-only
+  // tables, never the scorer's output, so under programmatic dependent
+  // launch (wait_inputs) they run before griddepcontrol.wait, overlapping
+  // the scorer's tail; mutable state is read through L2 (ld.cg).
   // ---- wave 1: everything addressed by the slot alone, issued together ----
-  const int p1v = lane < 6 ? p1[lane] : 0;
-  const int sb0 = lane < C ? s.slot_branch[rC + lane] : -1;
-  const int sb1 = lane + 32 < C ? s.slot_branch[rC + lane + 32] : -1;
-  double pr0 = 0.0, pr1 = 0.0;
-  if (dev_probs) {
-    if (lane < C) pr0 = __ldcg(probs + (rC + lane) * pol.n_layers);
-    if (lane + 32 < C) pr1 = __ldcg(probs + (rC + lane + 32) * pol.n_layers);
-  }
+  const int p1v = lane < 6 ? __ldcg(p1 + lane) : 0;
+  const int sb0 = lane < C ? __ldcg(s.slot_branch + rC + lane) : -1;
+  const int sb1 = lane + 32 < C ? __ldcg(s.slot_branch + rC + lane + 32) : -1;
   int tl0 = 0, tl1 = 0;
   if (small_tally) {
-    if (lane < s.answer_cap) tl0 = s.tally[rA + lane];
-    if (lane + 32 < s.answer_cap) tl1 = s.tally[rA + lane + 32];
+    if (lane < s.answer_cap) tl0 = __ldcg(s.tally + rA + lane);
+    if (lane + 32 < s.answer_cap) tl1 = __ldcg(s.tally + rA + lane + 32);
   }
-  const uint32_t mt_iw = mt_g[kMtN];
+  const uint32_t mt_iw = __ldcg(mt_g + kMtN);
   uint32_t mt_flag = mt_iw & kMtPristine;
   int mt_idx = int(mt_iw & ~kMtPristine);
-  const int nb = s.n_branches[r];
-  const int next_t = s.next_template[r];
+  const int nb = __ldcg(s.n_branches + r);
+  const int next_t = __ldcg(s.next_template + r);
   const int p = __shfl_sync(0xffffffffu, p1v, 5);
   if (lane < DUCHESS_REC_WORDS) {
     const int v = __shfl_sync(0x00000fffu, p1v, lane < DUCHESS_REC_NACTIONS ? lane : 5);
@@ -644,12 +643,12 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       if (j < C) c.bid[j] = b;
       if (b >= 0) {
         const int64_t bi = rB + b;
-        c.off[j] = s.br_offset[bi];
-        c.dec[j] = s.br_decoded[bi];
-        c.streak[j] = s.br_streak[bi];
-        c.status[j] = s.br_status[bi];
-        c.npred[j] = s.br_npred[bi];
-        c.lp[j] = s.br_last_pred[bi];
+        c.off[j] = __ldcg(s.br_offset + bi);
+        c.dec[j] = __ldcg(s.br_decoded + bi);
+        c.streak[j] = __ldcg(s.br_streak + bi);
+        c.status[j] = __ldcg(s.br_status + bi);
+        c.npred[j] = __ldcg(s.br_npred + bi);
+        c.lp[j] = __ldcg(s.br_last_pred + bi);
       }
     }
   }
@@ -674,9 +673,15 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
   const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
   if (words_ready)
-    for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(mt_src[mt_idx + k]);
+    for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
   __syncwarp();
   const int n_surv = order_slots(c, C, lane);
+  if (wait_inputs) pdl_wait();                     // the scorer's probabilities are final
+  double pr0 = 0.0, pr1 = 0.0;
+  if (dev_probs) {
+    if (lane < C) pr0 = __ldcg(probs + (rC + lane) * pol.n_layers);
+    if (lane + 32 < C) pr1 = __ldcg(probs + (rC + lane + 32) * pol.n_layers);
+  }
   trace_mark(s, r, 1, lane);
 
   // ---- phase 2: predictions, creation order (:357-363) ----
@@ -1112,19 +1117,27 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
 // refills; only their slot placement follows completion order), and phase 1
 // appends the slot's survivors to the other parity's list. The last warp
 // resets the consumed list and flips the parity.
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+// Two warps per CTA: small enough (18 KB shared) to become resident next to
+// the scorer's CTAs, which trigger this launch early (programmatic dependent
+// launch), so each slot's state prefetch overlaps the scorer's tail.
+constexpr int kRoundWarps = 2;
+
+__global__ void __launch_bounds__(32 * kRoundWarps)
 round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
+  __shared__ SlotCache cache[kRoundWarps];
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int r = blockIdx.x * kRoundWarps + (threadIdx.x >> 5);
   SlotCache& c = cache[threadIdx.x >> 5];
-  pdl_wait();   // probabilities from the scorer launched just before
   if (r >= s.n_slots) return;
   trace_mark(s, r, 12, lane);
+  const bool had_round = __ldcg(s.p1_rec + int64_t(r) * kP1Words) != 0;
+  if (had_round) {
+    decide_slot(pol, w, s, r, c, lane, probs, true);   // waits for the scorer inside
+  } else {
+    pdl_wait();
+    if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
+  }
   const int par = s.active_count[kListPar];
-  const bool had_round = s.p1_rec[int64_t(r) * kP1Words] != 0;
-  if (had_round) decide_slot(pol, w, s, r, c, lane, probs);
-  else if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
   trace_mark(s, r, 8, lane);
   clear_round_inputs(pol, s, r, lane);
   const int p = slot_prologue_fused(pol, w, s, r, c, lane, had_round, s.queue_head + 1);
@@ -1662,13 +1675,13 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   if (!state->active_rows || !state->active_count) return DUCHESS_EINVAL;
   if (policy->pred_source != DUCHESS_PRED_TRACE && probs == nullptr) return DUCHESS_EINVAL;
   if (state->n_slots == 0) return DUCHESS_OK;
-  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  const unsigned grid = unsigned((state->n_slots + kRoundWarps - 1) / kRoundWarps);
   DuchessPolicy pol = *policy;
   DuchessWorkload w = *workload;
   DuchessState st = *state;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(32 * kWarpsPerBlock);
+  cfg.blockDim = dim3(32 * kRoundWarps);
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, T
   tma_ring_init(t, rg);
   __syncthreads();
   pdl_wait();   // setup above overlaps the previous kernel; inputs are read below
+  // The previous round is complete: let the next launch (duchess_round)
+  // become resident and prefetch its state while this one streams.
+  pdl_launch_dependents();
   if (t.row_par) {                     // engine list: the parity duchess_round left
     const int par = *t.row_par;
     t.row_list += par * t.list_stride;

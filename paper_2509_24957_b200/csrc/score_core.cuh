@@ -177,10 +177,7 @@ __device__ __forceinline__ void tma_consume(const ScoreArgs& a, const TmaArgs& t
             const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
             if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                acc[j][2 * e] = __fadd_rn(acc[j][2 * e], bf16lo(w4[e]));
-                acc[j][2 * e + 1] = __fadd_rn(acc[j][2 * e + 1], bf16hi(w4[e]));
-              }
+              for (int e = 0; e < 4; ++e) add_bf16x2_f32(acc[j][2 * e], acc[j][2 * e + 1], w4[e]);
             } else {
 #pragma unroll
               for (int e = 0; e < 4; ++e) acc[j][e] = __fadd_rn(acc[j][e], __uint_as_float(w4[e]));
