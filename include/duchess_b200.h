@@ -312,6 +312,18 @@ int duchess_synthetic_predict(uint32_t* mt_state, int32_t n, const int32_t* conv
 /* sample_confused_level (predictor.py:376-386); matrix is 5x5 row-major fp64. */
 int duchess_confused_level(uint32_t* mt_state, int32_t n, const int32_t* true_level,
                            const double* matrix, int32_t* out, void* stream);
+/* sample_confused_level for n requests, request i drawing once from its own
+ * stream mt_states[i*625 .. +625) (simengine.py:223-227); states pre-twisted
+ * (index <= 622, see engine.pretwist); read-only. */
+int duchess_confused_levels(const uint32_t* mt_states, int32_t n, const int32_t* true_level,
+                            const double* matrix, int32_t* out, void* stream);
+/* run_simulation service timeline (simengine.py:247-257): for every slot whose
+ * round record is live, service_ms[req] += round_time(decoding, max_chunk) +
+ * probes * probe_cost_ms; first_token_ms[req] (init -1) := service_ms[req]
+ * after the first round that decoded tokens. Indexed by pool request. */
+int duchess_timeline(const int32_t* round_rec, int32_t n_slots, double ms_per_token,
+                     double ms_per_extra_branch, int64_t probe_cost_ms, int64_t* service_ms,
+                     int64_t* first_token_ms, void* stream);
 /* check_early_termination (orchestrator.py:167-174) over CSR prediction histories. */
 int duchess_early_termination(const double* history, const int32_t* offsets, int32_t n_sets,
                               double threshold, int32_t rounds, int32_t* out, void* stream);

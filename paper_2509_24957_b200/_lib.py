@@ -146,6 +146,10 @@ SYMBOLS = {
                                             C.c_void_p, C.c_void_p]),
     "duchess_confused_level": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]),
+    "duchess_confused_levels": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]),
+    "duchess_timeline": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_int64,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "duchess_early_termination": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
                                             C.c_int32, C.c_void_p, C.c_void_p]),
     "duchess_mlp_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32,

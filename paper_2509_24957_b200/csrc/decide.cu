@@ -1628,6 +1628,52 @@ __global__ void confusion_kernel(uint32_t* mt, int n, const int32_t* true_level,
   }
 }
 
+// sample_confused_level for many requests, each with its own fresh stream
+// (simengine.py:223-227: rng = random.Random(predict_seeds[order]), one draw).
+// States are [n][625] (words + index), pre-twisted by the host (index 0).
+__global__ void confusion_streams_kernel(const uint32_t* mt, int n, const int32_t* true_level,
+                                         const double* matrix, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* st = mt + int64_t(i) * DUCHESS_MT_WORDS;
+  const int idx = int(st[kMtN]);
+  const double u = mt_res53(mt_temper(st[idx]), mt_temper(st[idx + 1]));
+  const double* row = matrix + (true_level[i] - 1) * 5;
+  double acc = 0.0;
+  int lvl = 5;
+  for (int j = 0; j < 5; ++j) {
+    acc = __dadd_rn(acc, row[j]);
+    if (u < acc) { lvl = j + 1; break; }
+  }
+  out[i] = lvl;
+}
+
+// Service timeline of run_simulation (simengine.py:247-257) accumulated per
+// pool request from the round records: dt = round_time(decoding, max_chunk)
+// (when decoding) + probes * probe_cost; the first-token offset is the
+// accumulated time after the first round that decoded tokens.
+// round_time (simengine.py:51-56): int(round(tokens * (ms_per_token +
+// ms_per_extra_branch * (n - 1)))), Python round() = half to even = rint.
+__global__ void timeline_kernel(const int32_t* rec, int n_slots, double ms_per_token,
+                                double ms_per_extra_branch, long long probe_cost_ms,
+                                long long* service_ms, long long* first_token_ms) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_slots) return;
+  const int32_t* rr = rec + int64_t(r) * DUCHESS_REC_WORDS;
+  if (rr[DUCHESS_REC_ROUND] == 0) return;
+  const int p = rr[DUCHESS_REC_REQ];
+  const int decoding = rr[DUCHESS_REC_DECODING];
+  long long dt = 0;
+  if (decoding > 0) {
+    const double rate = __dadd_rn(ms_per_token, __dmul_rn(ms_per_extra_branch, double(decoding - 1)));
+    dt += (long long)rint(__dmul_rn(double(rr[DUCHESS_REC_MAX_CHUNK]), rate));
+  }
+  dt += (long long)rr[DUCHESS_REC_PROBES] * probe_cost_ms;
+  const long long t = service_ms[p] + dt;
+  service_ms[p] = t;
+  if (first_token_ms[p] < 0 && rr[DUCHESS_REC_DECODE] > 0) first_token_ms[p] = t;
+}
+
 // check_early_termination (orchestrator.py:167-174): last `rounds` strictly > threshold.
 __global__ void streak_kernel(const double* hist, const int32_t* off, int n_sets, double thr,
                               int rounds, int32_t* out) {
@@ -1894,5 +1940,27 @@ extern "C" int duchess_early_termination(const double* history, const int32_t* o
   if (n_sets == 0) return DUCHESS_OK;
   streak_kernel<<<(n_sets + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       history, offsets, n_sets, threshold, rounds, out);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_confused_levels(const uint32_t* mt_states, int32_t n,
+                                       const int32_t* true_level, const double* matrix,
+                                       int32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!mt_states || !true_level || !matrix || !out))) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  confusion_streams_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      mt_states, n, true_level, matrix, out);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_timeline(const int32_t* round_rec, int32_t n_slots, double ms_per_token,
+                                double ms_per_extra_branch, int64_t probe_cost_ms,
+                                int64_t* service_ms, int64_t* first_token_ms, void* stream) {
+  if (n_slots < 0 || (n_slots > 0 && (!round_rec || !service_ms || !first_token_ms)))
+    return DUCHESS_EINVAL;
+  if (n_slots == 0) return DUCHESS_OK;
+  timeline_kernel<<<(n_slots + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      round_rec, n_slots, ms_per_token, ms_per_extra_branch, (long long)probe_cost_ms,
+      reinterpret_cast<long long*>(service_ms), reinterpret_cast<long long*>(first_token_ms));
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

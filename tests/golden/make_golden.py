@@ -315,13 +315,75 @@ def primitives():
             "confusion": conf, "generate": gens}
 
 
+def simulation():
+    """run_simulation (simengine.py:150-281) outputs: the exact CSV and
+    summary-JSON bytes the reference writes, per case."""
+    import dataclasses
+    import tempfile
+
+    from branchsim.presets import PRESETS as P
+    from branchsim.scheduler import ArrivalConfig, gen_arrivals
+    from branchsim.simengine import (TimingModel, run_simulation, write_results_csv,
+                                     write_summary_json)
+    cases = []
+    specs = [
+        # name, preset, n, wseed, orch overrides, policy, schedule, qpm, aseed, timing, seed,
+        # rho, difficulty_mode, confusion
+        ("fcfs_duchess", "gsm8k-like", 40, 5, {}, "duchess", "fcfs", 3.0, 1,
+         (25.0, 0.0, 0.1), 9, 0.8, None, None),
+        ("actual_default_sc", "gsm8k-like", 30, 6, {}, "default-sc", "easiest-actual", 2.0, 2,
+         (25.0, 1.5, 0.2), 3, 0.8, None, None),
+        ("predicted_noisy_duchess", "math-like", 30, 7, {}, "duchess", "easiest-predicted",
+         4.0, 3, (20.0, 2.0, 0.3), 11, 0.7, "noisy-label", None),
+        ("predicted_actual_short_mk", "mmlu-like", 25, 8, {"short_m": 4}, "short-mk",
+         "easiest-predicted", 2.5, 4, (25.0, 0.5, 0.1), 5, 0.8, "actual", None),
+        ("fcfs_dynasor", "math-like", 25, 9, {"dynasor_window": 2}, "dynasor", "fcfs", 1.0, 5,
+         (30.0, 0.0, 0.0), 2, 0.8, None, None),
+        ("predicted_confusion_duchess", "gsm8k-like", 35, 10,
+         {"early_term_threshold": float("inf")}, "duchess", "easiest-predicted", 6.0, 6,
+         (25.0, 0.25, 0.1), 17, 0.9, "noisy-label",
+         [[0.5, 0.2, 0.1, 0.1, 0.1], [0.1, 0.5, 0.2, 0.1, 0.1], [0.1, 0.1, 0.5, 0.2, 0.1],
+          [0.1, 0.1, 0.1, 0.5, 0.2], [0.2, 0.1, 0.1, 0.1, 0.5]]),
+        ("burst_fcfs_duchess_lambda", "math-like", 30, 12, {"branch_out_temperature": 0.5,
+                                                            "max_branches": 6},
+         "duchess", "fcfs", 60.0, 7, (25.0, 3.0, 0.5), 23, 0.6, None, None),
+    ]
+    with tempfile.TemporaryDirectory() as tmp:
+        for (name, preset, n, wseed, over, policy, schedule, qpm, aseed, tm, seed, rho, dmode,
+             conf) in specs:
+            params = P[preset].synthetic
+            orch = dataclasses.replace(P[preset].orchestrator, **over)
+            workload = generate_synthetic(params, n, seed=wseed)
+            arrivals = gen_arrivals(ArrivalConfig(rate_qpm=qpm, n_requests=n, seed=aseed))
+            timing = TimingModel(*tm)
+            report, logs = run_simulation(workload, orch, policy, schedule, arrivals, timing,
+                                          seed, synthetic=SyntheticPredictorConfig(rho=rho),
+                                          difficulty_mode=dmode, confusion=conf)
+            cpath, jpath = Path(tmp) / "r.csv", Path(tmp) / "r.json"
+            write_results_csv(logs, policy, schedule, cpath)
+            write_summary_json(report.to_dict(), jpath)
+            orch_d = dataclasses.asdict(orch)
+            orch_d["early_term_threshold"] = float(orch_d["early_term_threshold"]).hex()
+            cases.append({"name": name, "params": dataclasses.asdict(params), "n": n,
+                          "workload_seed": wseed, "orchestrator": orch_d, "policy": policy,
+                          "schedule": schedule, "qpm": qpm, "arrival_seed": aseed,
+                          "arrivals": arrivals, "timing": list(tm), "seed": seed, "rho": rho,
+                          "difficulty_mode": dmode, "confusion": conf,
+                          "csv": cpath.read_bytes().decode(), "json": jpath.read_bytes().decode()})
+    return cases
+
+
 def main():
     (OUT / "decisions.json").write_text(json.dumps(decisions(), separators=(",", ":")))
     (OUT / "baselines.json").write_text(json.dumps(baselines(), separators=(",", ":")))
     (OUT / "primitives.json").write_text(json.dumps(primitives(), separators=(",", ":")))
+    (OUT / "simulation.json").write_text(json.dumps(simulation(), separators=(",", ":")))
     for p in sorted(OUT.glob("*.json")):
         print(p.name, p.stat().st_size)
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "simulation":
+        (OUT / "simulation.json").write_text(json.dumps(simulation(), separators=(",", ":")))
+    else:
+        main()
