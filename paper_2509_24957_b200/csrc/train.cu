@@ -127,10 +127,9 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
             const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
             if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                dots[q] = fmaf(wv[j][2 * e], bf16lo(xw[e]), dots[q]);
-                dots2[q] = fmaf(wv[j][2 * e + 1], bf16hi(xw[e]), dots2[q]);
-              }
+              for (int e = 0; e < 4; ++e)
+                ffma2(dots[q], dots2[q], wv[j][2 * e], wv[j][2 * e + 1], bf16lo(xw[e]),
+                      bf16hi(xw[e]));
             } else {
 #pragma unroll
               for (int e = 0; e < 4; e += 2) {
@@ -151,18 +150,23 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
       }
     }
     consumer_bar();
+    // lane q computes row q's residual (fixed-order sum of the warp partials),
+    // then every lane takes it by shuffle
+    float mine = 0.f;
+    if (lane < nr) {
+      float z = bias;
+#pragma unroll
+      for (int k = 0; k < kConsWarps; ++k) z += red[buf][k][lane];
+      float yl = 0.f;
+#pragma unroll
+      for (int q = 0; q < RB; ++q) yl = lane == q ? yv[q] : yl;
+      mine = 1.0f / (1.0f + expf(-z)) - yl;
+    }
     float res[RB];
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      res[q] = 0.f;
-      if (q < nr) {
-        float z = bias;
-#pragma unroll
-        for (int k = 0; k < kConsWarps; ++k) z += red[buf][k][q];
-        const float sig = 1.0f / (1.0f + expf(-z));
-        res[q] = sig - yv[q];
-        gb += res[q];
-      }
+      res[q] = __shfl_sync(0xffffffffu, mine, q);
+      gb += res[q];                                  // res = 0 for q >= nr
     }
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
@@ -176,10 +180,8 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
             const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
             if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                g[j][2 * e] += res[q] * bf16lo(xw[e]);
-                g[j][2 * e + 1] += res[q] * bf16hi(xw[e]);
-              }
+              for (int e = 0; e < 4; ++e)
+                ffma2(g[j][2 * e], g[j][2 * e + 1], res[q], res[q], bf16lo(xw[e]), bf16hi(xw[e]));
             } else {
 #pragma unroll
               for (int e = 0; e < 4; ++e) g[j][e] += res[q] * __uint_as_float(xw[e]);
