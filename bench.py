@@ -307,9 +307,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
 def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank=None):
     """Same step through the public API with the activations in pinned HOST
-    memory: per step H2D of the activation window slab, the round (one fused
-    launch, or advance / K1 / decide when split), and a D2H read of the round
-    records and actions (RoundReports)."""
+    memory: per step the H2D copy of the round's inputs (the survivors'
+    windows, gathered by one kernel over the device-side active list; the
+    whole slab for the other variants), the round (K1 + duchess_round, or one
+    fused launch), and a D2H read of the round records and actions
+    (RoundReports)."""
     import torch
     steps = max(2, min(args.e2e_steps, args.steps))
     host = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
@@ -320,18 +322,28 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, 
     from paper_2509_24957_b200 import _lib
     stream = torch.cuda.current_stream(dev)
 
+    survivors_only = args.mode == "split" and args.k1 == "list"
+
     def step():
-        dslab.copy_(host, non_blocking=True)
+        if survivors_only:
+            # only the windows of this round's survivors cross PCIe (the
+            # active list is on the device; one gather kernel reads them)
+            eng.upload_survivors(host, dslab)
+        else:
+            dslab.copy_(host, non_blocking=True)
         if args.mode == "fused":
             eng.step_fused(dslab, bank, logit.view(-1))
             rec_host.copy_(eng.t["round_rec"], non_blocking=True)
             act_host.copy_(eng.t["actions"], non_blocking=True)
             stream.synchronize()
             return
-        eng.advance()
-        scorer.score_active(dslab, logit, probs, eng) \
-            if args.k1 == "list" else scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
-        eng.decide()
+        # the round in flight was advanced by the previous round(): score it,
+        # decide it and advance into the next one, exactly as the timed loop
+        if args.k1 == "list":
+            scorer.score_active(dslab, logit, probs, eng)
+        else:
+            scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
+        eng.round()
         rec_host.copy_(eng.t["round_rec"], non_blocking=True)
         act_host.copy_(eng.t["actions"], non_blocking=True)
         stream.synchronize()
@@ -352,8 +364,13 @@ def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, 
         b = st[1:].clone()
         torch.distributed.all_reduce(b, op=torch.distributed.ReduceOp.SUM)
         dt, bs = float(a[0]), float(b[0])
+    row_bytes = host[0].numel() * host.element_size()
+    h2d = (bs / steps / max(world, 1) * row_bytes if survivors_only
+           else host.numel() * host.element_size())
     return {"value": bs / dt, "unit": UNIT,
-            "h2d_bytes_per_step": host.numel() * host.element_size(),
+            "h2d_bytes_per_step": h2d,
+            "h2d": ("survivor windows only (duchess_gather_active over the active list), "
+                    "average per rank" if survivors_only else "whole activation slab"),
             "d2h_bytes_per_step": (rec_host.numel() + act_host.numel()) * 4,
             "steps": steps, "timing": "host wall clock, stream-synchronised each step"}
 

@@ -226,6 +226,13 @@ int duchess_score_active(const void* acts, int32_t dtype, int64_t n_rows, int32_
                          int64_t token_stride, const float* wg, const float* c1,
                          const int32_t* active_rows, const int32_t* active_count,
                          float* out_logit, double* out_prob, void* stream);
+/* End-to-end input path: copy only the survivor rows (the engine's active list,
+ * as duchess_score_active reads it) of an [n_rows, row_bytes] activation array
+ * from src — pinned HOST memory (read over PCIe through its device mapping) or
+ * device memory — into the same rows of the device array dst. */
+int duchess_gather_active(const void* src, void* dst, int64_t row_bytes,
+                          const int32_t* active_rows, const int32_t* active_count,
+                          int64_t n_rows, void* stream);
 int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
                              int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
                              int64_t token_stride, uint64_t seed, const int64_t* row_req,

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) score_generic_kernel(ScoreArgs a) {
 // warps pool + LayerNorm + dot. Windows come from a compacted row list
 // (written by duchess_advance) or from all rows filtered by the mask.
 template <bool BF16, int VPT>
-__global__ void __launch_bounds__(kTmaCons + 32) score_tma_kernel(ScoreArgs a, TmaArgs t) {
+__global__ void __launch_bounds__(kTmaCons + 32, 2) score_tma_kernel(ScoreArgs a, TmaArgs t) {
   constexpr int ESZ = BF16 ? 2 : 4;
   extern __shared__ __align__(128) char ring[];
   __shared__ uint64_t full_bar[32], empty_bar[32];
@@ -316,6 +316,42 @@ __global__ void __launch_bounds__(256) fill_kernel(char* acts, int64_t row_strid
     const int64_t idx = off + int64_t(t) * token_stride + h;
     if constexpr (BF16) reinterpret_cast<uint16_t*>(acts)[idx] = f32_to_bf16_rne(x);
     else reinterpret_cast<float*>(acts)[idx] = x;
+  }
+}
+
+// Copy the listed rows of src (pinned host memory mapped into the device
+// address space, or device memory) into the same rows of dst: only the
+// survivors' windows cross PCIe. One CTA per listed row, 16-byte loads with
+// 8 in flight per thread.
+__global__ void __launch_bounds__(512) gather_rows_kernel(const char* src, char* dst,
+                                                          int64_t row_bytes,
+                                                          const int32_t* rows,
+                                                          const int32_t* count,
+                                                          const int32_t* par, int64_t stride) {
+  int64_t n = *count;
+  if (par) {
+    const int p = *par;
+    rows += p * stride;
+    n = count[p];
+  }
+  const int64_t nv = row_bytes / 16;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t row = rows[i];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + row * row_bytes);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + row * row_bytes);
+    for (int64_t v = threadIdx.x; v < nv; v += 8 * blockDim.x) {
+      uint4 buf[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t j = v + int64_t(k) * blockDim.x;
+        if (j < nv) buf[k] = __ldcg(s4 + j);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t j = v + int64_t(k) * blockDim.x;
+        if (j < nv) __stcs(d4 + j, buf[k]);
+      }
+    }
   }
 }
 
@@ -508,4 +544,25 @@ extern "C" int duchess_score_active(const void* acts, int32_t dtype, int64_t n_r
   return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
                     wg, c1, nullptr, active_rows, active_count, out_logit, out_prob, nullptr, 0, 0,
                     0, stream, active_count + 2, n_rows);
+}
+
+extern "C" int duchess_gather_active(const void* src, void* dst, int64_t row_bytes,
+                                     const int32_t* active_rows, const int32_t* active_count,
+                                     int64_t n_rows, void* stream) {
+  if (!src || !dst || !active_rows || !active_count || row_bytes <= 0 || row_bytes % 16 ||
+      n_rows < 0 || (reinterpret_cast<uintptr_t>(src) % 16) || (reinterpret_cast<uintptr_t>(dst) % 16))
+    return DUCHESS_EINVAL;
+  if (n_rows == 0) return DUCHESS_OK;
+  const void* s = src;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+    void* dp = nullptr;                          // pinned host memory: its device mapping
+    if (cudaHostGetDevicePointer(&dp, const_cast<void*>(src), 0) != cudaSuccess) return DUCHESS_EINVAL;
+    s = dp;
+  }
+  cudaGetLastError();
+  gather_rows_kernel<<<sm_count() * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char*>(s), static_cast<char*>(dst), row_bytes, active_rows, active_count,
+      active_count + 2, n_rows);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

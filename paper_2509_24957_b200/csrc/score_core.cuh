@@ -190,30 +190,36 @@ __device__ __forceinline__ void tma_consume(const ScoreArgs& a, const TmaArgs& t
       if (++s == t.stages) { s = 0; ph ^= 1u; }
     }
     const float* wrow = a.wg + int64_t(l) * a.H;
-    float wgv[VPT][VEC];
-    float s1 = 0.f, sw = 0.f;
+    float s1 = 0.f, unused = 0.f;
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const int v = j * kTmaCons + int(threadIdx.x);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const bool ok = v < nvec;
         acc[j][e] = pow2T ? __fmul_rn(acc[j][e], invT) : __fdiv_rn(acc[j][e], float(a.T));
-        wgv[j][e] = ok ? __ldg(wrow + v * VEC + e) : 0.f;
-        if (ok) { s1 = __fadd_rn(s1, acc[j][e]); sw = __fadd_rn(sw, wgv[j][e]); }
+        if (v < nvec) s1 = __fadd_rn(s1, acc[j][e]);
       }
     }
-    cons_sum2(s1, sw, red, k);
+    cons_sum2(s1, unused, red, k);
     const float mean = __fdiv_rn(s1, float(a.H));
+    // second pass: centred square sum and probe dot, one packed FFMA2 per
+    // element ({c*c + qq, w*c + d}); the folded weights come from L1/L2
     float qq = 0.f, d = 0.f;
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
-      if (j * kTmaCons + int(threadIdx.x) < nvec) {
+      const int v = j * kTmaCons + int(threadIdx.x);
+      if (v < nvec) {
+        const float4* w4 = reinterpret_cast<const float4*>(wrow + v * VEC);
+        float wv[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC / 4; ++q) {
+          const float4 t4 = __ldg(w4 + q);
+          wv[4 * q] = t4.x; wv[4 * q + 1] = t4.y; wv[4 * q + 2] = t4.z; wv[4 * q + 3] = t4.w;
+        }
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
           const float c = __fsub_rn(acc[j][e], mean);
-          qq = __fmaf_rn(c, c, qq);
-          d = __fmaf_rn(wgv[j][e], c, d);
+          ffma2(qq, d, c, wv[e], c, c);
         }
       }
     }

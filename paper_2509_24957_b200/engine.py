@@ -328,6 +328,27 @@ class BatchedDuchess:
         RC = self.R * self.C
         return self.fx["rows"][par * RC: par * RC + n], n
 
+    def upload_survivors(self, host_acts: torch.Tensor, dev_acts: torch.Tensor,
+                         stream=None) -> None:
+        """Copy only the survivor rows of the round in flight (the active list)
+        from pinned host memory host_acts [R*C, ...] into the same rows of
+        dev_acts (duchess_gather_active: one kernel, PCIe reads of the listed
+        rows only). Both arrays contiguous with identical shape / dtype."""
+        if host_acts.shape != dev_acts.shape or host_acts.dtype != dev_acts.dtype:
+            raise ValueError("host and device activation arrays must match")
+        if not host_acts.is_pinned() or not dev_acts.is_cuda:
+            raise ValueError("host_acts must be pinned host memory, dev_acts a CUDA tensor")
+        if not (host_acts.is_contiguous() and dev_acts.is_contiguous()):
+            raise ValueError("activation arrays must be contiguous")
+        rows = host_acts.shape[0]
+        if rows != self.R * self.C:
+            raise ValueError("activation arrays must have R*C rows")
+        row_bytes = host_acts[0].numel() * host_acts.element_size()
+        _lib.check(self.lib.duchess_gather_active(
+            host_acts.data_ptr(), dev_acts.data_ptr(), row_bytes,
+            self.t["active_rows"].data_ptr(), self.t["active_count"].data_ptr(), rows,
+            _lib.stream_handle(stream)), "duchess_gather_active")
+
     def active_list(self):
         """(rows, count) device views of the survivor list the next scorer
         launch reads (duchess_score_list): the parity duchess_round flips

@@ -144,3 +144,29 @@ def test_fused_step_steady_state_matches_split_kernels():
         rb = sorted((p, rep) for p, rep in b.round_reports())
         assert ra == rb, f"step {step}"
     assert (a.counters()[:5] == b.counters()[:5]).all()
+
+
+def test_upload_survivors_copies_only_listed_rows():
+    """duchess_gather_active: exactly the rows of the round in flight's active
+    list (either parity) arrive from pinned host memory; others untouched."""
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    knobs, traces, seeds = _setup(40, 8, 1.0)
+    R, C = 6, 8
+    eng = BatchedDuchess(traces, knobs, seeds, n_slots=R, pred_source=_lib.PRED_DEVICE,
+                         queue=list(range(len(traces))), cycle=True)
+    host = torch.randint(-1000, 1000, (R * C, 1, 3, 64), dtype=torch.int16).view(
+        torch.bfloat16).pin_memory()
+    eng.advance()
+    for step in range(6):
+        dev = torch.zeros_like(host, device="cuda")
+        eng.upload_survivors(host, dev)
+        torch.cuda.synchronize()
+        mask = eng.t["row_mask"].cpu().numpy().astype(bool)
+        d = dev.cpu().view(torch.int16)
+        h = host.view(torch.int16)
+        assert mask.any()
+        assert torch.equal(d[torch.from_numpy(mask)], h[torch.from_numpy(mask)])
+        assert not d[torch.from_numpy(~mask)].any()
+        eng.probs.fill_(0.5)
+        eng.round()
