@@ -598,10 +598,10 @@ def run_train_bench(args, rank, world, local_rank):
 # CPU reference (oracle port) — only here and in tests may oracle/ run.
 
 _CPU = {}
+CPU_POOL_BYTES = 64 << 20      # activation windows per CPU process (16 processes: 1 GiB)
 
 
 def _cpu_init(cfg_name, n_req, seed):
-    import oracle.activations as oact
     from oracle import port
     cfg = CONFIGS[cfg_name]
     H, T, L = cfg["H"], cfg["T"], cfg["L"]
@@ -611,10 +611,22 @@ def _cpu_init(cfg_name, n_req, seed):
     master = random.Random(seed + 1)
     seeds = [master.getrandbits(64) for _ in traces]
     w, b, g, beta = make_probe(H, L)
-    windows = [[oact.synth_window(7000 + k, k, 0, 0, l, T, H, cfg["dtype"] == "bf16")
-                for l in range(L)] for k in range(16)]
+    # Distinct windows streamed from DRAM like the GPU arm streams HBM: a
+    # per-process pool of CPU_POOL_BYTES (> the host caches), each branch-step
+    # scoring the next window. Values are bf16-rounded for bf16 configs but kept
+    # in fp32, so the CPU pays no conversion the GPU does in registers.
+    bf16 = cfg["dtype"] == "bf16"
+    n_pool = max(16, CPU_POOL_BYTES // (L * T * H * 4))
+    rng = np.random.default_rng(os.getpid())
+    pool = []
+    for _ in range(n_pool):
+        x = rng.standard_normal((L, T, H), dtype=np.float32)
+        if bf16:
+            u = x.view(np.uint32)
+            x = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).view(np.float32)
+        pool.append(x)
     _CPU.update(traces=traces, knobs=knobs, seeds=seeds, w=w, b=b, g=g, beta=beta,
-                windows=windows, L=L, next=0)
+                windows=pool, L=L, next=0, cursor=0)
 
 
 def _cpu_run(budget_s):
@@ -624,7 +636,8 @@ def _cpu_run(budget_s):
 
     def predictor(tmpl, position, _rng):
         count[0] += 1
-        win = st["windows"][(position * 31 + tmpl.natural_length) % len(st["windows"])]
+        win = st["windows"][st["cursor"] % len(st["windows"])]
+        st["cursor"] += 1
         ps = [port.pooled_linear_probe(win[l], st["w"][l], st["b"][l], st["g"][l],
                                        st["beta"][l])[1] for l in range(st["L"])]
         return ps[0] if len(ps) == 1 else sum(ps) / len(ps)
@@ -666,7 +679,9 @@ def cpu_baseline_entry(cfg_name, budget_total=12.0):
     return {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
             "sample": f"oracle/port.py DuchessRun restatement + numpy pooled LN probe "
                       f"(T={cfg['T']}, H={cfg['H']}, L={cfg['L']}) on {cfg['preset']} requests "
-                      f"(c={cfg['c']}), {procs} processes x {steps} x {budget_total/steps:.1f} s"}
+                      f"(c={cfg['c']}), each branch-step scoring the next of a 64 MiB pool of "
+                      f"distinct windows per process, {procs} processes x {steps} x "
+                      f"{budget_total/steps:.1f} s"}
 
 
 def cpu_fork_or_train(args):
@@ -755,7 +770,9 @@ def run_reference(args, cfg):
                                         "window": cfg["T"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": f"{procs} processes x {budget:.2f} s per step of "
-                                   f"oracle/port.py DuchessRun + numpy pooled probe"},
+                                   f"oracle/port.py DuchessRun + numpy pooled probe, each "
+                                   f"branch-step scoring the next of a 64 MiB pool of distinct "
+                                   f"windows per process (streamed from DRAM like the GPU arm)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
