@@ -205,7 +205,6 @@ def run_gpu(args, cfg, rank, world, local_rank):
         # `k1_every`-th timed step: an event record between two PDL-chained
         # kernels breaks their overlap, so sampling keeps the measurement from
         # inflating the step time.
-        timed = timed and (i % args.k1_every == 0)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -235,18 +234,42 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
+    graph = None
+    if args.graph:
+        # CUDA graph of one slab rotation (n_slabs rounds = 2*n_slabs launches,
+        # PDL edges kept), replayed; removes the host launch cost that bounds
+        # small configs. K1 is timed with events in an eager pass afterwards.
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for j in range(n_slabs):
+                one_step(args.warmup + j, False)
+        args.steps = -(-args.steps // n_slabs) * n_slabs
+        graph.replay()                  # one rotation untimed (warm the graph)
+        torch.cuda.synchronize(dev)
+        c0 = eng.t["counters"].clone()
     clocks = ClockSampler(local_rank) if rank == 0 else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for i in range(args.steps):
-        one_step(args.warmup + i, True)
+    if graph is not None:
+        for _ in range(args.steps // n_slabs):
+            graph.replay()
+    else:
+        for i in range(args.steps):
+            one_step(args.warmup + i, i % args.k1_every == 0)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None
+    if graph is not None:
+        # event timing inside a replayed graph is not meaningful: K1 is timed
+        # in an eager pass right after the timed region (same state, shapes)
+        cnt_g = (eng.t["counters"] - c0).cpu().numpy()
+        for i in range(8 * args.k1_every):
+            one_step(i, i % args.k1_every == 0)
+        torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
-    cnt = (eng.t["counters"] - c0).cpu().numpy()
+    cnt = cnt_g if graph is not None else (eng.t["counters"] - c0).cpu().numpy()
     branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
     k1_ms = sum(a.elapsed_time(b) for a, b in k1_ev) / max(len(k1_ev), 1) * args.steps
     stats = torch.tensor([ms, float(branch_steps), k1_ms], dtype=torch.float64, device=dev)
@@ -281,6 +304,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    f"(easiest-first), {n_slabs} rotating activation slabs "
                    f"({rows * L * T * H * esz / 2**30:.2f} GiB each, > L2)",
                    "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
+                   "launch": "CUDA graph replay" if args.graph else "eager stream (PDL)",
                    "l2": "inputs larger than L2 (rotating slabs)",
                    "parallelism": f"request-sharded x{world}"},
         "branch_steps_per_step": branch_steps / args.steps,
@@ -291,7 +315,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                      "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_share_of_step": k1_ms / ms,
-                     "k1_launches_timed": len(k1_ev),
+                     "k1_launches_timed": (f"{len(k1_ev)} (eager pass after the timed graph "
+                                           f"replays)") if args.graph else len(k1_ev),
                      "traffic": (None if k1_traffic_ratio()[0] is None
                                  else k1_traffic_ratio()[0] * bytes_per_launch),
                      "traffic_source": k1_traffic_ratio()[1]},
@@ -790,6 +815,8 @@ def main():
     ap.add_argument("--mode", default="split", choices=["fused", "split"],
                     help="split (default): K1 launch + duchess_round launch per round; "
                          "fused: one duchess_step launch per round (see DESIGN.md 7)")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the round loop as a CUDA graph (one slab rotation per graph)")
     ap.add_argument("--k1-every", type=int, default=4,
                     help="bracket K1 with CUDA events on every N-th timed step")
     ap.add_argument("--nsplit", type=int, default=2)
