@@ -357,6 +357,20 @@ int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, i
                          const float* s, const float* c, const float* w2, float b2,
                          float* out_logit, double* out_prob, void* stream);
 
+/* ---- tensor-core linear layer with fused epilogue (tcgen05 + TMEM + TMA) --
+ * One hidden layer of mlp_forward (predictor.py:126-151) batched over M rows:
+ * pre = ln_fold ? (X.W'_j)/sigma_i - (mu_i/sigma_i) S_j + C_j : X.W_j + C_j,
+ * out = act(pre * BS_j + BT_j) as bf16 [M, N] (act 0 none, 1 relu, 2 gelu).
+ * X [M, K] bf16, W [N, K] bf16 (K-major); K % 64 == 0, N % 256 == 0. With
+ * ln_fold the input LayerNorm is folded in (W' = W diag(gain), S = W' 1,
+ * C = W ln_bias + b; row mean / std computed on the device). */
+int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
+                      int32_t ln_fold, const float* S, const float* C, const float* BS,
+                      const float* BT, int32_t act, void* out, void* stream);
+/* Small classifier head: logits[M, n_out] = H (bf16 [M, K]) . W^T (fp32 [n_out, K]) + b. */
+int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W, const float* b,
+                        int32_t n_out, float* logits, void* stream);
+
 /* ---- difficulty ordering (scheduler.py:60-96) --------------------------- */
 int duchess_sort_difficulty(const uint64_t* keys, const int32_t* seg_offsets, int32_t n_segs,
                             int32_t* out_perm, void* stream);

@@ -1,0 +1,304 @@
+// Tensor-core linear layer with a fused per-column epilogue (tcgen05 + TMEM +
+// TMA), sm_100a: the hidden layers of the reference's MLP forward
+// (predictor.py:126-151) batched over M input rows. Used by the complexity
+// (difficulty) classifier, 4096 -> 2048 -> 1024 -> 512 -> 5 with batch-norm
+// and GeLU, which the reference evaluates one
+// vector at a time in fp64.
+//
+//   pre[i, j] = ln_fold ? (X_i . W'_j) / sigma_i - (mu_i / sigma_i) S_j + C_j
+//                       :  X_i . W_j + C_j
+//   y[i, j]   = act(pre[i, j] * BS_j + BT_j)        (act: none / relu / gelu)
+//
+// With ln_fold the input LayerNorm (predictor.py:134-138) is folded into the
+// first layer: W' = W diag(ln_gain), S = W' 1, C = W ln_bias + b; mu / sigma
+// are the row's population mean / std (eps 1e-5). BS / BT fold the
+// inference batch-norm (predictor.py:141-143). Output bf16 (next layer's
+// input) row-major [M, N].
+//
+// One CTA per (128-row, 256-column) tile: warp 0 TMA producer (A = X[128x64],
+// B = W[256x64] bf16, 128B swizzle, 4-stage ring), warp 1 TMEM allocator +
+// single-thread tcgen05.mma issuer (M128 N256 K16, fp32 accumulate), warps
+// 2-5 row statistics (first layer) and the epilogue (tcgen05.ld 32 columns at
+// a time, fold, activation, bf16 store).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "../../include/duchess_b200.h"
+
+namespace duchess {
+namespace tcl {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+constexpr int B_BYTES = BN * BK * 2;            // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
+constexpr int THREADS = 192;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+
+struct Args {
+  int64_t M;
+  int K, N;
+  int ln_fold, act;
+  const uint16_t* X;
+  const float* S;
+  const float* C;
+  const float* BS;
+  const float* BT;
+  uint16_t* out;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// kind::f16, A/B bf16 K-major, D fp32, M=128, N=256.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                           (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Exact (erf-based) GeLU, predictor.py:106-110.
+__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+              Args a) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int k_blocks = a.K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ---- TMA producer ----
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty_bar[s], ((kb / STAGES) & 1) ^ 1u);
+        char* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        tma_load_2d(st, &map_a, kb * BK, m0, &full_bar[s]);
+        tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                   // ---- MMA issuer ----
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full_bar[s], (kb / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const char* st = smem + s * STAGE_BYTES;
+        const uint64_t da = desc_sw128(st), db = desc_sw128(st + A_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          mma(tmem, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+        commit(&empty_bar[s]);
+      }
+      commit(&tmem_full);
+    }
+  } else {
+    // ---- statistics + epilogue: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
+    const int q = warp & 3;
+    const int64_t row = m0 + 32 * q + lane;
+    float rsig = 1.f, shift = 0.f;
+    if (a.ln_fold) {                                   // overlaps the MMAs
+      float sx = 0.f, sxx = 0.f;
+      if (row < a.M) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+        const int nv = a.K / 8;
+        for (int v0 = 0; v0 < nv; v0 += 8) {
+          uint4 buf[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) buf[u] = v0 + u < nv ? __ldg(rp + v0 + u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t w4[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+              sx += lo + hi;
+              sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+            }
+          }
+        }
+      }
+      const float mean = sx / float(a.K);
+      const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
+      rsig = rsqrtf(var + kLayerNormEps);
+      shift = mean * rsig;
+    }
+    mbar_wait(&tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t base = tmem + (uint32_t(32 * q) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(base + uint32_t(c0), v);
+      const int j0 = n0 + c0;
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float y[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = j0 + i + h;
+          float pre = a.ln_fold ? fmaf(v[i + h], rsig, fmaf(-shift, __ldg(a.S + j), __ldg(a.C + j)))
+                                : v[i + h] + __ldg(a.C + j);
+          pre = fmaf(pre, __ldg(a.BS + j), __ldg(a.BT + j));
+          y[h] = a.act == 1 ? fmaxf(pre, 0.f) : a.act == 2 ? gelu(pre) : pre;
+        }
+        packed[i / 2] = uint32_t(f32_to_bf16_rne(y[0])) | (uint32_t(f32_to_bf16_rne(y[1])) << 16);
+      }
+      if (row < a.M) {
+        uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.N + j0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          dst[u] = make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+// Classifier head (N small, e.g. 5): one warp per row, fp32 dots over the
+// bf16 hidden vector, logits out.
+__global__ void head_kernel(const uint16_t* Hm, int64_t M, int K, const float* W, const float* b,
+                            int NO, float* logits) {
+  const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const uint16_t* h = Hm + row * K;
+  for (int o = 0; o < NO; ++o) {
+    float acc = 0.f;
+    for (int k = lane; k < K; k += 32) acc = fmaf(__uint_as_float(uint32_t(h[k]) << 16), W[int64_t(o) * K + k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) logits[row * NO + o] = acc + b[o];
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                     uint32_t box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {uint32_t(BK), box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace tcl
+}  // namespace duchess
+
+using namespace duchess;
+
+extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
+                                 int32_t ln_fold, const float* S, const float* C, const float* BS,
+                                 const float* BT, int32_t act, void* out, void* stream) {
+  if (!X || !W || !C || !BS || !BT || !out || (ln_fold && !S)) return DUCHESS_EINVAL;
+  if (M < 0 || K < tcl::BK || K % tcl::BK || N < tcl::BN || N % tcl::BN || act < 0 || act > 2)
+    return DUCHESS_EINVAL;
+  if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16 ||
+      reinterpret_cast<uintptr_t>(out) % 16)
+    return DUCHESS_EINVAL;
+  if (M == 0) return DUCHESS_OK;
+  CUtensorMap ma, mb;
+  if (!tcl::make_map(&ma, X, uint64_t(M), uint64_t(K), tcl::BM)) return DUCHESS_ECUDA;
+  if (!tcl::make_map(&mb, W, uint64_t(N), uint64_t(K), tcl::BN)) return DUCHESS_ECUDA;
+  tcl::Args a{M, K, N, ln_fold, act, static_cast<const uint16_t*>(X), S, C, BS, BT,
+              static_cast<uint16_t*>(out)};
+  cudaFuncSetAttribute(tcl::linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl::SMEM);
+  const dim3 grid(unsigned((M + tcl::BM - 1) / tcl::BM), unsigned(N / tcl::BN));
+  tcl::linear_kernel<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W,
+                                   const float* b, int32_t n_out, float* logits, void* stream) {
+  if (!H || !W || !b || !logits || M < 0 || K < 1 || n_out < 1) return DUCHESS_EINVAL;
+  if (M == 0) return DUCHESS_OK;
+  tcl::head_kernel<<<unsigned((M + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(H), M, K, W, b, n_out, logits);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}

@@ -1,0 +1,81 @@
+"""Tensor-core difficulty classifier: tcgen05 hidden layers
+with LayerNorm / batch-norm / GeLU fused, checked against the fp64 forward
+(the facade's duchess_mlp_forward and the CPU oracle restatement of
+predictor.py:126-151). Levels (argmax + 1) must equal the fp64 ones for every
+row; logits within the bf16-chain tolerance stated below."""
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def complexity_mlp(seed, dims, head=5, act="gelu", batchnorm=True, layernorm=True):
+    from paper_2509_24957_b200.predictor import MlpWeights
+    rng = np.random.default_rng(seed)
+    hid = list(dims[1:])
+    full = [dims[0], *hid, head]
+    W = [rng.normal(0, 1 / np.sqrt(full[k]), (full[k + 1], full[k])) for k in range(len(full) - 1)]
+    W[-1] *= 3.0                                    # spread the 5 logits
+    b = [rng.normal(0, 0.1, full[k + 1]) for k in range(len(full) - 1)]
+    bn = dict(bn_mean=[rng.normal(0, 0.1, d) for d in hid],
+              bn_var=[rng.uniform(0.5, 2.0, d) for d in hid],
+              bn_gain=[rng.uniform(0.5, 1.5, d) for d in hid],
+              bn_bias=[rng.uniform(-0.1, 0.1, d) for d in hid]) if batchnorm else {}
+    ln = dict(ln_gain=rng.uniform(0.5, 1.5, dims[0]),
+              ln_bias=rng.uniform(-0.1, 0.1, dims[0])) if layernorm else {}
+    return MlpWeights(dims[0], hid, head, [act] * len(hid), W, b, **ln, **bn)
+
+
+def activations(seed, M, H):
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0, 1, (M, H))
+    x[:, 257::512] *= 20.0                          # outlier channels, as in real activations
+    return x
+
+
+@pytest.mark.parametrize("dims,act,bn,ln,M", [
+    ((4096, 2048, 1024, 512), "gelu", True, True, 1000),    # the paper's complexity MLP
+    ((512, 256, 256), "relu", False, True, 37),
+    ((1024, 512), "gelu", True, False, 300),
+])
+def test_tc_classifier_matches_fp64(dims, act, bn, ln, M):
+    from paper_2509_24957_b200.difficulty import TensorCoreClassifier
+    from paper_2509_24957_b200.predictor import mlp_forward_batch
+    w = complexity_mlp(1, dims, act=act, batchnorm=bn, layernorm=ln)
+    X = activations(2, M, dims[0])
+    clf = TensorCoreClassifier(w)
+    lg = clf.logits(X).cpu().numpy()
+    ref_logits, ref_probs = mlp_forward_batch(w, X)
+    err = np.abs(lg - ref_logits).max()
+    # bf16 operands and bf16 inter-layer activations, fp32 accumulation: the
+    # logit error stays far below the fallback margin / 2 (0.125)
+    assert err < 0.05, err
+    levels = clf.predict_levels(X)
+    assert (levels == ref_probs.argmax(axis=1) + 1).all()
+    for i in range(3):                              # fp64 device path == CPU oracle
+        o_logits, _ = port.mlp_forward(w, X[i])
+        assert np.allclose(ref_logits[i], o_logits, rtol=1e-9, atol=1e-9)
+
+
+def test_tc_classifier_shape_errors():
+    from paper_2509_24957_b200.difficulty import TensorCoreClassifier
+    from paper_2509_24957_b200.predictor import WeightFormatError
+    w = complexity_mlp(3, (512, 256))
+    clf = TensorCoreClassifier(w)
+    with pytest.raises(WeightFormatError):
+        clf.logits(np.zeros((4, 500)))
+    with pytest.raises(ValueError):
+        TensorCoreClassifier(complexity_mlp(3, (500, 256)))
+
+
+def test_predict_difficulty_batch_equals_single_calls():
+    from paper_2509_24957_b200.predictor import predict_difficulty, predict_difficulty_batch
+    w = complexity_mlp(4, (512, 256, 256))
+    X = activations(5, 40, 512)
+    batch = predict_difficulty_batch(w, X)
+    single = [predict_difficulty("mlp", activation=x, weights=w) for x in X[:10]]
+    assert batch[:10] == single
+    assert set(batch) <= {1, 2, 3, 4, 5}
