@@ -330,6 +330,217 @@ def run_gpu(args, cfg, rank, world, local_rank):
     return out
 
 
+def run_gpu_sharded(args, cfg, rank, world, local_rank):
+    """C2/C3 with the GPU's request slots split into `shards` independent
+    engines (interleaved request pools), each stepping on its own CUDA stream:
+    requests never interact, so this is the multi-GPU request
+    sharding applied inside one GPU. The HBM-bound scorer of one shard runs
+    while the latency-bound round kernel of another finishes (the small round
+    CTAs fit beside the scorer's), so the decision kernel leaves the critical
+    path. Same workload as run_gpu: R slots x C branches in total."""
+    import torch
+
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
+    from paper_2509_24957_b200.scheduler import difficulty_queue
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    S = args.shards
+    R, C, L, T, H = cfg["R"], cfg["c"], cfg["L"], cfg["T"], cfg["H"]
+    if R % S:
+        raise SystemExit(f"--shards {S} must divide the {R} request slots")
+    Rs = R // S
+    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    esz = 2 if cfg["dtype"] == "bf16" else 4
+    traces, knobs, seeds = make_workload(cfg, seed=1000 + 17 * rank)
+    w, b, g, beta = make_probe(H, L)
+    bank = ProbeBank.from_linear(w, b, g, beta, device=dev)
+    rows = Rs * C
+    slab_bytes = rows * L * T * H * esz
+    n_slabs = 4 if slab_bytes * S < (256 << 20) else max(2, min(4, int((4 << 30) // (slab_bytes * S)) or 2))
+    shards = []
+    for sh in range(S):
+        tr, sd = traces[sh::S], seeds[sh::S]
+        queue = difficulty_queue([t.difficulty for t in tr], device=dev)
+        eng = BatchedDuchess(tr, knobs, sd, n_slots=Rs, pred_source=_lib.PRED_DEVICE,
+                             queue=queue, cycle=True, n_layers=L, combine=1 if L > 1 else 0,
+                             device=dev)
+        slabs = [torch.empty((rows, L, T, H), dtype=tdtype, device=dev) for _ in range(n_slabs)]
+        for i, sl in enumerate(slabs):
+            fill_windows(sl, 7000 + 31 * rank + 7 * sh + i)
+        shards.append(dict(eng=eng, scorer=Scorer(bank, rows * L), slabs=slabs,
+                           logit=torch.empty((rows, L), dtype=torch.float32, device=dev),
+                           stream=torch.cuda.Stream(dev), ev=[]))
+    main = torch.cuda.current_stream(dev)
+
+    # The scorers of the shards take turns (each waits for the previous one's
+    # event): every K1 launch streams alone at full HBM bandwidth, while the
+    # round kernel of the shard scored just before runs beside it.
+    prev_k1 = [None]
+
+    def step(i, timed):
+        for sh in shards:
+            with torch.cuda.stream(sh["stream"]):
+                st = sh["stream"]
+                if prev_k1[0] is not None:
+                    st.wait_event(prev_k1[0])
+                if timed:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                sh["scorer"].score_active(sh["slabs"][i % n_slabs], sh["logit"],
+                                          sh["eng"].probs.view(rows, L), sh["eng"])
+                done = e1 if timed else torch.cuda.Event()
+                done.record(st)
+                if timed:
+                    sh["ev"].append((e0, e1))
+                prev_k1[0] = done
+                sh["eng"].round()
+
+    def join():
+        for sh in shards:
+            main.wait_stream(sh["stream"])
+
+    def fork():
+        for sh in shards:
+            sh["stream"].wait_stream(main)
+
+    fork()
+    for sh in shards:
+        with torch.cuda.stream(sh["stream"]):
+            sh["eng"].advance()
+    for i in range(args.warmup):
+        step(i, False)
+    join()
+    torch.cuda.synchronize(dev)
+    c0 = [sh["eng"].t["counters"].clone() for sh in shards]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(main)
+    fork()
+    for i in range(args.steps):
+        step(args.warmup + i, i % args.k1_every == 0)
+    join()
+    ev1.record(main)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    if world > 1:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1)
+    cnt = sum((sh["eng"].t["counters"] - c).cpu().numpy() for sh, c in zip(shards, c0))
+    branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
+    k1_us = [a.elapsed_time(b) * 1e3 for sh in shards for a, b in sh["ev"]]
+    k1_avg_s = sum(k1_us) / max(len(k1_us), 1) / 1e6
+    stats = torch.tensor([ms, float(branch_steps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = stats[:1].clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tot = stats[1:2].clone()
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        ms_all, bs_all = float(tmax[0]), float(tot[0])
+    else:
+        ms_all, bs_all = ms, float(branch_steps)
+
+    e2e = run_e2e_sharded(args, shards, rows, L, T, H, tdtype, dev, world, main)
+    if rank != 0:
+        return None
+    bytes_per_bs = T * H * esz * L
+    bytes_per_launch = branch_steps / args.steps / S * bytes_per_bs
+    peak, peak_kind = load_peaks()
+    achieved = bytes_per_launch / k1_avg_s / 1e9
+    return {
+        "metric": METRIC, "value": bs_all / (ms_all / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg["dtype"], "data": "synthetic (counter-hashed N(0,1) activations with "
+        "outlier channels; generate_synthetic workload, random-init probe)",
+        "config": {"workload": f"{args.config.upper()}: {R} request slots x {C} branches, "
+                   f"hidden {H}, {L} probe layer(s), T={T} pooling window, {cfg['dtype']}, "
+                   f"{cfg['preset']} knobs, cycling pool of {cfg['pool']} requests "
+                   f"(easiest-first), {n_slabs} rotating activation slabs per shard "
+                   f"({slab_bytes * S / 2**30:.2f} GiB per rotation, > L2); slots split into "
+                   f"{S} independent request shards on {S} CUDA streams",
+                   "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
+                   "shards_per_gpu": S, "launch": "eager streams (PDL within each shard)",
+                   "l2": "inputs larger than L2 (rotating slabs)",
+                   "parallelism": f"request-sharded x{world} GPUs x{S} streams"},
+        "branch_steps_per_step": branch_steps / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "kernel": "duchess_score (K1, list) per shard launch",
+                     "bytes_per_launch": bytes_per_launch,
+                     "k1_us_per_launch": k1_avg_s * 1e6,
+                     "k1_launches_timed": len(k1_us),
+                     "traffic": (None if k1_traffic_ratio()[0] is None
+                                 else k1_traffic_ratio()[0] * bytes_per_launch),
+                     "traffic_source": k1_traffic_ratio()[1]},
+        "e2e": e2e,
+        "gpu_launches": 2 * S * args.steps,
+        "clocks": clk,
+        "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
+                     "finished_requests": int(cnt[_lib.CNT_FINISHED]),
+                     "forks": int(cnt[_lib.CNT_FORKS])},
+    }
+
+
+def run_e2e_sharded(args, shards, rows, L, T, H, tdtype, dev, world, main):
+    """End to end through the public API with pinned HOST activations, per
+    shard on its stream: upload_survivors (only the survivors' windows cross
+    PCIe), K1, round, D2H of the round records and actions."""
+    import torch
+    from paper_2509_24957_b200 import _lib
+    steps = max(2, min(args.e2e_steps, args.steps))
+    row_bytes = L * T * H * torch.tensor([], dtype=tdtype).element_size()
+    for sh in shards:
+        sh["host"] = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
+        sh["host"].view(-1).zero_()
+        sh["dslab"] = torch.empty_like(sh["host"], device=dev)
+        sh["rec_h"] = torch.empty(sh["eng"].t["round_rec"].numel(), dtype=torch.int32,
+                                  pin_memory=True)
+        sh["act_h"] = torch.empty(sh["eng"].t["actions"].numel(), dtype=torch.int32,
+                                  pin_memory=True)
+
+    def step():
+        for sh in shards:
+            with torch.cuda.stream(sh["stream"]):
+                eng = sh["eng"]
+                eng.upload_survivors(sh["host"], sh["dslab"])
+                sh["scorer"].score_active(sh["dslab"], sh["logit"], eng.probs.view(rows, L), eng)
+                eng.round()
+                sh["rec_h"].copy_(eng.t["round_rec"], non_blocking=True)
+                sh["act_h"].copy_(eng.t["actions"], non_blocking=True)
+        for sh in shards:
+            sh["stream"].synchronize()
+
+    step()
+    c0 = [sh["eng"].t["counters"].clone() for sh in shards]
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    bs = sum(int((sh["eng"].t["counters"] - c)[_lib.CNT_BRANCH_STEPS]) for sh, c in zip(shards, c0))
+    st = torch.tensor([dt, float(bs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        a = st[:1].clone()
+        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
+        b = st[1:].clone()
+        torch.distributed.all_reduce(b, op=torch.distributed.ReduceOp.SUM)
+        dt, bs = float(a[0]), float(b[0])
+    return {"value": bs / dt, "unit": UNIT,
+            "h2d_bytes_per_step": bs / steps / max(world, 1) * row_bytes,
+            "h2d": "survivor windows only (duchess_gather_active over each shard's active "
+                   "list), average per rank",
+            "d2h_bytes_per_step": sum((sh["rec_h"].numel() + sh["act_h"].numel()) * 4
+                                      for sh in shards),
+            "steps": steps, "timing": "host wall clock, streams synchronised each step"}
+
+
 def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank=None):
     """Same step through the public API with the activations in pinned HOST
     memory: per step the H2D copy of the round's inputs (the survivors'
@@ -815,6 +1026,9 @@ def main():
     ap.add_argument("--mode", default="split", choices=["fused", "split"],
                     help="split (default): K1 launch + duchess_round launch per round; "
                          "fused: one duchess_step launch per round (see DESIGN.md 7)")
+    ap.add_argument("--shards", type=int, default=None,
+                    help="independent request shards (engines on separate CUDA streams) per "
+                         "GPU; default 2 for c3, 1 otherwise")
     ap.add_argument("--graph", action="store_true",
                     help="replay the round loop as a CUDA graph (one slab rotation per graph)")
     ap.add_argument("--k1-every", type=int, default=4,
@@ -825,6 +1039,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS.get(args.config)
+    if args.shards is None:
+        # C3 (43 GB per step): two shards hide the round kernel under the other
+        # shard's scorer (+9%). C2 (1 GB per step): the scorer launch's fixed
+        # ramp/tail (~10 us) outweighs the hidden round kernel; one engine.
+        args.shards = 2 if args.config == "c3" else 1
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -842,6 +1061,8 @@ def main():
         out = run_train_bench(args, rank, world, local_rank)
     elif args.config == "c3tc":
         out = run_tc_bench(args, rank, world, local_rank)
+    elif args.mode == "split" and args.k1 == "list" and not args.graph and args.shards > 1:
+        out = run_gpu_sharded(args, cfg, rank, world, local_rank)
     else:
         out = run_gpu(args, cfg, rank, world, local_rank)
     if rank == 0:
