@@ -150,6 +150,10 @@ def decisions():
                  replace(c1, max_branches=48, interval_tokens=32), 0.7, 20),
         run_case("c1_single", replace(gsm.synthetic, templates_per_request=3), 16, 17,
                  replace(c1, max_branches=1, early_term_rounds=1), 0.6, 21),
+        # the device limit: 64 branch slots (both lane sets full), lambda 0.8 pow path
+        run_case("max_c64", replace(gsm.synthetic, templates_per_request=160), 6, 18,
+                 replace(c1, max_branches=64, interval_tokens=24, branch_out_temperature=0.8,
+                         early_term_threshold=0.6, early_term_rounds=1), 0.6, 22),
     ]
     return cases
 
@@ -385,5 +389,7 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "simulation":
         (OUT / "simulation.json").write_text(json.dumps(simulation(), separators=(",", ":")))
+    elif len(sys.argv) > 1 and sys.argv[1] == "decisions":
+        (OUT / "decisions.json").write_text(json.dumps(decisions(), separators=(",", ":")))
     else:
         main()
