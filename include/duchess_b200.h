@@ -353,9 +353,13 @@ int duchess_mlp_forward(const double* params, const int32_t* dims, int32_t n_hid
  * the paper's MLP probe (one ReLU hidden layer, LayerNorm folded) batched as a
  * GEMM. X [M, K] bf16, W1g [NH, K] bf16 (K-major), s/c/w2 [NH] fp32;
  * K % 64 == 0, NH % 256 == 0. out_logit fp32 [M], out_prob fp64 [M]. */
+size_t duchess_mlp_probe_tc_workspace_bytes(int64_t M, int32_t NH);
+/* workspace: >= duchess_mlp_probe_tc_workspace_bytes(M, NH) bytes, 16-byte
+ * aligned, ZEROED before its first use; the kernel keeps it reusable. */
 int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, int32_t NH,
                          const float* s, const float* c, const float* w2, float b2,
-                         float* out_logit, double* out_prob, void* stream);
+                         float* out_logit, double* out_prob, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ---- tensor-core linear layer with fused epilogue (tcgen05 + TMEM + TMA) --
  * One hidden layer of mlp_forward (predictor.py:126-151) batched over M rows:

@@ -9,15 +9,23 @@
 //
 // with W1' = W1 * diag(ln_gain) (bf16), s_j = sum_k W1'_jk, c_j = W1 ln_bias + b1
 // (LayerNorm folded: predictor.py:134-140), mu_i / sigma_i the row's population
-// mean / std (eps 1e-5). One CTA per 128-row tile walks all hidden tiles of 256:
+// mean / std (eps 1e-5).
+//
+// Persistent: one CTA per SM walks work units u = (row tile m, hidden tile h)
+// of 128 rows x 256 hidden units in row-tile-major order (u += gridDim.x), so
+// the grid is busy to within one unit (no 1.73-wave tail) and the 8 units of a
+// row tile run at the same time on 8 CTAs (its A tiles stay L2-resident).
 //   warp 0     TMA producer: A = X[128 x 64] and B = W1'[256 x 64] bf16 tiles
 //              (128B swizzle) into a 4-stage shared-memory ring (mbarrier tx)
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//              (M=128, N=256, K=16, fp32 accumulators in TMEM, double buffered
-//              2 x 256 columns so the epilogue of tile j overlaps MMAs of j+1)
-//   warps 2-5  row statistics (read from global while the first tile's MMAs
-//              run), then the epilogue: tcgen05.ld 32 columns at a time, LN fold, bias,
-//              ReLU, dot with w2 accumulated per row in registers.
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
+//              N=256, K=16, fp32 in TMEM), accumulators double buffered across
+//              units (2 x 256 columns) so unit i's epilogue overlaps unit i+1
+//   warps 2-5  epilogue. Each unit sums its 1/n_tiles share of the row
+//              tile's columns for the LN statistics (during its MMAs) and
+//              publishes it; the units of a row tile combine the shares in
+//              fixed order. Each unit reduces its 256 hidden columns to a
+//              partial logit per row; the row tile's last unit sums the
+//              partials in fixed hidden-tile order (deterministic).
 // The hidden activations never touch HBM.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -44,7 +52,23 @@ struct TcArgs {
   float* out_logit;
   double* out_prob;
   const uint16_t* X;   // row statistics are read straight from global (L2-hot)
+  // workspace (zeroed once by the caller; kept consistent across launches)
+  int* hdr;            // [0] launch epoch, [1] exit counter
+  float2* stats;       // [M * n_tiles] per-unit partial (sum x, sum x^2) of the row
+  float* partial;      // [M * n_tiles] partial logits
+  int* ready;          // [n_row_tiles] published stat partials, cumulative over launches
+  int* done;           // [n_row_tiles] finished hidden tiles
+  int64_t n_units;     // n_row_tiles * n_tiles
 };
+
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void epi_bar() {   // the 4 epilogue warps
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             uint64_t* bar) {
@@ -107,9 +131,9 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   __shared__ uint64_t full_bar[kTcStages], empty_bar[kTcStages];
   __shared__ uint64_t tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base;
+  __shared__ int last_flag;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kTcBM;
   const int n_tiles = a.NH / kTcBN;
   const int k_blocks = a.K / kTcBK;
 
@@ -133,11 +157,13 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
+  const int stamp = a.hdr[0] + 1;          // this launch's "stats ready" stamp
 
   if (warp == 0) {
     if (lane == 0) {   // ---- TMA producer ----
       int it = 0;
-      for (int n = 0; n < n_tiles; ++n) {
+      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        const int m0 = int(u / n_tiles) * kTcBM, n0 = int(u % n_tiles) * kTcBN;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % kTcStages;
           const uint32_t ph = (it / kTcStages) & 1;
@@ -145,16 +171,16 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           char* st = smem + s * kTcStageBytes;
           mbar_expect_tx(&full_bar[s], kTcStageBytes);
           tma_load_2d(st, &map_a, kb * kTcBK, m0, &full_bar[s]);
-          tma_load_2d(st + kTcABytes, &map_b, kb * kTcBK, n * kTcBN, &full_bar[s]);
+          tma_load_2d(st + kTcABytes, &map_b, kb * kTcBK, n0, &full_bar[s]);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {   // ---- MMA issuer ----
-      int it = 0;
-      for (int n = 0; n < n_tiles; ++n) {
-        const int acc = n & 1;
-        mbar_wait(&tmem_empty[acc], ((n >> 1) & 1) ^ 1u);
+      int it = 0, i = 0;
+      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tmem_empty[acc], ((i >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * kTcBN);
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
@@ -173,63 +199,98 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
     }
   } else {
-    // ---- statistics + epilogue warps: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
+    // ---- epilogue warps: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
     const int q = warp & 3;
-    const int row_local = 32 * q + lane;
-    const int64_t row = m0 + row_local;
-    // Row statistics while the first hidden tile's MMAs run: 16-byte loads of the
-    // row from global memory (the TMA producer streams the same rows, so they
-    // are L2-resident), fp32 sums.
-    float sx = 0.f, sxx = 0.f;
-    if (row < a.M) {
-      const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
-      const int nv = a.K / 8;
-      for (int v0 = 0; v0 < nv; v0 += 8) {
-        uint4 buf[8];
+    int i = 0;
+    for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+      const int mt = int(u / n_tiles), h = int(u % n_tiles);
+      const int64_t row = int64_t(mt) * kTcBM + 32 * q + lane;
+      // LN statistics: unit h sums its 1/n_tiles share of each row's columns
+      // (while its MMAs run) and publishes the partial; every unit of the row
+      // tile then combines the n_tiles partials in fixed order.
+      {
+        const int nv = a.K / 8;
+        const int v_lo = int(int64_t(h) * nv / n_tiles), v_hi = int(int64_t(h + 1) * nv / n_tiles);
+        float sx = 0.f, sxx = 0.f;
+        if (row < a.M) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+          for (int v0 = v_lo; v0 < v_hi; v0 += 8) {
+            uint4 buf[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) buf[u] = v0 + u < nv ? __ldg(rp + v0 + u) : make_uint4(0, 0, 0, 0);
+            for (int w = 0; w < 8; ++w) buf[w] = v0 + w < v_hi ? __ldg(rp + v0 + w) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t w4[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+            for (int w = 0; w < 8; ++w) {
+              const uint32_t w4[4] = {buf[w].x, buf[w].y, buf[w].z, buf[w].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-            sx += lo + hi;
-            sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+              for (int e = 0; e < 4; ++e) {
+                const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+                sx += lo + hi;
+                sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+              }
+            }
           }
+          a.stats[row * n_tiles + h] = make_float2(sx, sxx);
         }
+        epi_bar();
+        if (threadIdx.x == 64) {
+          __threadfence();
+          atomicAdd(a.ready + mt, 1);
+        }
+        if (lane == 0)
+          while (ld_acquire_s32(a.ready + mt) < stamp * n_tiles) __nanosleep(64);
+        __syncwarp();
       }
-    }
-    const float mean = sx / float(a.K);
-    const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
-    const float rsig = rsqrtf(var + kLayerNormEps);
-    const float shift = mean * rsig;
-    float logit = 0.f;
-    for (int n = 0; n < n_tiles; ++n) {
-      const int acc = n & 1;
-      mbar_wait(&tmem_full[acc], (n >> 1) & 1);
+      float rsig = 1.f, shift = 0.f;
+      if (row < a.M) {
+        float sx = 0.f, sxx = 0.f;
+        for (int t = 0; t < n_tiles; ++t) {
+          const float2 p = __ldcg(a.stats + row * n_tiles + t);
+          sx += p.x;
+          sxx += p.y;
+        }
+        const float mean = sx / float(a.K);
+        const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
+        rsig = rsqrtf(var + kLayerNormEps);
+        shift = mean * rsig;
+      }
+      const int acc = i & 1;
+      mbar_wait(&tmem_full[acc], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * kTcBN);
+      float logit = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < kTcBN; c0 += 32) {
         float v[32];
         tmem_ld32(base + uint32_t(c0), v);
-        const int j0 = n * kTcBN + c0;
+        const int j0 = h * kTcBN + c0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float h = fmaf(v[i], rsig, fmaf(-shift, __ldg(a.s + j0 + i), __ldg(a.c + j0 + i)));
-          logit = fmaf(fmaxf(h, 0.f), __ldg(a.w2 + j0 + i), logit);
+        for (int j = 0; j < 32; ++j) {
+          const float hv = fmaf(v[j], rsig, fmaf(-shift, __ldg(a.s + j0 + j), __ldg(a.c + j0 + j)));
+          logit = fmaf(fmaxf(hv, 0.f), __ldg(a.w2 + j0 + j), logit);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-    }
-    if (row < a.M) {
-      const float z = logit + a.b2;
-      a.out_logit[row] = z;
-      double p = 1.0 / (1.0 + exp(-double(z)));
-      a.out_prob[row] = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
+      if (row < a.M) a.partial[row * n_tiles + h] = logit;
+      // the row tile's last finished hidden tile sums the partials in fixed order
+      epi_bar();
+      if (threadIdx.x == 64) {
+        __threadfence();
+        last_flag = atomicAdd(a.done + mt, 1) == n_tiles - 1;
+      }
+      epi_bar();
+      if (last_flag) {
+        __threadfence();
+        if (row < a.M) {
+          float z = a.b2;
+          for (int t = 0; t < n_tiles; ++t) z += __ldcg(a.partial + row * n_tiles + t);
+          a.out_logit[row] = z;
+          double p = 1.0 / (1.0 + exp(-double(z)));
+          a.out_prob[row] = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
+        }
+        if (threadIdx.x == 64) a.done[mt] = 0;   // ready for the next launch
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -237,6 +298,13 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  if (threadIdx.x == 0) {                        // last CTA out advances the epoch
+    __threadfence();
+    if (atomicAdd(a.hdr + 1, 1) == int(gridDim.x) - 1) {
+      a.hdr[1] = 0;
+      a.hdr[0] = stamp;
+    }
   }
 }
 
@@ -269,19 +337,51 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 using namespace duchess;
 
+extern "C" size_t duchess_mlp_probe_tc_workspace_bytes(int64_t M, int32_t NH) {
+  if (M < 0 || NH < kTcBN) return 0;
+  const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
+  return size_t(16 + M * nt * 8 + M * nt * 4 + 2 * mt * 4 + 256);
+}
+
 extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1,
                                     int32_t NH, const float* s, const float* c, const float* w2,
-                                    float b2, float* out_logit, double* out_prob, void* stream) {
+                                    float b2, float* out_logit, double* out_prob,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
   if (!X || !W1 || !s || !c || !w2 || !out_logit || !out_prob) return DUCHESS_EINVAL;
   if (M < 0 || K < kTcBK || K % kTcBK || NH < kTcBN || NH % kTcBN) return DUCHESS_EINVAL;
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W1) % 16) return DUCHESS_EINVAL;
+  if (!workspace || workspace_bytes < duchess_mlp_probe_tc_workspace_bytes(M, NH) ||
+      reinterpret_cast<uintptr_t>(workspace) % 16)
+    return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
   CUtensorMap ma, mb;
   if (!make_map(&ma, X, uint64_t(M), uint64_t(K), kTcBM)) return DUCHESS_ECUDA;
   if (!make_map(&mb, W1, uint64_t(NH), uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
-  TcArgs a{M, K, NH, s, c, w2, b2, out_logit, out_prob, static_cast<const uint16_t*>(X)};
+  const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
+  char* ws = static_cast<char*>(workspace);
+  TcArgs a{};
+  a.M = M;
+  a.K = K;
+  a.NH = NH;
+  a.s = s;
+  a.c = c;
+  a.w2 = w2;
+  a.b2 = b2;
+  a.out_logit = out_logit;
+  a.out_prob = out_prob;
+  a.X = static_cast<const uint16_t*>(X);
+  a.hdr = reinterpret_cast<int*>(ws);
+  a.stats = reinterpret_cast<float2*>(ws + 16);
+  a.partial = reinterpret_cast<float*>(ws + 16 + M * nt * 8);
+  a.ready = reinterpret_cast<int*>(ws + 16 + M * nt * 8 + M * nt * 4);
+  a.done = a.ready + mt;
+  a.n_units = mt * nt;
   cudaFuncSetAttribute(mlp_probe_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-  const unsigned grid = unsigned((M + kTcBM - 1) / kTcBM);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // every CTA resident (one per SM): units wait on statistics other CTAs publish
+  const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
   mlp_probe_tc_kernel<<<grid, kTcThreads, kTcSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

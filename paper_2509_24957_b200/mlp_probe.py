@@ -58,6 +58,7 @@ class TensorCoreMlpProbe:
         self.d_s = torch.from_numpy(self.s.astype(np.float32)).to(dev)
         self.d_c = torch.from_numpy(c.astype(np.float32)).to(dev)
         self.d_w2 = torch.from_numpy(w2.astype(np.float32)).to(dev)
+        self._ws = None                                 # zeroed workspace, grown on demand
 
     def __call__(self, X: torch.Tensor, out_logit: torch.Tensor | None = None,
                  out_prob: torch.Tensor | None = None, stream=None):
@@ -69,10 +70,14 @@ class TensorCoreMlpProbe:
             out_logit = torch.empty(M, dtype=torch.float32, device=X.device)
         if out_prob is None:
             out_prob = torch.empty(M, dtype=torch.float64, device=X.device)
+        need = int(self.lib.duchess_mlp_probe_tc_workspace_bytes(M, self.NHp))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=X.device)
         _lib.check(self.lib.duchess_mlp_probe_tc(
             X.data_ptr(), M, self.K, self.d_w1.data_ptr(), self.NHp, self.d_s.data_ptr(),
             self.d_c.data_ptr(), self.d_w2.data_ptr(), self.b2, out_logit.data_ptr(),
-            out_prob.data_ptr(), _lib.stream_handle(stream)), "duchess_mlp_probe_tc")
+            out_prob.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+            _lib.stream_handle(stream)), "duchess_mlp_probe_tc")
         return out_logit, out_prob
 
     def flops(self, M: int) -> float:
