@@ -368,9 +368,13 @@ int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, i
  * X [M, K] bf16, W [N, K] bf16 (K-major); K % 64 == 0, N % 256 == 0. With
  * ln_fold the input LayerNorm is folded in (W' = W diag(gain), S = W' 1,
  * C = W ln_bias + b; row mean / std computed on the device). */
+size_t duchess_tc_linear_workspace_bytes(int64_t M, int32_t N);
+/* workspace (ln_fold only; may be NULL otherwise): >= the queried bytes,
+ * 16-byte aligned, zeroed before first use, reusable afterwards. */
 int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
                       int32_t ln_fold, const float* S, const float* C, const float* BS,
-                      const float* BT, int32_t act, void* out, void* stream);
+                      const float* BT, int32_t act, void* out, void* workspace,
+                      size_t workspace_bytes, void* stream);
 /* Small classifier head: logits[M, n_out] = H (bf16 [M, K]) . W^T (fp32 [n_out, K]) + b. */
 int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W, const float* b,
                         int32_t n_out, float* logits, void* stream);

@@ -15,11 +15,14 @@
 // inference batch-norm (predictor.py:141-143). Output bf16 (next layer's
 // input) row-major [M, N].
 //
-// One CTA per (128-row, 256-column) tile: warp 0 TMA producer (A = X[128x64],
-// B = W[256x64] bf16, 128B swizzle, 4-stage ring), warp 1 TMEM allocator +
-// single-thread tcgen05.mma issuer (M128 N256 K16, fp32 accumulate), warps
-// 2-5 row statistics (first layer) and the epilogue (tcgen05.ld 32 columns at
-// a time, fold, activation, bf16 store).
+// Persistent: one CTA per SM walks (128-row, 256-column) output tiles in
+// row-tile-major order; warp 0 TMA producer (A = X[128x64], B = W[256x64]
+// bf16, 128B swizzle, 4-stage ring), warp 1 TMEM allocator + single-thread
+// tcgen05.mma issuer (M128 N256 K16, fp32 accumulate, two 256-column
+// accumulators so a tile's epilogue overlaps the next tile's MMAs), warps 2-5
+// the epilogue (tcgen05.ld 32 columns at a time, fold, activation, bf16
+// store). With ln_fold each tile sums its 1/n_col_tiles share of its rows for
+// the LN statistics and the row tile's tiles combine the shares (fixed order).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -46,7 +49,17 @@ struct Args {
   const float* BS;
   const float* BT;
   uint16_t* out;
+  int* hdr;            // ln_fold workspace: [0] launch epoch, [1] exit counter
+  float2* stats;       // [M * n_col_tiles] partial (sum x, sum x^2)
+  int* ready;          // [n_row_tiles] published partials, cumulative over launches
+  int64_t n_units;
 };
+
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             uint64_t* bar) {
@@ -108,22 +121,25 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
               Args a) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full;
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int k_blocks = a.K / BK;
+  const int n_tiles = a.N / BN;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
-    mbar_init(&tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -131,99 +147,145 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
+  const int stamp = a.ln_fold ? a.hdr[0] + 1 : 0;
 
   if (warp == 0) {
     if (lane == 0) {                                   // ---- TMA producer ----
-      for (int kb = 0; kb < k_blocks; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&empty_bar[s], ((kb / STAGES) & 1) ^ 1u);
-        char* st = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-        tma_load_2d(st, &map_a, kb * BK, m0, &full_bar[s]);
-        tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
+      int it = 0;
+      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        const int m0 = int(u / n_tiles) * BM, n0 = int(u % n_tiles) * BN;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1u);
+          char* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          tma_load_2d(st, &map_a, kb * BK, m0, &full_bar[s]);
+          tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---- MMA issuer ----
-      for (int kb = 0; kb < k_blocks; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&full_bar[s], (kb / STAGES) & 1);
+      int it = 0, i = 0;
+      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tmem_empty[acc], ((i >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const char* st = smem + s * STAGE_BYTES;
-        const uint64_t da = desc_sw128(st), db = desc_sw128(st + A_BYTES);
+        const uint32_t d = tmem + uint32_t(acc * BN);
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full_bar[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const char* st = smem + s * STAGE_BYTES;
+          const uint64_t da = desc_sw128(st), db = desc_sw128(st + A_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          mma(tmem, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
-        commit(&empty_bar[s]);
+          for (int k = 0; k < BK / 16; ++k)
+            mma(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+          commit(&empty_bar[s]);
+        }
+        commit(&tmem_full[acc]);
       }
-      commit(&tmem_full);
     }
   } else {
-    // ---- statistics + epilogue: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
+    // ---- epilogue: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
     const int q = warp & 3;
-    const int64_t row = m0 + 32 * q + lane;
-    float rsig = 1.f, shift = 0.f;
-    if (a.ln_fold) {                                   // overlaps the MMAs
-      float sx = 0.f, sxx = 0.f;
-      if (row < a.M) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+    int i = 0;
+    for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+      const int mt = int(u / n_tiles), nt = int(u % n_tiles);
+      const int64_t row = int64_t(mt) * BM + 32 * q + lane;
+      float rsig = 1.f, shift = 0.f;
+      if (a.ln_fold) {                                 // overlaps this tile's MMAs
         const int nv = a.K / 8;
-        for (int v0 = 0; v0 < nv; v0 += 8) {
-          uint4 buf[8];
+        const int v_lo = int(int64_t(nt) * nv / n_tiles), v_hi = int(int64_t(nt + 1) * nv / n_tiles);
+        float sx = 0.f, sxx = 0.f;
+        if (row < a.M) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+          for (int v0 = v_lo; v0 < v_hi; v0 += 8) {
+            uint4 buf[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) buf[u] = v0 + u < nv ? __ldg(rp + v0 + u) : make_uint4(0, 0, 0, 0);
+            for (int w = 0; w < 8; ++w) buf[w] = v0 + w < v_hi ? __ldg(rp + v0 + w) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t w4[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+            for (int w = 0; w < 8; ++w) {
+              const uint32_t w4[4] = {buf[w].x, buf[w].y, buf[w].z, buf[w].w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-              sx += lo + hi;
-              sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+              for (int e = 0; e < 4; ++e) {
+                const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+                sx += lo + hi;
+                sxx = fmaf(lo, lo, fmaf(hi, hi, sxx));
+              }
             }
           }
+          a.stats[row * n_tiles + nt] = make_float2(sx, sxx);
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          __threadfence();
+          atomicAdd(a.ready + mt, 1);
+        }
+        if (lane == 0)
+          while (ld_acquire_s32(a.ready + mt) < stamp * n_tiles) __nanosleep(64);
+        __syncwarp();
+        if (row < a.M) {
+          float tx = 0.f, txx = 0.f;
+          for (int t = 0; t < n_tiles; ++t) {
+            const float2 p = __ldcg(a.stats + row * n_tiles + t);
+            tx += p.x;
+            txx += p.y;
+          }
+          const float mean = tx / float(a.K);
+          const float var = fmaxf(txx / float(a.K) - mean * mean, 0.f);
+          rsig = rsqrtf(var + kLayerNormEps);
+          shift = mean * rsig;
         }
       }
-      const float mean = sx / float(a.K);
-      const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
-      rsig = rsqrtf(var + kLayerNormEps);
-      shift = mean * rsig;
-    }
-    mbar_wait(&tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t base = tmem + (uint32_t(32 * q) << 16);
+      const int acc = i & 1;
+      mbar_wait(&tmem_full[acc], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN);
+      const int n0 = nt * BN;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(base + uint32_t(c0), v);
-      const int j0 = n0 + c0;
-      uint32_t packed[16];
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(base + uint32_t(c0), v);
+        const int j0 = n0 + c0;
+        uint32_t packed[16];
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float y[2];
+        for (int k = 0; k < 32; k += 2) {
+          float y[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = j0 + i + h;
-          float pre = a.ln_fold ? fmaf(v[i + h], rsig, fmaf(-shift, __ldg(a.S + j), __ldg(a.C + j)))
-                                : v[i + h] + __ldg(a.C + j);
-          pre = fmaf(pre, __ldg(a.BS + j), __ldg(a.BT + j));
-          y[h] = a.act == 1 ? fmaxf(pre, 0.f) : a.act == 2 ? gelu(pre) : pre;
+          for (int h = 0; h < 2; ++h) {
+            const int j = j0 + k + h;
+            float pre = a.ln_fold ? fmaf(v[k + h], rsig, fmaf(-shift, __ldg(a.S + j), __ldg(a.C + j)))
+                                  : v[k + h] + __ldg(a.C + j);
+            pre = fmaf(pre, __ldg(a.BS + j), __ldg(a.BT + j));
+            y[h] = a.act == 1 ? fmaxf(pre, 0.f) : a.act == 2 ? gelu(pre) : pre;
+          }
+          packed[k / 2] = uint32_t(f32_to_bf16_rne(y[0])) | (uint32_t(f32_to_bf16_rne(y[1])) << 16);
         }
-        packed[i / 2] = uint32_t(f32_to_bf16_rne(y[0])) | (uint32_t(f32_to_bf16_rne(y[1])) << 16);
-      }
-      if (row < a.M) {
-        uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.N + j0);
+        if (row < a.M) {
+          uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.N + j0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          dst[u] = make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
+          for (int w = 0; w < 4; ++w)
+            dst[w] = make_uint4(packed[4 * w], packed[4 * w + 1], packed[4 * w + 2], packed[4 * w + 3]);
+        }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  if (a.ln_fold && threadIdx.x == 0) {               // last CTA out advances the epoch
+    __threadfence();
+    if (atomicAdd(a.hdr + 1, 1) == int(gridDim.x) - 1) {
+      a.hdr[1] = 0;
+      a.hdr[0] = stamp;
+    }
   }
 }
 
@@ -273,23 +335,55 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 using namespace duchess;
 
+extern "C" size_t duchess_tc_linear_workspace_bytes(int64_t M, int32_t N) {
+  if (M < 0 || N < tcl::BN) return 0;
+  const int64_t mt = (M + tcl::BM - 1) / tcl::BM, nt = N / tcl::BN;
+  return size_t(16 + M * nt * 8 + mt * 4 + 256);
+}
+
 extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
                                  int32_t ln_fold, const float* S, const float* C, const float* BS,
-                                 const float* BT, int32_t act, void* out, void* stream) {
+                                 const float* BT, int32_t act, void* out, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
   if (!X || !W || !C || !BS || !BT || !out || (ln_fold && !S)) return DUCHESS_EINVAL;
   if (M < 0 || K < tcl::BK || K % tcl::BK || N < tcl::BN || N % tcl::BN || act < 0 || act > 2)
     return DUCHESS_EINVAL;
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16 ||
       reinterpret_cast<uintptr_t>(out) % 16)
     return DUCHESS_EINVAL;
+  if (ln_fold && (!workspace || workspace_bytes < duchess_tc_linear_workspace_bytes(M, N) ||
+                  reinterpret_cast<uintptr_t>(workspace) % 16))
+    return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
   CUtensorMap ma, mb;
   if (!tcl::make_map(&ma, X, uint64_t(M), uint64_t(K), tcl::BM)) return DUCHESS_ECUDA;
   if (!tcl::make_map(&mb, W, uint64_t(N), uint64_t(K), tcl::BN)) return DUCHESS_ECUDA;
-  tcl::Args a{M, K, N, ln_fold, act, static_cast<const uint16_t*>(X), S, C, BS, BT,
-              static_cast<uint16_t*>(out)};
+  const int64_t mt = (M + tcl::BM - 1) / tcl::BM, nt = N / tcl::BN;
+  tcl::Args a{};
+  a.M = M;
+  a.K = K;
+  a.N = N;
+  a.ln_fold = ln_fold;
+  a.act = act;
+  a.X = static_cast<const uint16_t*>(X);
+  a.S = S;
+  a.C = C;
+  a.BS = BS;
+  a.BT = BT;
+  a.out = static_cast<uint16_t*>(out);
+  if (ln_fold) {
+    char* ws = static_cast<char*>(workspace);
+    a.hdr = reinterpret_cast<int*>(ws);
+    a.stats = reinterpret_cast<float2*>(ws + 16);
+    a.ready = reinterpret_cast<int*>(ws + 16 + M * nt * 8);
+  }
+  a.n_units = mt * nt;
   cudaFuncSetAttribute(tcl::linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl::SMEM);
-  const dim3 grid(unsigned((M + tcl::BM - 1) / tcl::BM), unsigned(N / tcl::BN));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one CTA per SM, all resident: with ln_fold tiles wait on statistics shares
+  const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
   tcl::linear_kernel<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

@@ -74,6 +74,7 @@ class TensorCoreClassifier:
             self.layers.append((Wd, S, C, _f32(bs, dev), _f32(bt, dev), act, width))
         self.head_w = _f32(weights.weights[-1], dev).contiguous()
         self.head_b = _f32(weights.biases[-1], dev)
+        self._ws = None                      # zeroed ln-fold workspace, grown on demand
 
     def logits(self, X) -> torch.Tensor:
         """X [M, input_dim] (numpy or torch) -> fp32 logits [M, head_dim] on the device."""
@@ -84,12 +85,17 @@ class TensorCoreClassifier:
         h = x.to(torch.bfloat16).contiguous()
         M = h.shape[0]
         stream = _lib.stream_handle()
+        need = int(self.lib.duchess_tc_linear_workspace_bytes(M, self.layers[0][6]))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         for k, (Wd, S, C, BS, BT, act, width) in enumerate(self.layers):
             out = torch.empty((M, width), dtype=torch.bfloat16, device=self.device)
+            ln = k == 0
             _lib.check(self.lib.duchess_tc_linear(
-                h.data_ptr(), M, h.shape[1], Wd.data_ptr(), width, int(k == 0),
+                h.data_ptr(), M, h.shape[1], Wd.data_ptr(), width, int(ln),
                 None if S is None else S.data_ptr(), C.data_ptr(), BS.data_ptr(), BT.data_ptr(),
-                act, out.data_ptr(), stream), "duchess_tc_linear")
+                act, out.data_ptr(), self._ws.data_ptr() if ln else None,
+                self._ws.numel() if ln else 0, stream), "duchess_tc_linear")
             h = out
         logits = torch.empty((M, self.weights.head_dim), dtype=torch.float32, device=self.device)
         _lib.check(self.lib.duchess_head_logits(
