@@ -1031,7 +1031,7 @@ def main():
                          "GPU; default 2 for c3, 1 otherwise")
     ap.add_argument("--graph", action="store_true",
                     help="replay the round loop as a CUDA graph (one slab rotation per graph)")
-    ap.add_argument("--k1-every", type=int, default=4,
+    ap.add_argument("--k1-every", type=int, default=8,
                     help="bracket K1 with CUDA events on every N-th timed step")
     ap.add_argument("--nsplit", type=int, default=2)
     ap.add_argument("--threads", type=int, default=128)

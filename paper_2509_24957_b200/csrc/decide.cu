@@ -278,6 +278,8 @@ struct SlotCache {
   double raw[kMaxC];
   double wts[kMaxC];
   double draws[kMaxC];
+  int nat[kMaxC];        // natural length of the template in slot j (for phase 1)
+  int t0, rounds, tok_dec, tok_prb;   // request's template base and counters
   int tally_delta[64];   // this round's terminations, per answer id (answer_cap <= 64)
   uint32_t words[2 * kMaxC];
   uint32_t mt[kMtN + 1];
@@ -313,6 +315,22 @@ __device__ __forceinline__ void load_slot(const DuchessState& s, int64_t rC, int
       c.lp[j] = s.br_last_pred[bi];
     }
   }
+  __syncwarp();
+}
+
+// Per-request fields phase 1 needs (template base, counters, the occupied
+// slots' template lengths) when the slot cache was not filled by decide_slot.
+__device__ __forceinline__ void load_meta(const DuchessWorkload& w, const DuchessState& s, int r,
+                                          int p, int C, SlotCache& c, int lane) {
+  const int t0 = w.tmpl_off[p];
+  if (lane == 0) {
+    c.t0 = t0;
+    c.rounds = s.rounds[r];
+    c.tok_dec = s.tokens_decode[r];
+    c.tok_prb = s.tokens_probe[r];
+  }
+  for (int j = lane; j < C; j += 32)
+    if (c.bid[j] >= 0) c.nat[j] = w.nat_len[t0 + c.bid[j]];
   __syncwarp();
 }
 
@@ -399,10 +417,12 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, int p, SlotCache& c, int lane) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
-  const int n_tmpl = w.tmpl_off[p + 1] - w.tmpl_off[p];
+  const int t0 = w.tmpl_off[p];
+  const int n_tmpl = w.tmpl_off[p + 1] - t0;
   const int seeded = min(C, n_tmpl);
   for (int j = lane; j < C; j += 32) {
     const bool live = j < seeded;
+    if (live) c.nat[j] = w.nat_len[t0 + j];
     c.bid[j] = live ? j : -1;
     c.off[j] = 0; c.dec[j] = 0; c.streak[j] = 0; c.status[j] = DUCHESS_ACTIVE;
     c.npred[j] = 0; c.lp[j] = 0.5;
@@ -427,6 +447,10 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     s.tokens_probe[r] = 0;
     s.rounds[r] = 0;
     s.done[r] = 0;
+    c.t0 = t0;
+    c.rounds = 0;
+    c.tok_dec = 0;
+    c.tok_prb = 0;
   }
   __syncwarp();
 }
@@ -476,7 +500,10 @@ __device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
   if (s.done[r]) return -1;
   const int p = s.slot_req[r];
   if (p < 0) return -1;
-  if (!cache_valid) load_slot(s, rC, rB, C, c, lane);
+  if (!cache_valid) {
+    load_slot(s, rC, rB, C, c, lane);
+    load_meta(w, s, r, p, C, c, lane);
+  }
   return p;
 }
 
@@ -510,7 +537,7 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   int32_t* p1 = s.p1_rec + int64_t(r) * kP1Words;
   // ---- phase 1: decode one interval per active branch (:344-355) ----
-  const int t0 = w.tmpl_off[p];
+  const int t0 = c.t0;
   int decoding = 0, max_chunk = 0, dtok = 0, probes = 0;
   for (int base = 0; base < C; base += 32) {
     const int j = base + lane;
@@ -519,7 +546,7 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     if (b >= 0) {
       const int64_t bi = rB + b;
       const int t = t0 + b;                           // branch_id == template_index (:260-266)
-      const int nat = w.nat_len[t];
+      const int nat = c.nat[j];
       int pos = c.off[j] + c.dec[j];
       const int room = min(nat, pol.token_cap) - pos;            // _decode_chunk :273-279
       const int chunk = max(0, min(pol.interval_tokens, room));
@@ -568,10 +595,13 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     max_chunk = max(max_chunk, __shfl_xor_sync(0xffffffffu, max_chunk, o));
   }
   if (lane == 0) {
-    const int rounds = s.rounds[r] + 1;
+    const int rounds = c.rounds + 1;
+    c.rounds = rounds;
+    c.tok_dec += dtok;
+    c.tok_prb += probes * pol.probe_cost_tokens;
     s.rounds[r] = rounds;
-    s.tokens_decode[r] += dtok;
-    s.tokens_probe[r] += probes * pol.probe_cost_tokens;
+    s.tokens_decode[r] = c.tok_dec;
+    s.tokens_probe[r] = c.tok_prb;
     p1[0] = rounds;
     p1[1] = decoding;
     p1[2] = max_chunk;
@@ -621,6 +651,8 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   int mt_idx = int(mt_iw & ~kMtPristine);
   const int nb = __ldcg(s.n_branches + r);
   const int next_t = __ldcg(s.next_template + r);
+  const int cnt_dec = __ldcg(s.tokens_decode + r), cnt_prb = __ldcg(s.tokens_probe + r);
+  const int cnt_rnd = __ldcg(s.rounds + r);
   const int p = __shfl_sync(0xffffffffu, p1v, 5);
   if (lane < DUCHESS_REC_WORDS) {
     const int v = __shfl_sync(0x00000fffu, p1v, lane < DUCHESS_REC_NACTIONS ? lane : 5);
@@ -671,6 +703,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   for (int k = lane; k < C && next_t + k < n_tmpl; k += 32)
     c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
+  if (sb0 >= 0) c.nat[lane] = w.nat_len[t0 + sb0];     // next round's phase 1
+  if (sb1 >= 0) c.nat[lane + 32] = w.nat_len[t0 + sb1];
+  if (lane == 0) c.t0 = t0;
   const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
   if (words_ready)
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
@@ -917,6 +952,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         const double a_lp = fetch_d(lp0, lp1, e);
         if (k < n_forks) {
           const int child_slot = c.free_slots[k];
+          c.nat[child_slot] = c.nat_child[k];
           c.bid[child_slot] = nb + k;
           c.off[child_slot] = min(a_pos, mm);
           c.dec[child_slot] = 0;
@@ -1019,7 +1055,10 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
   }
   if (lane == 0) {
-    s.tokens_probe[r] += n_term * pol.probe_cost_tokens;
+    c.rounds = cnt_rnd;
+    c.tok_dec = cnt_dec;
+    c.tok_prb = cnt_prb + n_term * pol.probe_cost_tokens;
+    s.tokens_probe[r] = c.tok_prb;
     rec[DUCHESS_REC_PROBES] = p1[4] + n_term;
     rec[DUCHESS_REC_NACTIONS] = n_surv + n_forks;
     rec[DUCHESS_REC_NFORKS] = n_forks;
@@ -1034,9 +1073,9 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       rec[DUCHESS_REC_FINAL] = empty ? -1 : best;
       s.out_final[p] = empty ? -1 : best;
       s.out_reason[p] = reason;
-      s.out_tokens_decode[p] = s.tokens_decode[r];
-      s.out_tokens_probe[p] = s.tokens_probe[r];
-      s.out_rounds[p] = s.rounds[r];
+      s.out_tokens_decode[p] = c.tok_dec;
+      s.out_tokens_probe[p] = c.tok_prb;
+      s.out_rounds[p] = c.rounds;
       s.out_error[p] = empty ? 1 : 0;
       add_counter(&s.counters[DUCHESS_CNT_FINISHED], 1ll);
       if (empty) add_counter(&s.counters[DUCHESS_CNT_ERRORS], 1ll);
@@ -1107,7 +1146,10 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
   if (s.done[r]) return -1;
   const int p = s.slot_req[r];
   if (p < 0) return -1;
-  if (!cache_valid) load_slot(s, int64_t(r) * C, int64_t(r) * s.branch_cap, C, c, lane);
+  if (!cache_valid) {
+    load_slot(s, int64_t(r) * C, int64_t(r) * s.branch_cap, C, c, lane);
+    load_meta(w, s, r, p, C, c, lane);
+  }
   return p;
 }
 
@@ -1122,7 +1164,7 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
 // launch), so each slot's state prefetch overlaps the scorer's tail.
 constexpr int kRoundWarps = 2;
 
-__global__ void __launch_bounds__(32 * kRoundWarps)
+__global__ void __maxnreg__(128)
 round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
   __shared__ SlotCache cache[kRoundWarps];
   const int lane = threadIdx.x & 31;
