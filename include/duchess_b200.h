@@ -143,6 +143,9 @@ typedef struct DuchessWorkload {
   const int32_t* pred_at;   /* [NQ] */
   const double* pred_p;     /* [NQ] */
   const int32_t* queue;     /* [queue_len] pool indices in service order */
+  const int32_t* queue_rec; /* [queue_len * 4] per queue position (pool index, template
+                               base, template count, MT index word), 16-byte aligned, or
+                               NULL: one load per refill instead of three */
 } DuchessWorkload;
 
 /* Mutable engine state: R request slots x C branch slots, Bmax branch ids. */

@@ -58,7 +58,7 @@ class Workload(C.Structure):
         ("nat_len", C.c_void_p), ("final_ans", C.c_void_p), ("conv", C.c_void_p),
         ("probe_off", C.c_void_p), ("probe_at", C.c_void_p), ("probe_ans", C.c_void_p),
         ("pred_off", C.c_void_p), ("pred_at", C.c_void_p), ("pred_p", C.c_void_p),
-        ("queue", C.c_void_p),
+        ("queue", C.c_void_p), ("queue_rec", C.c_void_p),
     ]
 
 

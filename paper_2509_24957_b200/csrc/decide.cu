@@ -280,6 +280,7 @@ struct SlotCache {
   double draws[kMaxC];
   int nat[kMaxC];        // natural length of the template in slot j (for phase 1)
   int t0, rounds, tok_dec, tok_prb;   // request's template base and counters
+  int need_refill;                    // set by decide_slot: the request just finished
   int tally_delta[64];   // this round's terminations, per answer id (answer_cap <= 64)
   uint32_t words[2 * kMaxC];
   uint32_t mt[kMtN + 1];
@@ -413,12 +414,15 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 }
 
 // Refill slot r with pool request p: RequestRun.__init__ (:242-248).
+// `qr` (optional): the queue position's record (pool index, template base,
+// template count, MT index word), one 16-byte load instead of three.
 __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
-                            const DuchessState& s, int r, int p, SlotCache& c, int lane) {
+                            const DuchessState& s, int r, int p, SlotCache& c, int lane,
+                            const int4* qr = nullptr) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
-  const int t0 = w.tmpl_off[p];
-  const int n_tmpl = w.tmpl_off[p + 1] - t0;
+  const int t0 = qr ? qr->y : w.tmpl_off[p];
+  const int n_tmpl = qr ? qr->z : w.tmpl_off[p + 1] - t0;
   const int seeded = min(C, n_tmpl);
   for (int j = lane; j < C; j += 32) {
     const bool live = j < seeded;
@@ -438,7 +442,7 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   for (int a = lane; a < s.answer_cap; a += 32) s.tally[int64_t(r) * s.answer_cap + a] = 0;
   if (lane == 0) {
     s.mt[int64_t(r) * DUCHESS_MT_WORDS + kMtN] =
-        kMtPristine | w.mt_init[int64_t(p) * DUCHESS_MT_WORDS + kMtN];   // copy-on-write
+        kMtPristine | (qr ? uint32_t(qr->w) : w.mt_init[int64_t(p) * DUCHESS_MT_WORDS + kMtN]);
     s.slot_req[r] = p;
     if (s.slot_aux) s.slot_aux[r] = 0;
     s.n_branches[r] = seeded;
@@ -1055,6 +1059,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     }
   }
   if (lane == 0) {
+    c.need_refill = done ? 1 : 0;
     c.rounds = cnt_rnd;
     c.tok_dec = cnt_dec;
     c.tok_prb = cnt_prb + n_term * pol.probe_cost_tokens;
@@ -1124,21 +1129,29 @@ __device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorklo
                                    const DuchessState& s, int r, SlotCache& c, int lane,
                                    bool cache_valid, int32_t* pop) {
   const int C = pol.max_branches;
-  if (s.needs_refill[r]) {
+  if (cache_valid ? c.need_refill : s.needs_refill[r]) {
     int q = 0;
     if (lane == 0) q = atomicAdd(pop, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
     int p = -1;
-    if (w.queue_len > 0) {
-      if (w.cycle) p = w.queue[q % w.queue_len];
-      else if (q < w.queue_len) p = w.queue[q];
+    int4 rec;
+    const int4* qr = nullptr;
+    if (w.queue_len > 0 && (w.cycle || q < w.queue_len)) {
+      const int qi = w.cycle ? q % w.queue_len : q;
+      if (w.queue_rec) {
+        rec = reinterpret_cast<const int4*>(w.queue_rec)[qi];
+        p = rec.x;
+        qr = &rec;
+      } else {
+        p = w.queue[qi];
+      }
     }
     if (p < 0) {
       if (lane == 0) { s.slot_req[r] = -1; s.done[r] = 1; s.needs_refill[r] = 0; }
       __syncwarp();
       return -1;
     }
-    refill_slot(pol, w, s, r, p, c, lane);
+    refill_slot(pol, w, s, r, p, c, lane, qr);
     if (lane == 0) s.needs_refill[r] = 0;
     __syncwarp();
     return p;

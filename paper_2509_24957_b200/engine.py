@@ -126,6 +126,14 @@ def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkloa
         .reshape(-1).to(device),
         "queue": i32(queue),
     }
+    # per queue position: (pool index, template base, template count, MT index word)
+    q = np.asarray(queue, dtype=np.int64).reshape(-1)
+    if len(q):
+        toff = np.asarray(tmpl_off, dtype=np.int64)
+        mtw = np.ascontiguousarray(mt_words, dtype=np.uint32).reshape(-1, _lib.MT_WORDS)
+        rec = np.stack([q, toff[q], toff[q + 1] - toff[q],
+                        mtw[q, -1].astype(np.int64)], axis=1).astype(np.int32)
+        tens["queue_rec"] = torch.from_numpy(np.ascontiguousarray(rec).reshape(-1)).to(device)
     st = _lib.Workload()
     st.n_requests = P
     st.queue_len = len(queue)

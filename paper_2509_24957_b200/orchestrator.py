@@ -312,7 +312,10 @@ class DuchessRun(RequestRun):
         words = mt_state_words(self.rng)
         if self.rounds == 0:      # the refill reads the pool state (pre-twisted)
             w = torch.from_numpy(pretwist(words).view(np.int32).copy())
-            self._engine.wl.tensors["mt_init"].copy_(w.to(self._engine.device))
+            tens = self._engine.wl.tensors
+            tens["mt_init"].copy_(w.to(self._engine.device))
+            if "queue_rec" in tens:   # the queue record caches the state's index word
+                tens["queue_rec"][3] = int(w[-1])
         else:
             self._engine.t["mt"].copy_(torch.from_numpy(words.view(np.int32).copy()))
 
