@@ -52,3 +52,20 @@ def gather_outcomes(local: dict, group=None) -> dict:
     for p in parts:
         merged.update(p)
     return merged
+
+
+def merge_difficulty_order(local_sorted_keys, group=None) -> list:
+    """Global easiest-first order across ranks: each rank
+    sorts its own segment of 64-bit (level, arrival, order) keys on its GPU
+    (scheduler.device_sort); the sorted runs are all-gathered (8 B per
+    request) and k-way merged on the host. Keys are unique, so the merge equals
+    one global sort (scheduler.py:60-96 pops over the union snapshot)."""
+    import heapq
+
+    import torch.distributed as dist
+    local = [int(k) for k in local_sorted_keys]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local
+    runs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(runs, local, group=group)
+    return list(heapq.merge(*runs))

@@ -104,3 +104,35 @@ def test_shard_range_covers_everything():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+
+
+def _difficulty_merge(rank, world, port_, out_q):
+    from paper_2509_24957_b200.distributed import merge_difficulty_order, shard_range
+    from paper_2509_24957_b200.scheduler import pack_keys
+    _init(rank, world, port_)
+    rng = np.random.default_rng(3)
+    n = 500
+    levels = rng.integers(1, 6, n)
+    arrivals = rng.integers(0, 10 ** 6, n)
+    keys = pack_keys(levels, arrivals, range(n))
+    lo, hi = shard_range(n, rank, world)
+    local = sorted(int(k) for k in keys[lo:hi])     # each rank's device sort (ordering only)
+    merged = merge_difficulty_order(local)
+    if rank == 0:
+        out_q.put((merged, sorted(int(k) for k in keys)))
+    dist.destroy_process_group()
+
+
+def test_difficulty_order_merges_across_ranks():
+    """per-rank sorted segments, all-gathered and k-way merged on
+    the host, equal one global sort of the (level, arrival, order) keys."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_difficulty_merge, args=(r, 2, port_, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged, want = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert merged == want
