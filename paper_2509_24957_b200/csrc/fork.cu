@@ -18,112 +18,121 @@
 
 namespace duchess {
 
-constexpr int kPlanThreads = 1024;
+constexpr int kPlanWarps = 16;          // groups per plan CTA (one warp each)
+constexpr int kScanThreads = 512;
 
 __device__ __forceinline__ int group_count(const int32_t* counts, int stride, int g, int cap) {
   return counts ? min(max(counts[int64_t(g) * stride], 0), cap) : cap;
 }
 
-// Block-wide exclusive scan (1024 threads) of one int per thread.
-__device__ __forceinline__ int block_excl_scan(int v, int* total, int* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+// Workspace (int32, zeroed before first use, self-cleaning afterwards):
+//   gcount[G], gtail[G], tbase[G], rank[G * cap], meta[4] = {cursor, tails, done, -}
+struct ForkWs {
+  int32_t* gcount;
+  int32_t* gtail;
+  int32_t* tbase;
+  int32_t* rank;
+  int32_t* meta;
+};
+
+// Plan, one warp per group: each record's tail flag (prefix not on a block
+// boundary) and its rank among the group's tail-needing records (ballot
+// prefix); the last CTA to finish scans the per-group tail counts into group
+// bases and reserves the tail blocks from the free list. A fork's tail block
+// is free_list[cursor + tbase[g] + rank] — the (group, record)-order rank, as
+// in the serial restatement.
+__global__ void __launch_bounds__(kPlanWarps * 32)
+fork_plan_kernel(const int32_t* forks, int group_cap, const int32_t* counts, int counts_stride,
+                 int n_groups, int block_tokens, ForkWs ws, int32_t* free_cursor,
+                 int free_list_len, int32_t* status) {
+  __shared__ int sh[kScanThreads / 32];
+  __shared__ int last;
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kPlanWarps + (threadIdx.x >> 5);
+  if (g < n_groups) {
+    const int c = group_count(counts, counts_stride, g, group_cap);
+    int running = 0;
+    for (int k0 = 0; k0 < c; k0 += 32) {
+      const int k = k0 + lane;
+      const int64_t rec = int64_t(g) * group_cap + k;
+      const bool flag = k < c && (forks[rec * 4 + 3] % block_tokens) != 0;
+      const unsigned m = __ballot_sync(0xffffffffu, flag);
+      if (k < c) ws.rank[rec] = flag ? running + __popc(m & ((1u << lane) - 1u)) : -1;
+      running += __popc(m);
+    }
+    if (lane == 0) {
+      ws.gcount[g] = c;
+      ws.gtail[g] = running;
+    }
   }
-  if (lane == 31) sh[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    int s = lane < (kPlanThreads / 32) ? sh[lane] : 0;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ws.meta + 2, 1) == int(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // exclusive scan of the group tail counts (fixed group order)
+  int base = 0;
+  for (int g0 = 0; g0 < n_groups; g0 += blockDim.x) {
+    const int gg = g0 + int(threadIdx.x);
+    const int v = gg < n_groups ? __ldcg(ws.gtail + gg) : 0;
+    int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    sh[lane] = s;   // inclusive warp totals
-  }
-  __syncthreads();
-  const int warp_base = warp ? sh[warp - 1] : 0;
-  *total = sh[kPlanThreads / 32 - 1];
-  __syncthreads();
-  return warp_base + x - v;
-}
-
-// Plan: group bases (scan of counts), per-fork (group, record) map and tail rank.
-__global__ void __launch_bounds__(kPlanThreads)
-fork_plan_kernel(const int32_t* forks, int group_cap, const int32_t* counts, int counts_stride,
-                 int n_groups, int block_tokens, int32_t* ws_base, int32_t* ws_map,
-                 int32_t* ws_tail, int32_t* ws_meta, int32_t* free_cursor, int free_list_len,
-                 int32_t* status) {
-  __shared__ int sh[32];
-  int running = 0;
-  for (int g0 = 0; g0 < n_groups; g0 += kPlanThreads) {
-    const int g = g0 + threadIdx.x;
-    const int c = g < n_groups ? group_count(counts, counts_stride, g, group_cap) : 0;
-    int total;
-    const int ex = block_excl_scan(c, &total, sh);
-    if (g < n_groups) ws_base[g] = running + ex;
-    running += total;
-  }
-  const int n_forks = running;
-  if (threadIdx.x == 0) ws_base[n_groups] = n_forks;
-  __syncthreads();
-  int tails = 0;
-  for (int f0 = 0; f0 < n_forks; f0 += kPlanThreads) {
-    const int f = f0 + threadIdx.x;
-    int flag = 0, rec = -1;
-    if (f < n_forks) {
-      int lo = 0, hi = n_groups;                 // last g with base[g] <= f
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (ws_base[mid] <= f) lo = mid; else hi = mid;
-      }
-      rec = lo * group_cap + (f - ws_base[lo]);
-      flag = (forks[int64_t(rec) * 4 + 3] % block_tokens) != 0;
-      ws_map[f] = rec;
+    const int warp = threadIdx.x >> 5;
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    int wbase = 0, total = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+      if (w < warp) wbase += sh[w];
+      total += sh[w];
     }
-    int total;
-    const int ex = block_excl_scan(flag, &total, sh);
-    if (f < n_forks) ws_tail[f] = flag ? tails + ex : -1;
-    tails += total;
+    if (gg < n_groups) ws.tbase[gg] = base + wbase + x - v;
+    base += total;
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     const int cursor = *free_cursor;
-    ws_meta[0] = n_forks;
-    ws_meta[1] = cursor;
-    if (cursor + tails > free_list_len) {
+    ws.meta[0] = cursor;
+    if (cursor + base > free_list_len) {
       if (status) status[0] = 1;
-      ws_meta[2] = free_list_len - cursor;     // tails beyond the list are skipped
+      ws.meta[1] = free_list_len - cursor;     // tails beyond the list are skipped
       *free_cursor = free_list_len;
     } else {
       if (status) status[0] = 0;
-      ws_meta[2] = tails;
-      *free_cursor = cursor + tails;
+      ws.meta[1] = base;
+      *free_cursor = cursor + base;
     }
+    ws.meta[2] = 0;                            // ready for the next call
   }
 }
 
+// One CTA per (group, record) slot: copy the root's full blocks into the
+// child's row (refcount += 1 each, order-independent), the reserved tail
+// block + its KV bytes, -1 for the rest.
 __global__ void __launch_bounds__(128)
-fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, const int32_t* ws_map,
-                 const int32_t* ws_tail, const int32_t* ws_meta, int32_t* table, int table_stride,
-                 int32_t* refcount, const int32_t* free_list, char* kv,
-                 int64_t kv_bytes_per_token, int block_tokens) {
-  const int f = blockIdx.x;
-  if (f >= ws_meta[0]) return;
-  const int rec = ws_map[f];
-  const int g = rec / group_cap;
-  const int32_t* fr = forks + int64_t(rec) * 4;
+fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, ForkWs ws,
+                 int32_t* table, int table_stride, int32_t* refcount, const int32_t* free_list,
+                 char* kv, int64_t kv_bytes_per_token, int block_tokens) {
+  const int64_t rec = blockIdx.x;
+  const int g = int(rec / group_cap), k = int(rec - int64_t(g) * group_cap);
+  if (k >= ws.gcount[g]) return;
+  const int32_t* fr = forks + rec * 4;
   const int child = fr[0], root = fr[2], prefix = fr[3];
   const int64_t gbase = int64_t(g) * rows_per_group;
   const int32_t* src = table + (gbase + root) * table_stride;
   int32_t* dst = table + (gbase + child) * table_stride;
   const int n_full = prefix / block_tokens;
   const int tail_tok = prefix - n_full * block_tokens;
-  const int rank = ws_tail[f];
-  const bool has_tail = tail_tok > 0 && rank >= 0 && rank < ws_meta[2];
-  const int tail_blk = has_tail ? free_list[ws_meta[1] + rank] : -1;
+  const int rank = ws.rank[rec];
+  const int trank = rank >= 0 ? ws.tbase[g] + rank : -1;
+  const bool has_tail = tail_tok > 0 && trank >= 0 && trank < ws.meta[1];
+  const int tail_blk = has_tail ? free_list[ws.meta[0] + trank] : -1;
   for (int j = threadIdx.x; j < table_stride; j += blockDim.x) {
     int v = -1;
     if (j < n_full) {
@@ -209,7 +218,7 @@ using namespace duchess;
 extern "C" size_t duchess_fork_workspace_bytes(int32_t n_groups, int32_t group_cap) {
   if (n_groups < 0 || group_cap < 0) return 0;
   const size_t nf = size_t(n_groups) * size_t(group_cap);
-  return (size_t(n_groups) + 1 + 2 * nf + 4) * sizeof(int32_t);
+  return (3 * size_t(n_groups) + nf + 4) * sizeof(int32_t);
 }
 
 extern "C" int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const int32_t* group_counts,
@@ -227,17 +236,16 @@ extern "C" int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const i
     return DUCHESS_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t nf = size_t(n_groups) * size_t(group_cap);
-  int32_t* ws_base = static_cast<int32_t*>(workspace);
-  int32_t* ws_map = ws_base + n_groups + 1;
-  int32_t* ws_tail = ws_map + nf;
-  int32_t* ws_meta = ws_tail + nf;
-  fork_plan_kernel<<<1, kPlanThreads, 0, s>>>(forks, group_cap, group_counts, counts_stride,
-                                             n_groups, block_tokens, ws_base, ws_map, ws_tail,
-                                             ws_meta, free_cursor, free_list_len, status);
-  fork_exec_kernel<<<unsigned(nf), 128, 0, s>>>(forks, rows_per_group, group_cap, ws_map, ws_tail,
-                                                ws_meta, block_table, table_stride, refcount,
-                                                free_list, static_cast<char*>(kv_pool),
-                                                kv_bytes_per_token, block_tokens);
+  int32_t* w = static_cast<int32_t*>(workspace);
+  ForkWs ws{w, w + n_groups, w + 2 * int64_t(n_groups), w + 3 * int64_t(n_groups),
+            w + 3 * int64_t(n_groups) + int64_t(nf)};
+  fork_plan_kernel<<<unsigned((n_groups + kPlanWarps - 1) / kPlanWarps), kPlanWarps * 32, 0, s>>>(
+      forks, group_cap, group_counts, counts_stride, n_groups, block_tokens, ws, free_cursor,
+      free_list_len, status);
+  fork_exec_kernel<<<unsigned(nf), 128, 0, s>>>(forks, rows_per_group, group_cap, ws, block_table,
+                                                table_stride, refcount, free_list,
+                                                static_cast<char*>(kv_pool), kv_bytes_per_token,
+                                                block_tokens);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 

@@ -51,7 +51,7 @@ def test_workspace_queries_need_no_gpu():
     lib = _lib.load()
     assert lib.duchess_score_workspace_bytes(4096, 1) == 0
     assert lib.duchess_score_workspace_bytes(4096, 2) == 4096 * 2 * 16 + 4096 * 4
-    assert lib.duchess_fork_workspace_bytes(4, 8) == (4 + 1 + 2 * 32 + 4) * 4
+    assert lib.duchess_fork_workspace_bytes(4, 8) == (3 * 4 + 32 + 4) * 4
 
 
 def test_invalid_arguments_are_rejected_before_launch():
