@@ -63,6 +63,16 @@ PRESET_GEN = {
 }
 
 
+def k3_traffic():
+    """DRAM bytes of one fork_exec launch from the committed ncu capture."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k3_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        return json.load(f)["dram_bytes"], os.path.relpath(files[-1], ROOT)
+
+
 def k1_traffic_ratio():
     """DRAM bytes / algorithmic bytes of K1 from the committed ncu --set full
     capture (tools/profile_all.sh -> profiles/<round>/k1_traffic.json)."""
@@ -665,8 +675,13 @@ def run_fork_bench(args, rank, world, local_rank):
     fk = torch.from_numpy(forks).to(dev)
     n_full = forks[:, :, 3] // bt
     tail = forks[:, :, 3] % bt
+    # Algorithmic bytes: table reads of the full blocks + refcount read/write,
+    # each child's table row and fork record, every child's private tail
+    # (write), and each DISTINCT source tail once (read): forks of one root
+    # share its partial tail block (children inherit root and prefix).
+    src_tails = {(r, int(forks[r, k, 2])): int(tail[r, k]) for r in range(R) for k in range(nf)}
     bytes_per_step = int((n_full * 4 * 3).sum() + R * nf * (max_blocks * 4 + 16)
-                         + (2 * tail * kvb).sum())
+                         + (tail * kvb).sum() + sum(src_tails.values()) * kvb)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         t.cursor.zero_()
@@ -705,7 +720,7 @@ def run_fork_bench(args, rank, world, local_rank):
                          "frac": achieved / peak, "peak_kind": kind,
                          "kernel": "duchess_fork_cow (plan + exec)",
                          "bytes_per_launch": bytes_per_step, "k3_us_per_launch": k3_ms * 1e3,
-                         "traffic": None},
+                         "traffic": k3_traffic()[0], "traffic_source": k3_traffic()[1]},
             "gpu_launches": 2 * args.steps, "clocks": clk}
 
 
