@@ -778,6 +778,145 @@ def run_tc_bench(args, rank, world, local_rank):
             "gpu_launches": args.steps, "clocks": clk}
 
 
+def run_difficulty_bench(args, rank, world, local_rank):
+    """the complexity MLP (4096 -> 2048 -> 1024 -> 512 -> 5, BN +
+    GeLU, softmax head) over a batch of request activations, hidden layers as
+    tcgen05 layers (duchess_tc_linear). CPU reference: the oracle's fp64
+    mlp_forward (the reference's per-vector forward) on a bounded sample."""
+    import torch
+    from paper_2509_24957_b200.difficulty import TensorCoreClassifier
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    M, dims, head = 32768, (4096, 2048, 1024, 512), 5
+    full = [*dims, head]
+    w = _complexity_weights()
+    clf = TensorCoreClassifier(w, device=dev)
+    X = [torch.randn((M, dims[0]), device=dev).to(torch.bfloat16) for _ in range(2)]
+    for i in range(args.warmup):
+        clf.logits(X[i % 2])
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        clf.logits(X[i % 2])
+    e1.record()
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    flops = 2.0 * M * sum(full[k] * full[k + 1] for k in range(3))
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak, kind = float(json.load(f)["bf16_tflops"]), "measured (burst)"
+    except Exception:  # noqa: BLE001
+        peak, kind = 1590.0, "fallback"
+    tf = flops / (ms / 1e3) / 1e12
+    out = {"metric": "difficulty predictions/s (complexity MLP, SURVEY 8(f)4)",
+           "value": M * world / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic N(0,1) activations, random-init complexity MLP",
+           "config": {"workload": f"{M} request activations, 4096 -> 2048 -> 1024 -> 512 -> 5, "
+                                  "BN + GeLU, LN folded, 2 rotating inputs (> L2)"},
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                        "frac": tf / peak, "peak_kind": kind,
+                        "kernel": "duchess_tc_linear (3 layers) + head", "flops_per_launch": flops,
+                        "traffic": None},
+           "gpu_launches": 4 * args.steps, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_difficulty(w)
+    return out
+
+
+def _complexity_weights():
+    from paper_2509_24957_b200.predictor import MlpWeights
+    rng = np.random.default_rng(1)
+    dims, head = (4096, 2048, 1024, 512), 5
+    full = [*dims, head]
+    hid = list(dims[1:])
+    W = [rng.normal(0, 1 / np.sqrt(full[k]), (full[k + 1], full[k])) for k in range(4)]
+    b = [rng.normal(0, 0.1, full[k + 1]) for k in range(4)]
+    return MlpWeights(dims[0], hid, head, ["gelu"] * 3, W, b, rng.uniform(0.5, 1.5, dims[0]),
+                      rng.uniform(-0.1, 0.1, dims[0]), [rng.normal(0, 0.1, d) for d in hid],
+                      [rng.uniform(0.5, 2.0, d) for d in hid],
+                      [rng.uniform(0.5, 1.5, d) for d in hid],
+                      [rng.uniform(-0.1, 0.1, d) for d in hid])
+
+
+def cpu_difficulty(w=None, budget_s=10.0):
+    from oracle import port
+    w = w or _complexity_weights()
+    Xs = np.random.default_rng(2).normal(0, 1, (8, w.input_dim))
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < budget_s:
+        port.mlp_forward(w, Xs[n % 8])
+        n += 1
+    return {"value": n / (time.perf_counter() - t0), "unit": "requests/s", "cores": 1,
+            "kind": "port", "sample": f"oracle/port.py fp64 mlp_forward per vector (the "
+                                      f"reference's forward), {budget_s:.0f} s on one core"}
+
+
+def run_sim_bench(args, rank, world, local_rank):
+    """run_simulation (simengine.py:150-281) end to end on the
+    device engine — every request's rounds in one batch, the timeline folded on
+    the device, the single-server queue replayed on the host. CPU reference:
+    the oracle's literal one-request-at-a-time replay on a bounded prefix."""
+    import torch
+
+    from paper_2509_24957_b200.orchestrator import OrchestratorConfig
+    from paper_2509_24957_b200.predictor import SyntheticPredictorConfig
+    from paper_2509_24957_b200.scheduler import ArrivalConfig, gen_arrivals
+    from paper_2509_24957_b200.simengine import TimingModel, run_simulation
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    torch.cuda.set_device(local_rank)
+    n = 4096
+    params = SyntheticParams(**PRESET_GEN["math-like"])
+    wl = generate_synthetic(params, n, seed=21 + rank)
+    arrivals = gen_arrivals(ArrivalConfig(rate_qpm=30.0, n_requests=n, seed=3))
+    orch = OrchestratorConfig(max_branches=10, **PRESET_KNOBS["math-like"])
+    synth = SyntheticPredictorConfig(rho=0.8)
+    run_simulation(wl, orch, "duchess", "easiest-predicted", arrivals[:], TimingModel(), 9,
+                   synthetic=synth, difficulty_mode="noisy-label")        # warm
+    times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        run_simulation(wl, orch, "duchess", "easiest-predicted", arrivals, TimingModel(), 9,
+                       synthetic=synth, difficulty_mode="noisy-label")
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    out = {"metric": "run_simulation requests/s (serving timeline, SURVEY 8(f)3)",
+           "value": n * world / dt, "unit": "requests/s", "n_gpus": world,
+           "steps": len(times), "warmup": 1, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
+           "data": "generate_synthetic math-like workload, Poisson arrivals",
+           "config": {"workload": f"{n} requests, duchess policy, easiest-predicted schedule "
+                                  "(noisy-label), default timing model; wall clock of one "
+                                  "run_simulation call incl. host packing and queue replay"},
+           "gpu_launches": None}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_sim(arrivals)
+    return out
+
+
+def cpu_sim(arrivals=None, k=256):
+    from oracle import port, simulate
+    from paper_2509_24957_b200.scheduler import ArrivalConfig, gen_arrivals
+    arrivals = arrivals or gen_arrivals(ArrivalConfig(rate_qpm=30.0, n_requests=k, seed=3))
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    traces = port.generate(port.GenParams(**PRESET_GEN["math-like"]), k, 21)
+    knobs = port.Knobs(max_branches=10, **PRESET_KNOBS["math-like"])
+    wl = generate_synthetic(SyntheticParams(**PRESET_GEN["math-like"]), k, seed=21)
+    t0 = time.perf_counter()
+    wl.content_hash()               # run_simulation hashes the workload (simengine.py:273)
+    simulate.simulate(traces[:k], knobs, "duchess", "easiest-predicted", arrivals[:k],
+                      (25.0, 0.0, 0.1), 9, 0.8, "noisy-label", None)
+    cdt = time.perf_counter() - t0
+    return {"value": k / cdt, "unit": "requests/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/simulate.py one-request-at-a-time replay of {k} requests plus "
+                      f"the workload hash (the reference's run_simulation restated), one core"}
+
+
 def run_train_bench(args, rank, world, local_rank):
     import torch
     from paper_2509_24957_b200.probe import fill_windows
@@ -993,6 +1132,15 @@ def cpu_fork_or_train(args):
 
 
 def run_reference(args, cfg):
+    if args.config in ("difficulty", "sim"):
+        cb = cpu_difficulty() if args.config == "difficulty" else cpu_sim()
+        return {"impl": "reference", "metric": f"{args.config} CPU reference", "value": cb["value"],
+                "unit": cb["unit"], "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+                "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.config + " (CPU)"}, "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
     if cfg is None:
         return cpu_fork_or_train(args)
     procs = os.cpu_count() or 1
@@ -1034,7 +1182,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3tc", "c4", "c5"])
+    ap.add_argument("--config", default="c2",
+                    choices=sorted(CONFIGS) + ["c3tc", "c4", "c5", "difficulty", "sim"])
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
@@ -1076,6 +1225,10 @@ def main():
         out = run_train_bench(args, rank, world, local_rank)
     elif args.config == "c3tc":
         out = run_tc_bench(args, rank, world, local_rank)
+    elif args.config == "difficulty":
+        out = run_difficulty_bench(args, rank, world, local_rank)
+    elif args.config == "sim":
+        out = run_sim_bench(args, rank, world, local_rank)
     elif args.mode == "split" and args.k1 == "list" and not args.graph and args.shards > 1:
         out = run_gpu_sharded(args, cfg, rank, world, local_rank)
     else:

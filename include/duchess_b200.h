@@ -322,6 +322,10 @@ int duchess_synthetic_predict(uint32_t* mt_state, int32_t n, const int32_t* conv
 /* sample_confused_level (predictor.py:376-386); matrix is 5x5 row-major fp64. */
 int duchess_confused_level(uint32_t* mt_state, int32_t n, const int32_t* true_level,
                            const double* matrix, int32_t* out, void* stream);
+/* random.Random(seed) for n non-negative 64-bit seeds (CPython init_by_array
+ * over the seed's 32-bit words) followed by the pending first twist: states
+ * [n][625] with index 0 (the stream of random.Random(seed), pre-twisted). */
+int duchess_mt_seed(const uint64_t* seeds, int32_t n, uint32_t* out_states, void* stream);
 /* sample_confused_level for n requests, request i drawing once from its own
  * stream mt_states[i*625 .. +625) (simengine.py:223-227); states pre-twisted
  * (index <= 622, see engine.pretwist); read-only. */

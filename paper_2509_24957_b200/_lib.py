@@ -148,6 +148,7 @@ SYMBOLS = {
                                             C.c_void_p, C.c_void_p]),
     "duchess_confused_level": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]),
+    "duchess_mt_seed": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "duchess_confused_levels": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]),
     "duchess_timeline": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_int64,

@@ -1683,6 +1683,42 @@ __global__ void confusion_kernel(uint32_t* mt, int n, const int32_t* true_level,
   }
 }
 
+// random.Random(seed) for many 64-bit seeds at once (CPython
+// Modules/_randommodule.c random_seed -> init_by_array over the seed's 32-bit
+// words), then the pending first twist (index 0, as engine.pretwist): one
+// warp per state; the seeding recurrences are serial (lane 0), the twist is
+// warp-parallel. States [n][625] (words + index).
+__global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, int n, uint32_t* out) {
+  __shared__ uint32_t sm[4][kMtN + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + warp;
+  if (i >= n) return;
+  uint32_t* mt = sm[warp];
+  if (lane == 0) {
+    const uint64_t sd = seeds[i];
+    const uint32_t key[2] = {uint32_t(sd), uint32_t(sd >> 32)};
+    const int klen = (sd >> 32) ? 2 : 1;
+    mt[0] = 19650218u;
+    for (int k = 1; k < kMtN; ++k) mt[k] = 1812433253u * (mt[k - 1] ^ (mt[k - 1] >> 30)) + uint32_t(k);
+    int a = 1, b = 0;
+    for (int k = 0; k < kMtN; ++k) {             // max(N, klen) == N
+      mt[a] = (mt[a] ^ ((mt[a - 1] ^ (mt[a - 1] >> 30)) * 1664525u)) + key[b] + uint32_t(b);
+      if (++a >= kMtN) { mt[0] = mt[kMtN - 1]; a = 1; }
+      if (++b >= klen) b = 0;
+    }
+    for (int k = 0; k < kMtN - 1; ++k) {
+      mt[a] = (mt[a] ^ ((mt[a - 1] ^ (mt[a - 1] >> 30)) * 1566083941u)) - uint32_t(a);
+      if (++a >= kMtN) { mt[0] = mt[kMtN - 1]; a = 1; }
+    }
+    mt[0] = 0x80000000u;
+  }
+  __syncwarp();
+  mt_twist_warp(mt, lane);
+  uint32_t* o = out + int64_t(i) * DUCHESS_MT_WORDS;
+  for (int k = lane; k < kMtN; k += 32) o[k] = mt[k];
+  if (lane == 0) o[kMtN] = 0u;
+}
+
 // sample_confused_level for many requests, each with its own fresh stream
 // (simengine.py:223-227: rng = random.Random(predict_seeds[order]), one draw).
 // States are [n][625] (words + index), pre-twisted by the host (index 0).
@@ -2017,5 +2053,12 @@ extern "C" int duchess_timeline(const int32_t* round_rec, int32_t n_slots, doubl
   timeline_kernel<<<(n_slots + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       round_rec, n_slots, ms_per_token, ms_per_extra_branch, (long long)probe_cost_ms,
       reinterpret_cast<long long*>(service_ms), reinterpret_cast<long long*>(first_token_ms));
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_mt_seed(const uint64_t* seeds, int32_t n, uint32_t* out_states, void* stream) {
+  if (n < 0 || (n > 0 && (!seeds || !out_states))) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  mt_seed_kernel<<<(n + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(seeds, n, out_states);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

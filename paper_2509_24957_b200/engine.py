@@ -59,6 +59,20 @@ def pretwist(words: np.ndarray) -> np.ndarray:
     return out
 
 
+def seed_states(seeds, out: torch.Tensor | None = None, device="cuda") -> torch.Tensor:
+    """random.Random(seed).getstate() words for many int seeds, pre-twisted
+    (index 0, as pretwist), built on the device by duchess_mt_seed: [n * 625]."""
+    n = len(seeds)
+    lib = _lib.load()
+    dev = out.device if out is not None else torch.device(device)
+    if out is None:
+        out = torch.empty(max(n, 1) * _lib.MT_WORDS, dtype=torch.int32, device=dev)
+    sd = torch.from_numpy(np.asarray([int(x) for x in seeds], dtype=np.uint64).view(np.int64)).to(dev)
+    _lib.check(lib.duchess_mt_seed(sd.data_ptr(), n, out.data_ptr(), _lib.stream_handle()),
+               "duchess_mt_seed")
+    return out
+
+
 def set_mt_state(rng: random.Random, words: np.ndarray) -> None:
     _v, _internal, gauss = rng.getstate()
     rng.setstate((3, tuple(int(x) for x in words), gauss))
@@ -81,35 +95,41 @@ def intern_answers(trace) -> list[str]:
     s = {NO_ANSWER, trace.ground_truth}
     for t in trace.templates:
         s.add(t.final_answer)
-        s.update(a for _, a in t.probes)
+        s.update([a for _, a in t.probes])
     return sorted(s)
 
 
 def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkload:
+    """Trace ingestion into the device SoA tables (workload.py:35-60): CSR
+    template / probe / prediction arrays with per-request interned answers."""
     P = len(traces)
     tmpl_off = [0]
     gt, nat, fin, conv = [], [], [], []
-    probe_off, probe_at, probe_ans = [0], [], []
-    pred_off, pred_at, pred_p = [0], [], []
+    probe_n, probe_at, probe_ans = [], [], []
+    pred_n, pred_at, pred_p = [], [], []
     answers = []
     for tr in traces:
         ans = intern_answers(tr)
-        idx = {a: i for i, a in enumerate(ans)}
+        idx = {a: i for i, a in enumerate(ans)}.__getitem__
         answers.append(ans)
-        gt.append(idx[tr.ground_truth])
-        for t in tr.templates:
-            nat.append(int(t.natural_length))
-            fin.append(idx[t.final_answer])
-            conv.append(-1 if t.oracle_convergence is None else int(t.oracle_convergence))
-            for at, a in t.probes:
-                probe_at.append(int(at))
-                probe_ans.append(idx[a])
-            probe_off.append(len(probe_at))
-            for at, p in (t.pred_probs or []):
-                pred_at.append(int(at))
-                pred_p.append(float(p))
-            pred_off.append(len(pred_at))
+        gt.append(idx(tr.ground_truth))
+        tm = tr.templates
+        nat += [t.natural_length for t in tm]
+        fin += [idx(t.final_answer) for t in tm]
+        conv += [-1 if t.oracle_convergence is None else t.oracle_convergence for t in tm]
+        for t in tm:
+            pr = t.probes
+            probe_n.append(len(pr))
+            probe_at += [at for at, _ in pr]
+            probe_ans += [idx(a) for _, a in pr]
+            pp = t.pred_probs or ()
+            pred_n.append(len(pp))
+            if pp:
+                pred_at += [at for at, _ in pp]
+                pred_p += [float(p) for _, p in pp]
         tmpl_off.append(len(nat))
+    probe_off = np.concatenate([[0], np.cumsum(probe_n, dtype=np.int64)]) if probe_n else [0]
+    pred_off = np.concatenate([[0], np.cumsum(pred_n, dtype=np.int64)]) if pred_n else [0]
 
     def i32(x):
         return torch.tensor(np.asarray(x, dtype=np.int32).reshape(-1) if len(x) else
@@ -122,17 +142,22 @@ def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkloa
         "pred_at": i32(pred_at),
         "pred_p": torch.tensor(np.asarray(pred_p if pred_p else [0.0], dtype=np.float64),
                                device=device),
-        "mt_init": torch.from_numpy(np.ascontiguousarray(mt_words, dtype=np.uint32).view(np.int32))
-        .reshape(-1).to(device),
+        "mt_init": (torch.empty(max(P, 1) * _lib.MT_WORDS, dtype=torch.int32, device=device)
+                    if mt_words is None else
+                    torch.from_numpy(np.ascontiguousarray(mt_words, dtype=np.uint32).view(np.int32))
+                    .reshape(-1).to(device)),
         "queue": i32(queue),
     }
     # per queue position: (pool index, template base, template count, MT index word)
     q = np.asarray(queue, dtype=np.int64).reshape(-1)
     if len(q):
         toff = np.asarray(tmpl_off, dtype=np.int64)
-        mtw = np.ascontiguousarray(mt_words, dtype=np.uint32).reshape(-1, _lib.MT_WORDS)
-        rec = np.stack([q, toff[q], toff[q + 1] - toff[q],
-                        mtw[q, -1].astype(np.int64)], axis=1).astype(np.int32)
+        if mt_words is None:                 # device-seeded states are pre-twisted: index 0
+            idx = np.zeros(len(q), dtype=np.int64)
+        else:
+            idx = np.ascontiguousarray(mt_words, dtype=np.uint32).reshape(-1, _lib.MT_WORDS)[q, -1]
+        rec = np.stack([q, toff[q], toff[q + 1] - toff[q], idx.astype(np.int64)],
+                       axis=1).astype(np.int32)
         tens["queue_rec"] = torch.from_numpy(np.ascontiguousarray(rec).reshape(-1)).to(device)
     st = _lib.Workload()
     st.n_requests = P
@@ -172,9 +197,16 @@ class BatchedDuchess:
         self.P, self.C = P, c
         self.R = n_slots if n_slots is not None else P
         queue = list(range(P)) if queue is None else list(queue)
-        mt = (np.stack([pretwist(mt_state_words(s)) for s in seeds]) if P
-              else np.zeros((0, 625), np.uint32))
+        int_seeds = P > 0 and all(isinstance(s, (int, np.integer)) and not isinstance(s, bool)
+                                  and 0 <= int(s) < (1 << 64) for s in seeds)
+        if int_seeds:      # random.Random(seed) states built on the device (duchess_mt_seed)
+            mt = None
+        else:
+            mt = (np.stack([pretwist(mt_state_words(s)) for s in seeds]) if P
+                  else np.zeros((0, 625), np.uint32))
         self.wl = pack_workload(traces, mt, queue, cycle, self.device)
+        if int_seeds:
+            seed_states(seeds, self.wl.tensors["mt_init"])
 
         pol = _lib.Policy()
         pol.max_branches = c

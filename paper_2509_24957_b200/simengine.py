@@ -206,7 +206,7 @@ def predicted_levels(workload: Workload, mode: str, predict_seeds: list, confusi
     random.Random(predict_seeds[order]) (simengine.py:223-227)."""
     import torch
 
-    from .engine import mt_state_words, pretwist
+    from .engine import seed_states
     labels = [r.difficulty for r in workload.requests]
     if mode == "actual":
         for lv in labels:
@@ -221,8 +221,7 @@ def predicted_levels(workload: Workload, mode: str, predict_seeds: list, confusi
     n = len(labels)
     _lib.require_cuda()
     lib = _lib.load()
-    states = np.stack([pretwist(mt_state_words(s)) for s in predict_seeds])
-    st = torch.from_numpy(states.view(np.int32).reshape(-1).copy()).to(device)
+    st = seed_states(predict_seeds, device=device)     # random.Random(seed), on the device
     lv = torch.tensor(labels, dtype=torch.int32, device=device)
     mat = torch.tensor(np.asarray(matrix, dtype=np.float64).reshape(-1), device=device)
     out = torch.empty(n, dtype=torch.int32, device=device)

@@ -125,3 +125,19 @@ def test_widest_tma_rows_match_oracle():
         win = oact.synth_window(9, 40 + r, 0, 16 * r, 0, T, H, True)
         ref, _ = port.pooled_linear_probe(win, w[0], 0.1, g[0], beta[0])
         assert abs(float(logit[r, 0]) - ref) <= 1e-4 * max(abs(ref), 1.0)
+
+
+def test_device_mt_seeding_matches_cpython():
+    """duchess_mt_seed == random.Random(seed).getstate() after its pending
+    twist (engine.pretwist), for seeds of one and two 32-bit words."""
+    from paper_2509_24957_b200.engine import mt_state_words, pretwist, seed_states
+    rng = random.Random(7)
+    seeds = [0, 1, 12345, 2 ** 32 - 1, 2 ** 32, 2 ** 64 - 1] + [rng.getrandbits(64) for _ in range(50)]
+    got = seed_states(seeds).cpu().numpy().view(np.uint32).reshape(len(seeds), 625)
+    for s, row in zip(seeds, got):
+        assert np.array_equal(row, pretwist(mt_state_words(s))), s
+        r = random.Random(s)
+        a = [r.random() for _ in range(3)]
+        r2 = random.Random()
+        r2.setstate((3, tuple(int(x) for x in row), None))
+        assert [r2.random() for _ in range(3)] == a
