@@ -917,6 +917,63 @@ def cpu_sim(arrivals=None, k=256):
                       f"the workload hash (the reference's run_simulation restated), one core"}
 
 
+def run_baselines_bench(args, rank, world, local_rank):
+    """the baseline policies (DefaultScRun, ShortMkRun,
+    DynasorRun, orchestrator.py:405-561) on the device slot machinery
+    (duchess_baseline_round): 256 slots over a cycling math-like pool; value =
+    finished requests/s of Default SC, the others reported beside it."""
+    import torch
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = dict(CONFIGS["c2"])
+    traces, knobs, seeds = make_workload(cfg, seed=1000 + 17 * rank)
+    res = {}
+    for pol in ("default-sc", "short-mk", "dynasor"):
+        eng = BatchedDuchess(traces, knobs, seeds, n_slots=256, queue=list(range(len(traces))),
+                             cycle=True, policy=pol, device=dev)
+        for _ in range(args.warmup):
+            eng.baseline_round()
+        torch.cuda.synchronize(dev)
+        c0 = eng.t["counters"].clone()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            eng.baseline_round()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        fin = int((eng.t["counters"] - c0)[2])
+        res[pol] = {"requests_per_s": fin / (ms / 1e3), "us_per_round": ms / args.steps * 1e3}
+    out = {"metric": "baseline-policy finished requests/s (Default SC, SURVEY 8(f)1)",
+           "value": res["default-sc"]["requests_per_s"] * world, "unit": "requests/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": res["default-sc"]["us_per_round"] / 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+           "data": "generate_synthetic math-like pool (2048 requests, cycling)",
+           "config": {"workload": "256 request slots x 16 branch slots, one round per step",
+                      "policies": res},
+           "gpu_launches": args.steps}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baselines()
+    return out
+
+
+def cpu_baselines(budget_s=5.0):
+    from oracle import port
+    cfg = CONFIGS["c2"]
+    traces = port.generate(port.GenParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]]),
+                           256, 1000)
+    knobs = port.Knobs(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+    t0, n = time.perf_counter(), 0
+    while time.perf_counter() - t0 < budget_s:
+        port.DefaultScRequest(traces[n % len(traces)], knobs).run()
+        n += 1
+    return {"value": n / (time.perf_counter() - t0), "unit": "requests/s", "cores": 1,
+            "kind": "port", "sample": f"oracle/port.py DefaultScRequest.run over math-like "
+                                      f"requests, {budget_s:.0f} s on one core"}
+
+
 def run_train_bench(args, rank, world, local_rank):
     import torch
     from paper_2509_24957_b200.probe import fill_windows
@@ -1132,8 +1189,8 @@ def cpu_fork_or_train(args):
 
 
 def run_reference(args, cfg):
-    if args.config in ("difficulty", "sim"):
-        cb = cpu_difficulty() if args.config == "difficulty" else cpu_sim()
+    if args.config in ("difficulty", "sim", "baselines"):
+        cb = {"difficulty": cpu_difficulty, "sim": cpu_sim, "baselines": cpu_baselines}[args.config]()
         return {"impl": "reference", "metric": f"{args.config} CPU reference", "value": cb["value"],
                 "unit": cb["unit"], "n_gpus": args.gpus, "steps": 1, "warmup": 0,
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
@@ -1183,7 +1240,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2",
-                    choices=sorted(CONFIGS) + ["c3tc", "c4", "c5", "difficulty", "sim"])
+                    choices=sorted(CONFIGS) + ["c3tc", "c4", "c5", "difficulty", "sim",
+                                               "baselines"])
     ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
                     help="K1 variant: persistent TMA over the compacted survivor list "
                          "(default), TMA over the row mask, or the per-window LDG kernel")
@@ -1229,6 +1287,8 @@ def main():
         out = run_difficulty_bench(args, rank, world, local_rank)
     elif args.config == "sim":
         out = run_sim_bench(args, rank, world, local_rank)
+    elif args.config == "baselines":
+        out = run_baselines_bench(args, rank, world, local_rank)
     elif args.mode == "split" and args.k1 == "list" and not args.graph and args.shards > 1:
         out = run_gpu_sharded(args, cfg, rank, world, local_rank)
     else:
