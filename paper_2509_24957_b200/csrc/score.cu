@@ -555,12 +555,19 @@ extern "C" int duchess_gather_active(const void* src, void* dst, int64_t row_byt
   if (n_rows == 0) return DUCHESS_OK;
   const void* s = src;
   cudaPointerAttributes attr{};
-  if (cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+  if (cudaPointerGetAttributes(&attr, src) != cudaSuccess) {
+    cudaGetLastError();
+    return DUCHESS_EINVAL;
+  }
+  if (attr.type == cudaMemoryTypeUnregistered) return DUCHESS_EINVAL;   // pageable host memory
+  if (attr.type == cudaMemoryTypeHost) {
     void* dp = nullptr;                          // pinned host memory: its device mapping
-    if (cudaHostGetDevicePointer(&dp, const_cast<void*>(src), 0) != cudaSuccess) return DUCHESS_EINVAL;
+    if (cudaHostGetDevicePointer(&dp, const_cast<void*>(src), 0) != cudaSuccess) {
+      cudaGetLastError();
+      return DUCHESS_EINVAL;
+    }
     s = dp;
   }
-  cudaGetLastError();
   gather_rows_kernel<<<sm_count() * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(s), static_cast<char*>(dst), row_bytes, active_rows, active_count,
       active_count + 2, n_rows);

@@ -109,7 +109,13 @@ class Scorer:
         if L != self.bank.L or H != self.bank.H:
             raise ValueError(f"activation shape (L={L}, H={H}) does not match probe bank "
                              f"(L={self.bank.L}, H={self.bank.H})")
-        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}[acts.dtype]
+        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}.get(acts.dtype)
+        if dtype is None:
+            raise ValueError("activations must be bf16 or fp32")
+        if out_logit.dtype != torch.float32 or out_logit.numel() < rows * L:
+            raise ValueError("out_logit must be fp32 with rows * L entries")
+        if out_prob.dtype != torch.float64 or out_prob.numel() < rows * L:
+            raise ValueError("out_prob must be fp64 with rows * L entries")
         st = acts.stride()
         _lib.check(self.lib.duchess_score_list(
             acts.data_ptr(), dtype, rows, L, T, H, st[0], st[1], st[2],
@@ -130,7 +136,15 @@ class Scorer:
                              f"(L={self.bank.L}, H={self.bank.H})")
         if rows != engine.R * engine.C:
             raise ValueError("acts must have R*C rows (one per branch slot)")
-        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}[acts.dtype]
+        if acts.stride(3) != 1:
+            raise ValueError("hidden dimension must be contiguous")
+        if out_logit.dtype != torch.float32 or out_logit.numel() < rows * L:
+            raise ValueError("out_logit must be fp32 with rows * L entries")
+        if out_prob.dtype != torch.float64 or out_prob.numel() < rows * L:
+            raise ValueError("out_prob must be fp64 with rows * L entries")
+        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}.get(acts.dtype)
+        if dtype is None:
+            raise ValueError("activations must be bf16 or fp32")
         st = acts.stride()
         _lib.check(self.lib.duchess_score_active(
             acts.data_ptr(), dtype, rows, L, T, H, st[0], st[1], st[2],

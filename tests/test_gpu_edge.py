@@ -141,3 +141,14 @@ def test_device_mt_seeding_matches_cpython():
         r2 = random.Random()
         r2.setstate((3, tuple(int(x) for x in row), None))
         assert [r2.random() for _ in range(3)] == a
+
+
+def test_upload_survivors_rejects_pageable_host_memory():
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    host = torch.zeros(1024, dtype=torch.uint8)                  # pageable
+    dev = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    rows = torch.zeros(4, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
+    assert lib.duchess_gather_active(host.data_ptr(), dev.data_ptr(), 256, rows.data_ptr(),
+                                     cnt.data_ptr(), 4, _lib.stream_handle()) == 1
