@@ -44,8 +44,21 @@ struct GradArgs {
   float* partial;  // [grid, H+1]
 };
 
-template <bool BF16, int VPT, int RB>
-__global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
+// Row q's VPT vectors of this thread from the stage (zeros past the row end or
+// past the stage's row count).
+template <int VPT, bool FULL>
+__device__ __forceinline__ void load_row(uint4 (&xv)[VPT], const char* base, int q, int nr,
+                                         int row_bytes, int nvec) {
+  const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * row_bytes);
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = j * kCons + int(threadIdx.x);
+    xv[j] = (q < nr && (FULL || v < nvec)) ? rowv[v] : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+template <bool BF16, int VPT, int RB, bool FULL>
+__global__ void __maxnreg__(112) lr_grad_kernel(GradArgs a) {   // 2 CTAs of 288 threads per SM
   constexpr int EPV = BF16 ? 8 : 4;   // elements per 16-byte vector
   extern __shared__ __align__(128) char smem[];
   __shared__ uint64_t full_bar[16], empty_bar[16];
@@ -71,15 +84,16 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
     // ---- producer: TMA bulk copies of row blocks into the ring ----
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t it = 0; it < n_iter; ++it) {
-        const int s = int(it % a.stages);
-        const uint32_t ph = uint32_t((it / a.stages) & 1);
         mbar_wait(&empty_bar[s], ph ^ 1u);
         const int64_t r = row0 + it * a.rb;
         const int nr = int(lmin(a.rb, row1 - r));
         const uint32_t bytes = uint32_t(nr) * uint32_t(a.row_bytes);
         mbar_expect_tx(&full_bar[s], bytes);
         bulk_g2s(smem + size_t(s) * stage_bytes, a.X + r * a.row_bytes, bytes, &full_bar[s], pol);
+        if (++s == a.stages) { s = 0; ph ^= 1u; }
       }
     }
     return;
@@ -102,9 +116,9 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
   const float bias = a.w[a.H];
   float gb = 0.f;
 
+  int s = 0;
+  uint32_t ph = 0;
   for (int64_t it = 0; it < n_iter; ++it) {
-    const int s = int(it % a.stages);
-    const uint32_t ph = uint32_t((it / a.stages) & 1);
     const int64_t r = row0 + it * a.rb;
     const int nr = int(lmin(a.rb, row1 - r));
     float yv[RB];                       // labels prefetched before the stage wait
@@ -115,30 +129,30 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
     float dots[RB], dots2[RB];
 #pragma unroll
     for (int q = 0; q < RB; ++q) { dots[q] = 0.f; dots2[q] = 0.f; }
+    // A row's shared loads are all issued before the first use, and each
+    // vector has its own accumulator pair, so the loads overlap and the FFMA2
+    // chains stay short.
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      if (q < nr) {
-        const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
+      uint4 xv[VPT];
+      load_row<VPT, FULL>(xv, base, q, nr, a.row_bytes, nvec);
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-          const int v = j * kCons + int(threadIdx.x);
-          if (v < nvec) {
-            const uint4 x = rowv[v];
-            const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
-            if constexpr (BF16) {
+      for (int j = 0; j < VPT; ++j) {
+        const uint32_t xw[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+        float p0 = 0.f, p1 = 0.f;
+        if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                ffma2(dots[q], dots2[q], wv[j][2 * e], wv[j][2 * e + 1], bf16lo(xw[e]),
-                      bf16hi(xw[e]));
-            } else {
+          for (int e = 0; e < 4; ++e)
+            ffma2(p0, p1, wv[j][2 * e], wv[j][2 * e + 1], bf16lo(xw[e]), bf16hi(xw[e]));
+        } else {
 #pragma unroll
-              for (int e = 0; e < 4; e += 2) {
-                dots[q] = fmaf(wv[j][e], __uint_as_float(xw[e]), dots[q]);
-                dots2[q] = fmaf(wv[j][e + 1], __uint_as_float(xw[e + 1]), dots2[q]);
-              }
-            }
+          for (int e = 0; e < 4; e += 2) {
+            p0 = fmaf(wv[j][e], __uint_as_float(xw[e]), p0);
+            p1 = fmaf(wv[j][e + 1], __uint_as_float(xw[e + 1]), p1);
           }
         }
+        dots[q] += p0;
+        dots2[q] += p1;
       }
     }
     const int buf = int(it & 1);
@@ -170,28 +184,24 @@ __global__ void __launch_bounds__(kCons + 32, 2) lr_grad_kernel(GradArgs a) {
     }
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      if (q < nr) {
-        const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
+      uint4 xv[VPT];
+      load_row<VPT, FULL>(xv, base, q, nr, a.row_bytes, nvec);
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-          const int v = j * kCons + int(threadIdx.x);
-          if (v < nvec) {
-            const uint4 x = rowv[v];
-            const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
-            if constexpr (BF16) {
+      for (int j = 0; j < VPT; ++j) {
+        const uint32_t xw[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+        if constexpr (BF16) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                ffma2(g[j][2 * e], g[j][2 * e + 1], res[q], res[q], bf16lo(xw[e]), bf16hi(xw[e]));
-            } else {
+          for (int e = 0; e < 4; ++e)
+            ffma2(g[j][2 * e], g[j][2 * e + 1], res[q], res[q], bf16lo(xw[e]), bf16hi(xw[e]));
+        } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) g[j][e] += res[q] * __uint_as_float(xw[e]);
-            }
-          }
+          for (int e = 0; e < 4; ++e) g[j][e] += res[q] * __uint_as_float(xw[e]);
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if (++s == a.stages) { s = 0; ph ^= 1u; }
   }
 
   float* out = a.partial + int64_t(blockIdx.x) * (a.H + 1);
@@ -224,7 +234,8 @@ __global__ void sgd_kernel(float* w, const float* g, int n, float lr) {
 
 template <bool BF16, int VPT, int RB>
 static cudaError_t launch_grad_rb(const GradArgs& a, int grid, size_t smem, cudaStream_t s) {
-  auto k = lr_grad_kernel<BF16, VPT, RB>;
+  auto k = a.row_bytes == VPT * kCons * 16 ? lr_grad_kernel<BF16, VPT, RB, true>
+                                           : lr_grad_kernel<BF16, VPT, RB, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<grid, kCons + 32, smem, s>>>(a);
   return cudaGetLastError();
