@@ -133,7 +133,13 @@ def test_engine_fork_records_drive_cow_fork():
 
 
 @pytest.mark.parametrize("dtype,N,H", [(torch.bfloat16, 3000, 1024), (torch.float32, 777, 512),
-                                       (torch.bfloat16, 5, 8192), (torch.bfloat16, 40000, 256)])
+                                       (torch.bfloat16, 5, 8192), (torch.bfloat16, 40000, 256),
+                                       # C5 row width, stage kept in registers, ragged last stage
+                                       (torch.bfloat16, 2999, 8192), (torch.float32, 1001, 8192),
+                                       # rows too wide to keep: two-CTA re-read kernel
+                                       (torch.bfloat16, 613, 16384),
+                                       # partial last vector column block
+                                       (torch.bfloat16, 1234, 5128)])
 def test_lr_grad_matches_fp64(dtype, N, H):
     from paper_2509_24957_b200.train import LogisticProbeTrainer
     g = torch.Generator(device="cuda").manual_seed(N + H)
