@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .oracle_free import bf16_round_np
+from .hostmath import bf16_round_np
 
 BN_TILE, BK = 256, 64
 
