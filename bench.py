@@ -1,7 +1,7 @@
 """Benchmark: branch-steps/s scored + decided (DUCHESS probe + orchestration).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1|c3|c4|c5|c3tc|baselines|difficulty|sim]
+                    [--config c2|c1|c3|c3t1|c4|c5|c3tc|baselines|difficulty|sim]
 
 One step = one orchestration round over every request slot on the GPU:
 duchess_score_active (K1: pooled LayerNorm + linear probe over each
@@ -50,6 +50,8 @@ CONFIGS = {
     "c2": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048),
     "c1": dict(R=8, c=8, L=1, T=1, H=4096, dtype="f32", preset="gsm8k-like", pool=128),
     "c3": dict(R=1024, c=32, L=4, T=32, H=5120, dtype="bf16", preset="math-like", pool=4096),
+    # SURVEY 8(d) C3 secondary row: the last token only (T=1, 40 960 B per branch-step)
+    "c3t1": dict(R=1024, c=32, L=4, T=1, H=5120, dtype="bf16", preset="math-like", pool=4096),
 }
 
 PRESET_KNOBS = {   # presets.py:30-68 (knobs) — max_branches overridden per config
@@ -1289,12 +1291,12 @@ def main():
     if args.shards is None:
         # two request shards per GPU on two streams hide each shard's round
         # kernel under the other's scoring
-        args.shards = 2 if args.config in ("c2", "c3") else 1
+        args.shards = 2 if args.config in ("c2", "c3", "c3t1") else 1
     if args.shard_order is None:
         # C2 (1 GB per step): concurrent scorers also fill each other's launch
         # ramp and tail; C3 (43 GB per step): taking turns keeps every launch
         # at full bandwidth
-        args.shard_order = "overlap" if args.config == "c2" else "turns"
+        args.shard_order = "overlap" if args.config in ("c2", "c3t1") else "turns"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -133,12 +133,22 @@ __global__ void __launch_bounds__(NT) score_fast_kernel(ScoreArgs a) {
   float wgv[PASSES][VEC];
   float s1 = 0.f, sw = 0.f;
   const float* wrow = a.wg + int64_t(l) * a.H;
+  if ((a.T & (a.T - 1)) != 0) {     // uniform branch: no discarded division
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[p][v] = acc[p][v] / float(a.T);
+  } else if (a.T != 1) {
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[p][v] = acc[p][v] * invT;
+  }
 #pragma unroll
   for (int p = 0; p < PASSES; ++p) {
     const int col = cbeg + (p * NT + int(threadIdx.x)) * VEC;
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      acc[p][v] = (a.T & (a.T - 1)) == 0 ? acc[p][v] * invT : acc[p][v] / float(a.T);
       wgv[p][v] = valid[p] ? __ldg(wrow + col + v) : 0.f;
       if (valid[p]) { s1 += acc[p][v]; sw += wgv[p][v]; }
     }
@@ -279,6 +289,170 @@ static cudaError_t launch_tma(const ScoreArgs& a, const TmaArgs& t, int vpt, int
     case 8: go(score_tma_kernel<BF16, 8>); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+
+// Last-token windows (T = 1: the paper's probe reads one token, PAPER.md:150;
+// C1 and C3-T1). A unit is one H-vector (10 KB at H = 5120 bf16), too small
+// for a CTA-wide LayerNorm reduction: each WARP scores whole units. A lane
+// issues all of its NV 16-byte loads of the unit at once (L1 no-allocate), so
+// 16 warps x 10 KB per SM are in flight; the two-pass LN statistics run on the
+// registers (exact centring, no second read) and the folded probe weights of
+// all layers sit in shared memory. Units are dealt round-robin over the grid's
+// warps; no CTA barrier after the weight load.
+constexpr int kRowsWarps = 16;
+constexpr int kRowsSmemMax = 160 * 1024;
+template <bool BF16, int NV, bool WSMEM>
+__global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_kernel(ScoreArgs a, TmaArgs t) {
+  constexpr int VEC = BF16 ? 8 : 4;
+  constexpr int ESZ = BF16 ? 2 : 4;
+  extern __shared__ __align__(16) float wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = t.row_bytes / 16;
+  if constexpr (WSMEM) {      // the folded weights are not written by the previous kernel
+    const int nw = a.L * a.H / 4;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x)
+      reinterpret_cast<float4*>(wsm)[i] = __ldg(reinterpret_cast<const float4*>(a.wg) + i);
+    __syncthreads();
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  if (t.row_par) {
+    const int par = *t.row_par;
+    t.row_list += par * t.list_stride;
+    t.row_count += par;
+  }
+  const int64_t n_units = (t.row_list ? int64_t(*t.row_count) : a.n_units / a.L) * a.L;
+  const int64_t gw = int64_t(blockIdx.x) * kRowsWarps + warp;
+  const int64_t nw = int64_t(gridDim.x) * kRowsWarps;
+  auto unit_src = [&](int64_t row, int l) {
+    return reinterpret_cast<const uint4*>(a.acts + (row * a.row_stride + int64_t(l) * a.layer_stride) * ESZ);
+  };
+  // next valid unit of this warp at or after u (n_units if none)
+  auto next_unit = [&](int64_t u, int64_t& row, int& l) {
+    for (; u < n_units; u += nw)
+      if (tma_unit(a, t, u, row, l)) return u;
+    return n_units;
+  };
+  auto load = [&](uint4 (&xv)[NV], int j, const uint4* src) {
+    const int v = j * 32 + lane;
+    xv[j] = v < nvec ? ldg_stream(src + v) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  int64_t row = 0;
+  int l = 0;
+  int64_t u = next_unit(gw, row, l);
+  uint4 xv[NV];
+  if (u < n_units) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) load(xv, j, unit_src(row, l));
+  }
+  // Rolling register pipeline: pass 2 of unit k reloads each vector register
+  // with unit k+1's data right after its last use, so the next unit's loads
+  // are in flight during pass 2 and the reductions.
+  while (u < n_units) {
+    // pass 1: eight independent chains; bf16 pairs are added straight into fp32
+    // (FHADD), so no converted copy of the vector stays live into pass 2
+    float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w4[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+      if constexpr (BF16) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) add_bf16x2_f32(s8[2 * e], s8[2 * e + 1], w4[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s8[e] = __fadd_rn(s8[e], __uint_as_float(w4[e]));
+      }
+    }
+#pragma unroll
+    for (int e = 1; e < 8; e <<= 1)
+#pragma unroll
+      for (int q = 0; q < 8; q += 2 * e) s8[q] = __fadd_rn(s8[q], s8[q + e]);
+    const float s1 = warp_sum(s8[0]);
+    const float mean = __fdiv_rn(s1, float(a.H));
+    int64_t nrow = 0;
+    int nl = 0;
+    const int64_t un = next_unit(u + nw, nrow, nl);
+    const uint4* nsrc = un < n_units ? unit_src(nrow, nl) : nullptr;
+    const float* wrow = (WSMEM ? wsm : a.wg) + int64_t(l) * a.H;
+    float qq = 0.f, d = 0.f, qq2 = 0.f, d2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int v = j * 32 + lane;
+      if (v < nvec) {
+        const uint32_t w4[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+        // centred values c = x - mean, rounded once: for bf16 one mixed-precision
+        // add per element straight from the packed pair (FHADD, no conversion)
+        float c[VEC];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if constexpr (BF16) {
+            c[2 * e] = -mean;
+            c[2 * e + 1] = -mean;
+            add_bf16x2_f32(c[2 * e], c[2 * e + 1], w4[e]);
+          } else {
+            c[e] = __fsub_rn(__uint_as_float(w4[e]), mean);
+          }
+        }
+        if (nsrc) load(xv, j, nsrc);
+        const float4* wp = reinterpret_cast<const float4*>(wrow + v * VEC);
+#pragma unroll
+        for (int q = 0; q < VEC / 4; ++q) {
+          const float4 t4 = WSMEM ? wp[q] : __ldg(wp + q);
+          ffma2(qq, d, c[4 * q], t4.x, c[4 * q], c[4 * q]);
+          ffma2(qq2, d2, c[4 * q + 1], t4.y, c[4 * q + 1], c[4 * q + 1]);
+          ffma2(qq, d, c[4 * q + 2], t4.z, c[4 * q + 2], c[4 * q + 2]);
+          ffma2(qq2, d2, c[4 * q + 3], t4.w, c[4 * q + 3], c[4 * q + 3]);
+        }
+      } else if (nsrc) {
+        load(xv, j, nsrc);
+      }
+    }
+    qq = warp_sum(__fadd_rn(qq, qq2));
+    d = warp_sum(__fadd_rn(d, d2));
+    if (lane == 0) {
+      const float var = __fdiv_rn(qq, float(a.H));
+      const float logit = __fadd_rn(__fdiv_rn(d, __fsqrt_rn(__fadd_rn(var, kLayerNormEps))), a.c1[l]);
+      write_score(a, row * a.L + l, logit);
+    }
+    u = un;
+    row = nrow;
+    l = nl;
+  }
+}
+
+template <bool BF16>
+static cudaError_t launch_rows(const ScoreArgs& a, const TmaArgs& t, int nv, int grid,
+                               cudaStream_t s) {
+  const size_t wbytes = size_t(a.L) * a.H * sizeof(float);
+  const bool wsmem = wbytes <= kRowsSmemMax;
+  const size_t smem = wsmem ? wbytes : 0;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRowsWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, t);
+  };
+#define DUCHESS_ROWS(NVV)                                                          \
+  case NVV:                                                                        \
+    if (wsmem) go(score_rows_kernel<BF16, NVV, true>);                             \
+    else go(score_rows_kernel<BF16, NVV, false>);                                  \
+    break;
+  switch (nv) {
+    DUCHESS_ROWS(1) DUCHESS_ROWS(2) DUCHESS_ROWS(4) DUCHESS_ROWS(8) DUCHESS_ROWS(12)
+    DUCHESS_ROWS(16) DUCHESS_ROWS(20) DUCHESS_ROWS(24)
+    default: return cudaErrorInvalidValue;
+  }
+#undef DUCHESS_ROWS
   return cudaGetLastError();
 }
 
@@ -439,6 +613,19 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     // Tunables (env, for sweeps): CTAs per SM and stage size target.
     static const int cps = [] { const char* e = getenv("DUCHESS_K1_CPS"); int v = e ? atoi(e) : 2; return v < 1 ? 1 : (v > 4 ? 4 : v); }();
     static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kTmaStageTarget; return v < 4096 ? 4096 : v; }();
+    const int nvec_row = int(row_bytes / 16);
+    static const bool rows_ok = [] { const char* e = getenv("DUCHESS_K1_ROWS"); return !e || atoi(e) != 0; }();
+    if (rows_ok && T == 1 && nvec_row <= 24 * 32 && (reinterpret_cast<uintptr_t>(wg) % 16) == 0) {
+      int nv = (nvec_row + 31) / 32;
+      nv = nv <= 2 ? nv : nv <= 4 ? 4 : nv <= 8 ? 8 : (nv + 3) / 4 * 4;
+      a.nsplit = 1;
+      a.chunk = H;
+      int grid = sm_count();
+      if (!row_list && int64_t(grid) * kRowsWarps > a.n_units)
+        grid = int((a.n_units + kRowsWarps - 1) / kRowsWarps);
+      const cudaError_t e = bf16 ? launch_rows<true>(a, t, nv, grid, s) : launch_rows<false>(a, t, nv, grid, s);
+      return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+    }
     t.tokens_per_stage = int(row_bytes >= stage_target ? 1 : stage_target / row_bytes);
     if (t.tokens_per_stage > T) t.tokens_per_stage = T;
     const int stage_bytes = t.tokens_per_stage * t.row_bytes;

@@ -191,14 +191,26 @@ __device__ __forceinline__ void tma_consume(const ScoreArgs& a, const TmaArgs& t
     }
     const float* wrow = a.wg + int64_t(l) * a.H;
     float s1 = 0.f, unused = 0.f;
+    // window mean: exact scaling for a power-of-two T (none for T = 1), IEEE
+    // division otherwise; a uniform branch, so the division is not evaluated
+    // (and discarded by a select) when T is a power of two
+    if (!pow2T) {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[j][e] = __fdiv_rn(acc[j][e], float(a.T));
+    } else if (a.T != 1) {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[j][e] = __fmul_rn(acc[j][e], invT);
+    }
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const int v = j * kTmaCons + int(threadIdx.x);
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        acc[j][e] = pow2T ? __fmul_rn(acc[j][e], invT) : __fdiv_rn(acc[j][e], float(a.T));
+      for (int e = 0; e < VEC; ++e)
         if (v < nvec) s1 = __fadd_rn(s1, acc[j][e]);
-      }
     }
     cons_sum2(s1, unused, red, k);
     const float mean = __fdiv_rn(s1, float(a.H));
