@@ -29,6 +29,12 @@ def _probe(H, L, seed):
     (torch.bfloat16, 8, 5120, 4, 8, 0, 0),          # C3 shape (4 layers)
     (torch.float32, 3, 12, 1, 5, 0, 0),             # tiny, odd T
     (torch.bfloat16, 5, 10, 2, 4, 0, 0),            # unaligned -> generic kernel
+    # T = 1: one warp per window (score_rows_kernel)
+    (torch.bfloat16, 1, 5120, 4, 40, 0, 0),         # C3-T1 shape
+    (torch.bfloat16, 1, 4096, 1, 300, 0, 0),
+    (torch.bfloat16, 1, 4104, 2, 9, 0, 0),          # partial last vector column (nvec = 513)
+    (torch.float32, 1, 1024, 3, 17, 0, 0),
+    (torch.bfloat16, 1, 64, 1, 5000, 0, 0),         # tiny rows, > 1 unit per warp
 ])
 def test_score_matches_oracle(dtype, T, H, L, rows, nsplit, threads):
     from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
@@ -60,9 +66,10 @@ def test_score_matches_oracle(dtype, T, H, L, rows, nsplit, threads):
     del wgf
 
 
-def test_score_mask_skips_rows():
+@pytest.mark.parametrize("T", [4, 1])
+def test_score_mask_skips_rows(T):
     from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
-    H, T, rows = 4096, 4, 8
+    H, rows = 4096, 8
     w, b, g, beta = _probe(H, 1, seed=3)
     bank = ProbeBank.from_linear(w, b, g, beta)
     acts = torch.empty((rows, 1, T, H), dtype=torch.bfloat16, device="cuda")
@@ -94,3 +101,36 @@ def test_score_deterministic():
         s(acts, lg, pr)
         outs.append(lg.clone())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_score_list_last_token_matches_oracle():
+    """T = 1 through the survivor-list path (warp per window): only listed rows
+    are written, in any list order, each within the north-star tolerance."""
+    from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
+    rows, L, H = 700, 2, 5120
+    w, b, g, beta = _probe(H, L, seed=11)
+    bank = ProbeBank.from_linear(w, b, g, beta)
+    acts = torch.empty((rows, L, 1, H), dtype=torch.bfloat16, device="cuda")
+    req = torch.arange(rows, dtype=torch.int64, device="cuda") + 100
+    tmpl = torch.zeros(rows, dtype=torch.int32, device="cuda")
+    pos = torch.full((rows,), 32, dtype=torch.int32, device="cuda")
+    fill_windows(acts, 4, req, tmpl, pos)
+    pick = np.random.default_rng(2).permutation(rows)[:333]
+    lst = torch.tensor(pick, dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([len(pick)], dtype=torch.int32, device="cuda")
+    logit = torch.full((rows, L), 9.0, device="cuda")
+    prob = torch.full((rows, L), 9.0, dtype=torch.float64, device="cuda")
+    Scorer(bank, rows * L).score_list(acts, logit, prob, lst, cnt)
+    torch.cuda.synchronize()
+    lg = logit.cpu().numpy()
+    chosen = set(int(r) for r in pick)
+    for r in range(rows):
+        if r not in chosen:
+            assert (lg[r] == 9.0).all()
+            continue
+        if r % 7:
+            continue
+        for l in range(L):
+            win = oact.synth_window(4, 100 + r, 0, 32, l, 1, H, True)
+            ref, _ = port.pooled_linear_probe(win, w[l], b[l], g[l], beta[l])
+            assert abs(float(lg[r, l]) - ref) <= 1e-4 * max(abs(ref), 1.0)
