@@ -79,11 +79,13 @@ def k3_traffic():
         return json.load(f)["dram_bytes"], os.path.relpath(files[-1], ROOT)
 
 
-def k1_traffic_ratio():
+def k1_traffic_ratio(T=32):
     """DRAM bytes / algorithmic bytes of K1 from the committed ncu --set full
-    capture (tools/profile_all.sh -> profiles/<round>/k1_traffic.json)."""
+    capture (tools/profile_all.sh -> profiles/<round>/k1_traffic.json; the
+    T = 1 rows kernel: k1rows_traffic.json)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k1_traffic.json")))
+    name = "k1rows_traffic.json" if T == 1 else "k1_traffic.json"
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", name)))
     if not files:
         return None, None
     with open(files[-1]) as f:
@@ -338,9 +340,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                      "k1_share_of_step": k1_ms / ms,
                      "k1_launches_timed": (f"{len(k1_ev)} (eager pass after the timed graph "
                                            f"replays)") if args.graph else len(k1_ev),
-                     "traffic": (None if k1_traffic_ratio()[0] is None
-                                 else k1_traffic_ratio()[0] * bytes_per_launch),
-                     "traffic_source": k1_traffic_ratio()[1]},
+                     "traffic": (None if k1_traffic_ratio(T)[0] is None
+                                 else k1_traffic_ratio(T)[0] * bytes_per_launch),
+                     "traffic_source": k1_traffic_ratio(T)[1]},
         "e2e": e2e,
         "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": clk,
@@ -503,15 +505,16 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
         "branch_steps_per_step": branch_steps / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "peak_note": PEAK_NOTE,
-                     "kernel": ("duchess_score (K1, list): the shards' concurrent launches, "
-                                "scoring bytes per step / whole step time" if overlap else
-                                "duchess_score (K1, list) per shard launch"),
+                     "kernel": (("duchess_score (K1, list{}): the shards' concurrent launches, "
+                                 "scoring bytes per step / whole step time" if overlap else
+                                 "duchess_score (K1, list{}) per shard launch").format(
+                                     ", score_rows_kernel" if T == 1 else "")),
                      "bytes_per_launch": bytes_per_launch,
                      "k1_us_per_launch": k1_avg_s * 1e6,
                      "k1_launches_timed": len(k1_us),
-                     "traffic": (None if k1_traffic_ratio()[0] is None
-                                 else k1_traffic_ratio()[0] * bytes_per_launch),
-                     "traffic_source": k1_traffic_ratio()[1]},
+                     "traffic": (None if k1_traffic_ratio(T)[0] is None
+                                 else k1_traffic_ratio(T)[0] * bytes_per_launch),
+                     "traffic_source": k1_traffic_ratio(T)[1]},
         "e2e": e2e,
         "gpu_launches": 2 * S * args.steps,
         "clocks": clk,
