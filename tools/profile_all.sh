@@ -8,6 +8,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file $D/launches_c2.csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 2 > $D/bench_c2_under_ncu.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:score_tma -s 2 -c 1 -o $D/k1_full -f python tools/k1_capture.py > $D/k1_full.log 2>&1
 ncu --set full --cache-control none --clock-control none --import-source on -k regex:round_kernel -s 6 -c 1 -o $D/round_full -f python bench.py --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 2 > $D/round_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:score_rows -s 6 -c 1 -o $D/k1rows_full -f python tools/k1_short.py 0 > $D/k1rows_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fork_exec -s 2 -c 1 -o $D/k3_full -f python bench.py --config c4 --steps 3 --warmup 1 --no-cpu-baseline > $D/k3_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:lr_grad_kernel -s 2 -c 1 -o $D/k4_full -f python bench.py --config c5 --steps 3 --warmup 1 --no-cpu-baseline > $D/k4_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:mlp_probe_tc -s 2 -c 1 -o $D/tc_full -f python bench.py --config c3tc --steps 3 --warmup 1 --no-cpu-baseline > $D/tc_full.log 2>&1

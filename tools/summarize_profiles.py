@@ -28,7 +28,7 @@ def raw(rep):
 
 
 summary = {}
-for name in ("k1_full", "round_full", "k3_full", "k4_full", "tc_full", "step_full"):
+for name in ("k1_full", "k1rows_full", "round_full", "k3_full", "k4_full", "tc_full", "step_full"):
     rep = f"{src}/{name}.ncu-rep"
     if not os.path.exists(rep):
         continue
