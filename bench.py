@@ -1309,8 +1309,13 @@ def main():
         return
     if world > 1:
         import torch
+        # DUCHESS_BENCH_BACKEND=gloo (test only): exercise the multi-rank path on
+        # a box with fewer GPUs than ranks (ranks share GPUs round-robin)
+        backend = os.environ.get("DUCHESS_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group(backend)
     if args.config == "c4":
         out = run_fork_bench(args, rank, world, local_rank)
     elif args.config == "c5":

@@ -1,0 +1,37 @@
+"""bench.py's N > 1 path (torchrun, one process per rank, barrier + max-over-ranks
+timing, rank 0 prints one JSON line) run with two ranks on the box's GPU(s).
+The collectives go over gloo (DUCHESS_BENCH_BACKEND, test only) so two ranks
+can share one GPU; on an 8-GPU node the same code runs with NCCL."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("config", ["c2", "c5"])
+def test_bench_two_ranks_prints_one_aggregate_line(config):
+    env = dict(os.environ, DUCHESS_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "2", "--config", config, "--steps", "3", "--warmup", "3",
+           "--e2e-steps", "2", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["steps"] == 3 and out["value"] > 0
+    assert out["scaling"] == "weak" and out["gpu_launches"] > 0
