@@ -372,7 +372,8 @@ int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, i
  * One hidden layer of mlp_forward (predictor.py:126-151) batched over M rows:
  * pre = ln_fold ? (X.W'_j)/sigma_i - (mu_i/sigma_i) S_j + C_j : X.W_j + C_j,
  * out = act(pre * BS_j + BT_j) as bf16 [M, N] (act 0 none, 1 relu, 2 gelu).
- * X [M, K] bf16, W [N, K] bf16 (K-major); K % 64 == 0, N % 256 == 0. With
+ * X [M, K] bf16, W [N, K] bf16 (K-major); K % 64 == 0, N % 256 == 0; X, W, out,
+ * S, C, BS, BT 16-byte aligned. With
  * ln_fold the input LayerNorm is folded in (W' = W diag(gain), S = W' 1,
  * C = W ln_bias + b; row mean / std computed on the device). */
 size_t duchess_tc_linear_workspace_bytes(int64_t M, int32_t N);

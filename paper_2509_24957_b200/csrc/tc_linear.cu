@@ -116,6 +116,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // Exact (erf-based) GeLU, predictor.py:106-110.
 __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
+// LNF / ACT are compile-time (one instantiation per layer kind), so the
+// epilogue evaluates only its own activation (no GeLU computed and discarded).
+template <bool LNF, int ACT>
 __global__ void __launch_bounds__(THREADS, 1)
 linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               Args a) {
@@ -147,7 +150,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  const int stamp = a.ln_fold ? a.hdr[0] + 1 : 0;
+  const int stamp = LNF ? a.hdr[0] + 1 : 0;
 
   if (warp == 0) {
     if (lane == 0) {                                   // ---- TMA producer ----
@@ -194,7 +197,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
       const int mt = int(u / n_tiles), nt = int(u % n_tiles);
       const int64_t row = int64_t(mt) * BM + 32 * q + lane;
       float rsig = 1.f, shift = 0.f;
-      if (a.ln_fold) {                                 // overlaps this tile's MMAs
+      if (LNF) {                                       // overlaps this tile's MMAs
         const int nv = a.K / 8;
         const int v_lo = int(int64_t(nt) * nv / n_tiles), v_hi = int(int64_t(nt + 1) * nv / n_tiles);
         float sx = 0.f, sxx = 0.f;
@@ -250,17 +253,24 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
         const int j0 = n0 + c0;
         uint32_t packed[16];
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          float y[2];
+        for (int k = 0; k < 32; k += 4) {
+          // per-column parameters of 4 columns at once (broadcast 16-byte loads)
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.C + j0 + k));
+          const float4 bs4 = __ldg(reinterpret_cast<const float4*>(a.BS + j0 + k));
+          const float4 bt4 = __ldg(reinterpret_cast<const float4*>(a.BT + j0 + k));
+          float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (LNF) s4 = __ldg(reinterpret_cast<const float4*>(a.S + j0 + k));
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, bs[4] = {bs4.x, bs4.y, bs4.z, bs4.w};
+          const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+          float y[4];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = j0 + k + h;
-            float pre = a.ln_fold ? fmaf(v[k + h], rsig, fmaf(-shift, __ldg(a.S + j), __ldg(a.C + j)))
-                                  : v[k + h] + __ldg(a.C + j);
-            pre = fmaf(pre, __ldg(a.BS + j), __ldg(a.BT + j));
-            y[h] = a.act == 1 ? fmaxf(pre, 0.f) : a.act == 2 ? gelu(pre) : pre;
+          for (int h = 0; h < 4; ++h) {
+            float pre = LNF ? fmaf(v[k + h], rsig, fmaf(-shift, ss[h], cc[h])) : v[k + h] + cc[h];
+            pre = fmaf(pre, bs[h], bt[h]);
+            y[h] = ACT == 1 ? fmaxf(pre, 0.f) : ACT == 2 ? gelu(pre) : pre;
           }
           packed[k / 2] = uint32_t(f32_to_bf16_rne(y[0])) | (uint32_t(f32_to_bf16_rne(y[1])) << 16);
+          packed[k / 2 + 1] = uint32_t(f32_to_bf16_rne(y[2])) | (uint32_t(f32_to_bf16_rne(y[3])) << 16);
         }
         if (row < a.M) {
           uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.N + j0);
@@ -280,7 +290,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
-  if (a.ln_fold && threadIdx.x == 0) {               // last CTA out advances the epoch
+  if (LNF && threadIdx.x == 0) {                     // last CTA out advances the epoch
     __threadfence();
     if (atomicAdd(a.hdr + 1, 1) == int(gridDim.x) - 1) {
       a.hdr[1] = 0;
@@ -349,7 +359,9 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
   if (M < 0 || K < tcl::BK || K % tcl::BK || N < tcl::BN || N % tcl::BN || act < 0 || act > 2)
     return DUCHESS_EINVAL;
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16 ||
-      reinterpret_cast<uintptr_t>(out) % 16)
+      reinterpret_cast<uintptr_t>(out) % 16 || reinterpret_cast<uintptr_t>(C) % 16 ||
+      reinterpret_cast<uintptr_t>(BS) % 16 || reinterpret_cast<uintptr_t>(BT) % 16 ||
+      (ln_fold && reinterpret_cast<uintptr_t>(S) % 16))      // per-column params read as float4
     return DUCHESS_EINVAL;
   if (ln_fold && (!workspace || workspace_bytes < duchess_tc_linear_workspace_bytes(M, N) ||
                   reinterpret_cast<uintptr_t>(workspace) % 16))
@@ -378,13 +390,18 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
     a.ready = reinterpret_cast<int*>(ws + 16 + M * nt * 8);
   }
   a.n_units = mt * nt;
-  cudaFuncSetAttribute(tcl::linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl::SMEM);
+  void (*kern)(CUtensorMap, CUtensorMap, tcl::Args) =
+      ln_fold ? (act == 2 ? tcl::linear_kernel<true, 2> : act == 1 ? tcl::linear_kernel<true, 1>
+                                                                   : tcl::linear_kernel<true, 0>)
+              : (act == 2 ? tcl::linear_kernel<false, 2> : act == 1 ? tcl::linear_kernel<false, 1>
+                                                                    : tcl::linear_kernel<false, 0>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl::SMEM);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one CTA per SM, all resident: with ln_fold tiles wait on statistics shares
   const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
-  tcl::linear_kernel<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
+  kern<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
