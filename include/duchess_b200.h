@@ -362,7 +362,8 @@ int duchess_mlp_forward(const double* params, const int32_t* dims, int32_t n_hid
  * K % 64 == 0, NH % 256 == 0. out_logit fp32 [M], out_prob fp64 [M]. */
 size_t duchess_mlp_probe_tc_workspace_bytes(int64_t M, int32_t NH);
 /* workspace: >= duchess_mlp_probe_tc_workspace_bytes(M, NH) bytes, 16-byte
- * aligned, ZEROED before its first use; the kernel keeps it reusable. */
+ * aligned, ZEROED before its first use; the kernel keeps it reusable.
+ * X, W1g, s, c, w2 16-byte aligned. */
 int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, int32_t NH,
                          const float* s, const float* c, const float* w2, float b2,
                          float* out_logit, double* out_prob, void* workspace,

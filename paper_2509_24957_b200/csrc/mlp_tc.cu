@@ -257,18 +257,29 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_wait(&tmem_full[acc], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * kTcBN);
-      float logit = 0.f;
+      // per-column parameters as broadcast float4 loads; four independent
+      // partial logits (one per column residue mod 4), summed in fixed order
+      float lg[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
       for (int c0 = 0; c0 < kTcBN; c0 += 32) {
         float v[32];
         tmem_ld32(base + uint32_t(c0), v);
         const int j0 = h * kTcBN + c0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float hv = fmaf(v[j], rsig, fmaf(-shift, __ldg(a.s + j0 + j), __ldg(a.c + j0 + j)));
-          logit = fmaf(fmaxf(hv, 0.f), __ldg(a.w2 + j0 + j), logit);
+        for (int j = 0; j < 32; j += 4) {
+          const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.s + j0 + j));
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.c + j0 + j));
+          const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.w2 + j0 + j));
+          const float ss[4] = {s4.x, s4.y, s4.z, s4.w}, cc[4] = {c4.x, c4.y, c4.z, c4.w};
+          const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float hv = fmaf(v[j + e], rsig, fmaf(-shift, ss[e], cc[e]));
+            lg[e] = fmaf(fmaxf(hv, 0.f), ww[e], lg[e]);
+          }
         }
       }
+      const float logit = (lg[0] + lg[1]) + (lg[2] + lg[3]);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
@@ -349,7 +360,10 @@ extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const v
                                     void* workspace, size_t workspace_bytes, void* stream) {
   if (!X || !W1 || !s || !c || !w2 || !out_logit || !out_prob) return DUCHESS_EINVAL;
   if (M < 0 || K < kTcBK || K % kTcBK || NH < kTcBN || NH % kTcBN) return DUCHESS_EINVAL;
-  if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W1) % 16) return DUCHESS_EINVAL;
+  if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W1) % 16 ||
+      reinterpret_cast<uintptr_t>(s) % 16 || reinterpret_cast<uintptr_t>(c) % 16 ||
+      reinterpret_cast<uintptr_t>(w2) % 16)                     // per-column params read as float4
+    return DUCHESS_EINVAL;
   if (!workspace || workspace_bytes < duchess_mlp_probe_tc_workspace_bytes(M, NH) ||
       reinterpret_cast<uintptr_t>(workspace) % 16)
     return DUCHESS_EINVAL;
