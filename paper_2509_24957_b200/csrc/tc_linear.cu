@@ -315,6 +315,47 @@ __global__ void head_kernel(const uint16_t* Hm, int64_t M, int K, const float* W
   }
 }
 
+// Vector path (K % 8 == 0, K <= 256 * HC, aligned): a lane loads its 8-element
+// chunks of the row once (16-byte loads), then forms every output's partial
+// against the weight rows (float4 loads, L1-resident) and reduces per output.
+template <int HC>
+__global__ void head_vec_kernel(const uint16_t* Hm, int64_t M, int K, const float* W, const float* b,
+                                int NO, float* logits) {
+  const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int nch = K / 8;
+  const uint4* h4 = reinterpret_cast<const uint4*>(Hm + row * K);
+  uint4 hv[HC];
+#pragma unroll
+  for (int c = 0; c < HC; ++c) {
+    const int ch = c * 32 + lane;
+    hv[c] = ch < nch ? ldg_stream(h4 + ch) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int o = 0; o < NO; ++o) {
+    const float4* w4 = reinterpret_cast<const float4*>(W + int64_t(o) * K);
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) {
+      const int ch = c * 32 + lane;
+      if (ch < nch) {
+        const float4 wa = __ldg(w4 + 2 * ch), wb = __ldg(w4 + 2 * ch + 1);
+        const uint32_t x[4] = {hv[c].x, hv[c].y, hv[c].z, hv[c].w};
+        acc0 = fmaf(bf16lo(x[0]), wa.x, acc0);
+        acc1 = fmaf(bf16hi(x[0]), wa.y, acc1);
+        acc0 = fmaf(bf16lo(x[1]), wa.z, acc0);
+        acc1 = fmaf(bf16hi(x[1]), wa.w, acc1);
+        acc0 = fmaf(bf16lo(x[2]), wb.x, acc0);
+        acc1 = fmaf(bf16hi(x[2]), wb.y, acc1);
+        acc0 = fmaf(bf16lo(x[3]), wb.z, acc0);
+        acc1 = fmaf(bf16hi(x[3]), wb.w, acc1);
+      }
+    }
+    const float acc = warp_sum(acc0 + acc1);
+    if (lane == 0) logits[row * NO + o] = acc + b[o];
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -409,7 +450,13 @@ extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const fl
                                    const float* b, int32_t n_out, float* logits, void* stream) {
   if (!H || !W || !b || !logits || M < 0 || K < 1 || n_out < 1) return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
-  tcl::head_kernel<<<unsigned((M + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(H), M, K, W, b, n_out, logits);
+  const unsigned grid = unsigned((M + 7) / 8);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint16_t* h = static_cast<const uint16_t*>(H);
+  const bool vec = K % 8 == 0 && reinterpret_cast<uintptr_t>(H) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(W) % 16 == 0 && K <= 256 * 8;
+  if (vec && K <= 256 * 2) tcl::head_vec_kernel<2><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
+  else if (vec) tcl::head_vec_kernel<8><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
+  else tcl::head_kernel<<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
