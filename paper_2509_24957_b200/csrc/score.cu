@@ -449,7 +449,7 @@ static cudaError_t launch_rows(const ScoreArgs& a, const TmaArgs& t, int nv, int
     break;
   switch (nv) {
     DUCHESS_ROWS(1) DUCHESS_ROWS(2) DUCHESS_ROWS(4) DUCHESS_ROWS(8) DUCHESS_ROWS(12)
-    DUCHESS_ROWS(16) DUCHESS_ROWS(20) DUCHESS_ROWS(24)
+    DUCHESS_ROWS(16) DUCHESS_ROWS(20)
     default: return cudaErrorInvalidValue;
   }
 #undef DUCHESS_ROWS
@@ -615,7 +615,10 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kTmaStageTarget; return v < 4096 ? 4096 : v; }();
     const int nvec_row = int(row_bytes / 16);
     static const bool rows_ok = [] { const char* e = getenv("DUCHESS_K1_ROWS"); return !e || atoi(e) != 0; }();
-    if (rows_ok && T == 1 && nvec_row <= 24 * 32 && (reinterpret_cast<uintptr_t>(wg) % 16) == 0) {
+    // spill-free instantiations: bf16 rows up to 20 vectors per lane (H <= 5120),
+    // fp32 up to 12 (H <= 1536); wider rows take the CTA kernel below
+    if (rows_ok && T == 1 && nvec_row <= (bf16 ? 20 : 12) * 32 &&
+        (reinterpret_cast<uintptr_t>(wg) % 16) == 0) {
       int nv = (nvec_row + 31) / 32;
       nv = nv <= 2 ? nv : nv <= 4 ? 4 : nv <= 8 ? 8 : (nv + 3) / 4 * 4;
       a.nsplit = 1;
