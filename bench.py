@@ -1215,9 +1215,37 @@ def cpu_fork_or_train(args):
                     "d2h_bytes_per_step": 0}}
 
 
+def cpu_c3tc(n=4096, reps=3):
+    """CPU reference for the C3 tensor-core MLP probe: the reference's
+    mlp_forward (predictor.py:126-151; LN -> 5120x2048 ReLU -> 1 logit) as
+    numpy fp32 BLAS on all threads over a bounded sample of windows."""
+    K, NH = 5120, 2048
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n, K), dtype=np.float32)
+    W1 = (rng.standard_normal((K, NH)) / np.sqrt(K)).astype(np.float32)
+    b1 = np.zeros(NH, dtype=np.float32)
+    w2 = (rng.standard_normal(NH) / np.sqrt(NH)).astype(np.float32)
+    g = rng.uniform(0.5, 1.5, K).astype(np.float32)
+    beta = rng.uniform(-0.1, 0.1, K).astype(np.float32)
+    times = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        mu = X.mean(axis=1, keepdims=True)
+        var = X.var(axis=1, keepdims=True)
+        z = (X - mu) / np.sqrt(var + 1e-5) * g + beta
+        h = np.maximum(z @ W1 + b1, 0.0)
+        _logit = h @ w2
+        times.append(time.perf_counter() - t0)
+    dt = sum(times[1:])
+    return {"value": n * reps / dt, "unit": "branch-steps/s", "cores": os.cpu_count() or 1,
+            "kind": "port", "sample": f"numpy fp32 BLAS mlp_forward (LN, {K}->{NH} ReLU, head) "
+                                      f"over {n} windows x {reps}, all threads"}
+
+
 def run_reference(args, cfg):
-    if args.config in ("difficulty", "sim", "baselines"):
-        cb = {"difficulty": cpu_difficulty, "sim": cpu_sim, "baselines": cpu_baselines}[args.config]()
+    if args.config in ("difficulty", "sim", "baselines", "c3tc"):
+        cb = {"difficulty": cpu_difficulty, "sim": cpu_sim, "baselines": cpu_baselines,
+              "c3tc": cpu_c3tc}[args.config]()
         return {"impl": "reference", "metric": f"{args.config} CPU reference", "value": cb["value"],
                 "unit": cb["unit"], "n_gpus": args.gpus, "steps": 1, "warmup": 0,
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
@@ -1335,6 +1363,13 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and cfg is not None:
             out["cpu_baseline"] = cpu_baseline_entry(args.config)
+        elif world == 1 and not args.no_cpu_baseline and args.config in ("c4", "c5"):
+            import copy
+            small = copy.copy(args)
+            small.steps, small.warmup = 3, 1           # bounded CPU sample
+            out["cpu_baseline"] = cpu_fork_or_train(small)["cpu_baseline"]
+        elif world == 1 and not args.no_cpu_baseline and args.config == "c3tc":
+            out["cpu_baseline"] = cpu_c3tc()
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch
