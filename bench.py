@@ -1249,7 +1249,8 @@ def run_reference(args, cfg):
         return {"impl": "reference", "metric": f"{args.config} CPU reference", "value": cb["value"],
                 "unit": cb["unit"], "n_gpus": args.gpus, "steps": 1, "warmup": 0,
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f32" if args.config == "c3tc" else "f64",
+                "data": "synthetic",
                 "config": {"workload": args.config + " (CPU)"}, "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
