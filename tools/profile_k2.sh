@@ -1,4 +1,5 @@
 #!/bin/bash
+# ncu --set full captures of the K2 kernels (advance / decide) and K1 variants inside the C2 bench (run under gpurun).
 mkdir -p gpurun_out
 TAG=${1:-r01c}
 for k in advance decide score_tma score_fast; do

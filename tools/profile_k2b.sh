@@ -1,4 +1,5 @@
 #!/bin/bash
+# ncu --set full captures of the barrier-free round kernel and advance kernel at C2, cold caches (run under gpurun).
 mkdir -p gpurun_out
 TAG=${1:-r01f}
 for k in round_kernel advance_kernel; do

@@ -1,3 +1,5 @@
+"""Diagnostics for the tcgen05 MLP probe: device logits vs the fp64 reference on
+small shapes, printing the worst rows (run under gpurun)."""
 import sys
 import numpy as np
 import torch
