@@ -1,5 +1,6 @@
-"""Diagnostics for the tcgen05 MLP probe: device logits vs the fp64 reference on
-small shapes, printing the worst rows (run under gpurun)."""
+"""Diagnostics for the tcgen05 MLP probe: max / median relative logit error vs
+the fp64 reference over a sweep of (M, K, NH) shapes and input means (run under
+gpurun)."""
 import sys
 import numpy as np
 import torch
