@@ -42,6 +42,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Untimed serving rounds before the W warm-up steps: every slot starts on a fresh
+# request, and the first rounds (all requests young, few finishing) are not the
+# steady state a serving GPU runs in; this burn-in is part of setup, not timed.
+BURN_IN_ROUNDS = 24
+
 METRIC = "branch-steps/sec scored+decided (HBM GB/s % of peak) at 1/2/4/8 B200 vs CPU"
 UNIT = "branch-steps/s"
 
@@ -250,7 +255,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         eng.begin_fused()              # round 0: refill every slot + phase 1
     else:
         eng.advance()
-    for i in range(args.warmup):
+    for i in range(BURN_IN_ROUNDS + args.warmup):
         one_step(i, False)
     torch.cuda.synchronize(dev)
     c0 = eng.t["counters"].clone()
@@ -265,7 +270,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for j in range(n_slabs):
-                one_step(args.warmup + j, False)
+                one_step(BURN_IN_ROUNDS + args.warmup + j, False)
         args.steps = -(-args.steps // n_slabs) * n_slabs
         graph.replay()                  # one rotation untimed (warm the graph)
         torch.cuda.synchronize(dev)
@@ -278,7 +283,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             graph.replay()
     else:
         for i in range(args.steps):
-            one_step(args.warmup + i, i % args.k1_every == 0)
+            one_step(BURN_IN_ROUNDS + args.warmup + i, i % args.k1_every == 0)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None
@@ -329,6 +334,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
                    "launch": "CUDA graph replay" if args.graph else "eager stream (PDL)",
                    "l2": "inputs larger than L2 (rotating slabs)",
+                   "burn_in_rounds": BURN_IN_ROUNDS,
                    "parallelism": f"request-sharded x{world}"},
         "branch_steps_per_step": branch_steps / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -436,7 +442,7 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
     for sh in shards:
         with torch.cuda.stream(sh["stream"]):
             sh["eng"].advance()
-    for i in range(args.warmup):
+    for i in range(BURN_IN_ROUNDS + args.warmup):
         step(i, False)
     join()
     torch.cuda.synchronize(dev)
@@ -449,7 +455,7 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
     ev0.record(main)
     fork()
     for i in range(args.steps):
-        step(args.warmup + i, i % args.k1_every == 0)
+        step(BURN_IN_ROUNDS + args.warmup + i, i % args.k1_every == 0)
     join()
     ev1.record(main)
     torch.cuda.synchronize(dev)
@@ -501,6 +507,7 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
                    "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
                    "shards_per_gpu": S, "launch": "eager streams (PDL within each shard)",
                    "l2": "inputs larger than L2 (rotating slabs)",
+                   "burn_in_rounds": BURN_IN_ROUNDS,
                    "parallelism": f"request-sharded x{world} GPUs x{S} streams"},
         "branch_steps_per_step": branch_steps / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
