@@ -128,3 +128,45 @@ def test_c5_full_shard_gradient_matches_fp64():
         ref[H] += r.sum()
     ref /= N
     torch.testing.assert_close(got, ref, rtol=1e-4, atol=1e-4 * float(ref.abs().max()))
+
+
+def test_c2_engine_scale_decisions_match_oracle():
+    """K2 at the C2 engine size: 256 request slots x 16 branches with the
+    math-like knobs over a 1024-request pool (64 templates each, easiest-first
+    queue, on-device refill) — every request's RoundReports and outcome equal
+    the oracle's (trace / synthetic predictor, rho 0.8)."""
+    import random
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    from paper_2509_24957_b200.scheduler import difficulty_queue
+    from tests.golden_util import port_report_tuple
+    import bench
+    knobs = port.Knobs(max_branches=16, **bench.PRESET_KNOBS["math-like"])
+    params = port.GenParams(templates_per_request=64, **bench.PRESET_GEN["math-like"])
+    traces = port.generate(params, 1024, seed=17)
+    master = random.Random(18)
+    seeds = [master.getrandbits(64) for _ in traces]
+    queue = difficulty_queue([t.difficulty for t in traces])
+    eng = BatchedDuchess(traces, knobs, seeds, n_slots=256, pred_source=_lib.PRED_TRACE,
+                         rho=0.8, queue=queue)
+    eng.advance()
+    reports = {}
+    for _ in range(100000):
+        eng.round()
+        for p, rep in eng.round_reports():
+            reports.setdefault(p, []).append(rep)
+        if eng.all_done():
+            break
+    assert eng.all_done()
+    assert int(eng.counters()[_lib.CNT_AMBIGUOUS]) == 0
+    outcomes = eng.outcomes()
+    for p, tr in enumerate(traces):
+        ref = port.DuchessRequest(tr, knobs, random.Random(seeds[p]), rho=0.8)
+        want = []
+        while not ref.done:
+            want.append(port_report_tuple(ref.step()))
+        assert reports[p] == want, f"request {p}"
+        o = ref.outcome
+        assert (outcomes[p]["final"], outcomes[p]["reason"], outcomes[p]["tally"],
+                outcomes[p]["tokens_decode"], outcomes[p]["rounds"]) == (
+            o.final, o.termination_reason, o.tally, o.tokens_decode, o.rounds)
