@@ -11,20 +11,25 @@ then refill and advance every slot into the next round). A branch-step is one
 survivor scored and decided (one `self._predict` call in reference
 orchestrator.py:358-362).
 
-Default workload (BASELINE.json configs[1], "C2"): 256 request slots x 16
-branch slots, hidden 4096, bf16 activations, 32-token pooling window, one
-probe layer, math-like knobs with max_branches=16 (presets.py:55-59), a
-cycling pool of 2048 synthetic requests (64 templates each) admitted in
-easiest-first order. Activations: 4 rotating slabs per shard (4x the 126 MB
-L2, so every step streams from HBM). The slots are split into two
-independent request shards stepping on two CUDA streams (requests never
-interact), so each shard's latency-bound round kernel runs while the other
-shard's scorer streams. Under torchrun each rank runs its own request shard
-(weak scaling, no data-path collective).
+Default workload at N = 1 (BASELINE.json configs[1], "C2"): 256 request
+slots x 16 branch slots, hidden 4096, bf16 activations, 32-token pooling
+window, one probe layer, math-like knobs with max_branches=16
+(presets.py:55-59), a cycling pool of 2048 synthetic requests (64 templates
+each) admitted in easiest-first order. Activations: rotating buffers per
+shard (> the 126 MB L2, so every step streams from HBM). The slots are split
+into two independent request shards stepping on two CUDA streams
+(serving.ShardedEngine: requests never interact), so each shard's
+latency-bound round kernel runs while the other shard's scorer streams.
 
---impl reference times the CPU restatement of the reference (oracle/port.py:
-the reference's DuchessRun with a predictor= that pools + LayerNorms + dots
-distinct windows in numpy) on all host cores.
+Under torchrun (N > 1) the default is C3 (configs[2]: 1024 request slots x 32
+branches, 4 probe layers, H 5120) strong-scaled: every rank builds the same
+request pool and serves its shard_range share of the slots and of the pool
+(no data-path collective); barrier + max-over-ranks timing.
+
+--impl reference times the reference's own DuchessRun + mlp_forward (vendored
+unmodified into oracle/_ref by oracle/vendor_ref.py; the restatement
+oracle/port.py when absent) with a predictor= that pools each distinct window
+(fp64 mean over T) on all host cores.
 """
 
 from __future__ import annotations
@@ -186,288 +191,151 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def run_gpu(args, cfg, rank, world, local_rank):
+def measure_read_peak(dev, buf=None, reps=6):
+    """Read-only HBM ceiling on this GPU, measured live: best of `reps`
+    passes of duchess_read_stream over >= 4 GiB (CUDA events)."""
     import torch
 
     from paper_2509_24957_b200 import _lib
-    from paper_2509_24957_b200.engine import BatchedDuchess
-    from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
-    from paper_2509_24957_b200.scheduler import difficulty_queue
-
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    R, C, L, T, H = cfg["R"], cfg["c"], cfg["L"], cfg["T"], cfg["H"]
-    tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
-    esz = 2 if cfg["dtype"] == "bf16" else 4
-    traces, knobs, seeds = make_workload(cfg, seed=1000 + 17 * rank)
-    queue = difficulty_queue([t.difficulty for t in traces], device=dev)
-    eng = BatchedDuchess(traces, knobs, seeds, n_slots=R, pred_source=_lib.PRED_DEVICE,
-                         queue=queue, cycle=True, n_layers=L, combine=1 if L > 1 else 0,
-                         device=dev)
-    w, b, g, beta = make_probe(H, L)
-    bank = ProbeBank.from_linear(w, b, g, beta, device=dev)
-    if args.k1 == "ldg":
-        scorer = Scorer(bank, R * C * L, nsplit=args.nsplit, threads=args.threads)
-    else:
-        scorer = Scorer(bank, R * C * L)          # persistent TMA-bulk kernel
-    rows = R * C
-    n_slabs = max(2, min(4, int((4 << 30) // (rows * L * T * H * esz)) or 2))
-    if rows * L * T * H * esz < (256 << 20):
-        n_slabs = 4
-    slabs = [torch.empty((rows, L, T, H), dtype=tdtype, device=dev) for _ in range(n_slabs)]
-    for i, s in enumerate(slabs):
-        fill_windows(s, 7000 + 31 * rank + i)
-    logit = torch.empty((rows, L), dtype=torch.float32, device=dev)
-    probs = eng.probs.view(rows, L)
-    stream = torch.cuda.current_stream(dev)
-    k1_ev = []
-
-    fused = args.mode == "fused"
-
-    def one_step(i, timed):
-        # fused: ONE persistent launch per round (duchess_step) —
-        # K1 streams the survivors' windows while a decision warp per CTA
-        # decides every request whose windows are scored and advances it into
-        # the next round. split (default): K1 launch, then duchess_round (decide k +
-        # advance k+1). The scoring kernel is bracketed by CUDA events on every
-        # `k1_every`-th timed step: an event record between two PDL-chained
-        # kernels breaks their overlap, so sampling keeps the measurement from
-        # inflating the step time.
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        if fused:
-            eng.step_fused(slabs[i % n_slabs], bank, logit.view(-1))
-            if timed:
-                e1.record(stream)
-                k1_ev.append((e0, e1))
-            return
-        if args.k1 == "list":
-            scorer.score_active(slabs[i % n_slabs], logit, probs, eng)
-        else:
-            scorer(slabs[i % n_slabs], logit, probs, row_mask=eng.t["row_mask"])
-        if timed:
-            e1.record(stream)
-            k1_ev.append((e0, e1))
-        eng.round()
-
-    if fused:
-        eng.begin_fused()              # round 0: refill every slot + phase 1
-    else:
-        eng.advance()
-    for i in range(BURN_IN_ROUNDS + args.warmup):
-        one_step(i, False)
-    torch.cuda.synchronize(dev)
-    c0 = eng.t["counters"].clone()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
-    graph = None
-    if args.graph:
-        # CUDA graph of one slab rotation (n_slabs rounds = 2*n_slabs launches,
-        # PDL edges kept), replayed; removes the host launch cost that bounds
-        # small configs. K1 is timed with events in an eager pass afterwards.
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for j in range(n_slabs):
-                one_step(BURN_IN_ROUNDS + args.warmup + j, False)
-        args.steps = -(-args.steps // n_slabs) * n_slabs
-        graph.replay()                  # one rotation untimed (warm the graph)
-        torch.cuda.synchronize(dev)
-        c0 = eng.t["counters"].clone()
-    clocks = ClockSampler(local_rank) if rank == 0 else None
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    if graph is not None:
-        for _ in range(args.steps // n_slabs):
-            graph.replay()
-    else:
-        for i in range(args.steps):
-            one_step(BURN_IN_ROUNDS + args.warmup + i, i % args.k1_every == 0)
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    clk = clocks.stop() if clocks else None
-    if graph is not None:
-        # event timing inside a replayed graph is not meaningful: K1 is timed
-        # in an eager pass right after the timed region (same state, shapes)
-        cnt_g = (eng.t["counters"] - c0).cpu().numpy()
-        for i in range(8 * args.k1_every):
-            one_step(i, i % args.k1_every == 0)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    ms = ev0.elapsed_time(ev1)
-    cnt = cnt_g if graph is not None else (eng.t["counters"] - c0).cpu().numpy()
-    branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
-    k1_ms = sum(a.elapsed_time(b) for a, b in k1_ev) / max(len(k1_ev), 1) * args.steps
-    stats = torch.tensor([ms, float(branch_steps), k1_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = stats[:1].clone()
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        tot = stats[1:2].clone()
-        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
-        ms_all, bs_all = float(tmax[0]), float(tot[0])
-    else:
-        ms_all, bs_all = ms, float(branch_steps)
-
-    # ---- end to end through the public API with host buffers ----
-    e2e = run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank)
-
-    if rank != 0:
-        return None
-    bytes_per_bs = T * H * esz * L
-    k1_avg_s = k1_ms / args.steps / 1e3
-    bytes_per_launch = branch_steps / args.steps * bytes_per_bs
-    peak, peak_kind = load_peaks()
-    achieved = bytes_per_launch / k1_avg_s / 1e9
-    out = {
-        "metric": METRIC, "value": bs_all / (ms_all / 1e3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": cfg["dtype"], "data": "synthetic (counter-hashed N(0,1) activations with "
-        "outlier channels; generate_synthetic workload, random-init probe)",
-        "config": {"workload": f"{args.config.upper()}: {R} request slots x {C} branches, "
-                   f"hidden {H}, {L} probe layer(s), T={T} pooling window, {cfg['dtype']}, "
-                   f"{cfg['preset']} knobs, cycling pool of {cfg['pool']} requests "
-                   f"(easiest-first), {n_slabs} rotating activation slabs "
-                   f"({rows * L * T * H * esz / 2**30:.2f} GiB each, > L2)",
-                   "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
-                   "launch": "CUDA graph replay" if args.graph else "eager stream (PDL)",
-                   "l2": "inputs larger than L2 (rotating slabs)",
-                   "burn_in_rounds": BURN_IN_ROUNDS,
-                   "parallelism": f"request-sharded x{world}"},
-        "branch_steps_per_step": branch_steps / args.steps,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_kind": peak_kind, "peak_note": PEAK_NOTE,
-                     "kernel": ("duchess_step (fused K1 scoring + decide + advance, one "
-                                "launch per round)" if fused else f"duchess_score (K1, {args.k1})"),
-                     "bytes_per_launch": bytes_per_launch,
-                     "k1_us_per_launch": k1_avg_s * 1e6,
-                     "k1_share_of_step": k1_ms / ms,
-                     "k1_launches_timed": (f"{len(k1_ev)} (eager pass after the timed graph "
-                                           f"replays)") if args.graph else len(k1_ev),
-                     "traffic": (None if k1_traffic_ratio(T)[0] is None
-                                 else k1_traffic_ratio(T)[0] * bytes_per_launch),
-                     "traffic_source": k1_traffic_ratio(T)[1]},
-        "e2e": e2e,
-        "gpu_launches": (1 if fused else 2) * args.steps,
-        "clocks": clk,
-        "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
-                     "finished_requests": int(cnt[_lib.CNT_FINISHED]),
-                     "forks": int(cnt[_lib.CNT_FORKS])},
-    }
-    return out
+    lib = _lib.load()
+    own = buf is None or buf.numel() * buf.element_size() < (4 << 30)
+    if own:
+        buf = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
+        buf.fill_(1)
+    nbytes = buf.numel() * buf.element_size() // 16 * 16
+    sink = torch.zeros(4, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    best = None
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        _lib.check(lib.duchess_read_stream(buf.data_ptr(), nbytes, sink.data_ptr(),
+                                           st.cuda_stream), "duchess_read_stream")
+        b.record(st)
+        b.synchronize()
+        gbs = nbytes / (a.elapsed_time(b) / 1e3) / 1e9
+        best = gbs if best is None else max(best, gbs)
+    del buf
+    return best
 
 
-def run_gpu_sharded(args, cfg, rank, world, local_rank):
-    """C2/C3 with the GPU's request slots split into `shards` independent
-    engines (interleaved request pools), each stepping on its own CUDA stream:
-    requests never interact, so this is the multi-GPU request
-    sharding applied inside one GPU. The HBM-bound scorer of one shard runs
-    while the latency-bound round kernel of another finishes (the small round
-    CTAs fit beside the scorer's), so the decision kernel leaves the critical
-    path. Same workload as run_gpu: R slots x C branches in total."""
+DATASHEET_HBM_GBS = 8000.0   # B200 HBM3e datasheet figure
+
+
+def roofline_figures(achieved, read_peak):
+    """The achieved GB/s against the three denominators BASELINE.md 2 asks
+    for: the driver's measured copy peak (the line's `peak`), the 8 TB/s
+    datasheet figure and the read-only stream measured in this run."""
+    peak, kind = load_peaks()
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_kind": kind, "peak_note": PEAK_NOTE,
+            "vs_datasheet": {"peak": DATASHEET_HBM_GBS, "frac": achieved / DATASHEET_HBM_GBS},
+            "vs_read_stream": (None if read_peak is None else
+                               {"peak": read_peak, "frac": achieved / read_peak,
+                                "how": "duchess_read_stream (read-only persistent kernel, "
+                                       ">= 4 GiB, best of 6, CUDA events) measured in this run"})}
+
+
+def serving_plan(cfg_name, world, rank):
+    """Slots and pool share of this rank. N = 1: the config as BASELINE.json
+    states it. N > 1: strong scaling of the same config — its R request slots
+    and request pool are split over the ranks (shard_range, contiguous), no
+    data-path collective (requests are independent)."""
+    from paper_2509_24957_b200.distributed import shard_range
+    cfg = CONFIGS[cfg_name]
+    lo, hi = shard_range(cfg["R"], rank, world)
+    plo, phi = shard_range(cfg["pool"], rank, world)
+    return hi - lo, (plo, phi)
+
+
+def run_serving(args, cfg, rank, world, local_rank):
+    """C1/C2/C3/C3-T1: the serving loop (serving.ShardedEngine): per round and
+    request shard, duchess_score_active (K1) + duchess_round (K2)."""
     import torch
 
     from paper_2509_24957_b200 import _lib
-    from paper_2509_24957_b200.engine import BatchedDuchess
-    from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows
+    from paper_2509_24957_b200.engine import pack_pool
+    from paper_2509_24957_b200.probe import ProbeBank, fill_windows
     from paper_2509_24957_b200.scheduler import difficulty_queue
+    from paper_2509_24957_b200.serving import ShardedEngine
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     S = args.shards
-    R, C, L, T, H = cfg["R"], cfg["c"], cfg["L"], cfg["T"], cfg["H"]
+    L, T, H, C = cfg["L"], cfg["T"], cfg["H"], cfg["c"]
+    R, (plo, phi) = serving_plan(args.config, world, rank)
     if R % S:
-        raise SystemExit(f"--shards {S} must divide the {R} request slots")
-    Rs = R // S
+        raise SystemExit(f"--shards {S} must divide this rank's {R} request slots")
     tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     esz = 2 if cfg["dtype"] == "bf16" else 4
-    traces, knobs, seeds = make_workload(cfg, seed=1000 + 17 * rank)
+    traces, knobs, seeds = make_workload(cfg, seed=1000)      # the same pool on every rank
+    order = difficulty_queue([t.difficulty for t in traces], device=dev)
+    queue = [p for p in order if plo <= p < phi]               # this rank's share, easiest first
     w, b, g, beta = make_probe(H, L)
     bank = ProbeBank.from_linear(w, b, g, beta, device=dev)
-    rows = Rs * C
+    rows = (R // S) * C
     slab_bytes = rows * L * T * H * esz
     n_slabs = 4 if slab_bytes * S < (256 << 20) else max(2, min(4, int((4 << 30) // (slab_bytes * S)) or 2))
-    shards = []
-    for sh in range(S):
-        tr, sd = traces[sh::S], seeds[sh::S]
-        queue = difficulty_queue([t.difficulty for t in tr], device=dev)
-        eng = BatchedDuchess(tr, knobs, sd, n_slots=Rs, pred_source=_lib.PRED_DEVICE,
-                             queue=queue, cycle=True, n_layers=L, combine=1 if L > 1 else 0,
-                             device=dev)
-        slabs = [torch.empty((rows, L, T, H), dtype=tdtype, device=dev) for _ in range(n_slabs)]
-        for i, sl in enumerate(slabs):
-            fill_windows(sl, 7000 + 31 * rank + 7 * sh + i)
-        shards.append(dict(eng=eng, scorer=Scorer(bank, rows * L), slabs=slabs,
-                           logit=torch.empty((rows, L), dtype=torch.float32, device=dev),
-                           stream=torch.cuda.Stream(dev), ev=[]))
+    packed = pack_pool(traces, seeds, dev)
+    srv = ShardedEngine(traces, knobs, seeds, bank, n_slots=R, shards=S, queue=queue, cycle=True,
+                        T=T, dtype=tdtype, device=dev, n_buffers=n_slabs, packed=packed)
+    for k, sh in enumerate(srv.shards):
+        for i, a in enumerate(sh["acts"]):
+            fill_windows(a, 7000 + 31 * rank + 7 * k + i)
+    read_peak = measure_read_peak(dev, srv.shards[0]["acts"][0]) if rank == 0 else None
     main = torch.cuda.current_stream(dev)
 
-    # The scorers of the shards take turns (each waits for the previous one's
-    # event): every K1 launch streams alone at full HBM bandwidth, while the
-    # round kernel of the shard scored just before runs beside it.
-    prev_k1 = [None]
-
-    def step(i, timed):
-        for sh in shards:
-            with torch.cuda.stream(sh["stream"]):
-                st = sh["stream"]
-                if prev_k1[0] is not None and args.shard_order == "turns":
-                    st.wait_event(prev_k1[0])
-                if timed:
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(st)
-                sh["scorer"].score_active(sh["slabs"][i % n_slabs], sh["logit"],
-                                          sh["eng"].probs.view(rows, L), sh["eng"])
-                if timed:
-                    e1.record(st)
-                    sh["ev"].append((e0, e1))
-                if args.shard_order == "turns":
-                    done = e1 if timed else torch.cuda.Event()
-                    if not timed:
-                        done.record(st)
-                    prev_k1[0] = done
-                sh["eng"].round()
-
-    def join():
-        for sh in shards:
-            main.wait_stream(sh["stream"])
-
-    def fork():
-        for sh in shards:
-            sh["stream"].wait_stream(main)
-
-    fork()
-    for sh in shards:
-        with torch.cuda.stream(sh["stream"]):
-            sh["eng"].advance()
+    srv.begin()
     for i in range(BURN_IN_ROUNDS + args.warmup):
-        step(i, False)
-    join()
+        srv.step(i)
+    srv.join()
     torch.cuda.synchronize(dev)
-    c0 = [sh["eng"].t["counters"].clone() for sh in shards]
+    first = BURN_IN_ROUNDS + args.warmup
+    graph = None
+    if args.graph:
+        # one CUDA graph = one rotation of the activation buffers (n_slabs
+        # rounds of every shard, the shard streams forked / joined inside),
+        # replayed: removes the host launch cost that bounds small configs
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            srv.fork()
+            for j in range(n_slabs):
+                srv.step(first + j)
+            srv.join()
+        args.steps = -(-args.steps // n_slabs) * n_slabs
+        graph.replay()                  # one rotation untimed
+        torch.cuda.synchronize(dev)
+    c0 = srv.counters()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local_rank) if rank == 0 else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(main)
-    fork()
-    for i in range(args.steps):
-        step(BURN_IN_ROUNDS + args.warmup + i, i % args.k1_every == 0)
-    join()
+    if graph is not None:
+        for _ in range(args.steps // n_slabs):
+            graph.replay()
+    else:
+        srv.fork()
+        for i in range(args.steps):
+            srv.step(first + i, timed=(S == 1 and i % args.k1_every == 0))
+        srv.join()
     ev1.record(main)
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None
+    cnt = srv.counters() - c0
+    ms = ev0.elapsed_time(ev1)
+    if S == 1 and graph is not None:
+        # events inside a replayed graph are not meaningful: K1 is timed in an
+        # eager pass right after the timed region (same state and shapes)
+        srv.fork()
+        for i in range(8 * args.k1_every):
+            srv.step(i, timed=(i % args.k1_every == 0))
+        srv.join()
+        torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
-    ms = ev0.elapsed_time(ev1)
-    cnt = sum((sh["eng"].t["counters"] - c).cpu().numpy() for sh, c in zip(shards, c0))
     branch_steps = int(cnt[_lib.CNT_BRANCH_STEPS])
-    k1_us = [a.elapsed_time(b) * 1e3 for sh in shards for a, b in sh["ev"]]
-    k1_avg_s = sum(k1_us) / max(len(k1_us), 1) / 1e6
-
     stats = torch.tensor([ms, float(branch_steps)], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = stats[:1].clone()
@@ -478,50 +346,57 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
     else:
         ms_all, bs_all = ms, float(branch_steps)
 
-    e2e = run_e2e_sharded(args, shards, rows, L, T, H, tdtype, dev, world, main)
+    e2e = run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world)
     if rank != 0:
         return None
     bytes_per_bs = T * H * esz * L
+    step_s = ms / args.steps / 1e3
+    k1_us = [a.elapsed_time(b) * 1e3 for a, b in srv.scorer_events()]
+    k1_avg_s = sum(k1_us) / max(len(k1_us), 1) / 1e6
     bytes_per_launch = branch_steps / args.steps / S * bytes_per_bs
-    peak, peak_kind = load_peaks()
-    overlap = args.shard_order == "overlap"
-    # turns: each scoring launch streams alone -> bytes per launch / its duration.
-    # overlap: the shards' launches share HBM and drift against each other, so a
-    # launch's duration is stretched by sharing; the scoring bytes of a step over
-    # the WHOLE step time (round kernels included) is the conservative figure.
-    achieved = (bytes_per_launch * S / (ms / args.steps / 1e3) if overlap
-                else bytes_per_launch / k1_avg_s) / 1e9
+    if S > 1:
+        # the shards' scorer launches run concurrently and share HBM: the
+        # step's scoring bytes over the WHOLE step time (round kernels
+        # included) is the conservative figure
+        achieved = bytes_per_launch * S / step_s / 1e9
+        kernel = (f"duchess_score_active (K1{', score_rows_kernel' if T == 1 else ''}): the "
+                  f"{S} shards' concurrent launches, scoring bytes per step / whole step time")
+    else:
+        achieved = bytes_per_launch / k1_avg_s / 1e9
+        kernel = (f"duchess_score_active (K1{', score_rows_kernel' if T == 1 else ''}) per "
+                  f"launch (CUDA events on the shard stream)")
+    roof = roofline_figures(achieved, read_peak)
+    ratio, src = k1_traffic_ratio(T)
+    roof.update({"kernel": kernel, "bytes_per_launch": bytes_per_launch,
+                 "bytes_per_branch_step": bytes_per_bs,
+                 "k1_us_per_launch": k1_avg_s * 1e6 if k1_us else None,
+                 "k1_launches_timed": len(k1_us),
+                 "traffic": None if ratio is None else ratio * bytes_per_launch,
+                 "traffic_source": src})
+    strong = world > 1
     return {
         "metric": METRIC, "value": bs_all / (ms_all / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": cfg["dtype"], "data": "synthetic (counter-hashed N(0,1) activations with "
-        "outlier channels; generate_synthetic workload, random-init probe)",
-        "config": {"workload": f"{args.config.upper()}: {R} request slots x {C} branches, "
-                   f"hidden {H}, {L} probe layer(s), T={T} pooling window, {cfg['dtype']}, "
-                   f"{cfg['preset']} knobs, cycling pool of {cfg['pool']} requests "
-                   f"(easiest-first), {n_slabs} rotating activation slabs per shard "
-                   f"({slab_bytes * S / 2**30:.2f} GiB per rotation, > L2); slots split into "
-                   f"{S} independent request shards on {S} CUDA streams "
-                   f"({'concurrent scorers' if args.shard_order == 'overlap' else 'scorers take turns'})",
-                   "requests": R, "branches": C, "hidden": H, "layers": L, "window": T,
-                   "shards_per_gpu": S, "launch": "eager streams (PDL within each shard)",
-                   "l2": "inputs larger than L2 (rotating slabs)",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (counter-hashed N(0,1) activations with outlier channels; "
+                "generate_synthetic workload, random-init probe)",
+        "config": {"workload": f"{args.config.upper()}: {cfg['R']} request slots x {C} branches"
+                   f"{f' split over {world} GPUs ({R} per GPU)' if strong else ''}, hidden {H}, "
+                   f"{L} probe layer(s){' (mean of probabilities)' if L > 1 else ''}, T={T} "
+                   f"pooling window, {cfg['dtype']}, {cfg['preset']} knobs, cycling pool of "
+                   f"{cfg['pool']} requests (easiest-first{', split over the GPUs' if strong else ''}), "
+                   f"{n_slabs} rotating activation buffers per shard "
+                   f"({slab_bytes * S / 2**30:.2f} GiB per rotation step, > L2); {S} request "
+                   f"shard(s) per GPU on {S} CUDA stream(s)",
+                   "requests": cfg["R"], "branches": C, "hidden": H, "layers": L, "window": T,
+                   "pool": cfg["pool"], "slots_per_gpu": R, "shards_per_gpu": S,
+                   "launch": "CUDA graph replay" if graph is not None else "eager streams (PDL)",
+                   "l2": "inputs larger than L2 (rotating buffers)",
                    "burn_in_rounds": BURN_IN_ROUNDS,
                    "parallelism": f"request-sharded x{world} GPUs x{S} streams"},
-        "branch_steps_per_step": branch_steps / args.steps,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_kind": peak_kind, "peak_note": PEAK_NOTE,
-                     "kernel": (("duchess_score (K1, list{}): the shards' concurrent launches, "
-                                 "scoring bytes per step / whole step time" if overlap else
-                                 "duchess_score (K1, list{}) per shard launch").format(
-                                     ", score_rows_kernel" if T == 1 else "")),
-                     "bytes_per_launch": bytes_per_launch,
-                     "k1_us_per_launch": k1_avg_s * 1e6,
-                     "k1_launches_timed": len(k1_us),
-                     "traffic": (None if k1_traffic_ratio(T)[0] is None
-                                 else k1_traffic_ratio(T)[0] * bytes_per_launch),
-                     "traffic_source": k1_traffic_ratio(T)[1]},
+        "branch_steps_per_step": bs_all / args.steps,
+        "roofline": roof,
         "e2e": e2e,
         "gpu_launches": 2 * S * args.steps,
         "clocks": clk,
@@ -531,44 +406,49 @@ def run_gpu_sharded(args, cfg, rank, world, local_rank):
     }
 
 
-def run_e2e_sharded(args, shards, rows, L, T, H, tdtype, dev, world, main):
-    """End to end through the public API with pinned HOST activations, per
-    shard on its stream: upload_survivors (only the survivors' windows cross
-    PCIe), K1, round, D2H of the round records and actions."""
+def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
+    """The same round through the public API with the activations in pinned
+    HOST memory: per round and shard, upload_survivors (one kernel gathers
+    exactly the survivors' windows over PCIe), K1 + round, and a D2H read of
+    the round records and actions (the RoundReports). The host buffers hold
+    the same counter-hashed windows as the device buffers (copied from them)."""
     import torch
+
     from paper_2509_24957_b200 import _lib
     steps = max(2, min(args.e2e_steps, args.steps))
     row_bytes = L * T * H * torch.tensor([], dtype=tdtype).element_size()
-    for sh in shards:
+    for sh in srv.shards:
         sh["host"] = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
-        sh["host"].view(-1).zero_()
+        sh["host"].copy_(sh["acts"][0])
         sh["dslab"] = torch.empty_like(sh["host"], device=dev)
         sh["rec_h"] = torch.empty(sh["eng"].t["round_rec"].numel(), dtype=torch.int32,
                                   pin_memory=True)
         sh["act_h"] = torch.empty(sh["eng"].t["actions"].numel(), dtype=torch.int32,
                                   pin_memory=True)
+    torch.cuda.synchronize(dev)
 
     def step():
-        for sh in shards:
+        for sh in srv.shards:
             with torch.cuda.stream(sh["stream"]):
                 eng = sh["eng"]
                 eng.upload_survivors(sh["host"], sh["dslab"])
-                sh["scorer"].score_active(sh["dslab"], sh["logit"], eng.probs.view(rows, L), eng)
+                sh["scorer"].score_active(sh["dslab"], sh["logit"],
+                                          eng.probs.view(rows, L), eng)
                 eng.round()
                 sh["rec_h"].copy_(eng.t["round_rec"], non_blocking=True)
                 sh["act_h"].copy_(eng.t["actions"], non_blocking=True)
-        for sh in shards:
+        for sh in srv.shards:
             sh["stream"].synchronize()
 
     step()
-    c0 = [sh["eng"].t["counters"].clone() for sh in shards]
+    c0 = srv.counters()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = time.perf_counter() - t0
-    bs = sum(int((sh["eng"].t["counters"] - c)[_lib.CNT_BRANCH_STEPS]) for sh, c in zip(shards, c0))
+    bs = int((srv.counters() - c0)[_lib.CNT_BRANCH_STEPS])
     st = torch.tensor([dt, float(bs)], dtype=torch.float64, device=dev)
     if world > 1:
         a = st[:1].clone()
@@ -576,83 +456,16 @@ def run_e2e_sharded(args, shards, rows, L, T, H, tdtype, dev, world, main):
         b = st[1:].clone()
         torch.distributed.all_reduce(b, op=torch.distributed.ReduceOp.SUM)
         dt, bs = float(a[0]), float(b[0])
+    for sh in srv.shards:
+        for k in ("host", "dslab"):
+            sh.pop(k)
     return {"value": bs / dt, "unit": UNIT,
             "h2d_bytes_per_step": bs / steps / max(world, 1) * row_bytes,
             "h2d": "survivor windows only (duchess_gather_active over each shard's active "
-                   "list), average per rank",
+                   "list), average per rank; host buffers hold the counter-hashed windows",
             "d2h_bytes_per_step": sum((sh["rec_h"].numel() + sh["act_h"].numel()) * 4
-                                      for sh in shards),
+                                      for sh in srv.shards),
             "steps": steps, "timing": "host wall clock, streams synchronised each step"}
-
-
-def run_e2e(args, eng, scorer, logit, probs, rows, L, T, H, tdtype, dev, world, bank=None):
-    """Same step through the public API with the activations in pinned HOST
-    memory: per step the H2D copy of the round's inputs (the survivors'
-    windows, gathered by one kernel over the device-side active list; the
-    whole slab for the other variants), the round (K1 + duchess_round, or one
-    fused launch), and a D2H read of the round records and actions
-    (RoundReports)."""
-    import torch
-    steps = max(2, min(args.e2e_steps, args.steps))
-    host = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
-    host.copy_(torch.zeros(1, dtype=tdtype).expand_as(host))
-    dslab = torch.empty_like(host, device=dev)
-    rec_host = torch.empty(eng.t["round_rec"].numel(), dtype=torch.int32, pin_memory=True)
-    act_host = torch.empty(eng.t["actions"].numel(), dtype=torch.int32, pin_memory=True)
-    from paper_2509_24957_b200 import _lib
-    stream = torch.cuda.current_stream(dev)
-
-    survivors_only = args.mode == "split" and args.k1 == "list"
-
-    def step():
-        if survivors_only:
-            # only the windows of this round's survivors cross PCIe (the
-            # active list is on the device; one gather kernel reads them)
-            eng.upload_survivors(host, dslab)
-        else:
-            dslab.copy_(host, non_blocking=True)
-        if args.mode == "fused":
-            eng.step_fused(dslab, bank, logit.view(-1))
-            rec_host.copy_(eng.t["round_rec"], non_blocking=True)
-            act_host.copy_(eng.t["actions"], non_blocking=True)
-            stream.synchronize()
-            return
-        # the round in flight was advanced by the previous round(): score it,
-        # decide it and advance into the next one, exactly as the timed loop
-        if args.k1 == "list":
-            scorer.score_active(dslab, logit, probs, eng)
-        else:
-            scorer(dslab, logit, probs, row_mask=eng.t["row_mask"])
-        eng.round()
-        rec_host.copy_(eng.t["round_rec"], non_blocking=True)
-        act_host.copy_(eng.t["actions"], non_blocking=True)
-        stream.synchronize()
-
-    step()
-    c0 = eng.t["counters"].clone()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
-    dt = time.perf_counter() - t0
-    bs = int((eng.t["counters"] - c0)[_lib.CNT_BRANCH_STEPS])
-    st = torch.tensor([dt, float(bs)], dtype=torch.float64, device=dev)
-    if world > 1:
-        a = st[:1].clone()
-        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
-        b = st[1:].clone()
-        torch.distributed.all_reduce(b, op=torch.distributed.ReduceOp.SUM)
-        dt, bs = float(a[0]), float(b[0])
-    row_bytes = host[0].numel() * host.element_size()
-    h2d = (bs / steps / max(world, 1) * row_bytes if survivors_only
-           else host.numel() * host.element_size())
-    return {"value": bs / dt, "unit": UNIT,
-            "h2d_bytes_per_step": h2d,
-            "h2d": ("survivor windows only (duchess_gather_active over the active list), "
-                    "average per rank" if survivors_only else "whole activation slab"),
-            "d2h_bytes_per_step": (rec_host.numel() + act_host.numel()) * 4,
-            "steps": steps, "timing": "host wall clock, stream-synchronised each step"}
 
 
 # ---------------------------------------------------------------------------
@@ -1009,44 +822,53 @@ def cpu_baselines(budget_s=5.0):
 
 
 def run_train_bench(args, rank, world, local_rank):
+    """C5: one full-batch logistic-regression step over BASELINE's 4 194 304
+    rows x 8192 (bf16), the rows split over the N ranks (strong scaling:
+    4M / N rows per GPU, 64 GiB at N = 1): K4 over the rank's shard, the
+    NCCL all-reduce of the 8193-float gradient (timed separately with events
+    on the same stream), SGD update."""
     import torch
+    from paper_2509_24957_b200.distributed import allreduce_sum, shard_range
     from paper_2509_24957_b200.probe import fill_windows
     from paper_2509_24957_b200.train import LogisticProbeTrainer
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     H = 8192
-    n_total = 4194304
-    n_local = n_total // 8          # the per-GPU shard of the 8-GPU configuration
+    n_total = int(os.environ.get("DUCHESS_C5_ROWS", 4194304))
+    lo, hi = shard_range(n_total, rank, world)
+    n_local = hi - lo
     X = torch.empty((n_local, 1, 1, H), dtype=torch.bfloat16, device=dev)
     fill_windows(X, 5000 + rank)
     X = X.view(n_local, H)
     g = torch.Generator(device=dev).manual_seed(5)
     w_true = torch.randn(H, generator=g, device=dev) / np.sqrt(H)
     y = torch.empty(n_local, device=dev)
-    for lo in range(0, n_local, 65536):
-        z = X[lo:lo + 65536].float() @ w_true
-        y[lo:lo + 65536] = (torch.rand(z.shape[0], generator=g, device=dev)
-                            < torch.sigmoid(z)).float()
+    for a in range(0, n_local, 65536):
+        z = X[a:a + 65536].float() @ w_true
+        y[a:a + 65536] = (torch.rand(z.shape[0], generator=g, device=dev)
+                          < torch.sigmoid(z)).float()
+    del z
     tr = LogisticProbeTrainer(H, device=dev, lr=0.5)
-    n_global = n_local * world
     stream = torch.cuda.current_stream(dev)
+    read_peak = measure_read_peak(dev, X) if rank == 0 else None
     for _ in range(args.warmup):
-        tr.step(X, y, n_global)
+        tr.step(X, y, n_total)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
     clocks = ClockSampler(local_rank) if rank == 0 else None
-    evs = []
+    k4_ev, ar_ev = [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(stream)
-        tr.local_grad(X, y, 1.0 / n_global)
+        tr.local_grad(X, y, 1.0 / n_total)
         b.record(stream)
-        evs.append((a, b))
-        from paper_2509_24957_b200.distributed import allreduce_sum
         allreduce_sum(tr.grad)
+        c.record(stream)
+        k4_ev.append((a, b))
+        ar_ev.append((b, c))
         tr.lib.duchess_sgd_update(tr.w.data_ptr(), tr.grad.data_ptr(), H + 1, 0.5,
                                   stream.cuda_stream)
     e1.record(stream)
@@ -1057,41 +879,84 @@ def run_train_bench(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
     ms = float(st[0])
-    k4_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    peak, kind = load_peaks()
+    k4_ms = sum(a.elapsed_time(b) for a, b in k4_ev) / args.steps
+    ar_us = sum(a.elapsed_time(b) for a, b in ar_ev) / args.steps * 1e3
     bytes_launch = n_local * (H * 2 + 4)
     achieved = bytes_launch / (k4_ms / 1e3) / 1e9
+    roof = roofline_figures(achieved, read_peak)
+    roof.update({"kernel": "duchess_lr_grad (K4)", "bytes_per_launch": bytes_launch,
+                 "k4_us_per_launch": k4_ms * 1e3, "traffic": None})
+    backend = torch.distributed.get_backend() if world > 1 else None
     return {"metric": "probe-training rows/s (C5 logistic regression, full-batch step)",
-            "value": n_local * world / (ms / 1e3), "unit": "rows/s", "n_gpus": world,
+            "value": n_total / (ms / 1e3), "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) activations, labels ~ Bernoulli(sigmoid(X w*))",
-            "config": {"workload": f"C5: {n_local} rows x {H} per GPU (8 GiB, the 8-GPU shard "
-                                   f"of 4M rows), grad + NCCL all-reduce (8193 f32) + SGD"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": kind, "peak_note": PEAK_NOTE,
-                         "kernel": "duchess_lr_grad (K4)", "bytes_per_launch": bytes_launch,
-                         "k4_us_per_launch": k4_ms * 1e3, "traffic": None},
+            "config": {"workload": f"C5: {n_total} rows x {H} bf16 split over {world} GPU(s) "
+                                   f"({n_local} rows, {bytes_launch / 2**30:.1f} GiB on rank 0), "
+                                   f"grad + all-reduce (8193 f32) + SGD",
+                       "rows": n_total, "rows_per_gpu": n_local, "hidden": H},
+            "roofline": roof,
+            "allreduce": {"us_per_step": ar_us, "bytes": (H + 1) * 4,
+                          "backend": backend or "none (one rank: no collective)"},
             "gpu_launches": 3 * args.steps, "clocks": clk}
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port) — only here and in tests may oracle/ run.
+# CPU reference — only here and in tests may oracle/ (incl. the vendored
+# reference in oracle/_ref) run.
 
 _CPU = {}
 CPU_POOL_BYTES = 64 << 20      # activation windows per CPU process (16 processes: 1 GiB)
 
 
-def _cpu_init(cfg_name, n_req, seed):
-    from oracle import port
+def cpu_kind() -> str:
+    """'reference' when the unmodified reference is vendored in oracle/_ref
+    (oracle/vendor_ref.py, checked against its SHA-256 manifest), else 'port'
+    (the pinned restatement oracle/port.py)."""
+    from oracle import vendor_ref
+    if vendor_ref.available():
+        ref = os.path.join(ROOT, "oracle", "_ref")
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        return "reference"
+    return "port"
+
+
+def _cpu_init(cfg_name, n_req, seed, kind):
     cfg = CONFIGS[cfg_name]
     H, T, L = cfg["H"], cfg["T"], cfg["L"]
-    params = port.GenParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]])
-    traces = port.generate(params, n_req, seed)
-    knobs = port.Knobs(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+    w, b, g, beta = make_probe(H, L)
+    if kind == "reference":
+        # the reference itself: generate_synthetic, DuchessRun, mlp_forward
+        from branchsim.orchestrator import DuchessRun, OrchestratorConfig
+        from branchsim.predictor import MlpWeights, mlp_forward
+        from branchsim.workload import SyntheticParams, generate_synthetic
+        params = SyntheticParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]])
+        traces = generate_synthetic(params, n_req, seed=seed).requests
+        knobs = OrchestratorConfig(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+        probes = [MlpWeights(input_dim=H, layer_dims=[], head_dim=1, activations=[],
+                             weights=[w[l].reshape(1, H).copy()], biases=[np.array([b[l]])],
+                             ln_gain=g[l].copy(), ln_bias=beta[l].copy()) for l in range(L)]
+
+        def score(l, m):
+            return float(mlp_forward(probes[l], m)[1][0])
+
+        def make_run(trace, rng, predictor):
+            return DuchessRun(trace, knobs, rng, predictor=predictor)
+    else:
+        from oracle import port
+        params = port.GenParams(templates_per_request=64, **PRESET_GEN[cfg["preset"]])
+        traces = port.generate(params, n_req, seed)
+        knobs = port.Knobs(max_branches=cfg["c"], **PRESET_KNOBS[cfg["preset"]])
+
+        def score(l, m):
+            return port.pooled_linear_probe(m[None, :], w[l], b[l], g[l], beta[l])[1]
+
+        def make_run(trace, rng, predictor):
+            return port.DuchessRequest(trace, knobs, rng, predictor=predictor)
     master = random.Random(seed + 1)
     seeds = [master.getrandbits(64) for _ in traces]
-    w, b, g, beta = make_probe(H, L)
     # Distinct windows streamed from DRAM like the GPU arm streams HBM: a
     # per-process pool of CPU_POOL_BYTES (> the host caches), each branch-step
     # scoring the next window. Values are bf16-rounded for bf16 configs but kept
@@ -1106,63 +971,121 @@ def _cpu_init(cfg_name, n_req, seed):
             u = x.view(np.uint32)
             x = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).view(np.float32)
         pool.append(x)
-    _CPU.update(traces=traces, knobs=knobs, seeds=seeds, w=w, b=b, g=g, beta=beta,
-                windows=pool, L=L, next=0, cursor=0)
+    _CPU.update(traces=traces, seeds=seeds, score=score, make_run=make_run, windows=pool,
+                L=L, next=0, cursor=0)
 
 
 def _cpu_run(budget_s):
-    from oracle import port
+    """Serve requests with the (reference's) DuchessRun for budget_s seconds;
+    predictor= pools the next window (fp64 mean over T, the north-star's
+    pooling) and scores it with mlp_forward per layer (mean of the layers'
+    probabilities, as the GPU's combine=1). Returns (branch-steps, seconds)."""
     st = _CPU
     count = [0]
+    score, L = st["score"], st["L"]
 
-    def predictor(tmpl, position, _rng):
+    def predictor(_tmpl, _position, _rng):
         count[0] += 1
         win = st["windows"][st["cursor"] % len(st["windows"])]
         st["cursor"] += 1
-        ps = [port.pooled_linear_probe(win[l], st["w"][l], st["b"][l], st["g"][l],
-                                       st["beta"][l])[1] for l in range(st["L"])]
-        return ps[0] if len(ps) == 1 else sum(ps) / len(ps)
+        ps = [score(l, win[l].mean(axis=0, dtype=np.float64)) for l in range(L)]
+        return ps[0] if L == 1 else sum(ps) / L
 
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < budget_s:
         i = st["next"] % len(st["traces"])
         st["next"] += 1
-        req = port.DuchessRequest(st["traces"][i], st["knobs"], random.Random(st["seeds"][i]),
-                                  predictor=predictor)
+        req = st["make_run"](st["traces"][i], random.Random(st["seeds"][i]), predictor)
         while not req.done and time.perf_counter() - t0 < budget_s:
             req.step()
     return count[0], time.perf_counter() - t0
 
 
-def cpu_measure(cfg_name, steps, budget_s, procs):
+def cpu_measure(cfg_name, steps, budget_s, procs, kind, warmup=1):
+    """Variant 1 (procs = 1) / variant 2 (procs = all cores; requests are
+    independent): branch-steps/s over `steps` timed rounds of
+    `budget_s` seconds per process."""
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    with ctx.Pool(procs, initializer=_cpu_init, initargs=(cfg_name, 64, 4242)) as pool:
-        pool.map(_cpu_run, [0.2] * procs)            # warm
+    with ctx.Pool(procs, initializer=_cpu_init, initargs=(cfg_name, 64, 4242, kind)) as pool:
+        for _ in range(warmup):
+            pool.map(_cpu_run, [min(budget_s, 0.5)] * procs)
         total_bs, total_t = 0, 0.0
-        per_step = []
         for _ in range(steps):
             t0 = time.perf_counter()
             res = pool.map(_cpu_run, [budget_s] * procs)
-            dt = time.perf_counter() - t0
-            bs = sum(r[0] for r in res)
-            total_bs += bs
-            total_t += dt
-            per_step.append(bs / dt)
-    return total_bs / total_t, per_step
+            total_t += time.perf_counter() - t0
+            total_bs += sum(r[0] for r in res)
+    return total_bs / total_t, total_t
+
+
+def cpu_vectorised(cfg_name, budget_s=3.0):
+    """Variant 3: vectorised numpy fp32 restatement of the
+    scoring (pool over T -> LayerNorm -> dot -> sigmoid) over batches of
+    distinct windows, BLAS on all threads; scoring only, no decisions."""
+    cfg = CONFIGS[cfg_name]
+    H, T, L = cfg["H"], cfg["T"], cfg["L"]
+    w, b, g, beta = make_probe(H, L)
+    wg = (w * g).astype(np.float32)
+    c1 = (np.einsum("lh,lh->l", w, beta) + b).astype(np.float32)
+    n = max(64, int((256 << 20) // (L * T * H * 4)))
+    X = np.random.default_rng(0).standard_normal((n, L, T, H), dtype=np.float32)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        m = X.mean(axis=2)                                   # [n, L, H]
+        mu = m.mean(axis=2, keepdims=True)
+        z = (m - mu) / np.sqrt(((m - mu) ** 2).mean(axis=2, keepdims=True) + 1e-5)
+        logit = np.einsum("nlh,lh->nl", z, wg) + c1
+        _p = 1.0 / (1.0 + np.exp(-logit))
+        done += n
+    return done / (time.perf_counter() - t0)
+
+
+def host_info():
+    import platform
+    model = None
+    try:
+        out = os.popen("lscpu 2>/dev/null").read()
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")}
+                for d in threadpool_info()]
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "python": platform.python_version(), "numpy": np.__version__, "blas": blas}
 
 
 def cpu_baseline_entry(cfg_name, budget_total=12.0):
+    """The GPU line's cpu_baseline: variant 2 (the reference on every host
+    core) as `value`, variants 1 and 3 beside it, host description."""
     procs = os.cpu_count() or 1
+    kind = cpu_kind()
     steps = 3
-    val, _ = cpu_measure(cfg_name, steps, budget_total / steps, procs)
+    v2, _ = cpu_measure(cfg_name, steps, budget_total / steps, procs, kind)
+    v1, _ = cpu_measure(cfg_name, 1, 4.0, 1, kind)
+    v3 = cpu_vectorised(cfg_name)
     cfg = CONFIGS[cfg_name]
-    return {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
-            "sample": f"oracle/port.py DuchessRun restatement + numpy pooled LN probe "
-                      f"(T={cfg['T']}, H={cfg['H']}, L={cfg['L']}) on {cfg['preset']} requests "
-                      f"(c={cfg['c']}), each branch-step scoring the next of a 64 MiB pool of "
-                      f"distinct windows per process, {procs} processes x {steps} x "
-                      f"{budget_total/steps:.1f} s"}
+    what = ("the unmodified reference (oracle/_ref/branchsim: generate_synthetic, DuchessRun, "
+            "mlp_forward)" if kind == "reference" else "oracle/port.py (restatement)")
+    return {"value": v2, "unit": UNIT, "cores": procs, "kind": kind,
+            "sample": f"{what} with predictor= pooling (fp64 mean over T) + scoring each "
+                      f"branch-step's next window of a 64 MiB pool of distinct windows "
+                      f"(T={cfg['T']}, H={cfg['H']}, L={cfg['L']}), {cfg['preset']} requests "
+                      f"(c={cfg['c']}), {procs} processes x {steps} x {budget_total/steps:.1f} s",
+            "variants": {"1_one_core": {"value": v1, "cores": 1, "kind": kind},
+                         "2_all_cores": {"value": v2, "cores": procs, "kind": kind},
+                         "3_numpy_fp32_vectorised_scoring_only": {
+                             "value": v3, "cores": procs, "kind": "port",
+                             "note": "pool + LN + dot + sigmoid, numpy/BLAS all threads, "
+                                     "no decisions"}},
+            "host": host_info()}
 
 
 def cpu_fork_or_train(args):
@@ -1264,34 +1187,27 @@ def run_reference(args, cfg):
     if cfg is None:
         return cpu_fork_or_train(args)
     procs = os.cpu_count() or 1
+    kind = cpu_kind()
     total = args.steps + args.warmup
     budget = max(0.5, min(5.0, 120.0 / max(total, 1)))
-    import multiprocessing as mp
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs, initializer=_cpu_init, initargs=(args.config, 64, 4242)) as pool:
-        for _ in range(args.warmup):
-            pool.map(_cpu_run, [budget] * procs)
-        total_bs, total_t = 0, 0.0
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_cpu_run, [budget] * procs)
-            total_t += time.perf_counter() - t0
-            total_bs += sum(r[0] for r in res)
-    val = total_bs / total_t
+    val, total_t = cpu_measure(args.config, args.steps, budget, procs, kind, warmup=args.warmup)
+    what = ("the unmodified reference (oracle/_ref/branchsim DuchessRun + mlp_forward)"
+            if kind == "reference" else "oracle/port.py DuchessRun restatement + pooled probe")
     return {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config.upper()} (CPU port)",
+        "data": "synthetic", "config": {"workload": f"{args.config.upper()} (CPU {kind})",
                                         "requests": cfg["R"], "branches": cfg["c"],
                                         "hidden": cfg["H"], "layers": cfg["L"],
                                         "window": cfg["T"]},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{procs} processes x {budget:.2f} s per step of "
-                                   f"oracle/port.py DuchessRun + numpy pooled probe, each "
-                                   f"branch-step scoring the next of a 64 MiB pool of distinct "
-                                   f"windows per process (streamed from DRAM like the GPU arm)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": kind,
+                         "sample": f"{procs} processes x {budget:.2f} s per step of {what}, "
+                                   f"predictor= pooling (fp64 mean over T) + scoring each "
+                                   f"branch-step's next window of a 64 MiB pool of distinct "
+                                   f"windows per process (streamed from DRAM like the GPU arm)",
+                         "host": host_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -1302,39 +1218,35 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2",
+    ap.add_argument("--config", default=None,
                     choices=sorted(CONFIGS) + ["c3tc", "c4", "c5", "difficulty", "sim",
-                                               "baselines"])
-    ap.add_argument("--k1", default="list", choices=["list", "mask", "ldg"],
-                    help="K1 variant: persistent TMA over the compacted survivor list "
-                         "(default), TMA over the row mask, or the per-window LDG kernel")
-    ap.add_argument("--mode", default="split", choices=["fused", "split"],
-                    help="split (default): K1 launch + duchess_round launch per round; "
-                         "fused: one duchess_step launch per round (see DESIGN.md 7)")
+                                               "baselines"],
+                    help="default: c2 on one GPU (BASELINE.json configs[1]); c3 strong-scaled "
+                         "over the GPUs when N > 1 (configs[2], 1024 requests sharded)")
     ap.add_argument("--shards", type=int, default=None,
                     help="independent request shards (engines on separate CUDA streams) per "
-                         "GPU; default 2 for c2 / c3, 1 otherwise")
-    ap.add_argument("--shard-order", default=None, choices=["turns", "overlap"],
-                    help="turns: the shards' scorers take turns (event chain); overlap: they "
-                         "run concurrently (default overlap for c2, turns for c3)")
-    ap.add_argument("--graph", action="store_true",
-                    help="replay the round loop as a CUDA graph (one slab rotation per graph)")
+                         "GPU; default 2 for c2 / c3 / c3t1, 1 otherwise")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the round loop as a CUDA graph (one buffer rotation per "
+                         "graph); auto = on for the launch-bound c1")
     ap.add_argument("--k1-every", type=int, default=8,
-                    help="bracket K1 with CUDA events on every N-th timed step")
-    ap.add_argument("--nsplit", type=int, default=2)
-    ap.add_argument("--threads", type=int, default=128)
+                    help="bracket K1 with CUDA events on every N-th timed step (1 shard)")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--slots", type=int, default=None,
+                    help="tests only: override the config's request slots (pool scaled)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = "c2" if world_env == 1 else "c3"
     cfg = CONFIGS.get(args.config)
+    if args.slots and cfg is not None:
+        CONFIGS[args.config] = cfg = dict(cfg, R=args.slots, pool=max(8 * args.slots, 64))
     if args.shards is None:
         # two request shards per GPU on two streams hide each shard's round
         # kernel under the other's scoring
         args.shards = 2 if args.config in ("c2", "c3", "c3t1") else 1
-    if args.shard_order is None:
-        # concurrent scorers also fill each other's launch ramp and tail
-        # (C3 with two-row stages: 5.64 vs 5.48-5.52 M/s taking turns)
-        args.shard_order = "overlap" if args.config in ("c2", "c3", "c3t1") else "turns"
+    args.graph = args.graph == "on" or (args.graph == "auto" and args.config == "c1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -1363,10 +1275,8 @@ def main():
         out = run_sim_bench(args, rank, world, local_rank)
     elif args.config == "baselines":
         out = run_baselines_bench(args, rank, world, local_rank)
-    elif args.mode == "split" and args.k1 == "list" and not args.graph and args.shards > 1:
-        out = run_gpu_sharded(args, cfg, rank, world, local_rank)
     else:
-        out = run_gpu(args, cfg, rank, world, local_rank)
+        out = run_serving(args, cfg, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and cfg is not None:
             out["cpu_baseline"] = cpu_baseline_entry(args.config)

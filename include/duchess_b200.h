@@ -65,8 +65,6 @@ extern "C" {
  * default decides from a warp prefix sum unless u is within the rounding
  * margin of a boundary; both give identical picks — the flag exists to test that). */
 #define DUCHESS_FLAG_EXACT_CDF 1
-/* Profiling only: duchess_step skips the decision warps (scoring alone). */
-#define DUCHESS_FLAG_PROFILE_NO_DECIDE 2
 
 /* Policies (orchestrator.py:47-52). DUCHESS runs through advance / decide /
  * round; the baselines through duchess_baseline_round. */
@@ -258,49 +256,10 @@ int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload* workload,
 int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                   const DuchessState* state, const double* probs, void* stream);
 
-/* ---- fused round: K1 scoring + decide + advance in ONE persistent launch ----
- * DuchessRun.step (orchestrator.py:329-402) for every slot with the
- * predictor seam (:358-363) served by the pooled linear probe (K1,
- * predictor.py:126-151). While the producer/consumer warps of each CTA
- * stream survivor windows from HBM, a decision warp per CTA takes every
- * request slot whose windows are all scored (each score store replaces a
- * sentinel the decision warp polls) and runs phases 2-5 for it, then refill + phase 1 of the next
- * round, appending its survivors to the next round's list. Decisions overlap
- * the streaming of other requests' windows; per-request results are those of
- * duchess_advance / duchess_score / duchess_decide. Refills pop the service
- * queue in completion order (the set of requests admitted per round is the
- * same; only their slot placement may differ from duchess_round).
- * Requires pred_source == DUCHESS_PRED_DEVICE and the DUCHESS policy. */
-typedef struct DuchessStepCtl {
-  int32_t* rows; /* [2 * R * C] survivor rows (r*C + slot) per round parity */
-  int32_t* reqs; /* [2 * R] request slots with a round, per round parity */
-  int32_t* idle; /* [R] slot went idle last step: clear its round record */
-  int32_t* ctl;  /* [DUCHESS_STEP_CTL_WORDS] counters, zero-initialised */
-} DuchessStepCtl;
-#define DUCHESS_STEP_CTL_WORDS 16
-#define DUCHESS_STEP_CTL_TAG 0   /* index of the next duchess_step launch */
-#define DUCHESS_STEP_CTL_POP 2   /* service-queue entries popped so far */
-#define DUCHESS_STEP_CTL_COUNT 4 /* +parity: survivor rows listed for the round */
-#define DUCHESS_STEP_CTL_NREQ 6  /* +parity: request slots listed for the round */
-
-/* Refill every slot and run phase 1 of the first round (call once on a fresh,
- * zeroed DuchessStepCtl). probs [R*C*L] fp64 is the array later passed to
- * duchess_step as out_prob (the survivors' entries are armed). */
-int duchess_step_begin(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                       const DuchessState* state, const DuchessStepCtl* ctl, double* probs,
-                       void* stream);
-/* One fused round. acts: [R*C rows, L, T, H] (row index r*C + slot), bf16 or
- * fp32, hidden contiguous, 16-byte aligned rows; L = policy->n_layers.
- * out_prob [R*C*L] fp64 doubles as the decisions' probability input. */
-int duchess_step(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                 const DuchessState* state, const DuchessStepCtl* ctl, const void* acts,
-                 int32_t dtype, int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
-                 int64_t token_stride, const float* wg, const float* c1, float* out_logit,
-                 double* out_prob, void* stream);
-
 /* One round of a baseline policy for every slot (DefaultScRun.step
  * orchestrator.py:408-435, ShortMkRun.step :466-516, DynasorRun.step
- * :529-561), refill included; cooperative launch. No predictions, no forks. */
+ * :529-561), refill included: a refill launch ranks the slots needing a
+ * request, then the policy launch runs the round. No predictions, no forks. */
 int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                            const DuchessState* state, void* stream);
 
@@ -421,6 +380,10 @@ int duchess_lr_grad(const void* X, int32_t dtype, const float* y, const float* w
 int duchess_sgd_update(float* w, const float* grad, int32_t n, float lr, void* stream);
 
 /* Build/runtime introspection. */
+/* Measurement: stream `bytes` of device memory (16-byte aligned) through a
+ * read-only persistent kernel (the read-only HBM ceiling, bench.py roofline). */
+int duchess_read_stream(const void* buf, int64_t bytes, uint32_t* sink, void* stream);
+
 const char* duchess_version(void);
 int duchess_device_arch(void);
 

@@ -21,7 +21,6 @@ REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
 PRED_DEVICE, PRED_TRACE, PRED_HOST = 0, 1, 2
 FLAG_EXACT_CDF = 1
-FLAG_PROFILE_NO_DECIDE = 2
 POLICY_DUCHESS, POLICY_DEFAULT_SC, POLICY_SHORT_MK, POLICY_DYNASOR = 0, 1, 2, 3
 MT_WORDS = 625
 MAX_SLOTS = 64
@@ -80,15 +79,6 @@ class State(C.Structure):
         (name, C.c_void_p) for name in STATE_PTR_FIELDS]
 
 
-class StepCtl(C.Structure):
-    _fields_ = [("rows", C.c_void_p), ("reqs", C.c_void_p), ("idle", C.c_void_p),
-                ("ctl", C.c_void_p)]
-
-
-STEP_CTL_WORDS = 16
-STEP_CTL_TAG, STEP_CTL_POP, STEP_CTL_COUNT, STEP_CTL_NREQ = 0, 2, 4, 6
-
-
 SYMBOLS = {
     # name: (restype, argtypes)
     "duchess_score_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
@@ -116,12 +106,7 @@ SYMBOLS = {
                                  C.c_void_p, C.c_void_p]),
     "duchess_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
                                 C.c_void_p, C.c_void_p]),
-    "duchess_step_begin": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
-                                     C.POINTER(StepCtl), C.c_void_p, C.c_void_p]),
-    "duchess_step": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
-                               C.POINTER(StepCtl), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                               C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
-                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    "duchess_read_stream": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "duchess_baseline_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload),
                                          C.POINTER(State), C.c_void_p]),
     "duchess_branch_out_sample": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,

@@ -511,20 +511,12 @@ __device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
   return p;
 }
 
-// Fused-step bookkeeping for phase 1 (duchess_step): survivors go to the
-// next round's window list, the slot to the next round's request list, and
-// the survivors' probability entries are armed with a sentinel (-1; scores
-// are clipped to [1e-12, 1 - 1e-12], predictor.py:148) that the scorer's
-// store replaces, so a decision warp knows a window is scored by reading the
-// score itself: no fence or atomic on the streaming path.
+// Survivor list phase 1 appends to (the round kernel writes the next round's
+// list parity while the scorer reads the current one).
 struct Phase1Out {
   int32_t* rows;
   int32_t* count;
-  int32_t* reqs;
-  int32_t* nreq;
-  double* probs;
 };
-constexpr double kUnscored = -1.0;
 
 __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, int p, SlotCache& c, int lane,
@@ -584,12 +576,6 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       basei = __shfl_sync(0xffffffffu, basei, 0);
       if (surv) list_rows[basei + __popc(m & ((1u << lane) - 1u))] = int32_t(rC + j);
     }
-  }
-  if (fo && fo->reqs) {
-    for (int j = lane; j < C; j += 32)
-      if (s.row_mask[rC + j])
-        for (int l = 0; l < pol.n_layers; ++l) fo->probs[(rC + j) * pol.n_layers + l] = kUnscored;
-    if (lane == 0) fo->reqs[atomicAdd(fo->nreq, 1)] = r;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1124,8 +1110,8 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
 }
 
 // Refill-or-load prologue with the service queue popped atomically in
-// completion order (the fused step has no grid-wide barrier to rank slots).
-__device__ int slot_prologue_fused(const DuchessPolicy& pol, const DuchessWorkload& w,
+// completion order (the round kernel has no grid-wide barrier to rank slots).
+__device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkload& w,
                                    const DuchessState& s, int r, SlotCache& c, int lane,
                                    bool cache_valid, int32_t* pop) {
   const int C = pol.max_branches;
@@ -1195,7 +1181,7 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   const int par = s.active_count[kListPar];
   trace_mark(s, r, 8, lane);
   clear_round_inputs(pol, s, r, lane);
-  const int p = slot_prologue_fused(pol, w, s, r, c, lane, had_round, s.queue_head + 1);
+  const int p = slot_prologue_atomic(pol, w, s, r, c, lane, had_round, s.queue_head + 1);
   trace_mark(s, r, 10, lane);
   if (p >= 0) {
     Phase1Out fo{};
@@ -1212,158 +1198,6 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
       s.active_count[kListPar] = par ^ 1;
       s.active_count[kListExit] = 0;
       s.queue_head[0] = s.queue_head[1];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Fused round (duchess_step): K1 scoring + decide + advance in one launch.
-//
-// ctl words: tag (index of the next step launch), exit counter, queue pops,
-// then per round parity: listed survivor windows, listed request slots,
-// decision claims. Launch `tag` consumes parity tag & 1 (built by the
-// previous launch or duchess_step_begin) and builds parity (tag + 1) & 1; its
-// last CTA resets the consumed parity and bumps the tag.
-enum : int {
-  kCtlTag = DUCHESS_STEP_CTL_TAG, kCtlExit = 1, kCtlPop = DUCHESS_STEP_CTL_POP,
-  kCtlCount = DUCHESS_STEP_CTL_COUNT, kCtlNReq = DUCHESS_STEP_CTL_NREQ, kCtlClaim = 10
-};
-
-__device__ __forceinline__ Phase1Out phase1_out(const DuchessStepCtl& x, int R, int C, int par,
-                                                double* probs) {
-  Phase1Out o;
-  o.rows = x.rows + int64_t(par) * R * C;
-  o.count = x.ctl + kCtlCount + par;
-  o.reqs = x.reqs + int64_t(par) * R;
-  o.nreq = x.ctl + kCtlNReq + par;
-  o.probs = probs;
-  return o;
-}
-
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-step_begin_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x,
-                  double* probs) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (r >= s.n_slots) return;
-  SlotCache& c = cache[threadIdx.x >> 5];
-  const int tag = x.ctl[kCtlTag];
-  clear_round_inputs(pol, s, r, lane);
-  const int p = slot_prologue_fused(pol, w, s, r, c, lane, false, x.ctl + kCtlPop);
-  if (p >= 0) {
-    const Phase1Out fo = phase1_out(x, s.n_slots, pol.max_branches, tag & 1, probs);
-    phase1_slot(pol, w, s, r, p, c, lane, &fo);
-  } else if (lane == 0) {
-    x.idle[r] = 1;
-  }
-}
-
-constexpr int kStepThreads = kTmaCons + 64;   // 8 consumer warps, producer, decision warp
-
-template <bool BF16, int VPT>
-__global__ void __launch_bounds__(kStepThreads, 2)
-step_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, DuchessStepCtl x, ScoreArgs a,
-            TmaArgs t) {
-  constexpr int ESZ = BF16 ? 2 : 4;
-  extern __shared__ __align__(128) char ring[];
-  __shared__ uint64_t full_bar[32], empty_bar[32];
-  __shared__ float2 red[2][kTmaConsWarps];
-  __shared__ SlotCache cache;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TmaRing rg{ring, full_bar, empty_bar, t.tokens_per_stage * t.row_bytes};
-  tma_ring_init(t, rg);
-  __syncthreads();
-  pdl_wait();   // the previous round's lists, counters and state are complete
-  const int tag = x.ctl[kCtlTag];
-  const int par = tag & 1;
-  const int R = s.n_slots, C = pol.max_branches, L = pol.n_layers;
-  t.row_list = x.rows + int64_t(par) * R * C;
-  const int64_t n_units = int64_t(x.ctl[kCtlCount + par]) * L;
-  if (s.trace && blockIdx.x == 0 && threadIdx.x == 0) {   // profiling: kernel start
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    s.trace[13] = (long long)t0;
-  }
-
-  if (warp == kTmaConsWarps) {                       // ---- producer ----
-    if (lane == 0) tma_produce<ESZ>(a, t, rg, n_units);
-  } else if (warp == kTmaConsWarps + 1) {            // ---- decisions ----
-    if (pol.flags & DUCHESS_FLAG_PROFILE_NO_DECIDE) {  // profiling: re-list, no decisions
-      const int nreq = x.ctl[kCtlNReq + par];
-      const Phase1Out fo = phase1_out(x, R, C, par ^ 1, a.out_prob);
-      for (int i = blockIdx.x; i < nreq; i += gridDim.x) {
-        const int r = x.reqs[int64_t(par) * R + i];
-        for (int j = lane; j < C; j += 32)
-          if (s.row_mask[int64_t(r) * C + j]) fo.rows[atomicAdd(fo.count, 1)] = int32_t(int64_t(r) * C + j);
-        if (lane == 0) fo.reqs[atomicAdd(fo.nreq, 1)] = r;
-      }
-      goto done;
-    }
-    for (int r = blockIdx.x * 32 + lane; r < R; r += gridDim.x * 32) {
-      if (x.idle[r]) {                               // slot ran no round this step
-        s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
-        x.idle[r] = 0;
-      }
-    }
-    const int nreq = x.ctl[kCtlNReq + par];
-    const int32_t* reqs = x.reqs + int64_t(par) * R;
-    const Phase1Out fo = phase1_out(x, R, C, par ^ 1, a.out_prob);
-    while (true) {
-      int i = 0;
-      if (lane == 0) i = atomicAdd(x.ctl + kCtlClaim + par, 1);
-      i = __shfl_sync(0xffffffffu, i, 0);
-      if (i >= nreq) break;
-      const int r = reqs[i];
-      const int64_t rC = int64_t(r) * C;
-      trace_mark(s, r, 9, lane);
-      // wait until every listed window of the slot is scored (its sentinel replaced)
-      for (int j = lane; j < C; j += 32) {
-        if (!s.row_mask[rC + j]) continue;
-        for (int l = 0; l < L; ++l) {
-          const double* pp = a.out_prob + (rC + j) * L + l;
-          int ns = 64;
-          while (__ldcv(pp) == kUnscored) {
-            __nanosleep(ns);
-            ns = ns < 512 ? 2 * ns : 512;
-          }
-        }
-      }
-      __syncwarp();
-      trace_mark(s, r, 12, lane);
-      decide_slot(pol, w, s, r, cache, lane, a.out_prob);
-      trace_mark(s, r, 8, lane);
-      clear_round_inputs(pol, s, r, lane);
-      const int p = slot_prologue_fused(pol, w, s, r, cache, lane, true, x.ctl + kCtlPop);
-      trace_mark(s, r, 10, lane);
-      if (p >= 0) phase1_slot(pol, w, s, r, p, cache, lane, &fo);
-      else if (lane == 0) x.idle[r] = 1;
-      trace_mark(s, r, 11, lane);
-      __syncwarp();
-    }
-  } else {                                           // ---- consumers ----
-    tma_consume<BF16, VPT>(a, t, rg, n_units, red, [](int64_t, int, int64_t) {});
-    if (s.trace && threadIdx.x == 0) {                // profiling: this CTA's last window
-      unsigned long long t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      atomicMax(reinterpret_cast<unsigned long long*>(s.trace + 14), t1);
-    }
-  }
-done:
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    pdl_launch_dependents();
-    __threadfence();
-    if (atomicAdd(x.ctl + kCtlExit, 1) == int(gridDim.x) - 1) {
-      __threadfence();
-      x.ctl[kCtlCount + par] = 0;
-      x.ctl[kCtlNReq + par] = 0;
-      x.ctl[kCtlClaim + par] = 0;
-      x.ctl[kCtlExit] = 0;
-      const int pops = x.ctl[kCtlPop];
-      s.queue_head[0] = pops;
-      s.queue_head[1] = pops;
-      x.ctl[kCtlTag] = tag + 1;
     }
   }
 }
@@ -1568,21 +1402,38 @@ __device__ void baseline_slot(const DuchessPolicy& pol, const DuchessWorkload& w
   if (cancel || !any_active) close_slot(s, r, p, DUCHESS_REASON_EXHAUSTED, lane, rec);
 }
 
+// Two launches per baseline round, so the refill ranking reads a stable
+// snapshot: baseline_refill_kernel ranks the slots flagged needs_refill (the
+// k-th flagged slot takes queue[head + k]; nothing in this launch writes the
+// flags) and refills them; baseline_kernel then runs the policy round, which
+// clears / sets the flags for the next round. queue_head[1] (written by slot
+// 0's warp) is published to queue_head[0] by the policy launch.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+baseline_refill_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+  __shared__ SlotCache cache[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= s.n_slots) return;
+  int32_t* rec0 = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
+  if (lane < DUCHESS_REC_WORDS) rec0[lane] = 0;
+  __syncwarp();
+  slot_prologue(pol, w, s, r, cache[threadIdx.x >> 5], lane, /*cache_valid=*/true);
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 baseline_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
   __shared__ SlotCache cache[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (blockIdx.x == 0 && threadIdx.x == 0) s.queue_head[0] = s.queue_head[1];
-  __threadfence();
-  cg::this_grid().sync();
   if (r >= s.n_slots) return;
+  if (s.done[r]) return;
+  const int p = s.slot_req[r];
+  if (p < 0) return;
   SlotCache& c = cache[threadIdx.x >> 5];
-  const int32_t* rec0 = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
-  if (lane < DUCHESS_REC_WORDS) const_cast<int32_t*>(rec0)[lane] = 0;
-  __syncwarp();
-  const int p = slot_prologue(pol, w, s, r, c, lane, false);
-  if (p >= 0) baseline_slot(pol, w, s, r, p, c, lane);
+  load_slot(s, int64_t(r) * pol.max_branches, int64_t(r) * s.branch_cap, pol.max_branches, c, lane);
+  load_meta(w, s, r, p, pol.max_branches, c, lane);
+  baseline_slot(pol, w, s, r, p, c, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1829,134 +1680,6 @@ extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload*
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
-static bool step_ctl_ok(const DuchessStepCtl* x) {
-  return x && x->rows && x->reqs && x->idle && x->ctl;
-}
-
-extern "C" int duchess_step_begin(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                                  const DuchessState* state, const DuchessStepCtl* ctl,
-                                  double* probs, void* stream) {
-  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl) || !probs) return DUCHESS_EINVAL;
-  if (policy->policy_kind != DUCHESS_POLICY_DUCHESS || policy->pred_source != DUCHESS_PRED_DEVICE)
-    return DUCHESS_EINVAL;
-  if (state->n_slots == 0) return DUCHESS_OK;
-  const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  step_begin_kernel<<<grid, 32 * kWarpsPerBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      *policy, *workload, *state, *ctl, probs);
-  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
-}
-
-template <bool BF16, int VPT>
-static cudaError_t launch_step(const DuchessPolicy& pol, const DuchessWorkload& w,
-                               const DuchessState& st, const DuchessStepCtl& x, const ScoreArgs& a,
-                               const TmaArgs& t, size_t smem, cudaStream_t stream) {
-  auto kern = step_kernel<BF16, VPT>;
-  // Grid = co-resident CTAs (decision warps wait on windows any CTA of the
-  // grid may hold, so every CTA must be resident at once). Cached per
-  // (device, instantiation, smem): the occupancy query costs host time.
-  static int cached_dev[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
-  static size_t cached_smem[2][4];
-  static int cached_grid[2][4];
-  const int vi = VPT == 1 ? 0 : VPT == 2 ? 1 : VPT == 4 ? 2 : 3;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int& cd = cached_dev[BF16][vi];
-  if (cd != dev || cached_smem[BF16][vi] != smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cached_grid[BF16][vi] = sms * (per_sm < 2 ? per_sm : 2);
-    cached_smem[BF16][vi] = smem;
-    cd = dev;
-  }
-  const int grid = cached_grid[BF16][vi];
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kStepThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, pol, w, st, x, a, t);
-}
-
-extern "C" int duchess_step(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                            const DuchessState* state, const DuchessStepCtl* ctl, const void* acts,
-                            int32_t dtype, int32_t T, int32_t H, int64_t row_stride,
-                            int64_t layer_stride, int64_t token_stride, const float* wg,
-                            const float* c1, float* out_logit, double* out_prob, void* stream) {
-  if (!state_ok(policy, state) || !workload || !step_ctl_ok(ctl)) return DUCHESS_EINVAL;
-  if (policy->policy_kind != DUCHESS_POLICY_DUCHESS || policy->pred_source != DUCHESS_PRED_DEVICE)
-    return DUCHESS_EINVAL;
-  if (!acts || !wg || !c1 || !out_logit || !out_prob || T < 1 || H < 1) return DUCHESS_EINVAL;
-  if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
-  if (policy->n_layers < 1) return DUCHESS_EINVAL;
-  if (state->n_slots == 0) return DUCHESS_OK;
-  const bool bf16 = dtype == DUCHESS_BF16;
-  const int esz = bf16 ? 2 : 4;
-  const int64_t row_bytes = int64_t(H) * esz;
-  // TMA bulk copies: 16-byte aligned token rows.
-  if ((reinterpret_cast<uintptr_t>(acts) % 16) || (row_bytes % 16) || ((row_stride * esz) % 16) ||
-      ((layer_stride * esz) % 16) || ((token_stride * esz) % 16) || row_bytes > 4 * kTmaStageTarget ||
-      (reinterpret_cast<uintptr_t>(wg) % 16))
-    return DUCHESS_EINVAL;
-  ScoreArgs a{};
-  a.acts = static_cast<const char*>(acts);
-  a.row_stride = row_stride;
-  a.layer_stride = layer_stride;
-  a.token_stride = token_stride;
-  a.n_units = int64_t(state->n_slots) * policy->max_branches * policy->n_layers;
-  a.L = policy->n_layers;
-  a.T = T;
-  a.H = H;
-  a.nsplit = 1;
-  a.chunk = H;
-  a.wg = wg;
-  a.c1 = c1;
-  a.out_logit = out_logit;
-  a.out_prob = out_prob;
-  TmaArgs t{};
-  t.row_bytes = int(row_bytes);
-  t.contiguous = token_stride == H;
-  // two token rows per bulk copy, as the stand-alone scorer (18.8 -> 20.3 M/s at C2)
-  static const int step_target = [] { const char* e = getenv("DUCHESS_STEP_STAGE"); int v = e ? atoi(e) : kScoreStageTarget; return v < 4096 ? 4096 : v; }();
-  t.tokens_per_stage = int(row_bytes >= step_target ? 1 : step_target / row_bytes);
-  if (t.tokens_per_stage > T) t.tokens_per_stage = T;
-  const int stage_bytes = t.tokens_per_stage * t.row_bytes;
-  // Two CTAs per SM: 2 x (ring + static shared (slot cache, barriers) + 1 KB
-  // reserved) within the 228 KB of an SM.
-  const int static_bytes = int(sizeof(SlotCache)) + 1024;
-  t.stages = (115712 - static_bytes) / stage_bytes;
-  if (const char* e = getenv("DUCHESS_STEP_STAGES")) { const int v = atoi(e); if (v >= 2 && v < t.stages) t.stages = v; }
-  if (t.stages > 32) t.stages = 32;
-  if (t.stages < 2) return DUCHESS_EINVAL;
-  const int nvec = int(row_bytes / 16);
-  int vpt = 1;
-  while (vpt * kTmaCons < nvec) vpt <<= 1;
-  if (vpt > 8) return DUCHESS_EINVAL;
-  const size_t smem = size_t(t.stages) * stage_bytes;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  auto go = [&](auto tag_bf16) -> cudaError_t {
-    constexpr bool B = decltype(tag_bf16)::value;
-    switch (vpt) {
-      case 1: return launch_step<B, 1>(*policy, *workload, *state, *ctl, a, t, smem, s);
-      case 2: return launch_step<B, 2>(*policy, *workload, *state, *ctl, a, t, smem, s);
-      case 4: return launch_step<B, 4>(*policy, *workload, *state, *ctl, a, t, smem, s);
-      default: return launch_step<B, 8>(*policy, *workload, *state, *ctl, a, t, smem, s);
-    }
-  };
-  e = bf16 ? go(std::true_type{}) : go(std::false_type{});
-  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
-}
-
 extern "C" int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                                       const DuchessState* state, void* stream) {
   if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
@@ -1969,14 +1692,10 @@ extern "C" int duchess_baseline_round(const DuchessPolicy* policy, const Duchess
     return DUCHESS_EINVAL;
   if (state->n_slots == 0) return DUCHESS_OK;
   const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  DuchessPolicy pol = *policy;
-  DuchessWorkload w = *workload;
-  DuchessState st = *state;
-  void* args[] = {&pol, &w, &st};
-  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(baseline_kernel),
-                                                    dim3(grid), dim3(32 * kWarpsPerBlock), args,
-                                                    0, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  baseline_refill_kernel<<<grid, 32 * kWarpsPerBlock, 0, st>>>(*policy, *workload, *state);
+  baseline_kernel<<<grid, 32 * kWarpsPerBlock, 0, st>>>(*policy, *workload, *state);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
 extern "C" int duchess_branch_out_sample(const double* probs, int32_t n, double inv_temperature,

@@ -87,6 +87,39 @@ class PackedWorkload:
     struct: _lib.Workload
     branch_cap: int
     answer_cap: int
+    tmpl_off: np.ndarray | None = None   # host copy [P + 1] (queue records)
+    mt_index: np.ndarray | None = None   # host MT index word per request (None: device-seeded, 0)
+
+    def with_queue(self, queue, cycle: bool) -> "PackedWorkload":
+        """The same (shared, read-only) tables with another service queue:
+        request shards of one pool (several engines on one GPU, or one rank's
+        share of the workload) pack the traces once."""
+        dev = self.tensors["tmpl_off"].device
+        tens = dict(self.tensors)
+        tens.update(_queue_tensors(queue, self.tmpl_off, self.mt_index, dev))
+        st = _lib.Workload()
+        st.n_requests = self.struct.n_requests
+        st.queue_len = len(queue)
+        st.cycle = 1 if cycle else 0
+        for k, v in tens.items():
+            setattr(st, k, v.data_ptr())
+        return PackedWorkload(self.answers, self.n_templates, tens, st, self.branch_cap,
+                              self.answer_cap, self.tmpl_off, self.mt_index)
+
+
+def _queue_tensors(queue, tmpl_off, mt_index, device) -> dict:
+    """Service queue + per position (pool index, template base, template
+    count, MT index word) records: one 16-byte load per refill."""
+    q = np.asarray(list(queue), dtype=np.int64).reshape(-1)
+    out = {"queue": torch.tensor(q.astype(np.int32) if len(q) else np.zeros(1, np.int32),
+                                 dtype=torch.int32, device=device)}
+    if len(q):
+        toff = np.asarray(tmpl_off, dtype=np.int64)
+        idx = np.zeros(len(q), dtype=np.int64) if mt_index is None else mt_index[q]
+        rec = np.stack([q, toff[q], toff[q + 1] - toff[q], idx.astype(np.int64)],
+                       axis=1).astype(np.int32)
+        out["queue_rec"] = torch.from_numpy(np.ascontiguousarray(rec).reshape(-1)).to(device)
+    return out
 
 
 def intern_answers(trace) -> list[str]:
@@ -146,19 +179,13 @@ def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkloa
                     if mt_words is None else
                     torch.from_numpy(np.ascontiguousarray(mt_words, dtype=np.uint32).view(np.int32))
                     .reshape(-1).to(device)),
-        "queue": i32(queue),
     }
-    # per queue position: (pool index, template base, template count, MT index word)
-    q = np.asarray(queue, dtype=np.int64).reshape(-1)
-    if len(q):
-        toff = np.asarray(tmpl_off, dtype=np.int64)
-        if mt_words is None:                 # device-seeded states are pre-twisted: index 0
-            idx = np.zeros(len(q), dtype=np.int64)
-        else:
-            idx = np.ascontiguousarray(mt_words, dtype=np.uint32).reshape(-1, _lib.MT_WORDS)[q, -1]
-        rec = np.stack([q, toff[q], toff[q + 1] - toff[q], idx.astype(np.int64)],
-                       axis=1).astype(np.int32)
-        tens["queue_rec"] = torch.from_numpy(np.ascontiguousarray(rec).reshape(-1)).to(device)
+    # device-seeded states are pre-twisted: index 0
+    mt_index = (None if mt_words is None else
+                np.ascontiguousarray(mt_words, dtype=np.uint32).reshape(-1, _lib.MT_WORDS)[:, -1]
+                .astype(np.int64))
+    toff_h = np.asarray(tmpl_off, dtype=np.int64)
+    tens.update(_queue_tensors(queue, toff_h, mt_index, device))
     st = _lib.Workload()
     st.n_requests = P
     st.queue_len = len(queue)
@@ -167,7 +194,48 @@ def pack_workload(traces, mt_words, queue, cycle: bool, device) -> PackedWorkloa
         setattr(st, k, v.data_ptr())
     n_t = np.diff(np.asarray(tmpl_off))
     return PackedWorkload(answers, n_t, tens, st, int(max(n_t.max() if P else 1, 1)),
-                          int(max(len(a) for a in answers) if P else 1))
+                          int(max(len(a) for a in answers) if P else 1), toff_h, mt_index)
+
+
+def pack_pool(traces, seeds, device, queue=None, cycle: bool = False) -> PackedWorkload:
+    """Pack a pool of traces with their per-request RNG streams: int seeds are
+    expanded to random.Random(seed) states on the device (duchess_mt_seed),
+    random.Random objects are copied from the host."""
+    P = len(traces)
+    queue = list(range(P)) if queue is None else list(queue)
+    int_seeds = P > 0 and all(isinstance(s, (int, np.integer)) and not isinstance(s, bool)
+                              and 0 <= int(s) < (1 << 64) for s in seeds)
+    if int_seeds:
+        mt = None
+    else:
+        mt = (np.stack([pretwist(mt_state_words(s)) for s in seeds]) if P
+              else np.zeros((0, 625), np.uint32))
+    wl = pack_workload(traces, mt, queue, cycle, device)
+    if int_seeds:
+        seed_states(seeds, wl.tensors["mt_init"])
+    return wl
+
+
+_KINDS = {_lib.ACT_CONTINUE: "continue", _lib.ACT_TERMINATE: "terminate",
+          _lib.ACT_BRANCH_OUT: "branch_out"}
+
+
+def decode_round(round_rec: np.ndarray, actions: np.ndarray, R: int, C: int):
+    """(pool index, RoundReport-tuple) per slot that ran a round, from host
+    copies of DuchessState.round_rec [R*REC_WORDS] and actions [R*2C*3]."""
+    rec = np.asarray(round_rec).reshape(R, _lib.REC_WORDS)
+    acts = np.asarray(actions).reshape(R, 2 * C, 3)
+    out = []
+    for r in np.nonzero(rec[:, _lib.REC_ROUND])[0]:
+        rr = rec[r]
+        n = int(rr[_lib.REC_NACTIONS])
+        actions_r = [(_KINDS[int(a[0])], int(a[1]), None if a[2] < 0 else int(a[2]))
+                     for a in acts[r, :n]]
+        out.append((int(rr[_lib.REC_REQ]),
+                    (int(rr[_lib.REC_ROUND]), int(rr[_lib.REC_DECODING]),
+                     int(rr[_lib.REC_MAX_CHUNK]), int(rr[_lib.REC_DECODE]),
+                     int(rr[_lib.REC_PROBES]), actions_r, bool(rr[_lib.REC_DONE]))))
+    return out
 
 
 class BatchedDuchess:
@@ -184,7 +252,8 @@ class BatchedDuchess:
     def __init__(self, traces, config, seeds, n_slots: int | None = None, *,
                  pred_source: int = _lib.PRED_TRACE, rho: float = 1.0, queue=None,
                  cycle: bool = False, n_layers: int = 1, combine: int = 0,
-                 policy: str = "duchess", device: str | torch.device = "cuda"):
+                 policy: str = "duchess", device: str | torch.device = "cuda",
+                 packed: PackedWorkload | None = None):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.device = torch.device(device)
@@ -197,17 +266,12 @@ class BatchedDuchess:
         self.P, self.C = P, c
         self.R = n_slots if n_slots is not None else P
         queue = list(range(P)) if queue is None else list(queue)
-        int_seeds = P > 0 and all(isinstance(s, (int, np.integer)) and not isinstance(s, bool)
-                                  and 0 <= int(s) < (1 << 64) for s in seeds)
-        if int_seeds:      # random.Random(seed) states built on the device (duchess_mt_seed)
-            mt = None
+        if packed is not None:         # shared tables of one pool (pack_pool), own queue
+            if packed.struct.n_requests != P:
+                raise ValueError("packed workload does not match the traces")
+            self.wl = packed.with_queue(queue, cycle)
         else:
-            mt = (np.stack([pretwist(mt_state_words(s)) for s in seeds]) if P
-                  else np.zeros((0, 625), np.uint32))
-        self.wl = pack_workload(traces, mt, queue, cycle, self.device)
-        if int_seeds:
-            seed_states(seeds, self.wl.tensors["mt_init"])
-
+            self.wl = pack_pool(traces, seeds, self.device, queue=queue, cycle=cycle)
         pol = _lib.Policy()
         pol.max_branches = c
         pol.interval_tokens = int(config.interval_tokens)
@@ -312,62 +376,6 @@ class BatchedDuchess:
                                           p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_round")
 
-    # ------------------------------------------------------------------
-    # Fused round: K1 scoring + decide + advance in one persistent launch.
-    def begin_fused(self, stream=None) -> None:
-        """Allocate the fused-round lists / ready queues and run refill +
-        phase 1 of the first round (duchess_step_begin). Only for
-        pred_source == PRED_DEVICE; call once, then step_fused() per round."""
-        if self.policy.pred_source != _lib.PRED_DEVICE or self.policy_name != "duchess":
-            raise ValueError("the fused round needs the DUCHESS policy with device probabilities")
-        R, C, dev = self.R, self.C, self.device
-        x = {"rows": torch.zeros(2 * R * C, dtype=torch.int32, device=dev),
-             "reqs": torch.zeros(2 * max(R, 1), dtype=torch.int32, device=dev),
-             "idle": torch.zeros(max(R, 1), dtype=torch.int32, device=dev),
-             "ctl": torch.zeros(_lib.STEP_CTL_WORDS, dtype=torch.int32, device=dev)}
-        sc = _lib.StepCtl()
-        for k, v in x.items():
-            setattr(sc, k, v.data_ptr())
-        self.fx, self.step_ctl = x, sc
-        _lib.check(self.lib.duchess_step_begin(self.policy, self.wl.struct, self.state, sc,
-                                               self.probs.data_ptr(), _lib.stream_handle(stream)),
-                   "duchess_step_begin")
-
-    def step_fused(self, acts: torch.Tensor, bank, out_logit: torch.Tensor, stream=None) -> None:
-        """One fused round (duchess_step). acts: [R*C, L, T, H] bf16/fp32
-        activation windows by branch slot (row r*C + slot); bank: ProbeBank
-        with L probes of width H; out_logit: [R*C*L] fp32. Probabilities land
-        in self.probs; round_reports() then describe the round just decided."""
-        if not hasattr(self, "step_ctl"):
-            raise RuntimeError("call begin_fused() first")
-        _lib.require_cuda(acts)
-        if acts.dim() != 4 or acts.shape[0] != self.R * self.C:
-            raise ValueError("acts must be [R*C, L, T, H]")
-        rows, L, T, H = acts.shape
-        if L != self.policy.n_layers or L != bank.L or H != bank.H:
-            raise ValueError(f"activation shape (L={L}, H={H}) does not match the probe bank "
-                             f"(L={bank.L}, H={bank.H}) / engine layers ({self.policy.n_layers})")
-        if acts.stride(3) != 1:
-            raise ValueError("hidden dimension must be contiguous")
-        dtype = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32}.get(acts.dtype)
-        if dtype is None:
-            raise ValueError("activations must be bf16 or fp32")
-        if out_logit.numel() < rows * L or out_logit.dtype != torch.float32:
-            raise ValueError("out_logit must be fp32 with R*C*L entries")
-        st = acts.stride()
-        _lib.check(self.lib.duchess_step(
-            self.policy, self.wl.struct, self.state, self.step_ctl, acts.data_ptr(), dtype, T, H,
-            st[0], st[1], st[2], bank.wg.data_ptr(), bank.c1.data_ptr(), out_logit.data_ptr(),
-            self.probs.data_ptr(), _lib.stream_handle(stream)), "duchess_step")
-
-    def fused_rows(self):
-        """(row list, count) of the survivors the next step_fused() will score."""
-        tag = int(self.fx["ctl"][_lib.STEP_CTL_TAG])
-        par = tag & 1
-        n = int(self.fx["ctl"][_lib.STEP_CTL_COUNT + par])
-        RC = self.R * self.C
-        return self.fx["rows"][par * RC: par * RC + n], n
-
     def upload_survivors(self, host_acts: torch.Tensor, dev_acts: torch.Tensor,
                          stream=None) -> None:
         """Copy only the survivor rows of the round in flight (the active list)
@@ -428,23 +436,8 @@ class BatchedDuchess:
         """Per-slot (pool index, RoundReport-tuple) of the latest round:
         (round_index, decoding, max_chunk, decode_tokens, probes,
         [(kind, branch_id, source_or_None)], done)."""
-        rec = self.t["round_rec"].view(self.R, _lib.REC_WORDS).cpu().numpy()
-        acts = self.t["actions"].view(self.R, 2 * self.C, 3).cpu().numpy()
-        kinds = {_lib.ACT_CONTINUE: "continue", _lib.ACT_TERMINATE: "terminate",
-                 _lib.ACT_BRANCH_OUT: "branch_out"}
-        out = []
-        for r in range(self.R):
-            rr = rec[r]
-            if rr[_lib.REC_ROUND] == 0:
-                continue
-            n = int(rr[_lib.REC_NACTIONS])
-            actions = [(kinds[int(a[0])], int(a[1]), None if a[2] < 0 else int(a[2]))
-                       for a in acts[r, :n]]
-            out.append((int(rr[_lib.REC_REQ]),
-                        (int(rr[_lib.REC_ROUND]), int(rr[_lib.REC_DECODING]),
-                         int(rr[_lib.REC_MAX_CHUNK]), int(rr[_lib.REC_DECODE]),
-                         int(rr[_lib.REC_PROBES]), actions, bool(rr[_lib.REC_DONE]))))
-        return out
+        return decode_round(self.t["round_rec"].cpu().numpy(), self.t["actions"].cpu().numpy(),
+                            self.R, self.C)
 
     def outcomes(self):
         """Per pool index: None (unfinished) or dict(tally, final, reason,

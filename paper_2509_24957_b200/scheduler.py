@@ -61,12 +61,31 @@ class QueueEntry:
 
 
 def pack_keys(levels, arrivals, orders) -> np.ndarray:
-    lv = np.asarray(levels, dtype=np.uint64)
-    ar = np.asarray(arrivals, dtype=np.uint64)
-    od = np.asarray(orders, dtype=np.uint64)
-    if (ar >= (1 << _ARRIVAL_BITS)).any() or (od >= (1 << _ORDER_BITS)).any() or (lv > 7).any():
-        raise ValueError("key field out of range (level < 8, arrival < 2^40 ms, order < 2^21)")
-    return (lv << np.uint64(61)) | (ar << np.uint64(_ORDER_BITS)) | od
+    """64-bit sort keys ordering like the tuples (level, arrival, order)
+    (scheduler.py:84-90). Fast path: level < 8, arrival < 2^40 ms,
+    order < 2^21 packed directly; otherwise each field is replaced by its
+    dense rank (order-preserving) and packed with just enough bits, so any
+    integer fields sort exactly as the reference's tuples."""
+    lv = np.asarray([int(x) for x in levels], dtype=object)
+    ar = np.asarray([int(x) for x in arrivals], dtype=object)
+    od = np.asarray([int(x) for x in orders], dtype=object)
+    n = len(lv)
+    if n == 0:
+        return np.zeros(0, dtype=np.uint64)
+    if (min(lv) >= 0 and max(lv) <= 7 and min(ar) >= 0 and max(ar) < (1 << _ARRIVAL_BITS)
+            and min(od) >= 0 and max(od) < (1 << _ORDER_BITS)):
+        return ((lv.astype(np.uint64) << np.uint64(61)) | (ar.astype(np.uint64) << np.uint64(_ORDER_BITS))
+                | od.astype(np.uint64))
+    fields, bits = [], []
+    for f in (lv, ar, od):
+        uniq = sorted(set(f.tolist()))
+        rank = {v: i for i, v in enumerate(uniq)}
+        fields.append(np.asarray([rank[v] for v in f.tolist()], dtype=np.uint64))
+        bits.append(max(1, (len(uniq) - 1).bit_length()))
+    if sum(bits) > 64:
+        raise ValueError("queue snapshot too large for 64-bit difficulty keys")
+    return ((fields[0] << np.uint64(bits[1] + bits[2])) | (fields[1] << np.uint64(bits[2]))
+            | fields[2])
 
 
 def device_sort(keys: np.ndarray, device="cuda") -> list:

@@ -1,0 +1,175 @@
+"""The serving loop: probe scoring + orchestration rounds over request shards.
+
+One GPU serves a pool of requests through ``S`` independent request shards
+(``BatchedDuchess`` engines over one packed pool, each with its own slice of
+the service queue), each stepping on its own CUDA stream. A round of a shard
+is two launches:
+
+  ``Scorer.score_active``  K1: pooled LayerNorm + linear probe(s) over the
+                           survivors of the round in flight (the device-side
+                           active list), probabilities by branch slot;
+  ``BatchedDuchess.round`` K2: decide the round (orchestrator.py:357-402),
+                           refill finished slots from the queue and advance
+                           every slot into the next round (:344-355).
+
+Requests never interact (reference SPEC.md:295), so shards are exact: each
+request's rounds depend only on its own state, RNG stream and activation
+windows, not on which shard or slot serves it. Two shards on one GPU keep one
+shard's latency-bound round kernel beside the other shard's HBM-bound scorer.
+The same class is the per-rank engine of the multi-GPU path
+(``distributed.run_sharded``). This is the loop ``bench.py`` times.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .engine import BatchedDuchess, pack_pool
+from .probe import Scorer, fill_windows
+
+
+class ShardedEngine:
+    """S request shards of one request pool on one GPU.
+
+    traces / config / seeds: the pool (RequestTrace-likes, OrchestratorConfig,
+    per-request seeds as for DuchessRun's rng). bank: ProbeBank (L probes of
+    width H). n_slots: request slots in total (split evenly over the shards).
+    queue: service order of pool indices (default: pool order); shard k takes
+    queue[k::S]. T, dtype: the activation window per branch-step.
+    """
+
+    def __init__(self, traces, config, seeds, bank, *, n_slots: int, shards: int = 2,
+                 queue=None, cycle: bool = False, T: int = 1, dtype=torch.bfloat16,
+                 device="cuda", combine: int | None = None, n_buffers: int = 1,
+                 packed=None):
+        _lib.require_cuda()
+        if shards < 1 or n_slots % shards:
+            raise ValueError(f"{shards} shards must evenly divide the {n_slots} request slots")
+        self.device = torch.device(device)
+        self.bank = bank
+        self.S, self.L, self.T, self.H = shards, bank.L, T, bank.H
+        self.dtype = dtype
+        self.C = int(config.max_branches)
+        self.Rs = n_slots // shards
+        self.rows = self.Rs * self.C
+        P = len(traces)
+        queue = list(range(P)) if queue is None else list(queue)
+        self.packed = packed if packed is not None else pack_pool(traces, seeds, self.device)
+        combine = (1 if bank.L > 1 else 0) if combine is None else combine
+        self.shards = []
+        for k in range(shards):
+            eng = BatchedDuchess(traces, config, seeds, n_slots=self.Rs,
+                                 pred_source=_lib.PRED_DEVICE, queue=queue[k::shards],
+                                 cycle=cycle, n_layers=bank.L, combine=combine,
+                                 device=self.device, packed=self.packed)
+            acts = [torch.zeros((self.rows, bank.L, T, bank.H), dtype=dtype, device=self.device)
+                    for _ in range(n_buffers)]
+            self.shards.append(dict(
+                eng=eng, scorer=Scorer(bank, self.rows * bank.L), acts=acts,
+                logit=torch.zeros((self.rows, bank.L), dtype=torch.float32, device=self.device),
+                stream=torch.cuda.Stream(self.device), ev=[]))
+        self.started = False
+
+    @property
+    def engines(self):
+        return [sh["eng"] for sh in self.shards]
+
+    # ------------------------------------------------------------------
+    def fork(self):
+        """Shard streams wait for the caller's (current) stream."""
+        cur = torch.cuda.current_stream(self.device)
+        for sh in self.shards:
+            sh["stream"].wait_stream(cur)
+
+    def join(self):
+        """The caller's (current) stream waits for every shard."""
+        cur = torch.cuda.current_stream(self.device)
+        for sh in self.shards:
+            cur.wait_stream(sh["stream"])
+
+    def begin(self):
+        """Refill every slot and run phase 1 of the first round."""
+        self.fork()
+        for sh in self.shards:
+            with torch.cuda.stream(sh["stream"]):
+                sh["eng"].advance()
+        self.started = True
+
+    def step(self, i: int = 0, *, fill=None, timed: bool = False, after_round=None):
+        """One round of every shard, each on its stream (no host sync).
+
+        i: round counter (selects activation buffer i % n_buffers).
+        fill(k, eng, acts): optional window source, called on shard k's stream
+            before scoring (e.g. the keyed synthetic fill of the round's
+            survivors, or a host upload); by default the buffer is used as is.
+        timed: bracket the scorer launch with CUDA events on the shard stream.
+        after_round(k, eng): optional hook on the shard stream after round().
+        """
+        if not self.started:
+            self.begin()
+        for k, sh in enumerate(self.shards):
+            st = sh["stream"]
+            with torch.cuda.stream(st):
+                eng = sh["eng"]
+                acts = sh["acts"][i % len(sh["acts"])]
+                if fill is not None:
+                    fill(k, eng, acts)
+                if timed:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                sh["scorer"].score_active(acts, sh["logit"], eng.probs.view(self.rows, self.L),
+                                          eng)
+                if timed:
+                    e1.record(st)
+                    sh["ev"].append((e0, e1))
+                eng.round()
+                if after_round is not None:
+                    after_round(k, eng)
+
+    def run(self, max_rounds: int = 100000, fill=None, after_round=None) -> int:
+        """Serve the queues to completion (non-cycling pools). Returns rounds."""
+        if not self.started:
+            self.begin()
+        for i in range(max_rounds):
+            self.step(i, fill=fill, after_round=after_round)
+            if i % 8 == 7:
+                self.join()
+                if self.all_done():
+                    return i + 1
+        self.join()
+        if not self.all_done():
+            raise RuntimeError(f"requests still running after {max_rounds} rounds")
+        return max_rounds
+
+    # ------------------------------------------------------------------
+    def all_done(self) -> bool:
+        torch.cuda.synchronize(self.device)
+        return all(sh["eng"].all_done() for sh in self.shards)
+
+    def counters(self):
+        return sum(sh["eng"].counters() for sh in self.shards)
+
+    def outcomes(self) -> dict:
+        """{pool index: outcome dict} over every shard (finished requests)."""
+        out = {}
+        for sh in self.shards:
+            for p, o in enumerate(sh["eng"].outcomes()):
+                if o is not None:
+                    out[p] = o
+        return out
+
+    def scorer_events(self):
+        return [ev for sh in self.shards for ev in sh["ev"]]
+
+
+def keyed_fill(seed: int):
+    """Window source keyed by (pool request, template, position): the
+    synthetic stand-in for the LLM's activations. oracle/activations.py
+    regenerates the same windows bit for bit on the CPU, and a request's
+    windows do not depend on its slot, shard or rank."""
+    def fill(_k, eng, acts):
+        t = eng.t
+        fill_windows(acts, seed, t["row_req"], t["row_tmpl"], t["row_pos"], t["row_mask"])
+    return fill

@@ -21,17 +21,27 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("config", ["c2", "c5"])
-def test_bench_two_ranks_prints_one_aggregate_line(config):
+@pytest.mark.parametrize("config,extra", [("c3", ["--slots", "64"]), ("c2", []),
+                                          ("c5", [])])
+def test_bench_two_ranks_prints_one_aggregate_line(config, extra):
+    """Strong scaling: the config's slots / pool (C3: 1024 requests, here 64
+    slots so two ranks fit one GPU) and C5's 4M rows are split over the ranks."""
     env = dict(os.environ, DUCHESS_BENCH_BACKEND="gloo")
+    if config == "c5":
+        env["DUCHESS_C5_ROWS"] = str(1 << 20)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--gpus", "2", "--config", config, "--steps", "3", "--warmup", "3",
-           "--e2e-steps", "2", "--no-cpu-baseline"]
+           "--e2e-steps", "2", "--no-cpu-baseline"] + extra
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["steps"] == 3 and out["value"] > 0
-    assert out["scaling"] == "weak" and out["gpu_launches"] > 0
+    assert out["scaling"] == "strong" and out["gpu_launches"] > 0
+    if config == "c5":
+        assert out["config"]["rows"] == 1 << 20 and out["config"]["rows_per_gpu"] == 1 << 19
+        assert out["allreduce"]["backend"] == "gloo"
+    else:
+        assert out["config"]["slots_per_gpu"] * 2 == out["config"]["requests"]
