@@ -422,6 +422,250 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_kernel(ScoreArg
   }
 }
 
+// Last-token windows, bulk-copy variant (default). Same per-window arithmetic
+// as score_rows_kernel (warp per window, two-pass LN statistics on registers),
+// restructured around the memory pipe:
+//  * each warp owns one shared-memory slot that a single cp.async.bulk fills
+//    with its NEXT window: right after the warp has copied window k from the
+//    slot into registers, lane 0 refills the slot with window k+1, so one
+//    window per warp is in flight for the whole time the warp pools, reduces
+//    and scores window k;
+//  * a CTA scores one probe layer (CTA b: layer b % L), so only that layer's
+//    folded weights (H floats) sit in shared memory and the rest of the 227 KB
+//    holds slots: 16 warps x one 10 KB window in flight per SM at H = 5120;
+//  * a warp's windows are taken in batches of 32: lane i holds the row of the
+//    batch's window i (one list load per lane per batch, fetched a batch ahead)
+//    and, once scored, its LN sums, so list loads and the fp64 sigmoid run once
+//    per 32 windows spread over the lanes, not on the per-window chain;
+//  * pass 2 runs on element pairs: two FHADD produce c = x - mean into an
+//    aligned register pair, then {qq} += c*c and {d} += w*c are packed FFMA2.
+constexpr int kBulkSlotAlign = 128;
+template <bool BF16, int NV, bool FULL>
+__global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_bulk_kernel(ScoreArgs a, TmaArgs t,
+                                                                          int wbytes, int slot_bytes) {
+  constexpr int VEC = BF16 ? 8 : 4;
+  constexpr int ESZ = BF16 ? 2 : 4;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[kRowsWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int nvec = t.row_bytes / 16;
+  const int l = int(blockIdx.x % unsigned(a.L));                 // this CTA's probe layer
+  const int64_t grp = blockIdx.x / unsigned(a.L), ngrp = gridDim.x / unsigned(a.L);
+  float* wsm = reinterpret_cast<float*>(smem);
+  char* slot = smem + wbytes + warp * slot_bytes;
+  {
+    // the layer's weights as VEC/4 planes (float4 q of vector v at plane q,
+    // index v), so a warp's 128-bit weight reads are contiguous (conflict-free)
+    const int per_layer = a.H / 4;
+    const float4* src = reinterpret_cast<const float4*>(a.wg) + int64_t(l) * per_layer;
+    for (int k = threadIdx.x; k < per_layer; k += blockDim.x) {
+      const int v = k / (VEC / 4), q = k - v * (VEC / 4);
+      reinterpret_cast<float4*>(wsm)[q * nvec + v] = __ldg(src + k);
+    }
+    if (lane == 0) {
+      mbar_init(&bar[warp], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  if (t.row_par) {
+    const int par = *t.row_par;
+    t.row_list += par * t.list_stride;
+    t.row_count += par;
+  }
+  const int64_t n_rows = t.row_list ? int64_t(*t.row_count) : a.n_units / a.L;
+  const int64_t nw = ngrp * nwarps;                 // warps scoring this layer
+  const int64_t bstride = 32 * nw;
+  const uint64_t pol = evict_first_policy();
+  // entry r of the warp's sequence r = gw + k * nw (list entry or masked row)
+  auto load_batch = [&](int64_t base, int64_t& row) -> unsigned {
+    const int64_t r = base + int64_t(lane) * nw;
+    row = 0;
+    bool ok = r < n_rows;
+    if (ok) {
+      if (t.row_list) {
+        row = t.row_list[r];
+      } else {
+        row = r;
+        ok = a.mask == nullptr || a.mask[r] != 0;
+      }
+    }
+    return __ballot_sync(0xffffffffu, ok);
+  };
+  auto refill = [&](int64_t row) {
+    mbar_expect_tx(&bar[warp], uint32_t(t.row_bytes));
+    bulk_g2s(slot, a.acts + (row * a.row_stride + int64_t(l) * a.layer_stride) * ESZ,
+             uint32_t(t.row_bytes), &bar[warp], pol);
+  };
+  int64_t base = grp * nwarps + warp;
+  int64_t rowc, rown;
+  unsigned mc = load_batch(base, rowc);
+  unsigned mn = load_batch(base + bstride, rown);
+  auto shift = [&]() {
+    base += bstride;
+    rowc = rown;
+    mc = mn;
+    mn = load_batch(base + bstride, rown);
+  };
+  while (mc == 0 && base < n_rows) shift();         // (mask path) skip empty batches
+  int i = mc ? __ffs(mc) - 1 : 0;
+  if (mc) {
+    const int64_t r0 = __shfl_sync(0xffffffffu, rowc, i);
+    if (lane == 0) refill(r0);
+  }
+  float my_q = 0.f, my_d = 0.f;
+  uint32_t ph = 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(slot);
+  const float c1 = a.c1[l];
+  while (mc) {
+    const unsigned rest = mc & ~((2u << i) - 1u);     // later windows of this batch
+    bool have_next = true;
+    int64_t nrow = 0;
+    if (rest) nrow = __shfl_sync(0xffffffffu, rowc, __ffs(rest) - 1);
+    else if (mn) nrow = __shfl_sync(0xffffffffu, rown, __ffs(mn) - 1);
+    else have_next = false;
+    mbar_wait(&bar[warp], ph);
+    ph ^= 1u;
+    uint4 xv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int v = j * 32 + lane;
+      xv[j] = (FULL || v < nvec) ? s4[v] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncwarp();
+    if (lane == 0 && have_next) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // slot reads before the refill
+      refill(nrow);
+    }
+    // pass 1: eight independent chains (FHADD straight from the packed pair)
+    float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w4[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+      if constexpr (BF16) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) add_bf16x2_f32(s8[2 * e], s8[2 * e + 1], w4[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s8[e] = __fadd_rn(s8[e], __uint_as_float(w4[e]));
+      }
+    }
+#pragma unroll
+    for (int e = 1; e < 8; e <<= 1)
+#pragma unroll
+      for (int q = 0; q < 8; q += 2 * e) s8[q] = __fadd_rn(s8[q], s8[q + e]);
+    const float s1 = warp_sum(s8[0]);
+    const float mean = __fdiv_rn(s1, float(a.H));
+    // pass 2 on element pairs
+    unsigned long long qa = 0ull, qb = 0ull, da = 0ull, db = 0ull;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int v = j * 32 + lane;
+      if (FULL || v < nvec) {
+        const uint32_t w4[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+        const float4* wp = reinterpret_cast<const float4*>(wsm) + v;
+#pragma unroll
+        for (int q = 0; q < VEC / 4; ++q) {
+          const float4 t4 = wp[q * nvec];
+          float c0, c1_, c2, c3;
+          if constexpr (BF16) {
+            c0 = -mean; c1_ = -mean; c2 = -mean; c3 = -mean;
+            add_bf16x2_f32(c0, c1_, w4[2 * q]);
+            add_bf16x2_f32(c2, c3, w4[2 * q + 1]);
+          } else {
+            c0 = __fsub_rn(__uint_as_float(w4[0]), mean);
+            c1_ = __fsub_rn(__uint_as_float(w4[1]), mean);
+            c2 = __fsub_rn(__uint_as_float(w4[2]), mean);
+            c3 = __fsub_rn(__uint_as_float(w4[3]), mean);
+          }
+          const unsigned long long cA = pack_f32x2(c0, c1_), cB = pack_f32x2(c2, c3);
+          fma_f32x2(qa, cA, cA);
+          fma_f32x2(qb, cB, cB);
+          fma_f32x2(da, cA, pack_f32x2(t4.x, t4.y));
+          fma_f32x2(db, cB, pack_f32x2(t4.z, t4.w));
+        }
+      }
+    }
+    float q0, q1, q2, q3, d0, d1, d2, d3;
+    unpack_f32x2(qa, q0, q1);
+    unpack_f32x2(qb, q2, q3);
+    unpack_f32x2(da, d0, d1);
+    unpack_f32x2(db, d2, d3);
+    const float qq = warp_sum(__fadd_rn(__fadd_rn(q0, q1), __fadd_rn(q2, q3)));
+    const float d = warp_sum(__fadd_rn(__fadd_rn(d0, d1), __fadd_rn(d2, d3)));
+    if (lane == i) {               // the butterfly leaves the sums in every lane
+      my_q = qq;
+      my_d = d;
+    }
+    if (rest) {
+      i = __ffs(rest) - 1;
+      continue;
+    }
+    // batch complete: every lane finishes its own window (LN scale, logit, sigmoid)
+    if ((mc >> lane) & 1u) {
+      const float var = __fdiv_rn(my_q, float(a.H));
+      const float logit = __fadd_rn(__fdiv_rn(my_d, __fsqrt_rn(__fadd_rn(var, kLayerNormEps))), c1);
+      write_score(a, rowc * a.L + l, logit);
+    }
+    shift();
+    if (!have_next) {
+      while (mc == 0 && base < n_rows) shift();
+      if (mc) {
+        i = __ffs(mc) - 1;
+        const int64_t r0 = __shfl_sync(0xffffffffu, rowc, i);
+        if (lane == 0) refill(r0);
+      }
+    } else {
+      i = __ffs(mc) - 1;
+    }
+  }
+}
+
+// Shared-memory plan of score_rows_bulk_kernel: warps that fit beside the weights.
+static int rows_bulk_warps(int64_t wbytes, int64_t row_bytes, int smem_max, int& slot_bytes) {
+  slot_bytes = int((row_bytes + kBulkSlotAlign - 1) / kBulkSlotAlign * kBulkSlotAlign);
+  const int64_t room = int64_t(smem_max) - wbytes;
+  if (room < slot_bytes) return 0;
+  return int(room / slot_bytes < kRowsWarps ? room / slot_bytes : kRowsWarps);
+}
+
+template <bool BF16>
+static cudaError_t launch_rows_bulk(const ScoreArgs& a, const TmaArgs& t, int nv, int grid,
+                                    int nwarps, int slot_bytes, cudaStream_t s) {
+  const int wbytes = (a.H * int(sizeof(float)) + kBulkSlotAlign - 1) / kBulkSlotAlign * kBulkSlotAlign;
+  const size_t smem = size_t(wbytes) + size_t(nwarps) * slot_bytes;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nwarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, t, wbytes, slot_bytes);
+  };
+  const bool full = t.row_bytes == nv * 32 * 16;
+#define DUCHESS_BULK(NVV)                                                          \
+  case NVV:                                                                        \
+    if (full) go(score_rows_bulk_kernel<BF16, NVV, true>);                         \
+    else go(score_rows_bulk_kernel<BF16, NVV, false>);                             \
+    break;
+  switch (nv) {
+    DUCHESS_BULK(1) DUCHESS_BULK(2) DUCHESS_BULK(4) DUCHESS_BULK(8) DUCHESS_BULK(12)
+    DUCHESS_BULK(16) DUCHESS_BULK(20)
+    default: return cudaErrorInvalidValue;
+  }
+#undef DUCHESS_BULK
+  return cudaGetLastError();
+}
+
 template <bool BF16>
 static cudaError_t launch_rows(const ScoreArgs& a, const TmaArgs& t, int nv, int grid,
                                cudaStream_t s) {
@@ -617,19 +861,35 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     // peak vs 0.95-0.98 with one row per copy
     static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kScoreStageTarget; return v < 4096 ? 4096 : v; }();
     const int nvec_row = int(row_bytes / 16);
-    static const bool rows_ok = [] { const char* e = getenv("DUCHESS_K1_ROWS"); return !e || atoi(e) != 0; }();
+    // 0: no warp-per-window kernel, 1: register pipeline, 2 (default): bulk-copy slots
+    static const int rows_mode = [] { const char* e = getenv("DUCHESS_K1_ROWS"); return e ? atoi(e) : 2; }();
     // spill-free instantiations: bf16 rows up to 20 vectors per lane (H <= 5120),
     // fp32 up to 12 (H <= 1536); wider rows take the CTA kernel below
-    if (rows_ok && T == 1 && nvec_row <= (bf16 ? 20 : 12) * 32 &&
+    if (rows_mode != 0 && T == 1 && nvec_row <= (bf16 ? 20 : 12) * 32 &&
         (reinterpret_cast<uintptr_t>(wg) % 16) == 0) {
       int nv = (nvec_row + 31) / 32;
       nv = nv <= 2 ? nv : nv <= 4 ? 4 : nv <= 8 ? 8 : (nv + 3) / 4 * 4;
       a.nsplit = 1;
       a.chunk = H;
+      int slot_bytes = 0;
+      const int64_t wbytes = (int64_t(H) * 4 + kBulkSlotAlign - 1) / kBulkSlotAlign * kBulkSlotAlign;
+      const int bw = rows_mode == 2 && n_layers <= sm_count()
+                         ? rows_bulk_warps(wbytes, row_bytes, 226 * 1024, slot_bytes) : 0;
+      const int warps = bw >= 8 ? bw : kRowsWarps;
       int grid = sm_count();
-      if (!row_list && int64_t(grid) * kRowsWarps > a.n_units)
-        grid = int((a.n_units + kRowsWarps - 1) / kRowsWarps);
-      const cudaError_t e = bf16 ? launch_rows<true>(a, t, nv, grid, s) : launch_rows<false>(a, t, nv, grid, s);
+      if (bw >= 8) {            // one probe layer per CTA: a multiple of L CTAs
+        int64_t per_layer = grid / n_layers;
+        if (!row_list && per_layer * warps > n_rows) per_layer = (n_rows + warps - 1) / warps;
+        grid = int(per_layer * n_layers);
+      } else if (!row_list && int64_t(grid) * warps > a.n_units) {
+        grid = int((a.n_units + warps - 1) / warps);
+      }
+      cudaError_t e;
+      if (bw >= 8)
+        e = bf16 ? launch_rows_bulk<true>(a, t, nv, grid, bw, slot_bytes, s)
+                 : launch_rows_bulk<false>(a, t, nv, grid, bw, slot_bytes, s);
+      else
+        e = bf16 ? launch_rows<true>(a, t, nv, grid, s) : launch_rows<false>(a, t, nv, grid, s);
       return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
     }
     t.tokens_per_stage = int(row_bytes >= stage_target ? 1 : stage_target / row_bytes);

@@ -7,7 +7,8 @@ import numpy as np  # noqa: E402
 from paper_2509_24957_b200.probe import ProbeBank, Scorer, fill_windows  # noqa: E402
 
 CASES = [(16384, 4, 1, 5120, torch.bfloat16), (4096, 1, 1, 4096, torch.float32),
-         (64, 1, 1, 4096, torch.float32), (4096, 1, 32, 4096, torch.bfloat16)]
+         (64, 1, 1, 4096, torch.float32), (4096, 1, 32, 4096, torch.bfloat16),
+         (65536, 4, 1, 5120, torch.bfloat16), (65536, 1, 1, 4096, torch.bfloat16)]
 for rows, L, T, H, dt in [CASES[int(i)] for i in sys.argv[1:]] or CASES:
     rng = np.random.default_rng(0)
     bank = ProbeBank.from_linear(rng.normal(0, 0.02, (L, H)), np.zeros(L))
