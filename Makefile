@@ -7,7 +7,7 @@ PKG     := paper_2509_24957_b200
 SRC_DIR := $(PKG)/csrc
 OBJ_DIR := build/obj
 LIB     := $(PKG)/libduchess_b200.so
-SRCS    := score decide fork train mlp mlp_tc tc_linear bw
+SRCS    := score decide fork kv train mlp mlp_tc tc_linear bw
 OBJS    := $(addprefix $(OBJ_DIR)/,$(addsuffix .o,$(SRCS)))
 HDRS    := $(SRC_DIR)/common.cuh include/duchess_b200.h
 

@@ -18,6 +18,9 @@
  *   duchess_sort_difficulty  <- scheduler.py:60-96  next_request pops over a snapshot
  *   duchess_fork_cow         <- orchestrator.py:254-268 _spawn(offset_base=source.position)
  *                               executed on a paged KV block table (extension)
+ *   duchess_kv_round         <- the same forks (orchestrator.py:378-388) plus the
+ *                               branches' decode / end / cancel lifecycle, applied every
+ *                               round to a persistent paged KV cache (extension)
  *   duchess_lr_grad          <- probe training (absent in reference)
  *
  * Conventions: every pointer is caller-owned DEVICE memory unless stated;
@@ -369,6 +372,51 @@ int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const int32_t* gro
                      const int32_t* free_list, int32_t free_list_len, int32_t* free_cursor,
                      void* kv_pool, int64_t kv_bytes_per_token, int32_t block_tokens,
                      int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K3 in the round: persistent paged KV cache ---------------------------
+ * Block tables for every branch of every request slot ([R*Bmax] rows of
+ * max_blocks entries, global block ids, -1 = none). Slot r owns the arena of
+ * blocks [r*P, (r+1)*P) (P = blocks_per_slot) with a LIFO free stack and a
+ * high-water mark; the KV bytes of block b live at kv_pool + b * block_tokens *
+ * kv_bytes_per_token (kv_pool may be NULL: tables only). arena[r*4 + k]: k = 0
+ * stack top, 1 high-water mark, 2 owning pool index (-1 none), 3 peak blocks.
+ * All arrays zero-initialised except table (-1) and arena[r*4+2] (-1). */
+#define DUCHESS_KV_CNT_ALLOC 0       /* blocks allocated (appends + fork tails) */
+#define DUCHESS_KV_CNT_FREE 1        /* blocks returned (refcount 0, arena resets) */
+#define DUCHESS_KV_CNT_TAIL_BYTES 2  /* KV bytes copied for fork tails */
+#define DUCHESS_KV_CNT_OVERFLOW 3    /* blocks that did not fit the arena / table */
+#define DUCHESS_KV_N_COUNTERS 4
+
+typedef struct DuchessKV {
+  int32_t block_tokens;       /* tokens per block (16) */
+  int32_t blocks_per_slot;    /* P */
+  int32_t max_blocks;         /* table width: blocks per branch row */
+  int32_t _pad;
+  int64_t kv_bytes_per_token; /* bytes of KV per token (one layer slice: 2*8*128*2) */
+  int32_t* table;             /* [R*Bmax*max_blocks] */
+  int32_t* kv_tokens;         /* [R*Bmax] tokens each row's blocks cover */
+  int32_t* refcount;          /* [R*P] by global block id */
+  int32_t* free_stack;        /* [R*P] local block ids */
+  int32_t* arena;             /* [R*4] */
+  int32_t* jobs;              /* [R*C*4] this round's tail copies (src, dst, tokens, -) */
+  int32_t* job_count;         /* [R] */
+  char* kv_pool;              /* [R*P*block_tokens*kv_bytes_per_token] or NULL */
+  long long* counters;        /* [DUCHESS_KV_N_COUNTERS] */
+} DuchessKV;
+
+/* Apply the round just completed by duchess_round (or, before the first round,
+ * the engine's first duchess_advance) to the KV cache, per slot in fixed order:
+ * (1) the round's forks (DuchessState.forks, record order) whose child is still
+ * active: the child row gets the root's first prefix/block_tokens blocks
+ * (refcount += 1) and a fresh block with a copy of the root's partial tail
+ * (prefix % block_tokens tokens of KV bytes); (2) rows of branches that are no
+ * longer active release their blocks (refcount -= 1; 0 -> pushed on the free
+ * stack, by branch id then block index); (3) active rows grow to
+ * ceil(position / block_tokens) blocks (popped from the stack, then above the
+ * high-water mark). A slot whose request finished this round resets its arena
+ * first. Deterministic: a request's tables depend only on its own rounds. */
+int duchess_kv_round(const DuchessPolicy* policy, const DuchessState* state, const DuchessKV* kv,
+                     void* stream);
 
 /* ---- K4: logistic-regression gradient for probe training ------------------
  * grad[h] = inv_n * sum_i (sigmoid(x_i . w + w[H]) - y_i) x_ih, grad[H] = the

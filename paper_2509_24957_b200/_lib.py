@@ -79,6 +79,18 @@ class State(C.Structure):
         (name, C.c_void_p) for name in STATE_PTR_FIELDS]
 
 
+KV_CNT_ALLOC, KV_CNT_FREE, KV_CNT_TAIL_BYTES, KV_CNT_OVERFLOW = range(4)
+KV_N_COUNTERS = 4
+KV_PTR_FIELDS = ["table", "kv_tokens", "refcount", "free_stack", "arena", "jobs", "job_count",
+                 "kv_pool", "counters"]
+
+
+class KV(C.Structure):
+    _fields_ = [("block_tokens", C.c_int32), ("blocks_per_slot", C.c_int32),
+                ("max_blocks", C.c_int32), ("_pad", C.c_int32),
+                ("kv_bytes_per_token", C.c_int64)] + [(n, C.c_void_p) for n in KV_PTR_FIELDS]
+
+
 SYMBOLS = {
     # name: (restype, argtypes)
     "duchess_score_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
@@ -123,6 +135,8 @@ SYMBOLS = {
                                    C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "duchess_kv_round": (C.c_int, [C.POINTER(Policy), C.POINTER(State), C.POINTER(KV),
+                                   C.c_void_p]),
     "duchess_lr_grad_workspace_bytes": (C.c_size_t, [C.c_int32]),
     "duchess_lr_grad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_int32, C.c_float, C.c_void_p, C.c_void_p, C.c_size_t,

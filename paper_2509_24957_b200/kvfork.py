@@ -1,4 +1,11 @@
-"""Paged KV block table with copy-on-write branch-out (K3, ``duchess_fork_cow``).
+"""Paged KV block tables with copy-on-write branch-out (K3).
+
+``PagedKVCache`` (``duchess_kv_round``) is the in-the-round path: a persistent
+paged KV cache that follows an engine's rounds — the round's forks share the
+root's full blocks and copy its partial tail, ended / cancelled branches
+release their blocks, decoding branches grow — with one block arena per
+request slot. ``BlockTable`` (``duchess_fork_cow``) applies a batch of fork
+records to a flat table (the C4 branch-out-heavy trace).
 
 The reference's fork is ``_spawn(offset_base=source.position)``
 (orchestrator.py:254-268): the child resumes at the parent's position and the
@@ -63,3 +70,86 @@ class BlockTable:
         forks = engine.t["forks"].view(R, C, 4)
         counts = engine.t["round_rec"][_lib.REC_NFORKS:]
         self.fork(forks, counts, _lib.REC_WORDS, engine.wl.branch_cap, stream)
+
+
+class PagedKVCache:
+    """Persistent paged KV cache of an engine's request slots (K3 in the round).
+
+    engine: BatchedDuchess (its R slots x branch_cap branch ids are the table
+    rows). blocks_per_slot: the arena of each slot (default: room for
+    max_branches branches at the token cap, i.e. no overflow possible).
+    kv_bytes_per_token: KV bytes per token in the pool (0: tables only; one
+    Llama-3-8B layer slice is 2*8*128*2 = 4096). Call ``round()`` right after
+    every ``engine.round()`` and once after the engine's first ``advance()``.
+    """
+
+    def __init__(self, engine, *, block_tokens: int = 16, blocks_per_slot: int | None = None,
+                 kv_bytes_per_token: int = 0, max_blocks: int | None = None):
+        _lib.require_cuda()
+        self.lib = _lib.load()
+        self.engine = engine
+        dev = engine.device
+        self.device = dev
+        R, B, C = engine.R, engine.wl.branch_cap, engine.C
+        cap = int(engine.policy.token_cap)
+        nb = -(-cap // block_tokens) if max_blocks is None else int(max_blocks)
+        P = C * nb if blocks_per_slot is None else int(blocks_per_slot)
+        if block_tokens < 1 or P < 1 or nb < 1:
+            raise ValueError("block_tokens, blocks_per_slot and max_blocks must be positive")
+        if R * P >= 2 ** 31:
+            raise ValueError("R * blocks_per_slot must fit int32 block ids")
+        self.R, self.B, self.C, self.P, self.NB = R, B, C, P, nb
+        self.block_tokens, self.kv_bytes_per_token = block_tokens, int(kv_bytes_per_token)
+        i32 = dict(dtype=torch.int32, device=dev)
+        t = {"table": torch.full((R * B * nb,), -1, **i32),
+             "kv_tokens": torch.zeros(R * B, **i32),
+             "refcount": torch.zeros(R * P, **i32),
+             "free_stack": torch.zeros(R * P, **i32),
+             "arena": torch.zeros(R * 4, **i32),
+             "jobs": torch.zeros(R * C * 4, **i32),
+             "job_count": torch.zeros(R, **i32),
+             "counters": torch.zeros(_lib.KV_N_COUNTERS, dtype=torch.int64, device=dev)}
+        t["arena"].view(R, 4)[:, 2] = -1
+        if kv_bytes_per_token:
+            t["kv_pool"] = torch.zeros(R * P * block_tokens * self.kv_bytes_per_token,
+                                       dtype=torch.uint8, device=dev)
+        self.t = t
+        st = _lib.KV()
+        st.block_tokens, st.blocks_per_slot, st.max_blocks = block_tokens, P, nb
+        st.kv_bytes_per_token = self.kv_bytes_per_token
+        for name in _lib.KV_PTR_FIELDS:
+            if name in t:
+                setattr(st, name, t[name].data_ptr())
+        self.struct = st
+
+    def round(self, stream=None) -> None:
+        """Apply the engine's latest round: forks, releases, appends (and the
+        tail copies of the forks' partial blocks)."""
+        _lib.check(self.lib.duchess_kv_round(self.engine.policy, self.engine.state, self.struct,
+                                             _lib.stream_handle(stream)), "duchess_kv_round")
+
+    def counters(self) -> dict:
+        c = self.t["counters"].cpu().numpy()
+        return {"blocks_allocated": int(c[_lib.KV_CNT_ALLOC]),
+                "blocks_released": int(c[_lib.KV_CNT_FREE]),
+                "tail_bytes": int(c[_lib.KV_CNT_TAIL_BYTES]),
+                "overflow": int(c[_lib.KV_CNT_OVERFLOW])}
+
+    def slot_snapshot(self, slot: int) -> dict:
+        """Host copy of one slot's arena with LOCAL block ids: per branch id
+        the table row (blocks covering kv_tokens), refcounts [0, hwm), the free
+        stack, hwm, the owning pool index and the peak."""
+        R, B, P, nb, bt = self.R, self.B, self.P, self.NB, self.block_tokens
+        ar = self.t["arena"].view(R, 4)[slot].cpu().numpy()
+        top, hwm = int(ar[0]), int(ar[1])
+        kvt = self.t["kv_tokens"].view(R, B)[slot].cpu().numpy()
+        tab = self.t["table"].view(R, B, nb)[slot].cpu().numpy()
+        rows = {}
+        for b in range(B):
+            n = -(-int(kvt[b]) // bt)
+            if n:
+                rows[b] = (int(kvt[b]), [int(x) - slot * P if x >= 0 else -1 for x in tab[b, :n]])
+        ref = self.t["refcount"].view(R, P)[slot, :hwm].cpu().numpy()
+        stack = self.t["free_stack"].view(R, P)[slot, :top].cpu().numpy()
+        return {"rows": rows, "refcount": [int(x) for x in ref], "stack": [int(x) for x in stack],
+                "hwm": hwm, "owner": int(ar[2]), "peak": int(ar[3])}
