@@ -60,6 +60,11 @@ CONFIGS = {
     "c2": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048),
     "c1": dict(R=8, c=8, L=1, T=1, H=4096, dtype="f32", preset="gsm8k-like", pool=128),
     "c3": dict(R=1024, c=32, L=4, T=32, H=5120, dtype="bf16", preset="math-like", pool=4096),
+    # C2 with K3 in the round: a paged KV cache (16-token blocks, one Llama-3-8B
+    # layer slice of KV = 2*8*128*2 = 4096 B per token) forked / grown / released
+    # every round
+    "c2kv": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048,
+                 kv=4096),
     # SURVEY 8(d) C3 secondary row: the last token only (T=1, 40 960 B per branch-step)
     "c3t1": dict(R=1024, c=32, L=4, T=1, H=5120, dtype="bf16", preset="math-like", pool=4096),
 }
@@ -277,8 +282,9 @@ def run_serving(args, cfg, rank, world, local_rank):
     slab_bytes = rows * L * T * H * esz
     n_slabs = 4 if slab_bytes * S < (256 << 20) else max(2, min(4, int((4 << 30) // (slab_bytes * S)) or 2))
     packed = pack_pool(traces, seeds, dev)
+    kv = (dict(block_tokens=16, kv_bytes_per_token=cfg["kv"]) if cfg.get("kv") else None)
     srv = ShardedEngine(traces, knobs, seeds, bank, n_slots=R, shards=S, queue=queue, cycle=True,
-                        T=T, dtype=tdtype, device=dev, n_buffers=n_slabs, packed=packed)
+                        T=T, dtype=tdtype, device=dev, n_buffers=n_slabs, packed=packed, kv=kv)
     for k, sh in enumerate(srv.shards):
         for i, a in enumerate(sh["acts"]):
             fill_windows(a, 7000 + 31 * rank + 7 * k + i)
@@ -306,6 +312,7 @@ def run_serving(args, cfg, rank, world, local_rank):
         graph.replay()                  # one rotation untimed
         torch.cuda.synchronize(dev)
     c0 = srv.counters()
+    kv0 = srv.kv_counters()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -324,6 +331,7 @@ def run_serving(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None
     cnt = srv.counters() - c0
+    kv1 = srv.kv_counters()
     ms = ev0.elapsed_time(ev1)
     if S == 1 and graph is not None:
         # events inside a replayed graph are not meaningful: K1 is timed in an
@@ -398,12 +406,31 @@ def run_serving(args, cfg, rank, world, local_rank):
         "branch_steps_per_step": bs_all / args.steps,
         "roofline": roof,
         "e2e": e2e,
-        "gpu_launches": 2 * S * args.steps,
+        "gpu_launches": (3 if kv1 else 2) * S * args.steps,
         "clocks": clk,
         "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
                      "finished_requests": int(cnt[_lib.CNT_FINISHED]),
                      "forks": int(cnt[_lib.CNT_FORKS])},
+        **({"kv_cache": kv_report(kv0, kv1, args.steps, srv, cfg)} if kv1 else {}),
     }
+
+
+def kv_report(kv0, kv1, steps, srv, cfg):
+    """K3-in-the-round figures over the timed steps (PagedKVCache counters)."""
+    sh = srv.shards[0]["kv"]
+    d = {k: kv1[k] - kv0[k] for k in ("blocks_allocated", "blocks_released", "tail_bytes",
+                                       "overflow")}
+    return {"kernels": "duchess_kv_round (kv_round_kernel: forks incl. tail copies, releases, "
+                       "appends) after every "
+                       "duchess_round, each shard's stream",
+            "block_tokens": sh.block_tokens, "kv_bytes_per_token": sh.kv_bytes_per_token,
+            "blocks_per_slot": sh.P,
+            "pool_gib": sum(s["kv"].t["kv_pool"].numel() for s in srv.shards) / 2**30,
+            "blocks_allocated_per_step": d["blocks_allocated"] / steps,
+            "blocks_released_per_step": d["blocks_released"] / steps,
+            "tail_bytes_per_step": d["tail_bytes"] / steps,
+            "overflow": d["overflow"],
+            "peak_blocks_per_slot": kv1["peak_blocks_per_slot"]}
 
 
 def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
@@ -417,6 +444,7 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
     from paper_2509_24957_b200 import _lib
     steps = max(2, min(args.e2e_steps, args.steps))
     row_bytes = L * T * H * torch.tensor([], dtype=tdtype).element_size()
+    srv.flush_kv()
     for sh in srv.shards:
         sh["host"] = torch.empty((rows, L, T, H), dtype=tdtype, pin_memory=True)
         sh["host"].copy_(sh["acts"][0])
@@ -435,6 +463,8 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
                 sh["scorer"].score_active(sh["dslab"], sh["logit"],
                                           eng.probs.view(rows, L), eng)
                 eng.round()
+                if sh["kv"] is not None:
+                    sh["kv"].round()
                 sh["rec_h"].copy_(eng.t["round_rec"], non_blocking=True)
                 sh["act_h"].copy_(eng.t["actions"], non_blocking=True)
         for sh in srv.shards:
@@ -1245,7 +1275,7 @@ def main():
     if args.shards is None:
         # two request shards per GPU on two streams hide each shard's round
         # kernel under the other's scoring
-        args.shards = 2 if args.config in ("c2", "c3", "c3t1") else 1
+        args.shards = 2 if args.config in ("c2", "c2kv", "c3", "c3t1") else 1
     args.graph = args.graph == "on" or (args.graph == "auto" and args.config == "c1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -386,12 +386,19 @@ int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const int32_t* gro
 #define DUCHESS_KV_CNT_TAIL_BYTES 2  /* KV bytes copied for fork tails */
 #define DUCHESS_KV_CNT_OVERFLOW 3    /* blocks that did not fit the arena / table */
 #define DUCHESS_KV_N_COUNTERS 4
+/* Launch overlapped with the preceding kernel in the stream (programmatic
+ * dependent launch): the call runs while that kernel still runs and completes
+ * only after it. Legal when the preceding kernel does not write the engine
+ * state read here and releases its dependents only after its own inputs are
+ * final — e.g. the next round's duchess_score_active, so the order per round
+ * is score(k+1) -> kv_round(k) -> duchess_round(k+1). */
+#define DUCHESS_KV_OVERLAP 1
 
 typedef struct DuchessKV {
   int32_t block_tokens;       /* tokens per block (16) */
   int32_t blocks_per_slot;    /* P */
   int32_t max_blocks;         /* table width: blocks per branch row */
-  int32_t _pad;
+  int32_t flags;              /* DUCHESS_KV_OVERLAP */
   int64_t kv_bytes_per_token; /* bytes of KV per token (one layer slice: 2*8*128*2) */
   int32_t* table;             /* [R*Bmax*max_blocks] */
   int32_t* kv_tokens;         /* [R*Bmax] tokens each row's blocks cover */
@@ -414,7 +421,9 @@ typedef struct DuchessKV {
  * stack, by branch id then block index); (3) active rows grow to
  * ceil(position / block_tokens) blocks (popped from the stack, then above the
  * high-water mark). A slot whose request finished this round resets its arena
- * first. Deterministic: a request's tables depend only on its own rounds. */
+ * first. Deterministic: a request's tables depend only on its own rounds.
+ * Tail KV bytes are copied by the same launch. Must run before the next
+ * duchess_round (which rewrites the round records and branch fields read). */
 int duchess_kv_round(const DuchessPolicy* policy, const DuchessState* state, const DuchessKV* kv,
                      void* stream);
 

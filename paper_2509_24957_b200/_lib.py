@@ -81,13 +81,14 @@ class State(C.Structure):
 
 KV_CNT_ALLOC, KV_CNT_FREE, KV_CNT_TAIL_BYTES, KV_CNT_OVERFLOW = range(4)
 KV_N_COUNTERS = 4
+KV_OVERLAP = 1
 KV_PTR_FIELDS = ["table", "kv_tokens", "refcount", "free_stack", "arena", "jobs", "job_count",
                  "kv_pool", "counters"]
 
 
 class KV(C.Structure):
     _fields_ = [("block_tokens", C.c_int32), ("blocks_per_slot", C.c_int32),
-                ("max_blocks", C.c_int32), ("_pad", C.c_int32),
+                ("max_blocks", C.c_int32), ("flags", C.c_int32),
                 ("kv_bytes_per_token", C.c_int64)] + [(n, C.c_void_p) for n in KV_PTR_FIELDS]
 
 

@@ -122,9 +122,13 @@ class PagedKVCache:
                 setattr(st, name, t[name].data_ptr())
         self.struct = st
 
-    def round(self, stream=None) -> None:
-        """Apply the engine's latest round: forks, releases, appends (and the
-        tail copies of the forks' partial blocks)."""
+    def round(self, stream=None, overlap: bool = False) -> None:
+        """Apply the engine's latest round: forks (with the tail copies of
+        their partial blocks), releases, appends. overlap: run beside the
+        preceding kernel in the stream (DUCHESS_KV_OVERLAP) — legal right
+        after the next round's scorer launch (score(k+1) -> kv(k) ->
+        round(k+1)), never after the engine's own round()."""
+        self.struct.flags = _lib.KV_OVERLAP if overlap else 0
         _lib.check(self.lib.duchess_kv_round(self.engine.policy, self.engine.state, self.struct,
                                              _lib.stream_handle(stream)), "duchess_kv_round")
 
@@ -135,21 +139,30 @@ class PagedKVCache:
                 "tail_bytes": int(c[_lib.KV_CNT_TAIL_BYTES]),
                 "overflow": int(c[_lib.KV_CNT_OVERFLOW])}
 
-    def slot_snapshot(self, slot: int) -> dict:
+    STATE = ("table", "kv_tokens", "refcount", "free_stack", "arena")
+
+    def state_copy(self) -> dict:
+        """Device clones of the cache state (stream-ordered, no sync): for
+        snapshots taken inside a stream of rounds; see snapshot_of."""
+        return {k: self.t[k].clone() for k in self.STATE}
+
+    def slot_snapshot(self, slot: int, state: dict | None = None) -> dict:
         """Host copy of one slot's arena with LOCAL block ids: per branch id
         the table row (blocks covering kv_tokens), refcounts [0, hwm), the free
-        stack, hwm, the owning pool index and the peak."""
+        stack, hwm, the owning pool index and the peak. state: a state_copy()
+        (default: the live state)."""
+        t = self.t if state is None else state
         R, B, P, nb, bt = self.R, self.B, self.P, self.NB, self.block_tokens
-        ar = self.t["arena"].view(R, 4)[slot].cpu().numpy()
+        ar = t["arena"].view(R, 4)[slot].cpu().numpy()
         top, hwm = int(ar[0]), int(ar[1])
-        kvt = self.t["kv_tokens"].view(R, B)[slot].cpu().numpy()
-        tab = self.t["table"].view(R, B, nb)[slot].cpu().numpy()
+        kvt = t["kv_tokens"].view(R, B)[slot].cpu().numpy()
+        tab = t["table"].view(R, B, nb)[slot].cpu().numpy()
         rows = {}
         for b in range(B):
             n = -(-int(kvt[b]) // bt)
             if n:
                 rows[b] = (int(kvt[b]), [int(x) - slot * P if x >= 0 else -1 for x in tab[b, :n]])
-        ref = self.t["refcount"].view(R, P)[slot, :hwm].cpu().numpy()
-        stack = self.t["free_stack"].view(R, P)[slot, :top].cpu().numpy()
+        ref = t["refcount"].view(R, P)[slot, :hwm].cpu().numpy()
+        stack = t["free_stack"].view(R, P)[slot, :top].cpu().numpy()
         return {"rows": rows, "refcount": [int(x) for x in ref], "stack": [int(x) for x in stack],
                 "hwm": hwm, "owner": int(ar[2]), "peak": int(ar[3])}

@@ -10,7 +10,11 @@ is two launches:
                            active list), probabilities by branch slot;
   ``BatchedDuchess.round`` K2: decide the round (orchestrator.py:357-402),
                            refill finished slots from the queue and advance
-                           every slot into the next round (:344-355).
+                           every slot into the next round (:344-355);
+  ``PagedKVCache.round``   K3 (optional, ``kv=``): the round's forks share
+                           their root's KV blocks copy-on-write, ended
+                           branches release theirs, decoding branches grow
+                           (kvfork.py, duchess_kv_round).
 
 Requests never interact (reference SPEC.md:295), so shards are exact: each
 request's rounds depend only on its own state, RNG stream and activation
@@ -26,6 +30,7 @@ import torch
 
 from . import _lib
 from .engine import BatchedDuchess, pack_pool
+from .kvfork import PagedKVCache
 from .probe import Scorer, fill_windows
 
 
@@ -36,13 +41,15 @@ class ShardedEngine:
     per-request seeds as for DuchessRun's rng). bank: ProbeBank (L probes of
     width H). n_slots: request slots in total (split evenly over the shards).
     queue: service order of pool indices (default: pool order); shard k takes
-    queue[k::S]. T, dtype: the activation window per branch-step.
+    queue[k::S]. T, dtype: the activation window per branch-step. kv: None,
+    or PagedKVCache keyword arguments (block_tokens, blocks_per_slot,
+    kv_bytes_per_token) for a paged KV cache per shard, updated every round.
     """
 
     def __init__(self, traces, config, seeds, bank, *, n_slots: int, shards: int = 2,
                  queue=None, cycle: bool = False, T: int = 1, dtype=torch.bfloat16,
                  device="cuda", combine: int | None = None, n_buffers: int = 1,
-                 packed=None):
+                 packed=None, kv: dict | None = None):
         _lib.require_cuda()
         if shards < 1 or n_slots % shards:
             raise ValueError(f"{shards} shards must evenly divide the {n_slots} request slots")
@@ -68,7 +75,8 @@ class ShardedEngine:
             self.shards.append(dict(
                 eng=eng, scorer=Scorer(bank, self.rows * bank.L), acts=acts,
                 logit=torch.zeros((self.rows, bank.L), dtype=torch.float32, device=self.device),
-                stream=torch.cuda.Stream(self.device), ev=[]))
+                stream=torch.cuda.Stream(self.device), ev=[],
+                kv=None if kv is None else PagedKVCache(eng, **kv), kv_pending=False))
         self.started = False
 
     @property
@@ -88,15 +96,26 @@ class ShardedEngine:
         for sh in self.shards:
             cur.wait_stream(sh["stream"])
 
+    def flush_kv(self):
+        """Apply the KV update still pending for the latest round (step()
+        defers it to overlap the next round's scorer)."""
+        for sh in self.shards:
+            if sh["kv_pending"]:
+                with torch.cuda.stream(sh["stream"]):
+                    sh["kv"].round()
+                sh["kv_pending"] = False
+
     def begin(self):
         """Refill every slot and run phase 1 of the first round."""
         self.fork()
         for sh in self.shards:
             with torch.cuda.stream(sh["stream"]):
                 sh["eng"].advance()
+            sh["kv_pending"] = sh["kv"] is not None        # K3 of the first phase 1
         self.started = True
 
-    def step(self, i: int = 0, *, fill=None, timed: bool = False, after_round=None):
+    def step(self, i: int = 0, *, fill=None, timed: bool = False, after_round=None,
+             before_round=None):
         """One round of every shard, each on its stream (no host sync).
 
         i: round counter (selects activation buffer i % n_buffers).
@@ -104,7 +123,10 @@ class ShardedEngine:
             before scoring (e.g. the keyed synthetic fill of the round's
             survivors, or a host upload); by default the buffer is used as is.
         timed: bracket the scorer launch with CUDA events on the shard stream.
-        after_round(k, eng): optional hook on the shard stream after round().
+        after_round(k, eng): optional hook on the shard stream after round() (with kv,
+            K3 of the round is applied during the next step: flush_kv() first).
+        before_round(k, eng): optional hook on the shard stream right before
+            round() — after K3 of the previous round completed.
         """
         if not self.started:
             self.begin()
@@ -124,20 +146,32 @@ class ShardedEngine:
                 if timed:
                     e1.record(st)
                     sh["ev"].append((e0, e1))
+                if sh["kv_pending"]:
+                    # K3 of the previous round, overlapped with this round's
+                    # scorer (which reads only the active list and windows);
+                    # it completes after the scorer, before this round()
+                    sh["kv"].round(overlap=not timed)
+                    sh["kv_pending"] = False
+                if before_round is not None:
+                    before_round(k, eng)
                 eng.round()
+                sh["kv_pending"] = sh["kv"] is not None
                 if after_round is not None:
                     after_round(k, eng)
 
-    def run(self, max_rounds: int = 100000, fill=None, after_round=None) -> int:
+    def run(self, max_rounds: int = 100000, fill=None, after_round=None,
+            before_round=None) -> int:
         """Serve the queues to completion (non-cycling pools). Returns rounds."""
         if not self.started:
             self.begin()
         for i in range(max_rounds):
-            self.step(i, fill=fill, after_round=after_round)
+            self.step(i, fill=fill, after_round=after_round, before_round=before_round)
             if i % 8 == 7:
+                self.flush_kv()
                 self.join()
                 if self.all_done():
                     return i + 1
+        self.flush_kv()
         self.join()
         if not self.all_done():
             raise RuntimeError(f"requests still running after {max_rounds} rounds")
@@ -159,6 +193,18 @@ class ShardedEngine:
                 if o is not None:
                     out[p] = o
         return out
+
+    def kv_counters(self) -> dict | None:
+        """Summed PagedKVCache counters over the shards (None without kv)."""
+        if self.shards[0]["kv"] is None:
+            return None
+        tot: dict = {}
+        for sh in self.shards:
+            for k, v in sh["kv"].counters().items():
+                tot[k] = tot.get(k, 0) + v
+        tot["peak_blocks_per_slot"] = max(
+            int(sh["kv"].t["arena"].view(-1, 4)[:, 3].max()) for sh in self.shards)
+        return tot
 
     def scorer_events(self):
         return [ev for sh in self.shards for ev in sh["ev"]]

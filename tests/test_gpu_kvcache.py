@@ -116,3 +116,74 @@ def test_kv_round_matches_oracle_forks_heavy(preset, c, bt):
     assert cnt["blocks_allocated"] > 0 and cnt["blocks_released"] > 0
     if knobs.interval_tokens % bt:
         assert n_jobs > 20 and cnt["tail_bytes"] > 0
+
+
+def test_serving_loop_kv_overlapped_matches_oracle():
+    """The measured loop with K3 (bench --config c2kv, scaled down): two
+    request shards, K1 + round per shard stream, each round's KV update
+    launched overlapped with the next round's scorer. After every K3 (taken
+    right before the next round) each occupied slot's arena equals the
+    oracle arena of its request, replayed from the oracle DuchessRun fed the
+    device's probabilities (predictor=, orchestrator.py:319-327)."""
+    import bench
+    from paper_2509_24957_b200.probe import ProbeBank
+    from paper_2509_24957_b200.scheduler import difficulty_queue
+    from paper_2509_24957_b200.serving import ShardedEngine, keyed_fill
+    T, H, L, R, pool, seed, P = 4, 512, 1, 32, 96, 5, 1024
+    cfg = dict(bench.CONFIGS["c2kv"], R=R, pool=pool, T=T, H=H, L=L)
+    traces, knobs, seeds = bench.make_workload(cfg, seed=1000)
+    w, b, g, beta = bench.make_probe(H, L)
+    bank = ProbeBank.from_linear(w, b, g, beta)
+    queue = difficulty_queue([t.difficulty for t in traces])
+    srv = ShardedEngine(traces, knobs, seeds, bank, n_slots=R, shards=2, queue=queue,
+                        cycle=False, T=T, dtype=torch.bfloat16,
+                        kv=dict(block_tokens=16, blocks_per_slot=P, kv_bytes_per_token=64))
+    keyed = keyed_fill(seed)
+    snaps = [[] for _ in range(2)]
+    preds = [[] for _ in range(2)]
+    pending = [None, None]
+
+    def fill(k, eng, acts):                      # the round in flight: its survivors
+        keyed(k, eng, acts)
+        pending[k] = [eng.t[n].clone() for n in ("row_mask", "row_req", "row_tmpl", "row_pos")]
+
+    def before(k, eng):
+        snaps[k].append((srv.shards[k]["kv"].state_copy(), eng.t["rounds"].clone()))
+
+    def after(k, eng):
+        preds[k].append(pending[k] + [eng.t["step_pred"].clone()])
+
+    srv.run(max_rounds=2000, fill=fill, after_round=after, before_round=before)
+    torch.cuda.synchronize()
+    seen = {}
+    for k in range(2):
+        for mask, req, tm, pos, pred in preds[k]:
+            mask = mask.cpu().numpy().astype(bool)
+            req, tm, pos, pred = (x.cpu().numpy() for x in (req, tm, pos, pred))
+            for row in np.nonzero(mask)[0]:
+                seen[(int(req[row]), int(tm[row]), int(pos[row]))] = float(pred[row])
+    oracle = []
+    for p, trace in enumerate(traces):
+        index = {id(tp): j for j, tp in enumerate(trace.templates)}
+
+        def predictor(tmpl, position, _rng, p=p, index=index):
+            return seen[(p, index[id(tmpl)], position)]
+
+        req = port.DuchessRequest(trace, knobs, random.Random(seeds[p]), predictor=predictor)
+        oracle.append(kvcache.replay(req, P))
+    checked = set()
+    for k in range(2):
+        kv = srv.shards[k]["kv"]
+        for state, rounds in snaps[k]:
+            rounds = rounds.cpu().numpy()
+            for r in range(kv.R):
+                snap = kv.slot_snapshot(r, state)
+                p = snap.pop("owner")
+                snap.pop("peak")
+                if p < 0:
+                    continue
+                i = int(rounds[r]) - 1
+                assert snap == oracle[p][i], f"shard {k} slot {r} request {p} after round {i}"
+                checked.add((p, i))
+    assert len(checked) > 500
+    assert srv.kv_counters()["overflow"] == 0
