@@ -5,17 +5,21 @@
 
 One step = one orchestration round over every request slot on the GPU:
 duchess_score_active (K1: pooled LayerNorm + linear probe over each
-survivor's activation window, read from HBM) -> duchess_round (decide the
+survivor's activation window, read from HBM) -> duchess_round (K2: decide the
 round: predict / early-terminate / branch-out / request termination + vote,
-then refill and advance every slot into the next round). A branch-step is one
-survivor scored and decided (one `self._predict` call in reference
-orchestrator.py:358-362).
+then refill and advance every slot into the next round) -> duchess_kv_round
+(K3: the round's branch-outs share their root's paged KV blocks copy-on-write,
+ended branches release theirs, decoding branches grow; launched overlapped
+with the next round's K1). A branch-step is one survivor scored and decided
+(one `self._predict` call in reference orchestrator.py:358-362).
 
 Default workload at N = 1 (BASELINE.json configs[1], "C2"): 256 request
 slots x 16 branch slots, hidden 4096, bf16 activations, 32-token pooling
 window, one probe layer, math-like knobs with max_branches=16
 (presets.py:55-59), a cycling pool of 2048 synthetic requests (64 templates
-each) admitted in easiest-first order. Activations: rotating buffers per
+each) admitted in easiest-first order, a paged KV cache of 16-token blocks
+with 4096 B of KV per token (one Llama-3-8B layer slice; `--config c2nokv`
+drops it). Activations: rotating buffers per
 shard (> the 126 MB L2, so every step streams from HBM). The slots are split
 into two independent request shards stepping on two CUDA streams
 (serving.ShardedEngine: requests never interact), so each shard's
@@ -57,14 +61,16 @@ UNIT = "branch-steps/s"
 
 CONFIGS = {
     # name: (R slots, c, L, T, H, dtype, preset, pool)
-    "c2": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048),
+    # C2 (configs[1]) with K3 in the round: a paged KV cache (16-token blocks, one
+    # Llama-3-8B layer slice of KV = 2*8*128*2 = 4096 B per token) forked / grown /
+    # released every round, so one step = K1 + K2 + K3 (north_star's three kernels)
+    "c2": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048,
+               kv=4096),
+    # the same step without the KV cache (K1 + K2 only; the round-1 default)
+    "c2nokv": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like",
+                   pool=2048),
     "c1": dict(R=8, c=8, L=1, T=1, H=4096, dtype="f32", preset="gsm8k-like", pool=128),
     "c3": dict(R=1024, c=32, L=4, T=32, H=5120, dtype="bf16", preset="math-like", pool=4096),
-    # C2 with K3 in the round: a paged KV cache (16-token blocks, one Llama-3-8B
-    # layer slice of KV = 2*8*128*2 = 4096 B per token) forked / grown / released
-    # every round
-    "c2kv": dict(R=256, c=16, L=1, T=32, H=4096, dtype="bf16", preset="math-like", pool=2048,
-                 kv=4096),
     # SURVEY 8(d) C3 secondary row: the last token only (T=1, 40 960 B per branch-step)
     "c3t1": dict(R=1024, c=32, L=4, T=1, H=5120, dtype="bf16", preset="math-like", pool=4096),
 }
@@ -1275,7 +1281,7 @@ def main():
     if args.shards is None:
         # two request shards per GPU on two streams hide each shard's round
         # kernel under the other's scoring
-        args.shards = 2 if args.config in ("c2", "c2kv", "c3", "c3t1") else 1
+        args.shards = 2 if args.config in ("c2", "c2nokv", "c3", "c3t1") else 1
     args.graph = args.graph == "on" or (args.graph == "auto" and args.config == "c1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -119,7 +119,7 @@ def test_kv_round_matches_oracle_forks_heavy(preset, c, bt):
 
 
 def test_serving_loop_kv_overlapped_matches_oracle():
-    """The measured loop with K3 (bench --config c2kv, scaled down): two
+    """The measured loop with K3 (bench.py default C2 with the KV cache, scaled down): two
     request shards, K1 + round per shard stream, each round's KV update
     launched overlapped with the next round's scorer. After every K3 (taken
     right before the next round) each occupied slot's arena equals the
@@ -130,7 +130,7 @@ def test_serving_loop_kv_overlapped_matches_oracle():
     from paper_2509_24957_b200.scheduler import difficulty_queue
     from paper_2509_24957_b200.serving import ShardedEngine, keyed_fill
     T, H, L, R, pool, seed, P = 4, 512, 1, 32, 96, 5, 1024
-    cfg = dict(bench.CONFIGS["c2kv"], R=R, pool=pool, T=T, H=H, L=L)
+    cfg = dict(bench.CONFIGS["c2"], R=R, pool=pool, T=T, H=H, L=L)
     traces, knobs, seeds = bench.make_workload(cfg, seed=1000)
     w, b, g, beta = bench.make_probe(H, L)
     bank = ProbeBank.from_linear(w, b, g, beta)
