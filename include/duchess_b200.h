@@ -330,6 +330,19 @@ int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1g, i
                          const float* s, const float* c, const float* w2, float b2,
                          float* out_logit, double* out_prob, void* workspace,
                          size_t workspace_bytes, void* stream);
+/* Grouped form: G probes (one per probe layer) in one launch. X is [M, G, K]
+ * (x_interleaved = 1: the engine's activation slab, one token per layer) or
+ * [G, M, K] (0: e.g. the previous grouped layer's output); W1g [G*NH, K];
+ * s/c/w2 [G*NH]; b2 [G] (device). ln = 0 skips the LayerNorm fold (a hidden
+ * layer's input: pre = X.W1g_j + c_j). out_logit fp32 / out_prob fp64 [M, G].
+ * The paper's probe LN -> 2048 -> 1024 -> 1 is
+ * duchess_tc_linear_grouped (LN fold, ReLU) then this call with ln = 0. */
+size_t duchess_mlp_probe_tc_grouped_workspace_bytes(int64_t M, int32_t G, int32_t NH);
+int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K, int32_t G,
+                                 int32_t x_interleaved, int32_t ln, const void* W1g, int32_t NH,
+                                 const float* s, const float* c, const float* w2, const float* b2,
+                                 float* out_logit, double* out_prob, void* workspace,
+                                 size_t workspace_bytes, void* stream);
 
 /* ---- tensor-core linear layer with fused epilogue (tcgen05 + TMEM + TMA) --
  * One hidden layer of mlp_forward (predictor.py:126-151) batched over M rows:
@@ -346,6 +359,15 @@ int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_
                       int32_t ln_fold, const float* S, const float* C, const float* BS,
                       const float* BT, int32_t act, void* out, void* workspace,
                       size_t workspace_bytes, void* stream);
+/* Grouped form: G independent layers in one launch (one per probe layer). X
+ * [M, G, K] (x_interleaved = 1) or [G, M, K] (0); W [G*N, K]; S/C/BS/BT [G*N];
+ * out bf16 [G, M, N] (group-major). */
+size_t duchess_tc_linear_grouped_workspace_bytes(int64_t M, int32_t G, int32_t N);
+int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, int32_t G,
+                              int32_t x_interleaved, const void* W, int32_t N, int32_t ln_fold,
+                              const float* S, const float* C, const float* BS, const float* BT,
+                              int32_t act, void* out, void* workspace, size_t workspace_bytes,
+                              void* stream);
 /* Small classifier head: logits[M, n_out] = H (bf16 [M, K]) . W^T (fp32 [n_out, K]) + b. */
 int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W, const float* b,
                         int32_t n_out, float* logits, void* stream);

@@ -163,6 +163,19 @@ SYMBOLS = {
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_float,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                        C.c_void_p]),
+    "duchess_mlp_probe_tc_grouped_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32,
+                                                                    C.c_int32]),
+    "duchess_mlp_probe_tc_grouped": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                               C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                               C.c_void_p]),
+    "duchess_tc_linear_grouped_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
+    "duchess_tc_linear_grouped": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                            C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t,
+                                            C.c_void_p]),
     "duchess_tc_linear_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32]),
     "duchess_tc_linear": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -45,12 +45,16 @@ constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024;  // + alignment slack
 struct TcArgs {
   int64_t M;
   int K, NH;
+  int G;               // groups (probe layers), each with its own W1 / s / c / w2 / b2
+  int a_interleaved;   // X rows: 1 = [M, G, K], 0 = [G, M, K]
+  int ln;              // 1 = LayerNorm folded into the GEMM (input layer), 0 = plain
+  int64_t n_rt;        // row tiles per group
   const float* s;
   const float* c;
   const float* w2;
-  float b2;
-  float* out_logit;
-  double* out_prob;
+  const float* b2;     // [G]
+  float* out_logit;    // [M, G]
+  double* out_prob;    // [M, G]
   const uint16_t* X;   // row statistics are read straight from global (L2-hot)
   // workspace (zeroed once by the caller; kept consistent across launches)
   int* hdr;            // [0] launch epoch, [1] exit counter
@@ -68,6 +72,24 @@ __device__ __forceinline__ int ld_acquire_s32(const int* p) {
 }
 __device__ __forceinline__ void epi_bar() {   // the 4 epilogue warps
   asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// unit -> (group, row tile, hidden tile), group-major then row-tile-major
+__device__ __forceinline__ void tc_unit(int64_t u, int64_t n_rt, int n_tiles, int& g, int& mt, int& h) {
+  const int64_t per_g = n_rt * n_tiles;
+  g = int(u / per_g);
+  const int64_t rem = u - int64_t(g) * per_g;
+  mt = int(rem / n_tiles);
+  h = int(rem - int64_t(mt) * n_tiles);
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
@@ -163,14 +185,17 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (lane == 0) {   // ---- TMA producer ----
       int it = 0;
       for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-        const int m0 = int(u / n_tiles) * kTcBM, n0 = int(u % n_tiles) * kTcBN;
+        int g, mt, h;
+        tc_unit(u, a.n_rt, n_tiles, g, mt, h);
+        const int m0 = mt * kTcBM, n0 = g * a.NH + h * kTcBN;
+        const int ay = a.a_interleaved ? g : m0, az = a.a_interleaved ? m0 : g;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % kTcStages;
           const uint32_t ph = (it / kTcStages) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1u);
           char* st = smem + s * kTcStageBytes;
           mbar_expect_tx(&full_bar[s], kTcStageBytes);
-          tma_load_2d(st, &map_a, kb * kTcBK, m0, &full_bar[s]);
+          tma_load_3d(st, &map_a, kb * kTcBK, ay, az, &full_bar[s]);
           tma_load_2d(st + kTcABytes, &map_b, kb * kTcBK, n0, &full_bar[s]);
         }
       }
@@ -203,17 +228,22 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const int q = warp & 3;
     int i = 0;
     for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
-      const int mt = int(u / n_tiles), h = int(u % n_tiles);
+      int g, mt, h;
+      tc_unit(u, a.n_rt, n_tiles, g, mt, h);
       const int64_t row = int64_t(mt) * kTcBM + 32 * q + lane;
-      // LN statistics: unit h sums its 1/n_tiles share of each row's columns
-      // (while its MMAs run) and publishes the partial; every unit of the row
-      // tile then combines the n_tiles partials in fixed order.
-      {
+      const int64_t grow = int64_t(g) * a.M + row;          // (group, row), group-major
+      const int64_t xrow = a.a_interleaved ? row * a.G + g : grow;
+      const int64_t gmt = int64_t(g) * a.n_rt + mt;
+      float rsig = 1.f, shift = 0.f;
+      if (a.ln) {
+        // LN statistics: unit h sums its 1/n_tiles share of each row's columns
+        // (while its MMAs run) and publishes the partial; every unit of the row
+        // tile then combines the n_tiles partials in fixed order.
         const int nv = a.K / 8;
         const int v_lo = int(int64_t(h) * nv / n_tiles), v_hi = int(int64_t(h + 1) * nv / n_tiles);
         float sx = 0.f, sxx = 0.f;
         if (row < a.M) {
-          const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+          const uint4* rp = reinterpret_cast<const uint4*>(a.X + xrow * a.K);
           for (int v0 = v_lo; v0 < v_hi; v0 += 8) {
             uint4 buf[8];
 #pragma unroll
@@ -229,29 +259,28 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               }
             }
           }
-          a.stats[row * n_tiles + h] = make_float2(sx, sxx);
+          a.stats[grow * n_tiles + h] = make_float2(sx, sxx);
         }
         epi_bar();
         if (threadIdx.x == 64) {
           __threadfence();
-          atomicAdd(a.ready + mt, 1);
+          atomicAdd(a.ready + gmt, 1);
         }
         if (lane == 0)
-          while (ld_acquire_s32(a.ready + mt) < stamp * n_tiles) __nanosleep(64);
+          while (ld_acquire_s32(a.ready + gmt) < stamp * n_tiles) __nanosleep(64);
         __syncwarp();
-      }
-      float rsig = 1.f, shift = 0.f;
-      if (row < a.M) {
-        float sx = 0.f, sxx = 0.f;
-        for (int t = 0; t < n_tiles; ++t) {
-          const float2 p = __ldcg(a.stats + row * n_tiles + t);
-          sx += p.x;
-          sxx += p.y;
+        if (row < a.M) {
+          float tx = 0.f, txx = 0.f;
+          for (int t = 0; t < n_tiles; ++t) {
+            const float2 p = __ldcg(a.stats + grow * n_tiles + t);
+            tx += p.x;
+            txx += p.y;
+          }
+          const float mean = tx / float(a.K);
+          const float var = fmaxf(txx / float(a.K) - mean * mean, 0.f);
+          rsig = rsqrtf(var + kLayerNormEps);
+          shift = mean * rsig;
         }
-        const float mean = sx / float(a.K);
-        const float var = fmaxf(sxx / float(a.K) - mean * mean, 0.f);
-        rsig = rsqrtf(var + kLayerNormEps);
-        shift = mean * rsig;
       }
       const int acc = i & 1;
       mbar_wait(&tmem_full[acc], (i >> 1) & 1);
@@ -264,10 +293,11 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       for (int c0 = 0; c0 < kTcBN; c0 += 32) {
         float v[32];
         tmem_ld32(base + uint32_t(c0), v);
-        const int j0 = h * kTcBN + c0;
+        const int64_t j0 = int64_t(g) * a.NH + h * kTcBN + c0;   // group's column parameters
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.s + j0 + j));
+          const float4 s4 = a.ln ? __ldg(reinterpret_cast<const float4*>(a.s + j0 + j))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.c + j0 + j));
           const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.w2 + j0 + j));
           const float ss[4] = {s4.x, s4.y, s4.z, s4.w}, cc[4] = {c4.x, c4.y, c4.z, c4.w};
@@ -283,24 +313,24 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-      if (row < a.M) a.partial[row * n_tiles + h] = logit;
+      if (row < a.M) a.partial[grow * n_tiles + h] = logit;
       // the row tile's last finished hidden tile sums the partials in fixed order
       epi_bar();
       if (threadIdx.x == 64) {
         __threadfence();
-        last_flag = atomicAdd(a.done + mt, 1) == n_tiles - 1;
+        last_flag = atomicAdd(a.done + gmt, 1) == n_tiles - 1;
       }
       epi_bar();
       if (last_flag) {
         __threadfence();
         if (row < a.M) {
-          float z = a.b2;
-          for (int t = 0; t < n_tiles; ++t) z += __ldcg(a.partial + row * n_tiles + t);
-          a.out_logit[row] = z;
+          float z = a.b2[g];
+          for (int t = 0; t < n_tiles; ++t) z += __ldcg(a.partial + grow * n_tiles + t);
+          a.out_logit[row * a.G + g] = z;
           double p = 1.0 / (1.0 + exp(-double(z)));
-          a.out_prob[row] = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
+          a.out_prob[row * a.G + g] = fmin(fmax(p, kProbClip), 1.0 - kProbClip);
         }
-        if (threadIdx.x == 64) a.done[mt] = 0;   // ready for the next launch
+        if (threadIdx.x == 64) a.done[gmt] = 0;   // ready for the next launch
       }
     }
   }
@@ -331,6 +361,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+static bool make_map_a3(CUtensorMap* map, const void* base, uint64_t M, uint64_t G, uint64_t K,
+                        bool interleaved) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {K, interleaved ? G : M, interleaved ? M : G};
+  const cuuint64_t strides[2] = {K * 2, (interleaved ? G : M) * K * 2};
+  const cuuint32_t box[3] = {uint32_t(kTcBK), interleaved ? 1u : uint32_t(kTcBM),
+                             interleaved ? uint32_t(kTcBM) : 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows) {
   auto enc = tensor_map_encoder();
@@ -348,35 +392,47 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 using namespace duchess;
 
-extern "C" size_t duchess_mlp_probe_tc_workspace_bytes(int64_t M, int32_t NH) {
-  if (M < 0 || NH < kTcBN) return 0;
+extern "C" size_t duchess_mlp_probe_tc_grouped_workspace_bytes(int64_t M, int32_t G, int32_t NH) {
+  if (M < 0 || G < 1 || NH < kTcBN) return 0;
   const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
-  return size_t(16 + M * nt * 8 + M * nt * 4 + 2 * mt * 4 + 256);
+  return size_t(16 + int64_t(G) * M * nt * 8 + int64_t(G) * M * nt * 4 + 2 * int64_t(G) * mt * 4 + 256);
 }
 
-extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1,
-                                    int32_t NH, const float* s, const float* c, const float* w2,
-                                    float b2, float* out_logit, double* out_prob,
-                                    void* workspace, size_t workspace_bytes, void* stream) {
-  if (!X || !W1 || !s || !c || !w2 || !out_logit || !out_prob) return DUCHESS_EINVAL;
-  if (M < 0 || K < kTcBK || K % kTcBK || NH < kTcBN || NH % kTcBN) return DUCHESS_EINVAL;
+extern "C" size_t duchess_mlp_probe_tc_workspace_bytes(int64_t M, int32_t NH) {
+  const size_t g = duchess_mlp_probe_tc_grouped_workspace_bytes(M, 1, NH);
+  return g ? g + 32 : 0;                  // + the device copy of the scalar b2
+}
+
+extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K, int32_t G,
+                                            int32_t x_interleaved, int32_t ln, const void* W1,
+                                            int32_t NH, const float* s, const float* c,
+                                            const float* w2, const float* b2, float* out_logit,
+                                            double* out_prob, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+  if (!X || !W1 || !c || !w2 || !b2 || !out_logit || !out_prob || (ln && !s)) return DUCHESS_EINVAL;
+  if (M < 0 || G < 1 || K < kTcBK || K % kTcBK || NH < kTcBN || NH % kTcBN) return DUCHESS_EINVAL;
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W1) % 16 ||
-      reinterpret_cast<uintptr_t>(s) % 16 || reinterpret_cast<uintptr_t>(c) % 16 ||
+      (ln && reinterpret_cast<uintptr_t>(s) % 16) || reinterpret_cast<uintptr_t>(c) % 16 ||
       reinterpret_cast<uintptr_t>(w2) % 16)                     // per-column params read as float4
     return DUCHESS_EINVAL;
-  if (!workspace || workspace_bytes < duchess_mlp_probe_tc_workspace_bytes(M, NH) ||
+  if (!workspace || workspace_bytes < duchess_mlp_probe_tc_grouped_workspace_bytes(M, G, NH) ||
       reinterpret_cast<uintptr_t>(workspace) % 16)
     return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, X, uint64_t(M), uint64_t(K), kTcBM)) return DUCHESS_ECUDA;
-  if (!make_map(&mb, W1, uint64_t(NH), uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
+  if (!make_map_a3(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
+    return DUCHESS_ECUDA;
+  if (!make_map(&mb, W1, uint64_t(G) * NH, uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
   const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
   char* ws = static_cast<char*>(workspace);
   TcArgs a{};
   a.M = M;
   a.K = K;
   a.NH = NH;
+  a.G = G;
+  a.a_interleaved = x_interleaved != 0;
+  a.ln = ln != 0;
+  a.n_rt = mt;
   a.s = s;
   a.c = c;
   a.w2 = w2;
@@ -386,10 +442,10 @@ extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const v
   a.X = static_cast<const uint16_t*>(X);
   a.hdr = reinterpret_cast<int*>(ws);
   a.stats = reinterpret_cast<float2*>(ws + 16);
-  a.partial = reinterpret_cast<float*>(ws + 16 + M * nt * 8);
-  a.ready = reinterpret_cast<int*>(ws + 16 + M * nt * 8 + M * nt * 4);
-  a.done = a.ready + mt;
-  a.n_units = mt * nt;
+  a.partial = reinterpret_cast<float*>(ws + 16 + int64_t(G) * M * nt * 8);
+  a.ready = reinterpret_cast<int*>(ws + 16 + int64_t(G) * M * nt * 8 + int64_t(G) * M * nt * 4);
+  a.done = a.ready + int64_t(G) * mt;
+  a.n_units = int64_t(G) * mt * nt;
   cudaFuncSetAttribute(mlp_probe_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -398,4 +454,19 @@ extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const v
   const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
   mlp_probe_tc_kernel<<<grid, kTcThreads, kTcSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1,
+                                    int32_t NH, const float* s, const float* c, const float* w2,
+                                    float b2, float* out_logit, double* out_prob,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  // one group, LayerNorm folded; the scalar b2 is staged after the grouped workspace
+  const size_t gbytes = duchess_mlp_probe_tc_grouped_workspace_bytes(M, 1, NH);
+  if (!workspace || gbytes == 0 || workspace_bytes < gbytes + 32) return DUCHESS_EINVAL;
+  float* b2d = reinterpret_cast<float*>(static_cast<char*>(workspace) + (gbytes + 15) / 16 * 16);
+  if (cudaMemcpyAsync(b2d, &b2, sizeof(float), cudaMemcpyHostToDevice,
+                      static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return DUCHESS_ECUDA;
+  return duchess_mlp_probe_tc_grouped(X, M, K, 1, 0, 1, W1, NH, s, c, w2, b2d, out_logit, out_prob,
+                                      workspace, gbytes, stream);
 }

@@ -43,6 +43,9 @@ struct Args {
   int64_t M;
   int K, N;
   int ln_fold, act;
+  int G;               // groups (probe layers): independent GEMMs sharing the launch
+  int a_interleaved;   // X rows: 1 = [M, G, K] (row-major over (row, group)), 0 = [G, M, K]
+  int64_t n_rt;        // row tiles per group
   const uint16_t* X;
   const float* S;
   const float* C;
@@ -68,6 +71,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Work unit u -> (group, row tile, column tile), group-major then row-tile-major,
+// so the column tiles of one (group, row tile) run together (A tile L2-hot).
+struct Unit {
+  int g, mt, nt;
+};
+__device__ __forceinline__ Unit unit_of(int64_t u, int64_t n_rt, int n_tiles) {
+  const int64_t per_g = n_rt * n_tiles;
+  Unit x;
+  x.g = int(u / per_g);
+  const int64_t rem = u - int64_t(x.g) * per_g;
+  x.mt = int(rem / n_tiles);
+  x.nt = int(rem - int64_t(x.mt) * n_tiles);
+  return x;
 }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
@@ -156,13 +183,15 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
     if (lane == 0) {                                   // ---- TMA producer ----
       int it = 0;
       for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-        const int m0 = int(u / n_tiles) * BM, n0 = int(u % n_tiles) * BN;
+        const Unit w = unit_of(u, a.n_rt, n_tiles);
+        const int m0 = w.mt * BM, n0 = w.g * a.N + w.nt * BN;
+        const int ay = a.a_interleaved ? w.g : m0, az = a.a_interleaved ? m0 : w.g;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1u);
           char* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_2d(st, &map_a, kb * BK, m0, &full_bar[s]);
+          tma_load_3d(st, &map_a, kb * BK, ay, az, &full_bar[s]);
           tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
         }
       }
@@ -194,22 +223,26 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
     const int q = warp & 3;
     int i = 0;
     for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
-      const int mt = int(u / n_tiles), nt = int(u % n_tiles);
+      const Unit w = unit_of(u, a.n_rt, n_tiles);
+      const int g = w.g, mt = w.mt, nt = w.nt;
       const int64_t row = int64_t(mt) * BM + 32 * q + lane;
+      const int64_t grow = int64_t(g) * a.M + row;       // (group, row) index, group-major
+      const int64_t xrow = a.a_interleaved ? row * a.G + g : grow;
+      const int64_t gmt = int64_t(g) * a.n_rt + mt;
       float rsig = 1.f, shift = 0.f;
       if (LNF) {                                       // overlaps this tile's MMAs
         const int nv = a.K / 8;
         const int v_lo = int(int64_t(nt) * nv / n_tiles), v_hi = int(int64_t(nt + 1) * nv / n_tiles);
         float sx = 0.f, sxx = 0.f;
         if (row < a.M) {
-          const uint4* rp = reinterpret_cast<const uint4*>(a.X + row * a.K);
+          const uint4* rp = reinterpret_cast<const uint4*>(a.X + xrow * a.K);
           for (int v0 = v_lo; v0 < v_hi; v0 += 8) {
             uint4 buf[8];
 #pragma unroll
-            for (int w = 0; w < 8; ++w) buf[w] = v0 + w < v_hi ? __ldg(rp + v0 + w) : make_uint4(0, 0, 0, 0);
+            for (int w8 = 0; w8 < 8; ++w8) buf[w8] = v0 + w8 < v_hi ? __ldg(rp + v0 + w8) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-              const uint32_t w4[4] = {buf[w].x, buf[w].y, buf[w].z, buf[w].w};
+            for (int w8 = 0; w8 < 8; ++w8) {
+              const uint32_t w4[4] = {buf[w8].x, buf[w8].y, buf[w8].z, buf[w8].w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
@@ -218,20 +251,20 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
               }
             }
           }
-          a.stats[row * n_tiles + nt] = make_float2(sx, sxx);
+          a.stats[grow * n_tiles + nt] = make_float2(sx, sxx);
         }
         asm volatile("bar.sync 2, 128;" ::: "memory");
         if (threadIdx.x == 64) {
           __threadfence();
-          atomicAdd(a.ready + mt, 1);
+          atomicAdd(a.ready + gmt, 1);
         }
         if (lane == 0)
-          while (ld_acquire_s32(a.ready + mt) < stamp * n_tiles) __nanosleep(64);
+          while (ld_acquire_s32(a.ready + gmt) < stamp * n_tiles) __nanosleep(64);
         __syncwarp();
         if (row < a.M) {
           float tx = 0.f, txx = 0.f;
           for (int t = 0; t < n_tiles; ++t) {
-            const float2 p = __ldcg(a.stats + row * n_tiles + t);
+            const float2 p = __ldcg(a.stats + grow * n_tiles + t);
             tx += p.x;
             txx += p.y;
           }
@@ -246,20 +279,22 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN);
       const int n0 = nt * BN;
+      const int64_t gp = int64_t(g) * a.N;               // group's per-column parameters
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
         tmem_ld32(base + uint32_t(c0), v);
         const int j0 = n0 + c0;
+        const int64_t pj = gp + j0;
         uint32_t packed[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
           // per-column parameters of 4 columns at once (broadcast 16-byte loads)
-          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.C + j0 + k));
-          const float4 bs4 = __ldg(reinterpret_cast<const float4*>(a.BS + j0 + k));
-          const float4 bt4 = __ldg(reinterpret_cast<const float4*>(a.BT + j0 + k));
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.C + pj + k));
+          const float4 bs4 = __ldg(reinterpret_cast<const float4*>(a.BS + pj + k));
+          const float4 bt4 = __ldg(reinterpret_cast<const float4*>(a.BT + pj + k));
           float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if constexpr (LNF) s4 = __ldg(reinterpret_cast<const float4*>(a.S + j0 + k));
+          if constexpr (LNF) s4 = __ldg(reinterpret_cast<const float4*>(a.S + pj + k));
           const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, bs[4] = {bs4.x, bs4.y, bs4.z, bs4.w};
           const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
           float y[4];
@@ -273,7 +308,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
           packed[k / 2 + 1] = uint32_t(f32_to_bf16_rne(y[2])) | (uint32_t(f32_to_bf16_rne(y[3])) << 16);
         }
         if (row < a.M) {
-          uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.N + j0);
+          uint4* dst = reinterpret_cast<uint4*>(a.out + grow * a.N + j0);
 #pragma unroll
           for (int w = 0; w < 4; ++w)
             dst[w] = make_uint4(packed[4 * w], packed[4 * w + 1], packed[4 * w + 2], packed[4 * w + 3]);
@@ -368,6 +403,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
+// A operand: 3D map {K, Y, Z} of bf16 rows, box {BK, 1, BM} (interleaved
+// [M, G, K]: Y = group, Z = row) or {BK, BM, 1} (group-major [G, M, K]).
+static bool make_map_a(CUtensorMap* map, const void* base, uint64_t M, uint64_t G, uint64_t K,
+                       bool interleaved) {
+  auto enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {K, interleaved ? G : M, interleaved ? M : G};
+  const cuuint64_t strides[2] = {K * 2, (interleaved ? G : M) * K * 2};
+  const cuuint32_t box[3] = {uint32_t(BK), interleaved ? 1u : uint32_t(BM), interleaved ? uint32_t(BM) : 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows) {
   auto enc = encoder();
@@ -386,36 +436,46 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 using namespace duchess;
 
-extern "C" size_t duchess_tc_linear_workspace_bytes(int64_t M, int32_t N) {
-  if (M < 0 || N < tcl::BN) return 0;
+extern "C" size_t duchess_tc_linear_grouped_workspace_bytes(int64_t M, int32_t G, int32_t N) {
+  if (M < 0 || G < 1 || N < tcl::BN) return 0;
   const int64_t mt = (M + tcl::BM - 1) / tcl::BM, nt = N / tcl::BN;
-  return size_t(16 + M * nt * 8 + mt * 4 + 256);
+  return size_t(16 + int64_t(G) * M * nt * 8 + int64_t(G) * mt * 4 + 256);
 }
 
-extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
-                                 int32_t ln_fold, const float* S, const float* C, const float* BS,
-                                 const float* BT, int32_t act, void* out, void* workspace,
-                                 size_t workspace_bytes, void* stream) {
+extern "C" size_t duchess_tc_linear_workspace_bytes(int64_t M, int32_t N) {
+  return duchess_tc_linear_grouped_workspace_bytes(M, 1, N);
+}
+
+extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, int32_t G,
+                                         int32_t x_interleaved, const void* W, int32_t N,
+                                         int32_t ln_fold, const float* S, const float* C,
+                                         const float* BS, const float* BT, int32_t act, void* out,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
   if (!X || !W || !C || !BS || !BT || !out || (ln_fold && !S)) return DUCHESS_EINVAL;
-  if (M < 0 || K < tcl::BK || K % tcl::BK || N < tcl::BN || N % tcl::BN || act < 0 || act > 2)
+  if (M < 0 || G < 1 || K < tcl::BK || K % tcl::BK || N < tcl::BN || N % tcl::BN || act < 0 ||
+      act > 2)
     return DUCHESS_EINVAL;
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16 ||
       reinterpret_cast<uintptr_t>(out) % 16 || reinterpret_cast<uintptr_t>(C) % 16 ||
       reinterpret_cast<uintptr_t>(BS) % 16 || reinterpret_cast<uintptr_t>(BT) % 16 ||
       (ln_fold && reinterpret_cast<uintptr_t>(S) % 16))      // per-column params read as float4
     return DUCHESS_EINVAL;
-  if (ln_fold && (!workspace || workspace_bytes < duchess_tc_linear_workspace_bytes(M, N) ||
+  if (ln_fold && (!workspace || workspace_bytes < duchess_tc_linear_grouped_workspace_bytes(M, G, N) ||
                   reinterpret_cast<uintptr_t>(workspace) % 16))
     return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
   CUtensorMap ma, mb;
-  if (!tcl::make_map(&ma, X, uint64_t(M), uint64_t(K), tcl::BM)) return DUCHESS_ECUDA;
-  if (!tcl::make_map(&mb, W, uint64_t(N), uint64_t(K), tcl::BN)) return DUCHESS_ECUDA;
+  if (!tcl::make_map_a(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
+    return DUCHESS_ECUDA;
+  if (!tcl::make_map(&mb, W, uint64_t(G) * N, uint64_t(K), tcl::BN)) return DUCHESS_ECUDA;
   const int64_t mt = (M + tcl::BM - 1) / tcl::BM, nt = N / tcl::BN;
   tcl::Args a{};
   a.M = M;
   a.K = K;
   a.N = N;
+  a.G = G;
+  a.a_interleaved = x_interleaved != 0;
+  a.n_rt = mt;
   a.ln_fold = ln_fold;
   a.act = act;
   a.X = static_cast<const uint16_t*>(X);
@@ -428,9 +488,9 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
     char* ws = static_cast<char*>(workspace);
     a.hdr = reinterpret_cast<int*>(ws);
     a.stats = reinterpret_cast<float2*>(ws + 16);
-    a.ready = reinterpret_cast<int*>(ws + 16 + M * nt * 8);
+    a.ready = reinterpret_cast<int*>(ws + 16 + int64_t(G) * M * nt * 8);
   }
-  a.n_units = mt * nt;
+  a.n_units = int64_t(G) * mt * nt;
   void (*kern)(CUtensorMap, CUtensorMap, tcl::Args) =
       ln_fold ? (act == 2 ? tcl::linear_kernel<true, 2> : act == 1 ? tcl::linear_kernel<true, 1>
                                                                    : tcl::linear_kernel<true, 0>)
@@ -444,6 +504,14 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
   const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
   kern<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
+
+extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
+                                 int32_t ln_fold, const float* S, const float* C, const float* BS,
+                                 const float* BT, int32_t act, void* out, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  return duchess_tc_linear_grouped(X, M, K, 1, 0, W, N, ln_fold, S, C, BS, BT, act, out, workspace,
+                                   workspace_bytes, stream);
 }
 
 extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W,

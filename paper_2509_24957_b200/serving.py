@@ -31,6 +31,7 @@ import torch
 from . import _lib
 from .engine import BatchedDuchess, pack_pool
 from .kvfork import PagedKVCache
+from .mlp_probe import MlpProbeBank, MlpScorer
 from .probe import Scorer, fill_windows
 
 
@@ -38,8 +39,9 @@ class ShardedEngine:
     """S request shards of one request pool on one GPU.
 
     traces / config / seeds: the pool (RequestTrace-likes, OrchestratorConfig,
-    per-request seeds as for DuchessRun's rng). bank: ProbeBank (L probes of
-    width H). n_slots: request slots in total (split evenly over the shards).
+    per-request seeds as for DuchessRun's rng). bank: ProbeBank (L linear
+    probes of width H, K1) or MlpProbeBank (the paper's MLP probe per layer on
+    the tensor cores, T = 1). n_slots: request slots in total (split evenly over the shards).
     queue: service order of pool indices (default: pool order); shard k takes
     queue[k::S]. T, dtype: the activation window per branch-step. kv: None,
     or PagedKVCache keyword arguments (block_tokens, blocks_per_slot,
@@ -72,8 +74,10 @@ class ShardedEngine:
                                  device=self.device, packed=self.packed)
             acts = [torch.zeros((self.rows, bank.L, T, bank.H), dtype=dtype, device=self.device)
                     for _ in range(n_buffers)]
+            scorer = (MlpScorer(bank) if isinstance(bank, MlpProbeBank)
+                      else Scorer(bank, self.rows * bank.L))
             self.shards.append(dict(
-                eng=eng, scorer=Scorer(bank, self.rows * bank.L), acts=acts,
+                eng=eng, scorer=scorer, acts=acts,
                 logit=torch.zeros((self.rows, bank.L), dtype=torch.float32, device=self.device),
                 stream=torch.cuda.Stream(self.device), ev=[],
                 kv=None if kv is None else PagedKVCache(eng, **kv), kv_pending=False))
