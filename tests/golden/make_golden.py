@@ -323,6 +323,7 @@ def simulation():
     """run_simulation (simengine.py:150-281) outputs: the exact CSV and
     summary-JSON bytes the reference writes, per case."""
     import dataclasses
+    import dataclasses
     import tempfile
 
     from branchsim.presets import PRESETS as P
@@ -377,7 +378,102 @@ def simulation():
     return cases
 
 
+def ingestion():
+    """(f)2: answer normalisation, the JSONL schema (bytes + content hash),
+    validate_trace violations and load_trace error messages of the reference
+    (core.py:24-39, workload.py:114-311)."""
+    import dataclasses
+    import tempfile
+
+    from branchsim.core import normalize_answer
+    from branchsim.workload import (TraceError, Workload, load_trace, save_trace,
+                                    trace_prediction, validate_trace)
+    raws = ["42", "  42 ", "\\boxed{42}", "\\boxed{ {X} }", "{{7}}", "{}", "", "   ",
+            "\\boxed{}", "ABC", "ǅemal", "{\\boxed{Yes}}", "\\boxed{a}b}", "{ 1/2 }",
+            "STRASSE", "İstanbul", "{\\boxed{{3.0}}}", "\\boxed{x", "x}", "{ }"]
+    out = {"normalize": [[r, normalize_answer(r)] for r in raws]}
+    out["jsonl"] = []
+    with tempfile.TemporaryDirectory() as d:
+        for name, params, n, seed in [("default", SyntheticParams(), 12, 4),
+                                      ("math", replace(PRESETS["math-like"].synthetic,
+                                                       templates_per_request=9), 7, 21)]:
+            w = generate_synthetic(params, n, seed=seed)
+            w = Workload(with_pred_probs(w.requests, seed)) if name == "math" else w
+            path = Path(d) / f"{name}.jsonl"
+            save_trace(w, path)
+            loaded = load_trace(path)
+            out["jsonl"].append({"name": name, "params": dataclasses.asdict(params), "n": n,
+                                 "seed": seed, "pred_probs_seed": seed if name == "math" else None,
+                                 "bytes": path.read_bytes().decode(),
+                                 "hash": w.content_hash(), "loaded_hash": loaded.content_hash()})
+        bad = []
+        good = {"v": 1, "id": "r0", "ground_truth": "42", "prompt_tokens": 10,
+                "branches": [{"natural_length": 100, "final_answer": "42",
+                              "probes": [{"at": 16, "answer": "7"}]}]}
+        def variant(**kw):
+            o = json.loads(json.dumps(good))
+            for k, v in kw.items():
+                if v is None:
+                    o.pop(k, None)
+                else:
+                    o[k] = v
+            return json.dumps(o)
+        cases = {
+            "missing_gt": variant(ground_truth=None),
+            "missing_id_and_gt": variant(id=None, ground_truth=None),
+            "bad_pt_and_branches": variant(prompt_tokens="x", branches=None),
+            "bool_pt": variant(prompt_tokens=True),
+            "bad_version": variant(v=2),
+            "bad_difficulty": variant(difficulty="hard"),
+            "bad_branch": variant(branches=[3]),
+            "branch_missing_fields": variant(branches=[{"probes": [{"at": "x"}]}]),
+            "bad_pred": variant(branches=[{"natural_length": 10, "final_answer": "1",
+                                           "pred_probs": [{"at": 1, "p": "hi"}]}]),
+            "probe_order": variant(branches=[{"natural_length": 100, "final_answer": "1",
+                                              "probes": [{"at": 20, "answer": "1"},
+                                                         {"at": 10, "answer": "2"}]}]),
+            "empty_gt": variant(ground_truth=" {} "),
+            "not_object": "[1, 2]",
+            "malformed": "{\"v\": 1,",
+            "duplicate": variant() + "\n" + variant(),
+        }
+        for name, text in cases.items():
+            path = Path(d) / f"bad_{name}.jsonl"
+            path.write_text(text + "\n")
+            try:
+                load_trace(path)
+                bad.append([name, text, None])
+            except TraceError as exc:
+                bad.append([name, text, str(exc)])
+        out["load_errors"] = bad
+    tv = []
+    mk = lambda n, fa, probes=(), conv=None, pp=None: BranchTemplate(n, fa, list(probes), conv, pp)
+    vcases = [
+        ("clean", [RequestTrace("a", "1", 5, [mk(100, "1")], 2)], None),
+        ("degraded", [RequestTrace("a", "1", 5, [mk(100, "1")], None)], 4),
+        ("empty_gt", [RequestTrace("a", "", 5, [mk(100, "1")], None)], None),
+        ("probe_beyond_conv", [RequestTrace("a", "42", 0, [mk(100, "42", [(95, "7")], 90)],
+                                            None)], None),
+        ("many", [RequestTrace("a", "1", -1, [], 9),
+                  RequestTrace("a", "1", 3, [mk(0, "1", [(5, "2"), (3, "1")], 200,
+                                                 [(3, 0.5), (2, 1.5)])], None)], 2),
+    ]
+    for name, reqs, mb in vcases:
+        vs = validate_trace(Workload(reqs), max_branches=mb)
+        tv.append([name, [[r.id, r.ground_truth, r.prompt_tokens, r.difficulty,
+                           [[t.natural_length, t.final_answer, [list(p) for p in t.probes],
+                             t.oracle_convergence,
+                             None if t.pred_probs is None else [list(x) for x in t.pred_probs]]
+                            for t in r.templates]] for r in reqs],
+                   mb, [[v.level, v.where, v.message] for v in vs]])
+    out["validate"] = tv
+    tp = mk(100, "1", pp=[(16, 0.25), (32, 0.75)])
+    out["trace_prediction"] = [[x, trace_prediction(tp, x).hex()] for x in (0, 10, 16, 20, 32, 99)]
+    return out
+
+
 def main():
+    (OUT / "ingestion.json").write_text(json.dumps(ingestion(), separators=(",", ":")))
     (OUT / "decisions.json").write_text(json.dumps(decisions(), separators=(",", ":")))
     (OUT / "baselines.json").write_text(json.dumps(baselines(), separators=(",", ":")))
     (OUT / "primitives.json").write_text(json.dumps(primitives(), separators=(",", ":")))
@@ -387,7 +483,9 @@ def main():
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "simulation":
+    if len(sys.argv) > 1 and sys.argv[1] == "ingestion":
+        (OUT / "ingestion.json").write_text(json.dumps(ingestion(), separators=(",", ":")))
+    elif len(sys.argv) > 1 and sys.argv[1] == "simulation":
         (OUT / "simulation.json").write_text(json.dumps(simulation(), separators=(",", ":")))
     elif len(sys.argv) > 1 and sys.argv[1] == "decisions":
         (OUT / "decisions.json").write_text(json.dumps(decisions(), separators=(",", ":")))
