@@ -40,6 +40,7 @@ extern "C" {
 
 #define DUCHESS_F32 0
 #define DUCHESS_BF16 1
+#define DUCHESS_F64 2   /* row_normalize input only */
 
 /* Branch status (orchestrator.py:35-40). */
 #define DUCHESS_ACTIVE 0
@@ -368,6 +369,11 @@ int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, int32_t G,
                               const float* S, const float* C, const float* BS, const float* BT,
                               int32_t act, void* out, void* workspace, size_t workspace_bytes,
                               void* stream);
+/* Input LayerNorm as a pass: Z (bf16 [M, K]) = (X - mean) / sqrt(var + 1e-5)
+ * per row of X ([M, K], DUCHESS_F32 or DUCHESS_F64), statistics in fp64
+ * (predictor.py:134-136). */
+int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, int32_t K, void* Z,
+                          void* stream);
 /* Small classifier head: logits[M, n_out] = H (bf16 [M, K]) . W^T (fp32 [n_out, K]) + b. */
 int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W, const float* b,
                         int32_t n_out, float* logits, void* stream);

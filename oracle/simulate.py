@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import random
 
+import numpy as np
+
 from . import port
 
 
@@ -56,7 +58,7 @@ def seeds(n: int, seed: int):
 
 
 def simulate(traces, knobs, policy, schedule, arrivals, timing, seed, rho,
-             difficulty_mode=None, confusion=None):
+             difficulty_mode=None, confusion=None, mlp_weights=None, mlp_activations=None):
     """simengine.py:150-281 (validation omitted): log rows, one per request,
     sorted by request id: (id, arrival, start, first_token, completion,
     tokens_decode, tokens_probe, answers, final, correct, reason, actual,
@@ -94,6 +96,9 @@ def simulate(traces, knobs, policy, schedule, arrivals, timing, seed, rho,
                 rng = random.Random(pred_seeds[i])
                 if difficulty_mode == "actual":
                     predicted[i] = traces[i].difficulty
+                elif difficulty_mode == "mlp":             # predictor.py:398-402
+                    _z, probs = port.mlp_forward(mlp_weights, mlp_activations[i])
+                    predicted[i] = int(np.argmax(probs)) + 1
                 else:
                     predicted[i] = port.confused_level(traces[i].difficulty, rng,
                                                        confusion or port.CONFUSION)

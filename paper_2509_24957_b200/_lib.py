@@ -15,7 +15,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libduchess_b200.so"
 
 DUCHESS_OK = 0
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 ACTIVE, EARLY_TERMINATED, NATURAL_END, CAPPED, CANCELLED = range(5)
 REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
@@ -180,6 +180,8 @@ SYMBOLS = {
     "duchess_tc_linear": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "duchess_row_normalize": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
+                                        C.c_void_p, C.c_void_p]),
     "duchess_head_logits": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_int32, C.c_void_p, C.c_void_p]),
     "duchess_version": (C.c_char_p, []),

@@ -334,6 +334,43 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   }
 }
 
+// Input LayerNorm normalisation (predictor.py:134-136) as its own pass: one
+// CTA per row, fp64 sums (mean, then the centred square sum), writes
+// z = (x - mean) / sqrt(var + 1e-5) as bf16. Feeding z (zero mean, unit scale)
+// to the first tensor-core layer instead of folding the statistics into its
+// epilogue avoids the cancellation of x.W' - mu * S for rows with a large
+// common offset (the fold is exact algebra but not in fp32 / bf16).
+template <typename TX>
+__global__ void __launch_bounds__(256) row_normalize_kernel(const TX* X, int64_t M, int K,
+                                                            uint16_t* Z) {
+  __shared__ double red[8];
+  const int64_t row = blockIdx.x;
+  const TX* x = X + row * K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto block_sum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    __syncthreads();
+    return t;
+  };
+  double s = 0.0;
+  for (int k = threadIdx.x; k < K; k += 256) s += double(x[k]);
+  const double mean = block_sum(s) / K;
+  double q = 0.0;
+  for (int k = threadIdx.x; k < K; k += 256) {
+    const double d = double(x[k]) - mean;
+    q += d * d;
+  }
+  const double inv = 1.0 / sqrt(block_sum(q) / K + double(kLayerNormEps));
+  for (int k = threadIdx.x; k < K; k += 256)
+    Z[row * K + k] = f32_to_bf16_rne(float((double(x[k]) - mean) * inv));
+}
+
 // Classifier head (N small, e.g. 5): one warp per row, fp32 dots over the
 // bf16 hidden vector, logits out.
 __global__ void head_kernel(const uint16_t* Hm, int64_t M, int K, const float* W, const float* b,
@@ -512,6 +549,21 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
                                  size_t workspace_bytes, void* stream) {
   return duchess_tc_linear_grouped(X, M, K, 1, 0, W, N, ln_fold, S, C, BS, BT, act, out, workspace,
                                    workspace_bytes, stream);
+}
+
+extern "C" int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, int32_t K, void* Z,
+                                     void* stream) {
+  if (!X || !Z || M < 0 || K < 1 || (dtype != DUCHESS_F32 && dtype != DUCHESS_F64))
+    return DUCHESS_EINVAL;
+  if (M == 0) return DUCHESS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == DUCHESS_F64)
+    tcl::row_normalize_kernel<double><<<unsigned(M), 256, 0, st>>>(
+        static_cast<const double*>(X), M, K, static_cast<uint16_t*>(Z));
+  else
+    tcl::row_normalize_kernel<float><<<unsigned(M), 256, 0, st>>>(
+        static_cast<const float*>(X), M, K, static_cast<uint16_t*>(Z));
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
 extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W,

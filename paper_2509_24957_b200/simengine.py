@@ -201,13 +201,22 @@ def device_service(workload: Workload, config: OrchestratorConfig, policy: str,
 
 
 def predicted_levels(workload: Workload, mode: str, predict_seeds: list, confusion,
-                     device="cuda") -> list:
+                     device="cuda", weights=None, activations=None) -> list:
     """predict_difficulty(mode, ...) for every request with its own stream
-    random.Random(predict_seeds[order]) (simengine.py:223-227)."""
+    random.Random(predict_seeds[order]) (simengine.py:223-227). mode "mlp"
+    (predictor.py:398-402: argmax of the complexity MLP + 1, which the
+    reference's simulation rejects, simengine.py:184-186) runs the tensor-core
+    classifier over every request's activation vector at once."""
     import torch
 
     from .engine import seed_states
     labels = [r.difficulty for r in workload.requests]
+    if mode == "mlp":
+        from .difficulty import TensorCoreClassifier
+        X = np.asarray(activations, dtype=np.float64)
+        if X.ndim != 2 or X.shape[0] != len(labels):
+            raise ValueError("mlp mode needs one activation vector per request")
+        return [int(v) for v in TensorCoreClassifier(weights, device=device).predict_levels(X)]
     if mode == "actual":
         for lv in labels:
             if lv is None:
@@ -238,9 +247,14 @@ def run_simulation(workload: Workload, orch_config: OrchestratorConfig, policy: 
                    schedule: str, arrivals: list, timing: TimingModel, seed: int,
                    synthetic: SyntheticPredictorConfig | None = None,
                    difficulty_mode: str | None = None,
-                   confusion=None) -> tuple:
+                   confusion=None, difficulty_weights=None,
+                   difficulty_activations=None) -> tuple:
     """One serving timeline over the whole workload (simengine.py:150-281).
-    Returns (MetricsReport, [RequestLogEntry sorted by request id])."""
+    Returns (MetricsReport, [RequestLogEntry sorted by request id]).
+    difficulty_mode "mlp" (an extension: the reference's simulation accepts
+    only "actual" / "noisy-label") predicts levels with the complexity MLP
+    `difficulty_weights` over `difficulty_activations` [n_requests, input_dim]
+    (predict_difficulty("mlp"), predictor.py:398-402)."""
     if policy not in POLICIES:
         raise SimulationError(f"unknown policy {policy!r}")
     if schedule not in SCHEDULES:
@@ -260,9 +274,12 @@ def run_simulation(workload: Workload, orch_config: OrchestratorConfig, policy: 
         if difficulty_mode is None:
             raise SimulationError("easiest-predicted needs a difficulty predictor: pass "
                                   "difficulty_mode 'actual' or 'noisy-label'")
-        if difficulty_mode not in ("actual", "noisy-label"):
+        if difficulty_mode not in ("actual", "noisy-label", "mlp"):
             raise SimulationError(
                 f"unsupported difficulty mode {difficulty_mode!r} for simulation")
+        if difficulty_mode == "mlp" and (difficulty_weights is None or
+                                         difficulty_activations is None):
+            raise SimulationError("mlp mode requires an activation vector and weights")
         if confusion is not None:
             validate_confusion(confusion)
     synthetic = synthetic or SyntheticPredictorConfig()
@@ -272,7 +289,8 @@ def run_simulation(workload: Workload, orch_config: OrchestratorConfig, policy: 
     predict_seeds = [master.getrandbits(64) for _ in reqs]
 
     fig = device_service(workload, orch_config, policy, policy_seeds, timing, synthetic)
-    levels = (predicted_levels(workload, difficulty_mode, predict_seeds, confusion)
+    levels = (predicted_levels(workload, difficulty_mode, predict_seeds, confusion,
+                               weights=difficulty_weights, activations=difficulty_activations)
               if schedule == EASIEST_PREDICTED else [None] * len(reqs))
     logs = replay_queue(workload, schedule, arrivals, timing, fig, levels)
     report = aggregate_metrics(logs, policy=policy, schedule=schedule, seed=seed,

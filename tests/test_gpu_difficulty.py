@@ -60,6 +60,24 @@ def test_tc_classifier_matches_fp64(dims, act, bn, ln, M):
         assert np.allclose(ref_logits[i], o_logits, rtol=1e-9, atol=1e-9)
 
 
+@pytest.mark.parametrize("offset,scale", [(1000.0, 1.0), (-3.0e4, 0.01), (5.0, 100.0)])
+def test_tc_classifier_large_common_offset(offset, scale):
+    """Rows with a large common offset / odd scale: the input is
+    LayerNorm-normalised in fp64 before the bf16 cast, so the tensor-core
+    logits stay within the calibrated margin's half and the levels equal the
+    fp64 forward's."""
+    from paper_2509_24957_b200.difficulty import TensorCoreClassifier
+    from paper_2509_24957_b200.predictor import mlp_forward_batch
+    w = complexity_mlp(3, (1024, 512, 256), act="gelu", batchnorm=True, layernorm=True)
+    X = activations(4, 400, 1024) * scale + offset
+    clf = TensorCoreClassifier(w)
+    lg = clf.logits(X).cpu().numpy()
+    ref_logits, ref_probs = mlp_forward_batch(w, X)
+    assert np.abs(lg - ref_logits).max() < clf.margin / 2, (np.abs(lg - ref_logits).max(),
+                                                            clf.margin)
+    assert (clf.predict_levels(X) == ref_probs.argmax(axis=1) + 1).all()
+
+
 def test_tc_classifier_shape_errors():
     from paper_2509_24957_b200.difficulty import TensorCoreClassifier
     from paper_2509_24957_b200.predictor import WeightFormatError

@@ -73,6 +73,9 @@ def test_simulation_input_validation():
         run_simulation(workload, orch, "duchess", "easiest-predicted", arr, timing, 0)
     with pytest.raises(SimulationError, match="unsupported difficulty mode"):
         run_simulation(workload, orch, "duchess", "easiest-predicted", arr, timing, 0,
+                       difficulty_mode="oracle")
+    with pytest.raises(SimulationError, match="mlp mode requires"):
+        run_simulation(workload, orch, "duchess", "easiest-predicted", arr, timing, 0,
                        difficulty_mode="mlp")
     assert isinstance(OrchestratorConfig(), OrchestratorConfig)
     assert TimingModel().ms_per_token == 25.0
@@ -111,3 +114,37 @@ def test_device_run_simulation_small_slot_pool(tmp_path):
     finally:
         simengine.device_service = orig
     assert _write(tmp_path, logs, report, case) == (case["csv"], case["json"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["duchess", "default-sc"])
+def test_device_run_simulation_mlp_difficulty_matches_oracle(policy, tmp_path):
+    """difficulty_mode="mlp" (the reference's simulation rejects
+    it, simengine.py:184-186): levels from the tensor-core complexity MLP over
+    per-request activations, the easiest-predicted queue and every byte of the
+    CSV equal the oracle extension (oracle/simulate.py: fp64 mlp_forward
+    argmax + 1 per request during its prefill, predictor.py:398-402)."""
+    import numpy as np
+
+    from oracle import simulate as osim
+    from paper_2509_24957_b200.simengine import run_simulation
+    from tests.test_gpu_difficulty import activations, complexity_mlp
+    case = next(c for c in cases() if c["schedule"] == "easiest-predicted")
+    workload, orch, timing, synth = facade_inputs(case)
+    n = len(workload.requests)
+    w = complexity_mlp(7, (512, 256, 256), head=5, act="gelu")
+    X = activations(8, n, 512)
+    report, logs = run_simulation(workload, orch, policy, "easiest-predicted", case["arrivals"],
+                                  timing, case["seed"], synthetic=synth, difficulty_mode="mlp",
+                                  difficulty_weights=w, difficulty_activations=X)
+    traces, knobs = oracle_traces_knobs(case)
+    rows = osim.simulate(traces, knobs, policy, "easiest-predicted",
+                         case["arrivals"], case["timing"], case["seed"], case["rho"],
+                         difficulty_mode="mlp", mlp_weights=w, mlp_activations=X)
+    assert [(lg.request_id, lg.difficulty_predicted) for lg in logs] == \
+        [(r[0], r[12]) for r in rows]
+    assert len({r[12] for r in rows}) > 1
+    c = tmp_path / "r.csv"
+    from paper_2509_24957_b200.simengine import write_results_csv
+    write_results_csv(logs, policy, "easiest-predicted", c)
+    assert c.read_bytes().decode() == osim.csv_text(rows, policy, "easiest-predicted")
