@@ -458,6 +458,23 @@ class DynasorRun(_BaselineRun):
             raise ValueError("dynasor_window must be >= 2")
         super().__init__(trace, config, rng)
 
+    def step(self) -> RoundReport:
+        """Every branch active at the round start and not at its natural end is
+        probed this round (orchestrator.py:539-556): its probe_history gets the
+        (position, answer) of every round, not only the terminal one."""
+        if self.done:
+            raise RuntimeError("request already terminated")
+        from .workload import probe_answer
+        was_active = [b.status == ACTIVE for b in self.branches]
+        self._engine.baseline_round()
+        kept = [len(b.probe_history) for b in self.branches]
+        rep = DuchessRun._mirror_round(self)
+        for b, br in enumerate(self.branches[:len(was_active)]):
+            if was_active[b] and br.status != NATURAL_END:
+                del br.probe_history[kept[b]:]
+                br.probe_history.append((br.position, probe_answer(br.template, br.position)))
+        return rep
+
 
 def make_request_run(policy: str, trace: RequestTrace, config: OrchestratorConfig,
                      rng: random.Random | None = None,

@@ -416,3 +416,27 @@ def test_baseline_facades_match_reference_behaviour():
     with pytest.raises(RuntimeError, match="request already terminated"):
         run.step()
     del CANCELLED
+
+
+def test_dynasor_facade_probe_history_matches_oracle():
+    """DynasorRun probes every active branch each round (orchestrator.py:539-556);
+    the facade mirrors every probe into probe_history, as the oracle's
+    DynasorRequest (and the reference) record them."""
+    from oracle import port
+    from paper_2509_24957_b200.orchestrator import DynasorRun, OrchestratorConfig
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    wl = generate_synthetic(SyntheticParams(templates_per_request=6), 6, seed=5)
+    cfg = OrchestratorConfig(max_branches=4, interval_tokens=32, dynasor_window=3)
+    knobs = port.Knobs(max_branches=4, interval_tokens=32, dynasor_window=3)
+    for t in wl.requests:
+        run = DynasorRun(t, cfg)
+        run.run()
+        ref = port.DynasorRequest(port.Trace(t.id, t.ground_truth, t.prompt_tokens,
+                                             [port.Tmpl(x.natural_length, x.final_answer,
+                                                        list(x.probes), x.oracle_convergence,
+                                                        x.pred_probs) for x in t.templates],
+                                             t.difficulty), knobs)
+        ref.run()
+        assert [b.probe_history for b in run.branches] == \
+            [b.probe_history for b in ref.branches], t.id
+        assert any(len(b.probe_history) > 1 for b in run.branches)
