@@ -28,7 +28,8 @@ def raw(rep):
 
 
 summary = {}
-for name in ("k1_full", "k1rows_full", "round_full", "k3_full", "k4_full", "tc_full", "step_full"):
+for name in ("k1_full", "k1rows_full", "round_full", "kv_full", "k3_full", "k4_full", "tc_full",
+             "mlp1_full", "mlp2_full", "step_full"):
     rep = f"{src}/{name}.ncu-rep"
     if not os.path.exists(rep):
         continue
@@ -45,29 +46,45 @@ for name in ("k1_full", "k1rows_full", "round_full", "k3_full", "k4_full", "tc_f
 with open(f"{dst}/ncu_full_summary.json", "w") as f:
     json.dump(summary, f, indent=1)
 
-# launch list of the default bench (C2)
-rows = list(csv.reader(open(f"{src}/launches_c2.csv")))
-hdr, data = None, collections.defaultdict(dict)
-for r in rows:
-    if r and r[0] == "ID":
-        hdr = r
-        continue
-    if hdr and len(r) == len(hdr):
-        d = dict(zip(hdr, r))
-        data[(int(d["ID"]), d["Kernel Name"])][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
-agg = collections.defaultdict(list)
-for (i, k), m in sorted(data.items()):
-    agg[k.split("(")[0]].append(m)
-with open(f"{dst}/launches_c2_summary.txt", "w") as f:
-    f.write("ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-            "--clock-control none  python bench.py --steps 8 --warmup 3 (cold-cache, serialised)\n")
-    f.write(f"{'kernel':55s} {'n':>4s} {'mean_us':>9s} {'min_us':>8s} {'max_us':>8s} {'rd_MB':>9s} {'wr_MB':>8s}\n")
-    for k, ms in agg.items():
-        t = [m["gpu__time_duration.sum"] / 1e3 for m in ms]
-        rd = [m.get("dram__bytes_read.sum", 0) / 1e6 for m in ms]
-        wr = [m.get("dram__bytes_write.sum", 0) / 1e6 for m in ms]
-        f.write(f"{k[:55]:55s} {len(t):4d} {sum(t)/len(t):9.2f} {min(t):8.2f} {max(t):8.2f} "
-                f"{sum(rd)/len(rd):9.2f} {sum(wr)/len(wr):8.2f}\n")
-os.system(f"cp {src}/launches_c2.csv {dst}/launches_c2.csv")
-print(open(f"{dst}/launches_c2_summary.txt").read())
+UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+        "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+
+
+def launch_list(csv_name: str, title: str) -> None:
+    """Per-kernel summary of an ncu launch list (us, MB; units from the CSV)."""
+    path = f"{src}/{csv_name}.csv"
+    if not os.path.exists(path):
+        return
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, collections.defaultdict(dict)
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            v = float(d["Metric Value"].replace(",", "")) * UNIT.get(d["Metric Unit"], 1.0)
+            data[(int(d["ID"]), d["Kernel Name"])][d["Metric Name"]] = v
+    agg = collections.defaultdict(list)
+    for (_i, k), m in sorted(data.items()):
+        agg[k.split("(")[0]].append(m)
+    tot = sum(m["gpu__time_duration.sum"] for ms in agg.values() for m in ms)
+    with open(f"{dst}/{csv_name}_summary.txt", "w") as f:
+        f.write(title + "\n")
+        f.write(f"{'kernel':55s} {'n':>4s} {'mean_us':>9s} {'min_us':>8s} {'max_us':>8s} "
+                f"{'rd_MB':>9s} {'wr_MB':>8s} {'share':>6s}\n")
+        for k, ms in sorted(agg.items(), key=lambda x: -sum(m["gpu__time_duration.sum"] for m in x[1])):
+            t = [m["gpu__time_duration.sum"] for m in ms]
+            rd = [m.get("dram__bytes_read.sum", 0) for m in ms]
+            wr = [m.get("dram__bytes_write.sum", 0) for m in ms]
+            f.write(f"{k[:55]:55s} {len(t):4d} {sum(t)/len(t):9.2f} {min(t):8.2f} {max(t):8.2f} "
+                    f"{sum(rd)/len(rd):9.2f} {sum(wr)/len(wr):8.2f} {sum(t)/tot:6.1%}\n")
+    os.system(f"cp {path} {dst}/{csv_name}.csv")
+    print(open(f"{dst}/{csv_name}_summary.txt").read())
+
+
+launch_list("launches_c2", "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+            "dram__bytes_write.sum --clock-control none  python bench.py --steps 8 --warmup 3 "
+            "(cold-cache, serialised: compare shares, not absolutes)")
+launch_list("launches_c3mlp", "the same for python bench.py --config c3mlp --steps 4 --warmup 2")
 print(json.dumps(summary, indent=1))
