@@ -60,32 +60,36 @@ class QueueEntry:
     predicted_difficulty: int | None = None
 
 
-def pack_keys(levels, arrivals, orders) -> np.ndarray:
+def pack_keys(levels, arrivals, orders, tiebreak=None) -> np.ndarray:
     """64-bit sort keys ordering like the tuples (level, arrival, order)
     (scheduler.py:84-90). Fast path: level < 8, arrival < 2^40 ms,
     order < 2^21 packed directly; otherwise each field is replaced by its
     dense rank (order-preserving) and packed with just enough bits, so any
-    integer fields sort exactly as the reference's tuples."""
-    lv = np.asarray([int(x) for x in levels], dtype=object)
-    ar = np.asarray([int(x) for x in arrivals], dtype=object)
-    od = np.asarray([int(x) for x in orders], dtype=object)
-    n = len(lv)
+    integer fields sort exactly as the reference's tuples. `tiebreak` (e.g.
+    the queue index) appends a last field so equal tuples keep the order the
+    reference's strict `<` scan gives them (the first in the queue wins)."""
+    cols = [levels, arrivals, orders] + ([] if tiebreak is None else [tiebreak])
+    cols = [np.asarray([int(x) for x in f], dtype=object) for f in cols]
+    n = len(cols[0])
     if n == 0:
         return np.zeros(0, dtype=np.uint64)
-    if (min(lv) >= 0 and max(lv) <= 7 and min(ar) >= 0 and max(ar) < (1 << _ARRIVAL_BITS)
-            and min(od) >= 0 and max(od) < (1 << _ORDER_BITS)):
+    lv, ar, od = cols[:3]
+    if (tiebreak is None and min(lv) >= 0 and max(lv) <= 7 and min(ar) >= 0
+            and max(ar) < (1 << _ARRIVAL_BITS) and min(od) >= 0 and max(od) < (1 << _ORDER_BITS)):
         return ((lv.astype(np.uint64) << np.uint64(61)) | (ar.astype(np.uint64) << np.uint64(_ORDER_BITS))
                 | od.astype(np.uint64))
     fields, bits = [], []
-    for f in (lv, ar, od):
+    for f in cols:
         uniq = sorted(set(f.tolist()))
         rank = {v: i for i, v in enumerate(uniq)}
         fields.append(np.asarray([rank[v] for v in f.tolist()], dtype=np.uint64))
         bits.append(max(1, (len(uniq) - 1).bit_length()))
     if sum(bits) > 64:
         raise ValueError("queue snapshot too large for 64-bit difficulty keys")
-    return ((fields[0] << np.uint64(bits[1] + bits[2])) | (fields[1] << np.uint64(bits[2]))
-            | fields[2])
+    key = np.zeros(n, dtype=np.uint64)
+    for f, b in zip(fields, bits):
+        key = (key << np.uint64(b)) | f
+    return key
 
 
 def device_sort(keys: np.ndarray, device="cuda") -> list:
@@ -149,5 +153,9 @@ def next_request(queue: list, policy: str, now: int) -> QueueEntry:
         od.append(e.order)
     if not idx:
         raise ValueError("no eligible request")
-    first = device_sort(pack_keys(lv, ar, od))[0]
+    # equal (level, arrival, order) tuples: the reference keeps the first in
+    # queue order (strict `<`); the bitonic sort is not stable, so the queue
+    # position becomes a last key field
+    dup = len(set(zip(lv, ar, od))) < len(idx)
+    first = device_sort(pack_keys(lv, ar, od, tiebreak=range(len(idx)) if dup else None))[0]
     return queue.pop(idx[first])

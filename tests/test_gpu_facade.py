@@ -357,6 +357,40 @@ def test_next_request_golden_orders():
     del EASIEST_ACTUAL
 
 
+def test_next_request_ties_and_wide_fields_match_reference_scan():
+    """Duplicate (level, arrival, order) tuples keep the first queue entry
+    (the reference's strict `<` scan, scheduler.py:91-93); negative, large
+    and > 7 levels go through the rank-packed keys."""
+    from paper_2509_24957_b200.scheduler import EASIEST_ACTUAL, FCFS, QueueEntry, next_request
+    from paper_2509_24957_b200.workload import BranchTemplate, RequestTrace
+
+    def ref_pick(q, policy):
+        best, bk = -1, None
+        for i, e in enumerate(q):
+            k = ((e.arrival, e.order) if policy == FCFS
+                 else (e.trace.difficulty, e.arrival, e.order))
+            if bk is None or k < bk:
+                best, bk = i, k
+        return best
+
+    rng = random.Random(9)
+    for case in range(40):
+        n = rng.randint(1, 24)
+        wide = case % 2 == 1
+        q = []
+        for j in range(n):
+            lv = rng.choice([-3, 0, 9, 2 ** 40]) if wide else rng.randint(1, 3)
+            ar = rng.choice([0, 5, 2 ** 45]) if wide else rng.randint(0, 3)
+            od = rng.choice([0, 1, 2 ** 30]) if wide else rng.randint(0, 2)
+            q.append(QueueEntry(RequestTrace(f"q{j}", "1", 0, [BranchTemplate(10, "1")], lv),
+                                ar, od))
+        policy = FCFS if case % 3 == 0 else EASIEST_ACTUAL
+        qr = list(q)
+        while q:
+            want = qr.pop(ref_pick(qr, policy))
+            assert next_request(q, policy, 2 ** 50) is want
+
+
 def test_difficulty_queue_large_pool_matches_sorted():
     from paper_2509_24957_b200.scheduler import difficulty_queue
     rng = random.Random(2)

@@ -96,3 +96,25 @@ def test_trace_prediction_steps_match_reference():
     t = W.BranchTemplate(100, "1", [], None, [(16, 0.25), (32, 0.75)])
     for pos, want in G["trace_prediction"]:
         assert W.trace_prediction(t, pos) == float.fromhex(want)
+
+
+def test_pack_keys_order_like_tuples():
+    """pack_keys sorts like (level, arrival, order[, tiebreak]) tuples on both
+    the fixed-width fast path and the rank-packed path (scheduler.py:84-93)."""
+    import random as _r
+
+    import numpy as _np
+
+    from paper_2509_24957_b200.scheduler import pack_keys
+    rng = _r.Random(4)
+    for wide in (False, True):
+        for _ in range(20):
+            n = rng.randint(1, 50)
+            lv = [rng.choice([-2, 0, 7, 40]) if wide else rng.randint(0, 7) for _ in range(n)]
+            ar = [rng.choice([0, 3, 2 ** 44]) if wide else rng.randint(0, 9) for _ in range(n)]
+            od = [rng.randint(0, 5) for _ in range(n)]
+            tb = list(range(n))
+            keys = pack_keys(lv, ar, od, tiebreak=tb)
+            got = [int(i) for i in _np.argsort(keys, kind="stable")]
+            assert got == sorted(range(n), key=lambda j: (lv[j], ar[j], od[j], j))
+            assert len(set(keys.tolist())) == n
