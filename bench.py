@@ -1356,6 +1356,44 @@ def run_reference(args, cfg):
     }
 
 
+# BASELINE configs measured after the C2 headline on the plain `python bench.py`
+# run (N = 1), so every config's number comes from the driver's own run:
+# configs[0] (c1), configs[2] per GPU (c3, its T = 1 row c3t1, its tensor-core
+# MLP-probe variant c3mlp), configs[3] (c4), configs[4] per GPU (c5).
+SECONDARY = ["c1", "c3", "c3t1", "c3mlp", "c4", "c5"]
+SECONDARY_TIMEOUT_S = 300
+SECONDARY_KEYS = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "dtype",
+                  "scaling", "config", "roofline", "e2e", "cpu_baseline", "clocks",
+                  "gpu_launches", "counters", "error")
+
+
+def run_secondary(names):
+    """One `bench.py --config <name>` subprocess per name (same interpreter,
+    default K / W, bounded by SECONDARY_TIMEOUT_S); returns {name: its JSON
+    line, trimmed to the contract's keys} or {name: {"error": ...}}."""
+    import subprocess
+    res = {}
+    for name in names:
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", name,
+               "--secondary", "none"]
+        if name in ("c3t1", "c3mlp"):
+            cmd += ["--e2e-steps", "4"]
+        t0 = time.time()
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=SECONDARY_TIMEOUT_S,
+                               cwd=ROOT)
+            lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+            if p.returncode != 0 or not lines:
+                res[name] = {"error": f"rc={p.returncode}: {p.stderr.strip()[-300:]}"}
+            else:
+                d = json.loads(lines[-1])
+                res[name] = {k: d[k] for k in SECONDARY_KEYS if k in d}
+        except subprocess.TimeoutExpired:
+            res[name] = {"error": f"timeout after {SECONDARY_TIMEOUT_S} s"}
+        res[name]["wall_s"] = round(time.time() - t0, 1)
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1379,7 +1417,12 @@ def main():
     ap.add_argument("--slots", type=int, default=None,
                     help="tests only: override the config's request slots (pool scaled)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default=None,
+                    help="comma-separated configs measured after the headline and embedded "
+                         "in its line under 'secondary' (one subprocess each, bounded); "
+                         f"default on the plain N = 1 run: {','.join(SECONDARY)}; 'none' skips")
     args = ap.parse_args()
+    default_run = args.config is None
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config is None:
         args.config = "c2" if world_env == 1 else "c3"
@@ -1432,6 +1475,13 @@ def main():
             out["cpu_baseline"] = cpu_fork_or_train(small)["cpu_baseline"]
         elif world == 1 and not args.no_cpu_baseline and args.config == "c3tc":
             out["cpu_baseline"] = cpu_c3tc()
+        names = (SECONDARY if args.secondary is None and default_run and world == 1
+                 else [] if args.secondary in (None, "none")
+                 else [x for x in args.secondary.split(",") if x])
+        if names:
+            # the other BASELINE configs, measured by this same driver-run command
+            # (each in its own process: C3 alone holds ~100 GB of activation slabs)
+            out["secondary"] = run_secondary(names)
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch

@@ -3,5 +3,5 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider --deselect tests/test_gpu_zz_bench_multirank.py > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 tail -5 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo bench rc=$?
+timeout 600 python bench.py --config c2 --steps 50 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo bench rc=$?
 tail -c 3000 gpurun_out/bench_c2.json

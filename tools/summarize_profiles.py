@@ -47,7 +47,12 @@ with open(f"{dst}/ncu_full_summary.json", "w") as f:
     json.dump(summary, f, indent=1)
 
 UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
-        "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+        "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6,
+        "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3,
+        "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
+
+
+STEP_KERNELS = ("score_", "round_kernel", "kv_round_kernel", "mlp_probe_tc", "linear_kernel")
 
 
 def launch_list(csv_name: str, title: str) -> None:
@@ -69,16 +74,21 @@ def launch_list(csv_name: str, title: str) -> None:
     for (_i, k), m in sorted(data.items()):
         agg[k.split("(")[0]].append(m)
     tot = sum(m["gpu__time_duration.sum"] for ms in agg.values() for m in ms)
+    # share of the serving step: the per-round kernels only (setup fills, the e2e
+    # pass's host gathers and the read-only peak probe excluded)
+    is_step = {k: any(s in k for s in STEP_KERNELS) for k in agg}
+    step_tot = sum(m["gpu__time_duration.sum"] for k, ms in agg.items() if is_step[k] for m in ms)
     with open(f"{dst}/{csv_name}_summary.txt", "w") as f:
         f.write(title + "\n")
         f.write(f"{'kernel':55s} {'n':>4s} {'mean_us':>9s} {'min_us':>8s} {'max_us':>8s} "
-                f"{'rd_MB':>9s} {'wr_MB':>8s} {'share':>6s}\n")
+                f"{'rd_MB':>9s} {'wr_MB':>8s} {'share':>6s} {'step':>6s}\n")
         for k, ms in sorted(agg.items(), key=lambda x: -sum(m["gpu__time_duration.sum"] for m in x[1])):
             t = [m["gpu__time_duration.sum"] for m in ms]
             rd = [m.get("dram__bytes_read.sum", 0) for m in ms]
             wr = [m.get("dram__bytes_write.sum", 0) for m in ms]
             f.write(f"{k[:55]:55s} {len(t):4d} {sum(t)/len(t):9.2f} {min(t):8.2f} {max(t):8.2f} "
-                    f"{sum(rd)/len(rd):9.2f} {sum(wr)/len(wr):8.2f} {sum(t)/tot:6.1%}\n")
+                    f"{sum(rd)/len(rd):9.2f} {sum(wr)/len(wr):8.2f} {sum(t)/tot:6.1%} "
+                    + (f"{sum(t)/step_tot:6.1%}" if is_step[k] else f"{'-':>6s}") + "\n")
     os.system(f"cp {path} {dst}/{csv_name}.csv")
     print(open(f"{dst}/{csv_name}_summary.txt").read())
 
