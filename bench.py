@@ -1480,7 +1480,15 @@ def main():
                  else [x for x in args.secondary.split(",") if x])
         if names:
             # the other BASELINE configs, measured by this same driver-run command
-            # (each in its own process: C3 alone holds ~100 GB of activation slabs)
+            # (each in its own process: C3 alone holds ~100 GB of activation slabs,
+            # so this process first hands its cached device memory back)
+            import gc
+
+            import torch
+            gc.collect()
+            torch.cuda.empty_cache()
+            print(f"secondary configs: {torch.cuda.memory_reserved() / 2**30:.2f} GiB still "
+                  f"reserved by the headline process", file=sys.stderr)
             out["secondary"] = run_secondary(names)
         print(json.dumps(out), flush=True)
     if world > 1:

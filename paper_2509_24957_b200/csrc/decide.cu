@@ -336,7 +336,32 @@ __device__ __forceinline__ void load_meta(const DuchessWorkload& w, const Duches
 }
 
 // Creation-order ranks of occupied slots; returns the number occupied.
-__device__ __forceinline__ int order_slots(SlotCache& c, int C, int lane) {
+// Branch ids are unique within a request, so with C <= 32 and ids < 256 a
+// slot's rank is a popcount over a warp-wide OR of id bits (one redux per 32
+// ids, all independent) instead of a serial scan of the C slots.
+__device__ __forceinline__ int order_slots(SlotCache& c, int C, int B, int lane) {
+  if (C <= 32 && B <= 256) {
+    const int b = lane < C ? c.bid[lane] : -1;
+    const bool occ = b >= 0;
+    const int bw = b >> 5;
+    const unsigned bit = 1u << (b & 31);
+    int rk = 0, n = 0;
+    const int nw = (B + 31) >> 5;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q >= nw) break;
+      const unsigned m = __reduce_or_sync(0xffffffffu, occ && bw == q ? bit : 0u);
+      const int pc = __popc(m);
+      rk += bw > q ? pc : (bw == q ? __popc(m & (bit - 1u)) : 0);
+      n += pc;
+    }
+    if (occ) {
+      c.rank[lane] = rk;
+      c.order[rk] = lane;
+    }
+    __syncwarp();
+    return n;
+  }
   int n = 0;
   for (int base = 0; base < C; base += 32) {
     const int j = base + lane;
@@ -609,8 +634,8 @@ __device__ void clear_round_inputs(const DuchessPolicy& pol, const DuchessState&
 }
 
 // Phases 2-5 for slot r whose phase-1 record is live (cache not yet loaded
-// unless cache_loaded). Completes round_rec.
-__device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
+// unless cache_loaded). Completes round_rec. Returns the pool request decided.
+__device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, SlotCache& c, int lane,
                             const double* probs, bool wait_inputs = false) {
   const int C = pol.max_branches;
@@ -700,7 +725,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   if (words_ready)
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
   __syncwarp();
-  const int n_surv = order_slots(c, C, lane);
+  const int n_surv = order_slots(c, C, s.branch_cap, lane);
   if (wait_inputs) pdl_wait();                     // the scorer's probabilities are final
   double pr0 = 0.0, pr1 = 0.0;
   if (dev_probs) {
@@ -851,16 +876,21 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     // 0..k-1 (each child repeats its source's raw); lane k % 32 records idx_k.
     // Child fields are resolved after the loop.
     int pick0 = -1, pick1 = -1, n = n_alive, amb = 0;
+    // Tree prefix of the last entry, tracked in a register: each child's prefix
+    // is p_last + raw, the same sum the appending lane stores.
+    double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
+    // margin factor 4 (2n + 9) ulp, stepped by 8 ulp per appended entry
+    constexpr double kUlp4 = 4.0 * 1.1102230246251565e-16;
+    double mfac = double(2 * n + 9) * kUlp4;
     for (int k = 0; k < n_forks; ++k) {
       const double u = __shfl_sync(0xffffffffu, k < 32 ? u0 : u1, k & 31);
-      const double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
       // The reference picks the first j with u < acc_j, acc_j the sequential
       // sum of fl(raw_i / total_c). acc_j, P_j / total and the running sum
       // differ by less than (3n + 10) ulp of the total, so away from a
       // 4 (2n + 9) ulp margin the pick is read off the prefixes; otherwise
       // lane 0 replays the exact sequential walk with the compensated total.
       const double thr = __dmul_rn(u, run_sum);
-      const double margin = 4.0 * double(2 * n + 9) * 1.1102230246251565e-16 * run_sum;
+      const double margin = mfac * run_sum;
       const bool v0 = lane < n, v1 = lane + 32 < n;
       const bool near = (v0 && fabs(thr - P0) <= margin) || (v1 && fabs(thr - P1) <= margin);
       int idx;
@@ -869,6 +899,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         const unsigned b1 = __ballot_sync(0xffffffffu, v1 && thr < P1);
         idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
       } else {
+        __syncwarp();                                       // c.raw[0, n) written
         NeumaierSum sum;
         for (int q = 0; q < n; ++q) sum.add(c.raw[q]);
         const double total = sum.result();
@@ -884,18 +915,20 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         idx = __shfl_sync(0xffffffffu, idx, 0);
       }
       const double src_raw = __shfl_sync(0xffffffffu, idx >= 32 ? rw1 : rw0, idx & 31);
+      p_last = p_last + src_raw;
       if (lane == (n & 31)) {                               // append child k as entry n
-        if (n < 32) { rw0 = src_raw; P0 = p_last + src_raw; }
-        else        { rw1 = src_raw; P1 = p_last + src_raw; }
+        if (n < 32) { rw0 = src_raw; P0 = p_last; }
+        else        { rw1 = src_raw; P1 = p_last; }
       }
       if (lane == (k & 31)) {
         if (k < 32) pick0 = idx; else pick1 = idx;
       }
       if (lane == 0) c.raw[n] = src_raw;                    // for the exact fallback
       run_sum = __dadd_rn(run_sum, src_raw);
+      mfac += 2.0 * kUlp4;
       ++n;
-      __syncwarp();
     }
+    __syncwarp();
     // Resolve children by pointer jumping over the pick chains: a child's
     // source is an alive entry or an earlier child. Root / last_prediction
     // come from the alive entry at the chain's end; the offset is the
@@ -1074,6 +1107,7 @@ __device__ void decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       s.needs_refill[r] = 0;
     }
   }
+  return p;
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
@@ -1113,7 +1147,7 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
 // completion order (the round kernel has no grid-wide barrier to rank slots).
 __device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkload& w,
                                    const DuchessState& s, int r, SlotCache& c, int lane,
-                                   bool cache_valid, int32_t* pop) {
+                                   bool cache_valid, int32_t* pop, int p_decided = -1) {
   const int C = pol.max_branches;
   if (cache_valid ? c.need_refill : s.needs_refill[r]) {
     int q = 0;
@@ -1142,6 +1176,8 @@ __device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkl
     __syncwarp();
     return p;
   }
+  // decided this round and not finished: still serving the same request
+  if (cache_valid && p_decided >= 0) return p_decided;
   if (s.done[r]) return -1;
   const int p = s.slot_req[r];
   if (p < 0) return -1;
@@ -1172,8 +1208,9 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   if (r >= s.n_slots) return;
   trace_mark(s, r, 12, lane);
   const bool had_round = __ldcg(s.p1_rec + int64_t(r) * kP1Words) != 0;
+  int p_dec = -1;
   if (had_round) {
-    decide_slot(pol, w, s, r, c, lane, probs, true);   // waits for the scorer inside
+    p_dec = decide_slot(pol, w, s, r, c, lane, probs, true);   // waits for the scorer inside
   } else {
     pdl_wait();
     if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
@@ -1181,7 +1218,8 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   const int par = s.active_count[kListPar];
   trace_mark(s, r, 8, lane);
   clear_round_inputs(pol, s, r, lane);
-  const int p = slot_prologue_atomic(pol, w, s, r, c, lane, had_round, s.queue_head + 1);
+  const int p = slot_prologue_atomic(pol, w, s, r, c, lane, had_round, s.queue_head + 1,
+                                     p_dec);
   trace_mark(s, r, 10, lane);
   if (p >= 0) {
     Phase1Out fo{};
@@ -1200,6 +1238,7 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
       s.queue_head[0] = s.queue_head[1];
     }
   }
+  trace_mark(s, r, 13, lane);
 }
 
 // ---------------------------------------------------------------------------

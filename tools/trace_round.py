@@ -5,7 +5,8 @@ phase times from the kernel's globaltimer marks (DuchessState.trace):
 w123 = state gather waves + scorer wait, p23 = predictions + early
 termination, alive = alive list + raws, forks = branch-out loop + child
 resolution, p5 = request termination + vote, end = outcome stores,
-prologue = refill (atomic pop) or reload, phase1 = next round's phase 1.
+prologue = refill (atomic pop) or reload, phase1 = next round's phase 1,
+exit = the list-parity exit counter (fence + atomic).
 
     python tools/trace_round.py [R] [config]
 """
@@ -36,7 +37,7 @@ fill_windows(slab, 3)
 logit = torch.empty((rows, cfg["L"]), device="cuda")
 eng.advance()
 tr = None
-names = ["w123", "p23", "alive", "forks", "p5", "end", "prologue", "phase1"]
+names = ["w123", "p23", "alive", "forks", "p5", "end", "prologue", "phase1", "exit"]
 agg, durs, allph = [], [], []
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for step in range(140):
@@ -59,13 +60,13 @@ for step in range(140):
     t0 = t[:, 12].min()
     live = t[:, 0] > 0
     rel = lambda k: (t[:, k] - t0) / 1e3  # noqa: E731
-    marks = [rel(k) for k in (0, 1, 2, 3, 4, 5, 8, 10, 11)]
-    endt = rel(11)
-    ph_all = np.stack([marks[i + 1] - marks[i] for i in range(8)], 1)[live]
+    marks = [rel(k) for k in (0, 1, 2, 3, 4, 5, 8, 10, 11, 13)]
+    endt = rel(13)
+    ph_all = np.stack([marks[i + 1] - marks[i] for i in range(9)], 1)[live]
     allph.append(ph_all)
     worst = np.argsort(np.where(live, endt, -1))[-5:]
     for r in worst:
-        agg.append([marks[i + 1][r] - marks[i][r] for i in range(8)]
+        agg.append([marks[i + 1][r] - marks[i][r] for i in range(9)]
                    + [endt[r], rel(0)[r], t[r, 6], t[r, 7]])
 a = np.array(agg)
 ph = np.concatenate(allph)
@@ -75,6 +76,6 @@ print("all-slot phase medians (us):",
       {n: round(float(np.median(ph[:, i])), 2) for i, n in enumerate(names)})
 print("slowest-slot phase medians (us):",
       {n: round(float(np.median(a[:, i])), 2) for i, n in enumerate(names)})
-print("slowest end (us from first start) median", round(float(np.median(a[:, 8])), 2),
-      "| first mark after start median", round(float(np.median(a[:, 9])), 2),
-      "| forks", float(np.median(a[:, 10])), "terms", float(np.median(a[:, 11])))
+print("slowest end (us from first start) median", round(float(np.median(a[:, 9])), 2),
+      "| first mark after start median", round(float(np.median(a[:, 10])), 2),
+      "| forks", float(np.median(a[:, 11])), "terms", float(np.median(a[:, 12])))
