@@ -276,10 +276,11 @@ struct SlotCache {
   int alive_root[kMaxC];
   int src_idx[kMaxC];
   double raw[kMaxC];
+  double raw_slot[kMaxC];  // branch_raw of slot j's new prediction (phase 2)
   double wts[kMaxC];
   double draws[kMaxC];
   int nat[kMaxC];        // natural length of the template in slot j (for phase 1)
-  int t0, rounds, tok_dec, tok_prb;   // request's template base and counters
+  int t0, n_tmpl, rounds, tok_dec, tok_prb;   // request's template base / count, counters
   int need_refill;                    // set by decide_slot: the request just finished
   int tally_delta[64];   // this round's terminations, per answer id (answer_cap <= 64)
   uint32_t words[2 * kMaxC];
@@ -324,8 +325,10 @@ __device__ __forceinline__ void load_slot(const DuchessState& s, int64_t rC, int
 __device__ __forceinline__ void load_meta(const DuchessWorkload& w, const DuchessState& s, int r,
                                           int p, int C, SlotCache& c, int lane) {
   const int t0 = w.tmpl_off[p];
+  const int t1 = w.tmpl_off[p + 1];
   if (lane == 0) {
     c.t0 = t0;
+    c.n_tmpl = t1 - t0;
     c.rounds = s.rounds[r];
     c.tok_dec = s.tokens_decode[r];
     c.tok_prb = s.tokens_probe[r];
@@ -477,6 +480,7 @@ __device__ void refill_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     s.rounds[r] = 0;
     s.done[r] = 0;
     c.t0 = t0;
+    c.n_tmpl = n_tmpl;
     c.rounds = 0;
     c.tok_dec = 0;
     c.tok_prb = 0;
@@ -623,6 +627,8 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     p1[3] = dtok;
     p1[4] = probes;
     p1[5] = p;
+    p1[6] = t0;                  // template base / count: the decision of this
+    p1[7] = c.n_tmpl;            // round gathers the template headers in wave 2
   }
 }
 
@@ -653,7 +659,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   // launch (wait_inputs) they run before griddepcontrol.wait, overlapping
   // the scorer's tail; mutable state is read through L2 (ld.cg).
   // ---- wave 1: everything addressed by the slot alone, issued together ----
-  const int p1v = lane < 6 ? __ldcg(p1 + lane) : 0;
+  const int p1v = lane < kP1Words ? __ldcg(p1 + lane) : 0;
   const int sb0 = lane < C ? __ldcg(s.slot_branch + rC + lane) : -1;
   const int sb1 = lane + 32 < C ? __ldcg(s.slot_branch + rC + lane + 32) : -1;
   int tl0 = 0, tl1 = 0;
@@ -675,10 +681,11 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   if (lane < 64) c.tally_delta[lane] = 0;
   c.tally_delta[lane + 32 < 64 ? lane + 32 : 63] = 0;
-  // ---- wave 2: template base + branch fields ----
-  const int t0 = w.tmpl_off[p];
+  // template base / count, recorded by phase 1 (no dependent tmpl_off load)
+  const int t0 = __shfl_sync(0xffffffffu, p1v, 6);
+  const int n_tmpl = __shfl_sync(0xffffffffu, p1v, 7);
+  // ---- wave 2: branch fields, template headers (below) ----
   const uint32_t* mt_src = mt_flag ? w.mt_init + int64_t(p) * DUCHESS_MT_WORDS : mt_g;
-  const int n_tmpl = w.tmpl_off[p + 1] - t0;
   c.bid[lane] = -1;
   if (lane + 32 < kMaxC) c.bid[lane + 32] = -1;
   {
@@ -720,7 +727,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     c.nat_child[k] = w.nat_len[t0 + next_t + k];      // templates a fork could consume
   if (sb0 >= 0) c.nat[lane] = w.nat_len[t0 + sb0];     // next round's phase 1
   if (sb1 >= 0) c.nat[lane + 32] = w.nat_len[t0 + sb1];
-  if (lane == 0) c.t0 = t0;
+  if (lane == 0) { c.t0 = t0; c.n_tmpl = n_tmpl; }
   const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
   if (words_ready)
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
@@ -788,6 +795,9 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       }
       const int streak = pr > tau ? c.streak[j] + 1 : 0;   // strict > (:363)
       c.lp[j] = pr;
+      // branch-out weight of this prediction (:183), computed here so its pow
+      // overlaps the phase-3 stores; read back for the branches still alive
+      c.raw_slot[j] = branch_raw(pr, pol.inv_temperature);
       c.npred[j] += 1;
       c.streak[j] = streak;
       s.step_pred[rC + j] = pr;
@@ -841,12 +851,12 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   double lp0 = 0.0, lp1 = 0.0, rw0 = 0.0, rw1 = 0.0;
   if (lane < n_alive) {
     sl0 = c.alive_slot[lane]; rt0 = c.bid[sl0]; ps0 = c.off[sl0] + c.dec[sl0]; lp0 = c.lp[sl0];
-    rw0 = branch_raw(lp0, pol.inv_temperature);
+    rw0 = c.raw_slot[sl0];
     c.raw[lane] = rw0;
   }
   if (lane + 32 < n_alive) {
     sl1 = c.alive_slot[lane + 32]; rt1 = c.bid[sl1]; ps1 = c.off[sl1] + c.dec[sl1]; lp1 = c.lp[sl1];
-    rw1 = branch_raw(lp1, pol.inv_temperature);
+    rw1 = c.raw_slot[sl1];
     c.raw[lane + 32] = rw1;
   }
   const int n_forks = n_alive > 0 ? max(0, min(C - n_alive, n_tmpl - next_t)) : 0;
@@ -859,12 +869,6 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     } else {
       mt_idx = mt_words_global(mt_g, mt_src, mt_flag, c.mt, mt_idx, 2 * n_forks, c.words, lane);
     }
-    // The reference's normaliser is CPython's compensated sum() (:184). The fast
-    // path only needs it to within a few ulp (the margin below absorbs that), so
-    // it tracks a plain running sum; the exact compensated sum is replayed from
-    // the raws (creation order) only on the rare fallback.
-    double run_sum = 0.0;
-    for (int q = 0; q < n_alive; ++q) run_sum = __dadd_rn(run_sum, c.raw[q]);
     // Tree-order prefix sums of the raws, extended by one entry per fork.
     double P0 = warp_incl_scan(rw0, lane);
     double P1 = warp_incl_scan(rw1, lane) + __shfl_sync(0xffffffffu, P0, 31);
@@ -877,7 +881,12 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     // Child fields are resolved after the loop.
     int pick0 = -1, pick1 = -1, n = n_alive, amb = 0;
     // Tree prefix of the last entry, tracked in a register: each child's prefix
-    // is p_last + raw, the same sum the appending lane stores.
+    // is p_last + raw, the same sum the appending lane stores. It is also the
+    // normaliser of the fast path: the reference's is CPython's compensated
+    // sum() (:184), which the fast path needs only to within a few ulp (a sum
+    // of n positive terms in any order is within (n - 1) ulp of the exact
+    // total; the margin below absorbs that), and the exact compensated sum is
+    // replayed from the raws (creation order) only on the rare fallback.
     double p_last = __shfl_sync(0xffffffffu, (n - 1) >= 32 ? P1 : P0, (n - 1) & 31);
     // margin factor 4 (2n + 9) ulp, stepped by 8 ulp per appended entry
     constexpr double kUlp4 = 4.0 * 1.1102230246251565e-16;
@@ -889,8 +898,8 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       // differ by less than (3n + 10) ulp of the total, so away from a
       // 4 (2n + 9) ulp margin the pick is read off the prefixes; otherwise
       // lane 0 replays the exact sequential walk with the compensated total.
-      const double thr = __dmul_rn(u, run_sum);
-      const double margin = mfac * run_sum;
+      const double thr = __dmul_rn(u, p_last);
+      const double margin = mfac * p_last;
       const bool v0 = lane < n, v1 = lane + 32 < n;
       const bool near = (v0 && fabs(thr - P0) <= margin) || (v1 && fabs(thr - P1) <= margin);
       int idx;
@@ -915,7 +924,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         idx = __shfl_sync(0xffffffffu, idx, 0);
       }
       const double src_raw = __shfl_sync(0xffffffffu, idx >= 32 ? rw1 : rw0, idx & 31);
-      p_last = p_last + src_raw;
+      p_last = __dadd_rn(p_last, src_raw);
       if (lane == (n & 31)) {                               // append child k as entry n
         if (n < 32) { rw0 = src_raw; P0 = p_last; }
         else        { rw1 = src_raw; P1 = p_last; }
@@ -924,7 +933,6 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         if (k < 32) pick0 = idx; else pick1 = idx;
       }
       if (lane == 0) c.raw[n] = src_raw;                    // for the exact fallback
-      run_sum = __dadd_rn(run_sum, src_raw);
       mfac += 2.0 * kUlp4;
       ++n;
     }
@@ -1228,14 +1236,17 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
     phase1_slot(pol, w, s, r, p, c, lane, &fo);
   }
   trace_mark(s, r, 11, lane);
+  // Exit counter: the last warp out flips the list parity. No fence before
+  // the increment: everything this warp wrote is read only after the kernel
+  // boundary, and its queue pop (a returning atomic, consumed above) was
+  // performed before this increment was issued; the last warp reads the pop
+  // counter with an atomic, at L2.
   if (lane == 0) {
-    __threadfence();
     if (atomicAdd(s.active_count + kListExit, 1) == s.n_slots - 1) {
-      __threadfence();
       s.active_count[par] = 0;                   // consumed by the scorer this round
       s.active_count[kListPar] = par ^ 1;
       s.active_count[kListExit] = 0;
-      s.queue_head[0] = s.queue_head[1];
+      s.queue_head[0] = atomicAdd(s.queue_head + 1, 0);
     }
   }
   trace_mark(s, r, 13, lane);
