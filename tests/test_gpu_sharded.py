@@ -58,7 +58,10 @@ def _free_port():
 def _worker(rank, world, port_, q):
     import torch.distributed as dist
     torch.cuda.set_device(rank % torch.cuda.device_count())
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_}", rank=rank,
+    # NCCL (the product's backend) when every rank has its own GPU; ranks sharing
+    # one GPU use gloo (NCCL refuses two ranks on one device)
+    backend = "nccl" if torch.cuda.device_count() >= world else "gloo"
+    dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port_}", rank=rank,
                             world_size=world)
     out, order = _run()
     if rank == 0:
