@@ -484,9 +484,15 @@ def kv_report(kv0, kv1, steps, srv, cfg):
     sh = srv.shards[0]["kv"]
     d = {k: kv1[k] - kv0[k] for k in ("blocks_allocated", "blocks_released", "tail_bytes",
                                        "overflow")}
-    return {"kernels": "duchess_kv_round (kv_round_kernel: forks incl. tail copies, releases, "
-                       "appends) after every "
-                       "duchess_round, each shard's stream",
+    how = {"lead": "duchess_kv_round (kv_round_kernel: forks incl. tail copies, releases, "
+                   "appends) right after every duchess_round, releasing the next round's "
+                   "scorer, which streams beside it (DUCHESS_KV_LEAD + "
+                   "DUCHESS_SCORE_NO_INPUT_WAIT)",
+           "overlap": "duchess_kv_round after the next round's scorer, beside it "
+                      "(DUCHESS_KV_OVERLAP)",
+           "fused": "duchess_round_kv (the round kernel applies its K3 update) + "
+                    "duchess_kv_copy_tails"}[srv.kv_mode]
+    return {"kernels": how, "kv_mode": srv.kv_mode,
             "block_tokens": sh.block_tokens, "kv_bytes_per_token": sh.kv_bytes_per_token,
             "blocks_per_slot": sh.P,
             "pool_gib": sum(s["kv"].t["kv_pool"].numel() for s in srv.shards) / 2**30,

@@ -248,10 +248,10 @@ __global__ void __launch_bounds__(kTmaCons + 32, 2) score_tma_kernel(ScoreArgs a
   TmaRing rg{ring, full_bar, empty_bar, t.tokens_per_stage * t.row_bytes};
   tma_ring_init(t, rg);
   __syncthreads();
-  pdl_wait();   // setup above overlaps the previous kernel; inputs are read below
-  // The previous round is complete: let the next launch (duchess_round)
-  // become resident and prefetch its state while this one streams.
-  pdl_launch_dependents();
+  // setup above overlaps the previous kernel; inputs are read below. Then let
+  // the next launch (duchess_round) become resident and prefetch its state
+  // while this one streams.
+  k1_begin(t);
   if (t.row_par) {                     // engine list: the parity duchess_round left
     const int par = *t.row_par;
     t.row_list += par * t.list_stride;
@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kTmaCons + 32, 2) score_tma_kernel(ScoreArgs a
     return;
   }
   tma_consume<BF16, VPT>(a, t, rg, n_units, red, [](int64_t, int, int64_t) {});
+  k1_end(t);                           // thread 0 is a consumer
 }
 
 template <bool BF16>
@@ -316,8 +317,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_kernel(ScoreArg
       reinterpret_cast<float4*>(wsm)[i] = __ldg(reinterpret_cast<const float4*>(a.wg) + i);
     __syncthreads();
   }
-  pdl_wait();
-  pdl_launch_dependents();
+  k1_begin(t);
   if (t.row_par) {
     const int par = *t.row_par;
     t.row_list += par * t.list_stride;
@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_kernel(ScoreArg
     row = nrow;
     l = nl;
   }
+  k1_end(t);
 }
 
 // Last-token windows, bulk-copy variant (default). Same per-window arithmetic
@@ -469,8 +470,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_bulk_kernel(Sco
     }
     __syncthreads();
   }
-  pdl_wait();
-  pdl_launch_dependents();
+  k1_begin(t);
   if (t.row_par) {
     const int par = *t.row_par;
     t.row_list += par * t.list_stride;
@@ -622,6 +622,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) score_rows_bulk_kernel(Sco
       i = __ffs(mc) - 1;
     }
   }
+  k1_end(t);
 }
 
 // Shared-memory plan of score_rows_bulk_kernel: warps that fit beside the weights.
@@ -800,7 +801,8 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
                       const uint8_t* row_mask, const int32_t* row_list, const int32_t* row_count,
                       float* out_logit, double* out_prob, void* workspace, size_t workspace_bytes,
                       int32_t nsplit, int32_t threads, void* stream,
-                      const int32_t* row_par = nullptr, int64_t list_stride = 0) {
+                      const int32_t* row_par = nullptr, int64_t list_stride = 0,
+                      int32_t flags = 0) {
   if (n_rows < 0 || n_layers < 1 || T < 1 || H < 1) return DUCHESS_EINVAL;
   if (dtype != DUCHESS_F32 && dtype != DUCHESS_BF16) return DUCHESS_EINVAL;
   if (!acts || !wg || !c1 || !out_logit || !out_prob) return DUCHESS_EINVAL;
@@ -852,6 +854,7 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     t.row_count = row_count;
     t.row_par = row_par;
     t.list_stride = list_stride;
+    t.no_input_wait = (flags & DUCHESS_SCORE_NO_INPUT_WAIT) ? 1 : 0;
     t.row_bytes = int(row_bytes);
     t.contiguous = token_stride == H;
     // Tunables (env, for sweeps): CTAs per SM and stage size target.
@@ -986,17 +989,29 @@ extern "C" int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_row
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
+extern "C" int duchess_score_active_ex(const void* acts, int32_t dtype, int64_t n_rows,
+                                       int32_t n_layers, int32_t T, int32_t H, int64_t row_stride,
+                                       int64_t layer_stride, int64_t token_stride, const float* wg,
+                                       const float* c1, const int32_t* active_rows,
+                                       const int32_t* active_count, float* out_logit,
+                                       double* out_prob, int32_t flags, void* stream) {
+  if (!active_rows || !active_count) return DUCHESS_EINVAL;
+  if (flags & ~DUCHESS_SCORE_NO_INPUT_WAIT) return DUCHESS_EINVAL;
+  // DuchessState.active_count: [0..1] per-parity counts, [2] current parity
+  return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
+                    wg, c1, nullptr, active_rows, active_count, out_logit, out_prob, nullptr, 0, 0,
+                    0, stream, active_count + 2, n_rows, flags);
+}
+
 extern "C" int duchess_score_active(const void* acts, int32_t dtype, int64_t n_rows,
                                     int32_t n_layers, int32_t T, int32_t H, int64_t row_stride,
                                     int64_t layer_stride, int64_t token_stride, const float* wg,
                                     const float* c1, const int32_t* active_rows,
                                     const int32_t* active_count, float* out_logit,
                                     double* out_prob, void* stream) {
-  if (!active_rows || !active_count) return DUCHESS_EINVAL;
-  // DuchessState.active_count: [0..1] per-parity counts, [2] current parity
-  return score_impl(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride, token_stride,
-                    wg, c1, nullptr, active_rows, active_count, out_logit, out_prob, nullptr, 0, 0,
-                    0, stream, active_count + 2, n_rows);
+  return duchess_score_active_ex(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride,
+                                 token_stride, wg, c1, active_rows, active_count, out_logit,
+                                 out_prob, 0, stream);
 }
 
 extern "C" int duchess_gather_active(const void* src, void* dst, int64_t row_bytes,

@@ -62,7 +62,22 @@ struct TmaArgs {
   int stages;
   int row_bytes;             // H * esz
   int contiguous;            // token_stride == H
+  int no_input_wait;         // DUCHESS_SCORE_NO_INPUT_WAIT: see k1_begin
 };
+
+// Programmatic dependent launch protocol of the scorers. By default the
+// inputs (survivor list, windows) are read after griddepcontrol.wait, i.e.
+// after the preceding kernel in the stream completed. With no_input_wait the
+// inputs were final before that kernel even started (it is another request
+// shard's round), so streaming starts at once and the wait moves to the end:
+// this grid still completes only after its predecessor.
+__device__ __forceinline__ void k1_begin(const TmaArgs& t) {
+  if (!t.no_input_wait) pdl_wait();
+  pdl_launch_dependents();
+}
+__device__ __forceinline__ void k1_end(const TmaArgs& t) {
+  if (t.no_input_wait && threadIdx.x == 0) pdl_wait();
+}
 
 struct TmaRing {
   char* ring;

@@ -125,10 +125,13 @@ class Scorer:
 
 
     def score_active(self, acts: torch.Tensor, out_logit: torch.Tensor, out_prob: torch.Tensor,
-                     engine, stream=None) -> None:
+                     engine, stream=None, no_input_wait: bool = False) -> None:
         """Score the survivors of the engine's round in flight (the active list
         duchess_advance / duchess_round left; parity chosen on the device).
-        acts: [R*C, L, T, H] by branch slot."""
+        acts: [R*C, L, T, H] by branch slot. no_input_wait: the preceding
+        kernel in the stream does not produce these inputs (another request
+        shard's round launched with FLAG_EARLY_TRIGGER): stream at once
+        (duchess_score_active_ex, DUCHESS_SCORE_NO_INPUT_WAIT)."""
         _lib.require_cuda(acts)
         rows, L, T, H = acts.shape
         if L != self.bank.L or H != self.bank.H:
@@ -146,11 +149,12 @@ class Scorer:
         if dtype is None:
             raise ValueError("activations must be bf16 or fp32")
         st = acts.stride()
-        _lib.check(self.lib.duchess_score_active(
+        _lib.check(self.lib.duchess_score_active_ex(
             acts.data_ptr(), dtype, rows, L, T, H, st[0], st[1], st[2],
             self.bank.wg.data_ptr(), self.bank.c1.data_ptr(), engine.t["active_rows"].data_ptr(),
             engine.t["active_count"].data_ptr(), out_logit.data_ptr(), out_prob.data_ptr(),
-            _lib.stream_handle(stream)), "duchess_score_active")
+            _lib.SCORE_NO_INPUT_WAIT if no_input_wait else 0, _lib.stream_handle(stream)),
+            "duchess_score_active_ex")
 
 
 def fill_windows(acts: torch.Tensor, seed: int, row_req=None, row_tmpl=None, row_pos=None,

@@ -8,7 +8,10 @@ resolution, p5 = request termination + vote, end = outcome stores,
 prologue = refill (atomic pop) or reload, phase1 = next round's phase 1,
 exit = the list-parity exit counter (fence + atomic).
 
-    python tools/trace_round.py [R] [config]
+    python tools/trace_round.py [R] [config] [kv]
+
+With `kv` the round launch carries the K3 update (duchess_round_kv) and the
+K3 phases are reported: kv_forks (reset + forks), kv_release, kv_append.
 """
 import sys
 
@@ -24,6 +27,7 @@ from paper_2509_24957_b200.scheduler import difficulty_queue  # noqa: E402
 
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 name = sys.argv[2] if len(sys.argv) > 2 else "c2nokv"
+use_kv = len(sys.argv) > 3 and sys.argv[3] == "kv"
 cfg = dict(bench.CONFIGS[name], R=R)
 traces, knobs, seeds = bench.make_workload(cfg, 1000)
 eng = BatchedDuchess(traces, knobs, seeds, n_slots=R, pred_source=_lib.PRED_DEVICE,
@@ -36,9 +40,14 @@ slab = torch.empty((rows, cfg["L"], cfg["T"], cfg["H"]), dtype=torch.bfloat16, d
 fill_windows(slab, 3)
 logit = torch.empty((rows, cfg["L"]), device="cuda")
 eng.advance()
+kv = None
+if use_kv:
+    from paper_2509_24957_b200.kvfork import PagedKVCache
+    kv = PagedKVCache(eng, block_tokens=16, blocks_per_slot=4096, kv_bytes_per_token=4096)
+    kv.round()
 tr = None
 names = ["w123", "p23", "alive", "forks", "p5", "end", "prologue", "phase1", "exit"]
-agg, durs, allph = [], [], []
+agg, durs, allph, kvph = [], [], [], []
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for step in range(140):
     if step == 60:
@@ -48,8 +57,10 @@ for step in range(140):
     if tr is not None:
         tr.zero_()
     ev0.record()
-    eng.round()
+    eng.round(kv=kv, defer_copy=kv is not None)
     ev1.record()
+    if kv is not None:
+        kv.copy_tails()
     torch.cuda.synchronize()
     if step < 40:
         continue
@@ -65,6 +76,10 @@ for step in range(140):
     ph_all = np.stack([marks[i + 1] - marks[i] for i in range(9)], 1)[live]
     allph.append(ph_all)
     worst = np.argsort(np.where(live, endt, -1))[-5:]
+    if kv is not None:
+        forked = live & (t[:, 9] > 0)          # decided, not reset (the fork / release phases)
+        kvp = np.stack([rel(9) - rel(13), rel(15) - rel(9), rel(14) - rel(15)], 1)[forked]
+        kvph.append(kvp)
     for r in worst:
         agg.append([marks[i + 1][r] - marks[i][r] for i in range(9)]
                    + [endt[r], rel(0)[r], t[r, 6], t[r, 7]])
@@ -79,3 +94,9 @@ print("slowest-slot phase medians (us):",
 print("slowest end (us from first start) median", round(float(np.median(a[:, 9])), 2),
       "| first mark after start median", round(float(np.median(a[:, 10])), 2),
       "| forks", float(np.median(a[:, 11])), "terms", float(np.median(a[:, 12])))
+if kvph:
+    k = np.concatenate(kvph)
+    print("K3 phases, all-slot median / p95 / max (us):",
+          {n: (round(float(np.median(k[:, i])), 2), round(float(np.percentile(k[:, i], 95)), 2),
+               round(float(k[:, i].max()), 2))
+           for i, n in enumerate(["kv_forks", "kv_release", "kv_append"])})
