@@ -69,11 +69,6 @@ extern "C" {
  * default decides from a warp prefix sum unless u is within the rounding
  * margin of a boundary; both give identical picks — the flag exists to test that). */
 #define DUCHESS_FLAG_EXACT_CDF 1
-/* duchess_round releases its dependent launch (programmatic dependent launch)
- * as soon as its scorer's results are in, before deciding: the next kernel in
- * the stream (another request shard's scorer with DUCHESS_SCORE_NO_INPUT_WAIT)
- * starts streaming while this round is decided. */
-#define DUCHESS_FLAG_EARLY_TRIGGER 2
 
 /* Policies (orchestrator.py:47-52). DUCHESS runs through advance / decide /
  * round; the baselines through duchess_baseline_round. */
@@ -84,6 +79,8 @@ extern "C" {
 
 #define DUCHESS_MT_WORDS 625 /* 624 MT19937 words + index, as random.Random.getstate() */
 #define DUCHESS_MAX_SLOTS 64 /* max_branches limit of the warp-per-request kernel */
+/* words per slot of the optional phase trace (DuchessState.trace) */
+#define DUCHESS_TRACE_WORDS 24
 #define DUCHESS_REC_WORDS 12
 
 /* Round record fields (RoundReport, orchestrator.py:149-159, plus bookkeeping). */
@@ -210,7 +207,7 @@ typedef struct DuchessState {
   int32_t* out_error;
   int32_t* out_tally;  /* [P*A] */
   long long* counters; /* [DUCHESS_N_COUNTERS] */
-  long long* trace;    /* [R*16] optional per-slot phase timestamps (ns), or NULL */
+  long long* trace;    /* [R*DUCHESS_TRACE_WORDS] optional per-slot phase timestamps (ns), or NULL */
 } DuchessState;
 
 /* ---- K1: pooled LayerNorm + linear-probe scoring ------------------------ */
@@ -238,8 +235,8 @@ int duchess_score_active(const void* acts, int32_t dtype, int64_t n_rows, int32_
                          float* out_logit, double* out_prob, void* stream);
 /* duchess_score_active with flags: DUCHESS_SCORE_NO_INPUT_WAIT — the kernel
  * preceding this call in the stream does not produce its inputs (they were
- * final before that kernel started, e.g. it is another request shard's
- * duchess_round launched with DUCHESS_FLAG_EARLY_TRIGGER): the scorer streams
+ * final before that kernel started, e.g. duchess_kv_round with
+ * DUCHESS_KV_LEAD right after the round that produced them): the scorer streams
  * without waiting for it (programmatic dependent launch) and still completes
  * only after it. */
 #define DUCHESS_SCORE_NO_INPUT_WAIT 1
@@ -438,19 +435,17 @@ int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const int32_t* gro
  * final — e.g. the next round's duchess_score_active, so the order per round
  * is score(k+1) -> kv_round(k) -> duchess_round(k+1). */
 #define DUCHESS_KV_OVERLAP 1
-/* the forks' tail KV bytes are left to duchess_kv_copy_tails (jobs record them) */
-#define DUCHESS_KV_DEFER_COPY 2
 /* launched right after the engine's duchess_round (waits for it), releasing
  * the next launch at once: the next round's duchess_score_active_ex with
  * DUCHESS_SCORE_NO_INPUT_WAIT streams beside this update and completes only
  * after it, so the round after that sees the KV update done. */
-#define DUCHESS_KV_LEAD 4
+#define DUCHESS_KV_LEAD 2
 
 typedef struct DuchessKV {
   int32_t block_tokens;       /* tokens per block (16) */
   int32_t blocks_per_slot;    /* P */
   int32_t max_blocks;         /* table width: blocks per branch row */
-  int32_t flags;              /* DUCHESS_KV_OVERLAP | DUCHESS_KV_DEFER_COPY | DUCHESS_KV_LEAD */
+  int32_t flags;              /* DUCHESS_KV_OVERLAP or DUCHESS_KV_LEAD */
   int64_t kv_bytes_per_token; /* bytes of KV per token (one layer slice: 2*8*128*2) */
   int32_t* table;             /* [R*Bmax*max_blocks] */
   int32_t* kv_tokens;         /* [R*Bmax] tokens each row's blocks cover */
@@ -478,23 +473,6 @@ typedef struct DuchessKV {
  * duchess_round (which rewrites the round records and branch fields read). */
 int duchess_kv_round(const DuchessPolicy* policy, const DuchessState* state, const DuchessKV* kv,
                      void* stream);
-
-/* duchess_round, then (same launch, same warp per slot) the duchess_kv_round
- * update of that round on `kv` (replaces the pair duchess_round ->
- * duchess_kv_round; the KV state after the launch is identical). Requires
- * kv_warp_words(branch_cap) * 4 * 2 <= 48 KB (branch_cap <= ~6000). */
-int duchess_round_kv(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                     const DuchessState* state, const double* probs, const DuchessKV* kv,
-                     void* stream);
-
-/* The tail copies a round recorded in kv->jobs / job_count (with
- * DUCHESS_KV_DEFER_COPY): every job's partial block, all slots in one launch
- * (one CTA per slot, 256 threads, up to 64 KB in flight per CTA). Must run
- * before the next round's KV update. With DUCHESS_KV_OVERLAP in kv->flags it
- * runs beside the preceding kernel in the stream (which must not touch the
- * jobs' blocks) and waits for it only at its end. */
-int duchess_kv_copy_tails(const DuchessPolicy* policy, const DuchessState* state,
-                          const DuchessKV* kv, void* stream);
 
 /* ---- K4: logistic-regression gradient for probe training ------------------
  * grad[h] = inv_n * sum_i (sigmoid(x_i . w + w[H]) - y_i) x_ih, grad[H] = the

@@ -21,7 +21,6 @@ REASON_NONE, REASON_CONSENSUS, REASON_COVERAGE, REASON_EXHAUSTED = range(4)
 ACT_CONTINUE, ACT_TERMINATE, ACT_BRANCH_OUT = 1, 2, 3
 PRED_DEVICE, PRED_TRACE, PRED_HOST = 0, 1, 2
 FLAG_EXACT_CDF = 1
-FLAG_EARLY_TRIGGER = 2
 SCORE_NO_INPUT_WAIT = 1
 POLICY_DUCHESS, POLICY_DEFAULT_SC, POLICY_SHORT_MK, POLICY_DYNASOR = 0, 1, 2, 3
 MT_WORDS = 625
@@ -84,8 +83,8 @@ class State(C.Structure):
 KV_CNT_ALLOC, KV_CNT_FREE, KV_CNT_TAIL_BYTES, KV_CNT_OVERFLOW = range(4)
 KV_N_COUNTERS = 4
 KV_OVERLAP = 1
-KV_DEFER_COPY = 2
-KV_LEAD = 4
+KV_LEAD = 2
+TRACE_WORDS = 24    # DUCHESS_TRACE_WORDS
 KV_PTR_FIELDS = ["table", "kv_tokens", "refcount", "free_stack", "arena", "jobs", "job_count",
                  "kv_pool", "counters"]
 
@@ -146,10 +145,6 @@ SYMBOLS = {
                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "duchess_kv_round": (C.c_int, [C.POINTER(Policy), C.POINTER(State), C.POINTER(KV),
                                    C.c_void_p]),
-    "duchess_round_kv": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload), C.POINTER(State),
-                                   C.c_void_p, C.POINTER(KV), C.c_void_p]),
-    "duchess_kv_copy_tails": (C.c_int, [C.POINTER(Policy), C.POINTER(State), C.POINTER(KV),
-                                        C.c_void_p]),
     "duchess_lr_grad_workspace_bytes": (C.c_size_t, [C.c_int32]),
     "duchess_lr_grad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_int32, C.c_float, C.c_void_p, C.c_void_p, C.c_size_t,

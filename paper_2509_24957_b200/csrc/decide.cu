@@ -20,7 +20,6 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "kv_core.cuh"
 #include "score_core.cuh"
 #include "../../include/duchess_b200.h"
 
@@ -494,7 +493,7 @@ __device__ __forceinline__ void trace_mark(const DuchessState& s, int r, int k, 
   if (s.trace && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    s.trace[int64_t(r) * 16 + k] = (long long)t;
+    s.trace[int64_t(r) * DUCHESS_TRACE_WORDS + k] = (long long)t;
   }
 }
 
@@ -734,10 +733,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
   __syncwarp();
   const int n_surv = order_slots(c, C, s.branch_cap, lane);
-  if (wait_inputs) {
-    pdl_wait();                                    // the scorer's probabilities are final
-    if (pol.flags & DUCHESS_FLAG_EARLY_TRIGGER) pdl_launch_dependents();
-  }
+  if (wait_inputs) pdl_wait();                     // the scorer's probabilities are final
   double pr0 = 0.0, pr1 = 0.0;
   if (dev_probs) {
     if (lane < C) pr0 = __ldcg(probs + (rC + lane) * pol.n_layers);
@@ -1079,7 +1075,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   if (reason == DUCHESS_REASON_NONE && !any_active) reason = DUCHESS_REASON_EXHAUSTED;
   const bool done = reason != DUCHESS_REASON_NONE;
   trace_mark(s, r, 5, lane);
-  if (s.trace && lane == 0) { s.trace[int64_t(r) * 16 + 6] = n_forks; s.trace[int64_t(r) * 16 + 7] = n_term; }
+  if (s.trace && lane == 0) { s.trace[int64_t(r) * DUCHESS_TRACE_WORDS + 6] = n_forks; s.trace[int64_t(r) * DUCHESS_TRACE_WORDS + 7] = n_term; }
   if (done) {
     if (small_tally) {
       if (lane < s.answer_cap) s.out_tally[int64_t(p) * s.answer_cap + lane] = cnt0;
@@ -1210,18 +1206,10 @@ __device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkl
 // the scorer's CTAs, which trigger this launch early (programmatic dependent
 // launch), so each slot's state prefetch overlaps the scorer's tail.
 constexpr int kRoundWarps = 2;
-// dynamic shared memory cap of the fused K3 update (kv_warp_words(B) per warp):
-// branch ids up to ~6000 per request
-constexpr int kRoundKvSmemMax = 48 * 1024;
 
-// With `kv.table` set (duchess_round_kv) each warp then applies its slot's
-// K3 update (kv_slot_round: the round's forks, releases, appends) in the same
-// launch, on kv_warp_words(B) words of dynamic shared memory per warp.
 __global__ void __maxnreg__(128)
-round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs,
-             DuchessKV kv) {
+round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double* probs) {
   __shared__ SlotCache cache[kRoundWarps];
-  extern __shared__ int32_t round_kv_smem[];
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kRoundWarps + (threadIdx.x >> 5);
   SlotCache& c = cache[threadIdx.x >> 5];
@@ -1233,7 +1221,6 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
     p_dec = decide_slot(pol, w, s, r, c, lane, probs, true);   // waits for the scorer inside
   } else {
     pdl_wait();
-    if (pol.flags & DUCHESS_FLAG_EARLY_TRIGGER) pdl_launch_dependents();
     if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
   }
   const int par = s.active_count[kListPar];
@@ -1263,12 +1250,6 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
     }
   }
   trace_mark(s, r, 13, lane);
-  if (kv.table) {
-    __syncwarp();
-    kv_slot_round(pol, s, kv, r, lane,
-                  round_kv_smem + int64_t(threadIdx.x >> 5) * kv_warp_words(s.branch_cap));
-    trace_mark(s, r, 14, lane);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1726,9 +1707,8 @@ extern "C" int duchess_decide(const DuchessPolicy* policy, const DuchessWorkload
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
-static int launch_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                        const DuchessState* state, const double* probs, const DuchessKV* kv,
-                        void* stream) {
+extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
+                             const DuchessState* state, const double* probs, void* stream) {
   if (!state_ok(policy, state) || !workload) return DUCHESS_EINVAL;
   if (!state->active_rows || !state->active_count) return DUCHESS_EINVAL;
   if (policy->pred_source != DUCHESS_PRED_TRACE && probs == nullptr) return DUCHESS_EINVAL;
@@ -1737,51 +1717,17 @@ static int launch_round(const DuchessPolicy* policy, const DuchessWorkload* work
   DuchessPolicy pol = *policy;
   DuchessWorkload w = *workload;
   DuchessState st = *state;
-  DuchessKV k{};
-  size_t smem = 0;
-  if (kv) {
-    k = *kv;
-    smem = size_t(kv_warp_words(state->branch_cap)) * 4 * kRoundWarps;
-    if (smem > size_t(kRoundKvSmemMax)) return DUCHESS_EINVAL;
-    static unsigned long long attr_set = 0;   // opt-in size, once per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !(attr_set >> dev & 1ull)) {
-      cudaFuncSetAttribute(round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kRoundKvSmemMax);
-      attr_set |= 1ull << dev;
-    }
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32 * kRoundWarps);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, round_kernel, pol, w, st, probs, k);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, round_kernel, pol, w, st, probs);
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
-}
-
-extern "C" int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                             const DuchessState* state, const double* probs, void* stream) {
-  return launch_round(policy, workload, state, probs, nullptr, stream);
-}
-
-extern "C" int duchess_round_kv(const DuchessPolicy* policy, const DuchessWorkload* workload,
-                                const DuchessState* state, const double* probs,
-                                const DuchessKV* kv, void* stream) {
-  if (!kv) return DUCHESS_EINVAL;
-  if (kv->block_tokens < 1 || kv->blocks_per_slot < 1 || kv->max_blocks < 1) return DUCHESS_EINVAL;
-  if (!kv->table || !kv->kv_tokens || !kv->refcount || !kv->free_stack || !kv->arena ||
-      !kv->jobs || !kv->job_count || !kv->counters)
-    return DUCHESS_EINVAL;
-  if (kv->kv_pool && kv->kv_bytes_per_token < 1) return DUCHESS_EINVAL;
-  if (int64_t(state->n_slots) * kv->blocks_per_slot > INT32_MAX) return DUCHESS_EINVAL;
-  return launch_round(policy, workload, state, probs, kv, stream);
 }
 
 extern "C" int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,

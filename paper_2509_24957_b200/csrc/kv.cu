@@ -52,46 +52,6 @@ kv_round_kernel(DuchessPolicy pol, DuchessState s, DuchessKV kv) {
   if (!lead) pdl_wait();
 }
 
-// Deferred tail copies (DUCHESS_KV_DEFER_COPY): one CTA per slot copies each
-// job's partial block (src block -> dst block, tokens * kv_bytes_per_token
-// bytes) with 256 threads x up to 16 16-byte loads in flight, then the stores.
-constexpr int kTailThreads = 256, kTailVec = 16;
-
-__global__ void __launch_bounds__(kTailThreads)
-kv_copy_tails_kernel(DuchessState s, DuchessKV kv, int C) {
-  pdl_launch_dependents();
-  const int r = blockIdx.x;
-  const int n = kv.job_count[r];
-  const int64_t block_bytes = kv.kv_bytes_per_token * kv.block_tokens;
-  for (int q = 0; q < n; ++q) {
-    const int32_t* jb = kv.jobs + (int64_t(r) * C + q) * 4;
-    const char* sp = kv.kv_pool + int64_t(jb[0]) * block_bytes;
-    char* dp = kv.kv_pool + int64_t(jb[1]) * block_bytes;
-    const int64_t nbytes = int64_t(jb[2]) * kv.kv_bytes_per_token;
-    if (((reinterpret_cast<uintptr_t>(sp) | reinterpret_cast<uintptr_t>(dp) | uintptr_t(nbytes)) & 15) == 0) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(sp);
-      uint4* d4 = reinterpret_cast<uint4*>(dp);
-      const int64_t nv = nbytes / 16;
-      for (int64_t i0 = 0; i0 < nv; i0 += kTailVec * kTailThreads) {
-        uint4 v[kTailVec];
-#pragma unroll
-        for (int u = 0; u < kTailVec; ++u) {
-          const int64_t i = i0 + u * kTailThreads + threadIdx.x;
-          if (i < nv) v[u] = ldg_stream(s4 + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kTailVec; ++u) {
-          const int64_t i = i0 + u * kTailThreads + threadIdx.x;
-          if (i < nv) __stcs(d4 + i, v[u]);
-        }
-      }
-    } else {
-      for (int64_t i = threadIdx.x; i < nbytes; i += kTailThreads) dp[i] = sp[i];
-    }
-  }
-  pdl_wait();
-}
-
 }  // namespace duchess
 
 using namespace duchess;
@@ -129,20 +89,3 @@ extern "C" int duchess_kv_round(const DuchessPolicy* policy, const DuchessState*
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
-extern "C" int duchess_kv_copy_tails(const DuchessPolicy* policy, const DuchessState* state,
-                                     const DuchessKV* kv, void* stream) {
-  if (!policy || !state || !kv) return DUCHESS_EINVAL;
-  if (!kv->jobs || !kv->job_count) return DUCHESS_EINVAL;
-  if (!kv->kv_pool || state->n_slots == 0) return DUCHESS_OK;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(state->n_slots));
-  cfg.blockDim = dim3(kTailThreads);
-  cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (kv->flags & DUCHESS_KV_OVERLAP) ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kv_copy_tails_kernel, *state, *kv, int(policy->max_branches));
-  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
-}

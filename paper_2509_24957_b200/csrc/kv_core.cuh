@@ -1,5 +1,4 @@
-// K3 slot update shared by kv_round_kernel (kv.cu) and the fused round
-// kernel (decide.cu, duchess_round_kv). See kv.cu for the design.
+// K3 slot update (kv_round_kernel, kv.cu; see there for the design).
 #pragma once
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
@@ -60,21 +59,21 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total) {
 // and stores over 32-entry chunks rather than a chain of dependent accesses:
 // the branch fields and fork records are read in one wave, the released rows'
 // entries in one window of 512, the blocks the appends pop in one wave.
-// Optional phase timestamps (DuchessState.trace, words 9 / 15 of the slot's
-// 16: after the forks / after the releases).
+// Optional phase timestamps (DuchessState.trace, words 16-19 of the slot's
+// record: start, after the forks, after the releases, end).
 __device__ __forceinline__ void kv_trace(const DuchessState& s, int r, int k, int lane) {
   if (s.trace && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    s.trace[int64_t(r) * 16 + k] = (long long)t;
+    s.trace[int64_t(r) * DUCHESS_TRACE_WORDS + k] = (long long)t;
   }
 }
 
 // The update of slot r (one warp; `ws` = kv_warp_words(B) shared words of
-// this warp). Called by kv_round_kernel, and at the end of round_kernel when
-// the round and the KV update are one launch (duchess_round_kv).
+// this warp).
 static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, const DuchessState& s,
                                            const DuchessKV& kv, int r, int lane, int32_t* ws) {
+  kv_trace(s, r, 16, lane);
   const int B = s.branch_cap, C = pol.max_branches, NB = kv.max_blocks, bt = kv.block_tokens;
   const int P = kv.blocks_per_slot;
   int32_t* bk = ws;                                                // [B] tokens covered
@@ -209,7 +208,7 @@ static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, cons
           jb[2] = tl;
         }
       }
-      if (kv.kv_pool && !(kv.flags & DUCHESS_KV_DEFER_COPY)) {
+      if (kv.kv_pool) {
         // copy the partial tails' KV bytes (warp-wide 16-byte streams)
         const int64_t block_bytes = kv.kv_bytes_per_token * bt;
         unsigned m = __ballot_sync(0xffffffffu, tblk >= 0);
@@ -267,7 +266,7 @@ static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, cons
               jb[2] = tail;
             }
           }
-          if (blk >= 0 && kv.kv_pool && !(kv.flags & DUCHESS_KV_DEFER_COPY)) {
+          if (blk >= 0 && kv.kv_pool) {
             // copy the partial tail's KV bytes (warp-wide 16-byte streams,
             // 8 in flight per lane); tails average a few KB
             const int sblk = __shfl_sync(0xffffffffu, lane == 0 ? src[n_full] : 0, 0);
@@ -281,7 +280,7 @@ static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, cons
         __syncwarp();
       }
     }
-    kv_trace(s, r, 9, lane);
+    kv_trace(s, r, 17, lane);
     // 2. releases in (branch id, block index) order. The released rows'
     // entries are flattened in that order, read (and cleared to -1 in the
     // table) a window of 512 at a time — lane l holds entries l, l+32, ... —
@@ -337,7 +336,7 @@ static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, cons
     __syncwarp();
   }
 
-  kv_trace(s, r, 15, lane);
+  kv_trace(s, r, 18, lane);
   // 3. appends: every active row grows to ceil(position / bt) blocks; the
   // allocation sequence is (branch id, block index), one lane per block
   if (req >= 0) {
@@ -399,6 +398,7 @@ static __device__ __noinline__ void kv_slot_round(const DuchessPolicy& pol, cons
     if (n_jobs) add_counter(&kv.counters[DUCHESS_KV_CNT_TAIL_BYTES], tail_bytes);
     if (overflow) add_counter(&kv.counters[DUCHESS_KV_CNT_OVERFLOW], overflow);
   }
+  kv_trace(s, r, 19, lane);
   __syncwarp();
 }
 

@@ -350,7 +350,8 @@ class BatchedDuchess:
     # ------------------------------------------------------------------
     def enable_trace(self) -> torch.Tensor:
         """Per-slot decide phase timestamps (globaltimer ns) for profiling."""
-        self.t["trace"] = torch.zeros(self.R * 16, dtype=torch.int64, device=self.device)
+        self.t["trace"] = torch.zeros(self.R * _lib.TRACE_WORDS, dtype=torch.int64,
+                                      device=self.device)
         self.state.trace = self.t["trace"].data_ptr()
         return self.t["trace"]
 
@@ -367,22 +368,11 @@ class BatchedDuchess:
                                            p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_decide")
 
-    def round(self, probs: torch.Tensor | None = None, stream=None, kv=None,
-              defer_copy: bool = False) -> None:
+    def round(self, probs: torch.Tensor | None = None, stream=None) -> None:
         """Fused decide(k) + advance(k+1) (duchess_round, one launch, no grid
         barrier). After it, round_reports() describe round k and the row mask /
-        active list describe the survivors of round k+1. kv: a PagedKVCache of
-        this engine — its K3 update of the round runs in the same launch
-        (duchess_round_kv; the same KV state as round() then kv.round());
-        defer_copy: leave the forks' tail KV bytes to kv.copy_tails()."""
+        active list describe the survivors of round k+1."""
         p = probs if probs is not None else self.probs
-        if kv is not None:
-            kv.struct.flags = _lib.KV_DEFER_COPY if defer_copy else 0
-            _lib.check(self.lib.duchess_round_kv(self.policy, self.wl.struct, self.state,
-                                                 p.data_ptr(), kv.struct,
-                                                 _lib.stream_handle(stream)),
-                       "duchess_round_kv")
-            return
         _lib.check(self.lib.duchess_round(self.policy, self.wl.struct, self.state,
                                           p.data_ptr(), _lib.stream_handle(stream)),
                    "duchess_round")

@@ -122,13 +122,6 @@ class PagedKVCache:
                 setattr(st, name, t[name].data_ptr())
         self.struct = st
 
-    @property
-    def fusable(self) -> bool:
-        """Whether the engine's round launch can carry this cache's update
-        (BatchedDuchess.round(kv=...), duchess_round_kv): the per-warp scratch
-        of 4 * branch_cap + 4 words for 2 warps fits its 48 KB."""
-        return (4 * self.B + 4) * 4 * 2 <= 48 * 1024
-
     def round(self, stream=None, overlap: bool = False, lead: bool = False) -> None:
         """Apply the engine's latest round: forks (with the tail copies of
         their partial blocks), releases, appends. overlap: run beside the
@@ -142,16 +135,6 @@ class PagedKVCache:
         self.struct.flags = _lib.KV_OVERLAP if overlap else (_lib.KV_LEAD if lead else 0)
         _lib.check(self.lib.duchess_kv_round(self.engine.policy, self.engine.state, self.struct,
                                              _lib.stream_handle(stream)), "duchess_kv_round")
-
-    def copy_tails(self, stream=None, overlap: bool = False) -> None:
-        """The tail copies of the latest round applied with deferred copies
-        (engine.round(kv=self, defer_copy=True)): every job in one launch
-        (duchess_kv_copy_tails). Must run before the next round. overlap: run
-        beside the preceding kernel in the stream (the next round's scorer)."""
-        self.struct.flags = _lib.KV_OVERLAP if overlap else 0
-        _lib.check(self.lib.duchess_kv_copy_tails(self.engine.policy, self.engine.state,
-                                                  self.struct, _lib.stream_handle(stream)),
-                   "duchess_kv_copy_tails")
 
     def counters(self) -> dict:
         c = self.t["counters"].cpu().numpy()

@@ -129,9 +129,9 @@ class Scorer:
         """Score the survivors of the engine's round in flight (the active list
         duchess_advance / duchess_round left; parity chosen on the device).
         acts: [R*C, L, T, H] by branch slot. no_input_wait: the preceding
-        kernel in the stream does not produce these inputs (another request
-        shard's round launched with FLAG_EARLY_TRIGGER): stream at once
-        (duchess_score_active_ex, DUCHESS_SCORE_NO_INPUT_WAIT)."""
+        kernel in the stream does not produce these inputs (the engine's K3
+        launched with lead=True right after the round that did): stream at
+        once, beside it (duchess_score_active_ex, DUCHESS_SCORE_NO_INPUT_WAIT)."""
         _lib.require_cuda(acts)
         rows, L, T, H = acts.shape
         if L != self.bank.L or H != self.bank.H:

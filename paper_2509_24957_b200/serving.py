@@ -3,7 +3,7 @@
 One GPU serves a pool of requests through ``S`` independent request shards
 (``BatchedDuchess`` engines over one packed pool, each with its own slice of
 the service queue), each stepping on its own CUDA stream. A round of a shard
-is two launches:
+is two or three launches:
 
   ``Scorer.score_active``  K1: pooled LayerNorm + linear probe(s) over the
                            survivors of the round in flight (the device-side
@@ -14,7 +14,10 @@ is two launches:
   ``PagedKVCache.round``   K3 (optional, ``kv=``): the round's forks share
                            their root's KV blocks copy-on-write, ended
                            branches release theirs, decoding branches grow
-                           (kvfork.py, duchess_kv_round).
+                           (kvfork.py, duchess_kv_round). It runs right after
+                           its round and releases the next round's scorer,
+                           which streams beside it (``kv_mode="lead"``), so it
+                           is off the scorer -> round chain.
 
 Requests never interact (reference SPEC.md:295), so shards are exact: each
 request's rounds depend only on its own state, RNG stream and activation
@@ -53,8 +56,7 @@ class ShardedEngine:
     def __init__(self, traces, config, seeds, bank, *, n_slots: int, shards: int = 2,
                  queue=None, cycle: bool = False, T: int = 1, dtype=torch.bfloat16,
                  device="cuda", combine: int | None = None, n_buffers: int = 1,
-                 packed=None, kv: dict | None = None, interleave: bool | None = None,
-                 kv_mode: str | None = None):
+                 packed=None, kv: dict | None = None, kv_mode: str | None = None):
         _lib.require_cuda()
         if shards < 1 or n_slots % shards:
             raise ValueError(f"{shards} shards must evenly divide the {n_slots} request slots")
@@ -64,25 +66,12 @@ class ShardedEngine:
         #       next round's scorer at once; the scorer streams beside it
         #       (SCORE_NO_INPUT_WAIT) and completes after it, so the round after
         #       sees it done: K3 is off the scorer -> round chain;
-        #   "overlap": its own launch right after the next round's scorer, beside
-        #       it (the next round waits for it);
-        #   "fused": inside the round launch (duchess_round_kv), the tail KV
-        #       copies as one wide launch after it.
-        # (DUCHESS_KV_MODE, for measurement.)
+        #   "overlap": its own launch right after the next round's scorer,
+        #       beside it; the next round waits for it (measured 0-4% slower at
+        #       C2; DUCHESS_KV_MODE=overlap, for measurement).
         self.kv_mode = kv_mode or os.environ.get("DUCHESS_KV_MODE", "lead")
-        if self.kv_mode not in ("lead", "overlap", "fused"):
+        if self.kv_mode not in ("lead", "overlap"):
             raise ValueError(f"unknown kv_mode {self.kv_mode!r}")
-        # interleave: all shards' launches in ONE stream, K1(A) -> round(A) ->
-        # K1(B) -> round(B) -> ...: each round releases the next launch once its
-        # scorer's results are in (FLAG_EARLY_TRIGGER) and the next shard's
-        # scorer streams without waiting for that round (its inputs came from
-        # its own previous round). Measured slower at C2 (each scorer then runs
-        # alone and its tail is exposed), so off by default (DUCHESS_INTERLEAVE=1).
-        if interleave is None:
-            interleave = os.environ.get("DUCHESS_INTERLEAVE", "0") != "0"
-        self.interleave = bool(interleave) and shards > 1
-        if self.interleave and self.kv_mode == "lead":
-            self.kv_mode = "fused"               # nothing between a round and the next scorer
         self.bank = bank
         self.S, self.L, self.T, self.H = shards, bank.L, T, bank.H
         self.dtype = dtype
@@ -94,7 +83,6 @@ class ShardedEngine:
         self.packed = packed if packed is not None else pack_pool(traces, seeds, self.device)
         combine = (1 if bank.L > 1 else 0) if combine is None else combine
         self.shards = []
-        shared = torch.cuda.Stream(self.device) if self.interleave else None
         for k in range(shards):
             eng = BatchedDuchess(traces, config, seeds, n_slots=self.Rs,
                                  pred_source=_lib.PRED_DEVICE, queue=queue[k::shards],
@@ -107,13 +95,10 @@ class ShardedEngine:
             self.shards.append(dict(
                 eng=eng, scorer=scorer, acts=acts,
                 logit=torch.zeros((self.rows, bank.L), dtype=torch.float32, device=self.device),
-                stream=shared if shared is not None else torch.cuda.Stream(self.device), ev=[],
-                kv=None if kv is None else PagedKVCache(eng, **kv), kv_pending=False))
-        if self.interleave:
-            for sh in self.shards:
-                sh["eng"].policy.flags |= _lib.FLAG_EARLY_TRIGGER
+                stream=torch.cuda.Stream(self.device), ev=[],
+                kv=None if kv is None else PagedKVCache(eng, **kv), kv_pending=False,
+                kv_led=False))
         self.started = False
-        self._chained = False
 
     @property
     def engines(self):
@@ -128,28 +113,21 @@ class ShardedEngine:
 
     def join(self):
         """The caller's (current) stream waits for every shard."""
-        self._chained = False
         cur = torch.cuda.current_stream(self.device)
         for sh in self.shards:
             cur.wait_stream(sh["stream"])
 
     def flush_kv(self):
-        """Apply the KV update still pending for the latest round (step()
-        defers it, or its tail copies, to overlap the next round's scorer)."""
-        self._chained = False
+        """Apply the KV update still pending for the latest round (kv_mode
+        "overlap" defers it to run beside the next round's scorer)."""
         for sh in self.shards:
             if sh["kv_pending"]:
                 with torch.cuda.stream(sh["stream"]):
                     sh["kv"].round()
                 sh["kv_pending"] = False
-            if sh.get("tails_pending"):
-                with torch.cuda.stream(sh["stream"]):
-                    sh["kv"].copy_tails()
-                sh["tails_pending"] = False
 
     def begin(self):
         """Refill every slot and run phase 1 of the first round."""
-        self._chained = False
         self.fork()
         for sh in self.shards:
             with torch.cuda.stream(sh["stream"]):
@@ -169,8 +147,9 @@ class ShardedEngine:
             before scoring (e.g. the keyed synthetic fill of the round's
             survivors, or a host upload); by default the buffer is used as is.
         timed: bracket the scorer launch with CUDA events on the shard stream.
-        after_round(k, eng): optional hook on the shard stream after round() (with kv,
-            K3 of the round is applied during the next step: flush_kv() first).
+        after_round(k, eng): optional hook on the shard stream after round() (and,
+            with kv_mode "lead", after K3 of the round; with "overlap" K3 of the
+            round is applied during the next step: flush_kv() first).
         before_round(k, eng): optional hook on the shard stream right before
             round() — after K3 of the previous round completed.
         """
@@ -187,18 +166,12 @@ class ShardedEngine:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record(st)
-                # The last PDL launch before this scorer did not produce its
-                # inputs (hooks in between launch ordinary kernels, which
-                # complete before it starts), so it streams at once and
-                # completes after that launch:
-                #  - kv "lead": this shard's K3, released by its round, which
-                #    completed before K3 started;
-                #  - interleaved: another shard's round, released only after its
-                #    own scorer finished, which completed only after THIS
-                #    shard's previous round.
-                chained = (not timed and isinstance(sh["scorer"], Scorer)
-                           and (sh.get("kv_led") or (self.interleave and self._chained)))
-                if chained:
+                # kv "lead": the launch before this scorer is this shard's K3,
+                # which started only after the round that produced the inputs
+                # here completed (hooks in between launch ordinary kernels,
+                # which complete before the scorer starts): the scorer streams
+                # at once, beside K3, and completes after it
+                if sh["kv_led"] and not timed and isinstance(sh["scorer"], Scorer):
                     sh["scorer"].score_active(acts, sh["logit"],
                                               eng.probs.view(self.rows, self.L), eng,
                                               no_input_wait=True)
@@ -215,33 +188,17 @@ class ShardedEngine:
                     # it completes after the scorer, before this round()
                     sh["kv"].round(overlap=not timed)
                     sh["kv_pending"] = False
-                if sh.get("tails_pending"):
-                    sh["kv"].copy_tails(overlap=not timed)
-                    sh["tails_pending"] = False
                 if before_round is not None:
                     before_round(k, eng)
-                kv = sh["kv"]
-                if kv is None:
-                    eng.round()
-                elif self.kv_mode == "fused" and kv.fusable:
-                    # K2 + K3 of this round in one launch; the tail KV copies
-                    # as one wide launch (a slot's warp would copy up to 60 KB
-                    # serially), or by the slot's warp when interleaved
-                    if self.interleave:
-                        eng.round(kv=kv)
+                eng.round()
+                if sh["kv"] is not None:
+                    if self.kv_mode == "lead":
+                        sh["kv"].round(lead=True)
+                        sh["kv_led"] = True
                     else:
-                        eng.round(kv=kv, defer_copy=True)
-                        kv.copy_tails()
-                elif self.kv_mode == "lead":
-                    eng.round()
-                    kv.round(lead=True)
-                    sh["kv_led"] = True
-                else:
-                    eng.round()
-                    sh["kv_pending"] = True
+                        sh["kv_pending"] = True
                 if after_round is not None:
                     after_round(k, eng)
-                self._chained = True
 
     def run(self, max_rounds: int = 100000, fill=None, after_round=None,
             before_round=None) -> int:

@@ -38,11 +38,7 @@ def _gen(n_req, templates, c, preset, seed=7):
     return knobs, traces, [master.getrandbits(64) for _ in traces]
 
 
-def _run(traces, knobs, seeds, rho, slots, P, kv_bytes=64, block_tokens=16, check_bytes=True,
-         mode="separate"):
-    """mode: "separate" (duchess_round then duchess_kv_round), "fused" (one
-    duchess_round_kv launch, tails copied by the slot's warp), "deferred"
-    (duchess_round_kv with DUCHESS_KV_DEFER_COPY, then duchess_kv_copy_tails)."""
+def _run(traces, knobs, seeds, rho, slots, P, kv_bytes=64, block_tokens=16, check_bytes=True):
     from paper_2509_24957_b200 import _lib
     from paper_2509_24957_b200.engine import BatchedDuchess
     from paper_2509_24957_b200.kvfork import PagedKVCache
@@ -87,14 +83,8 @@ def _run(traces, knobs, seeds, rho, slots, P, kv_bytes=64, block_tokens=16, chec
     kv.round()
     check()
     for _ in range(100000):
-        if mode == "separate":
-            eng.round()
-            kv.round()
-        elif mode == "fused":
-            eng.round(kv=kv)
-        else:
-            eng.round(kv=kv, defer_copy=True)
-            kv.copy_tails()
+        eng.round()
+        kv.round()
         check()
         if eng.all_done():
             break
@@ -112,10 +102,9 @@ def test_kv_round_matches_oracle_golden_workloads(case):
     _run(traces, case_knobs(case), seeds, case["rho"], slots=min(5, len(traces)), P=512)
 
 
-@pytest.mark.parametrize("mode", ["separate", "fused", "deferred"])
 @pytest.mark.parametrize("preset,c,bt", [("gsm8k", 8, 16), ("math", 16, 16), ("math", 16, 32),
                                          ("gsm8k", 8, 24)])
-def test_kv_round_matches_oracle_forks_heavy(preset, c, bt, mode):
+def test_kv_round_matches_oracle_forks_heavy(preset, c, bt):
     """Survivors sit on multiples of interval_tokens (a partial chunk ends the
     branch), so most forks need a tail copy only when the block size does not
     divide the interval (math-like i = 80 with 32-token blocks, gsm8k-like
@@ -123,18 +112,18 @@ def test_kv_round_matches_oracle_forks_heavy(preset, c, bt, mode):
     same-round child clamped to its natural length (orchestrator.py:263)
     starts off a block boundary."""
     knobs, traces, seeds = _gen(24, 64, c, preset)
-    cnt, n_jobs = _run(traces, knobs, seeds, 0.7, slots=6, P=c * 4096 // bt, block_tokens=bt,
-                       mode=mode)
+    cnt, n_jobs = _run(traces, knobs, seeds, 0.7, slots=6, P=c * 4096 // bt, block_tokens=bt)
     assert cnt["blocks_allocated"] > 0 and cnt["blocks_released"] > 0
     if knobs.interval_tokens % bt:
         assert n_jobs > 20 and cnt["tail_bytes"] > 0
 
 
-@pytest.mark.parametrize("mode", ["lead", "overlap", "fused", "interleaved"])
+@pytest.mark.parametrize("mode", ["lead", "overlap"])
 def test_serving_loop_kv_overlapped_matches_oracle(mode):
     """The measured loop with K3 (bench.py default C2 with the KV cache, scaled down): two
-    request shards, K1 + round per shard stream, each round's KV update
-    launched overlapped with the next round's scorer. After every K3 (taken
+    request shards, K1 + round + K3 per shard stream — K3 launched right after
+    its round with the next scorer streaming beside it ("lead", the default),
+    or beside the next round's scorer ("overlap"). After every K3 (taken
     right before the next round) each occupied slot's arena equals the
     oracle arena of its request, replayed from the oracle DuchessRun fed the
     device's probabilities (predictor=, orchestrator.py:319-327)."""
@@ -148,16 +137,12 @@ def test_serving_loop_kv_overlapped_matches_oracle(mode):
     w, b, g, beta = bench.make_probe(H, L)
     bank = ProbeBank.from_linear(w, b, g, beta)
     queue = difficulty_queue([t.difficulty for t in traces])
-    # lead: K3 right after each round, the next scorer streaming beside it;
-    # overlap: K3 beside the next round's scorer; fused: K3 inside the round
-    # launch + one tail-copy launch; interleaved: both shards in one stream
+    # lead: K3 right after each round, the next scorer streaming beside it
+    # (DUCHESS_SCORE_NO_INPUT_WAIT); overlap: K3 beside the next round's scorer
     srv = ShardedEngine(traces, knobs, seeds, bank, n_slots=R, shards=2, queue=queue,
                         cycle=False, T=T, dtype=torch.bfloat16,
                         kv=dict(block_tokens=16, blocks_per_slot=P, kv_bytes_per_token=64),
-                        kv_mode="overlap" if mode == "overlap" else
-                        ("lead" if mode == "lead" else "fused"),
-                        interleave=mode == "interleaved")
-    assert srv.shards[0]["kv"].fusable
+                        kv_mode=mode)
     keyed = keyed_fill(seed)
     snaps = [[] for _ in range(2)]
     preds = [[] for _ in range(2)]

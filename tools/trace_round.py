@@ -10,7 +10,7 @@ exit = the list-parity exit counter (fence + atomic).
 
     python tools/trace_round.py [R] [config] [kv]
 
-With `kv` the round launch carries the K3 update (duchess_round_kv) and the
+With `kv` each round is followed by its K3 update (duchess_kv_round) and the
 K3 phases are reported: kv_forks (reset + forks), kv_release, kv_append.
 """
 import sys
@@ -57,17 +57,17 @@ for step in range(140):
     if tr is not None:
         tr.zero_()
     ev0.record()
-    eng.round(kv=kv, defer_copy=kv is not None)
+    eng.round()
     ev1.record()
     if kv is not None:
-        kv.copy_tails()
+        kv.round()
     torch.cuda.synchronize()
     if step < 40:
         continue
     if tr is None:
         durs.append(ev0.elapsed_time(ev1) * 1e3)
         continue
-    t = tr.view(-1, 16).cpu().numpy().astype(np.float64)
+    t = tr.view(-1, _lib.TRACE_WORDS).cpu().numpy().astype(np.float64)
     t0 = t[:, 12].min()
     live = t[:, 0] > 0
     rel = lambda k: (t[:, k] - t0) / 1e3  # noqa: E731
@@ -77,8 +77,9 @@ for step in range(140):
     allph.append(ph_all)
     worst = np.argsort(np.where(live, endt, -1))[-5:]
     if kv is not None:
-        forked = live & (t[:, 9] > 0)          # decided, not reset (the fork / release phases)
-        kvp = np.stack([rel(9) - rel(13), rel(15) - rel(9), rel(14) - rel(15)], 1)[forked]
+        forked = live & (t[:, 17] > 0)         # decided, not reset (the fork / release phases)
+        kvp = np.stack([rel(17) - rel(16), rel(18) - rel(17), rel(19) - rel(18),
+                        rel(19) - rel(16)], 1)[forked]
         kvph.append(kvp)
     for r in worst:
         agg.append([marks[i + 1][r] - marks[i][r] for i in range(9)]
@@ -99,4 +100,4 @@ if kvph:
     print("K3 phases, all-slot median / p95 / max (us):",
           {n: (round(float(np.median(k[:, i])), 2), round(float(np.percentile(k[:, i], 95)), 2),
                round(float(k[:, i].max()), 2))
-           for i, n in enumerate(["kv_forks", "kv_release", "kv_append"])})
+           for i, n in enumerate(["kv_forks", "kv_release", "kv_append", "kv_total"])})
