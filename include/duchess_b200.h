@@ -395,6 +395,13 @@ int duchess_head_logits(const void* H, int64_t M, int32_t K, const float* W, con
 /* ---- difficulty ordering (scheduler.py:60-96) --------------------------- */
 int duchess_sort_difficulty(const uint64_t* keys, const int32_t* seg_offsets, int32_t n_segs,
                             int32_t* out_perm, void* stream);
+/* The whole snapshot as one sequence (any n): out_perm = the permutation
+ * sorting (key, index) ascending — 4096-key tiles sorted in shared memory,
+ * then merge-path merge passes (device only; workspace from
+ * duchess_sort_keys_workspace_bytes(n)). */
+size_t duchess_sort_keys_workspace_bytes(int64_t n);
+int duchess_sort_keys(const uint64_t* keys, int64_t n, int32_t* out_perm, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* ---- K3: copy-on-write block-table fork ----------------------------------
  * Fork records are (child, source, table_root, prefix_tokens) int32 quads laid

@@ -136,6 +136,9 @@ SYMBOLS = {
                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "duchess_template_lookup": (C.c_int, [C.POINTER(Workload), C.c_void_p, C.c_void_p,
                                           C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "duchess_sort_keys_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "duchess_sort_keys": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t,
+                                    C.c_void_p]),
     "duchess_sort_difficulty": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                           C.c_void_p]),
     "duchess_fork_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),

@@ -13,6 +13,8 @@
 // scheduling. Chains (a child forked from a child of the same round) arrive
 // pre-resolved to the table root by duchess_decide, and the root's rows are
 // never written here, so forks are independent and run one CTA each.
+#include <utility>
+
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
 
@@ -211,9 +213,116 @@ segsort_kernel(const uint64_t* keys, const int32_t* seg_off, int32_t* out_perm) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) out_perm[lo + i] = lo + v[i];
 }
 
+// ---------------------------------------------------------------------------
+// Whole-queue sort for snapshots longer than one CTA's 4096 keys: (1) tiles of
+// kSortMax keys bitonic-sorted in shared memory (segsort_kernel over uniform
+// tiles, pairs (key, index) written to a ping-pong buffer); (2) merge passes
+// doubling the run width, each output element placed by a merge-path search:
+// thread t produces kMergeItems consecutive outputs of its pair of runs, finding
+// where its diagonal crosses the two runs by binary search, then merging
+// sequentially. Ordering is (key, index), so equal keys keep input order.
+constexpr int kMergeThreads = 256, kMergeItems = 8;
+
+__device__ __forceinline__ bool pair_less(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(1024)
+tile_sort_kernel(const uint64_t* keys, int64_t n, uint64_t* out_k, int32_t* out_i) {
+  __shared__ uint64_t k[kSortMax];
+  __shared__ int32_t v[kSortMax];
+  const int64_t lo = int64_t(blockIdx.x) * kSortMax;
+  const int cnt = int(n - lo < kSortMax ? n - lo : int64_t(kSortMax));
+  int m = 1;
+  while (m < cnt) m <<= 1;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    k[i] = i < cnt ? keys[lo + i] : ~0ull;
+    v[i] = i < cnt ? int32_t(lo + i) : 0x7fffffff;
+  }
+  __syncthreads();
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const bool gt = pair_less(k[j], v[j], k[i], v[i]);
+          if (gt == up) {
+            const uint64_t tk = k[i]; k[i] = k[j]; k[j] = tk;
+            const int32_t tv = v[i]; v[i] = v[j]; v[j] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    out_k[lo + i] = k[i];
+    out_i[lo + i] = v[i];
+  }
+}
+
+__global__ void __launch_bounds__(kMergeThreads)
+merge_pass_kernel(const uint64_t* in_k, const int32_t* in_i, int64_t n, int64_t width,
+                  uint64_t* out_k, int32_t* out_i) {
+  const int64_t d0 = (int64_t(blockIdx.x) * kMergeThreads + threadIdx.x) * kMergeItems;
+  if (d0 >= n) return;
+  const int64_t pair = d0 / (2 * width);
+  const int64_t a0 = pair * 2 * width;
+  const int64_t a1 = a0 + width < n ? a0 + width : n, b1 = a0 + 2 * width < n ? a0 + 2 * width : n;
+  const int64_t na = a1 - a0, nb = b1 - a1;
+  const int64_t d = d0 - a0;                          // diagonal within the pair
+  // merge path: the number i of A elements among the first d outputs
+  int64_t lo = d - nb > 0 ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const int64_t i = (lo + hi) >> 1;                 // A[i] vs B[d - 1 - i]
+    const int64_t j = d - 1 - i;
+    if (pair_less(in_k[a1 + j], in_i[a1 + j], in_k[a0 + i], in_i[a0 + i])) hi = i;
+    else lo = i + 1;
+  }
+  int64_t i = lo, j = d - lo;
+  const int64_t end = d0 + kMergeItems < b1 ? d0 + kMergeItems : b1;
+  for (int64_t o = d0; o < end; ++o) {
+    bool take_a;
+    if (i >= na) take_a = false;
+    else if (j >= nb) take_a = true;
+    else take_a = !pair_less(in_k[a1 + j], in_i[a1 + j], in_k[a0 + i], in_i[a0 + i]);
+    if (take_a) { out_k[o] = in_k[a0 + i]; out_i[o] = in_i[a0 + i]; ++i; }
+    else        { out_k[o] = in_k[a1 + j]; out_i[o] = in_i[a1 + j]; ++j; }
+  }
+}
+
 }  // namespace duchess
 
 using namespace duchess;
+
+extern "C" size_t duchess_sort_keys_workspace_bytes(int64_t n) {
+  if (n <= 0) return 0;
+  return size_t(n) * 2 * (sizeof(uint64_t) + sizeof(int32_t)) + 64;
+}
+
+extern "C" int duchess_sort_keys(const uint64_t* keys, int64_t n, int32_t* out_perm,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!keys || !out_perm))) return DUCHESS_EINVAL;
+  if (n > INT32_MAX) return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  if (!workspace || workspace_bytes < duchess_sort_keys_workspace_bytes(n)) return DUCHESS_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t* k0 = static_cast<uint64_t*>(workspace);
+  uint64_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  tile_sort_kernel<<<unsigned((n + kSortMax - 1) / kSortMax), 1024, 0, s>>>(keys, n, k0, i0);
+  const unsigned grid = unsigned((n + int64_t(kMergeThreads) * kMergeItems - 1) /
+                                 (int64_t(kMergeThreads) * kMergeItems));
+  for (int64_t w = kSortMax; w < n; w <<= 1) {
+    merge_pass_kernel<<<grid, kMergeThreads, 0, s>>>(k0, i0, n, w, k1, i1);
+    std::swap(k0, k1);
+    std::swap(i0, i1);
+  }
+  cudaMemcpyAsync(out_perm, i0, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
 
 extern "C" size_t duchess_fork_workspace_bytes(int32_t n_groups, int32_t group_cap) {
   if (n_groups < 0 || group_cap < 0) return 0;

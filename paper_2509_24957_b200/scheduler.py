@@ -9,7 +9,6 @@ sort over the eligible entries, popping the first.
 
 from __future__ import annotations
 
-import heapq
 import random
 from dataclasses import dataclass
 
@@ -93,8 +92,10 @@ def pack_keys(levels, arrivals, orders, tiebreak=None) -> np.ndarray:
 
 
 def device_sort(keys: np.ndarray, device="cuda") -> list:
-    """Permutation sorting unique uint64 keys ascending, on the GPU (segments
-    of <= SEGMENT_MAX keys sorted on device, merged on the host)."""
+    """Permutation sorting uint64 keys ascending (equal keys keep input order),
+    on the GPU: one CTA's shared-memory bitonic sort up to SEGMENT_MAX keys
+    (duchess_sort_difficulty), else 4096-key tiles plus merge-path merge
+    passes (duchess_sort_keys)."""
     import torch
 
     from . import _lib
@@ -103,18 +104,18 @@ def device_sort(keys: np.ndarray, device="cuda") -> list:
         return []
     lib = _lib.load()
     _lib.require_cuda()
-    segs = list(range(0, n, SEGMENT_MAX)) + [n]
     k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(device)
-    off = torch.tensor(segs, dtype=torch.int32, device=device)
     perm = torch.empty(n, dtype=torch.int32, device=device)
-    _lib.check(lib.duchess_sort_difficulty(k.data_ptr(), off.data_ptr(), len(segs) - 1,
-                                           perm.data_ptr(), _lib.stream_handle()),
-               "duchess_sort_difficulty")
-    p = perm.cpu().numpy()
-    if len(segs) == 2:
-        return [int(x) for x in p]
-    runs = [[(int(keys[j]), int(j)) for j in p[a:b]] for a, b in zip(segs[:-1], segs[1:])]
-    return [j for _, j in heapq.merge(*runs)]
+    if n <= SEGMENT_MAX:
+        off = torch.tensor([0, n], dtype=torch.int32, device=device)
+        _lib.check(lib.duchess_sort_difficulty(k.data_ptr(), off.data_ptr(), 1, perm.data_ptr(),
+                                               _lib.stream_handle()), "duchess_sort_difficulty")
+    else:
+        ws = torch.empty(int(lib.duchess_sort_keys_workspace_bytes(n)), dtype=torch.uint8,
+                         device=device)
+        _lib.check(lib.duchess_sort_keys(k.data_ptr(), n, perm.data_ptr(), ws.data_ptr(),
+                                         ws.numel(), _lib.stream_handle()), "duchess_sort_keys")
+    return [int(x) for x in perm.cpu().numpy()]
 
 
 def difficulty_queue(levels, arrivals=None, device="cuda") -> list:

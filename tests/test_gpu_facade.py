@@ -401,6 +401,19 @@ def test_difficulty_queue_large_pool_matches_sorted():
         assert difficulty_queue(levels, arrivals) == want
 
 
+def test_device_sort_merge_passes_any_size_stable():
+    """duchess_sort_keys (4096-key tiles + merge-path passes) equals a stable
+    host sort for sizes around the tile / pass boundaries, with many equal keys
+    (ties keep input order, like the reference's first-in-queue pick)."""
+    from paper_2509_24957_b200.scheduler import device_sort
+    rng = np.random.default_rng(5)
+    for n in (4097, 8191, 8192, 12289, 65536 + 3, 300001):
+        keys = rng.integers(0, max(2, n // 7), size=n, dtype=np.uint64) << np.uint64(20)
+        got = device_sort(keys)
+        want = np.argsort(keys, kind="stable").tolist()
+        assert got == want, n
+
+
 def test_probe_answer_and_trace_prediction():
     from paper_2509_24957_b200.workload import probe_answer, trace_prediction
     t = tmpl(100, "42", probes=[(16, "7"), (32, "13")], conv=64)
