@@ -25,10 +25,13 @@ into two independent request shards stepping on two CUDA streams
 (serving.ShardedEngine: requests never interact), so each shard's
 latency-bound round kernel runs while the other shard's scorer streams.
 
-Under torchrun (N > 1) the default is C3 (configs[2]: 1024 request slots x 32
-branches, 4 probe layers, H 5120) strong-scaled: every rank builds the same
-request pool and serves its shard_range share of the slots and of the pool
-(no data-path collective); barrier + max-over-ranks timing.
+Under torchrun (N > 1) the default stays C2, weak-scaled: every rank serves
+one GPU's C2 workload (256 slots) from its own share of a pool N times as large,
+so value = the whole job's branch-steps / the max-over-ranks time ("scaling":
+"weak"). `--config c3` (and c3t1 / c3mlp) strong-scales BASELINE configs[2]:
+its 1024 request slots and pool are split over the ranks. No data-path
+collective either way (requests are independent); barrier + max-over-ranks
+timing.
 
 --impl reference times the reference's own DuchessRun + mlp_forward (vendored
 unmodified into oracle/_ref by oracle/vendor_ref.py; the restatement
@@ -278,16 +281,27 @@ def roofline_figures(achieved, read_peak):
                                        ">= 4 GiB, best of 6, CUDA events) measured in this run"})}
 
 
+# Configs whose N > 1 run splits the config's requests over the ranks (BASELINE
+# configs[2]: "1024 requests ... sharded over 2/4/8 B200"); the others keep the
+# per-GPU workload fixed and add GPUs (weak scaling).
+STRONG_SCALED = ("c3", "c3t1", "c3mlp")
+
+
 def serving_plan(cfg_name, world, rank):
-    """Slots and pool share of this rank. N = 1: the config as BASELINE.json
-    states it. N > 1: strong scaling of the same config — its R request slots
-    and request pool are split over the ranks (shard_range, contiguous), no
-    data-path collective (requests are independent)."""
+    """Slots of this rank, its share of the request pool, and the pool size to
+    generate. N = 1: the config as BASELINE.json states it. N > 1, C3 variants:
+    strong scaling — the config's R request slots and its pool are split over
+    the ranks (shard_range, contiguous). N > 1, others (C1 / C2: one GPU's
+    workload): weak scaling — every rank serves R slots from its own share of a
+    pool N times as large. No data-path collective either way (requests are
+    independent, SPEC.md:295)."""
     from paper_2509_24957_b200.distributed import shard_range
     cfg = CONFIGS[cfg_name]
-    lo, hi = shard_range(cfg["R"], rank, world)
-    plo, phi = shard_range(cfg["pool"], rank, world)
-    return hi - lo, (plo, phi)
+    if cfg_name in STRONG_SCALED or world == 1:
+        lo, hi = shard_range(cfg["R"], rank, world)
+        return hi - lo, shard_range(cfg["pool"], rank, world), cfg["pool"]
+    pool = cfg["pool"] * world
+    return cfg["R"], shard_range(pool, rank, world), pool
 
 
 def run_serving(args, cfg, rank, world, local_rank):
@@ -305,12 +319,12 @@ def run_serving(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     S = args.shards
     L, T, H, C = cfg["L"], cfg["T"], cfg["H"], cfg["c"]
-    R, (plo, phi) = serving_plan(args.config, world, rank)
+    R, (plo, phi), pool = serving_plan(args.config, world, rank)
     if R % S:
         raise SystemExit(f"--shards {S} must divide this rank's {R} request slots")
     tdtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     esz = 2 if cfg["dtype"] == "bf16" else 4
-    traces, knobs, seeds = make_workload(cfg, seed=1000)      # the same pool on every rank
+    traces, knobs, seeds = make_workload(dict(cfg, pool=pool), seed=1000)   # same on every rank
     order = difficulty_queue([t.difficulty for t in traces], device=dev)
     queue = [p for p in order if plo <= p < phi]               # this rank's share, easiest first
     if cfg.get("mlp"):
@@ -445,7 +459,8 @@ def run_serving(args, cfg, rank, world, local_rank):
                 "flops_per_branch_step": flops_bs, "flops_per_launch": fl_launch,
                 "dense_flops_per_launch": dense,
                 "scorer_us_per_launch": t_s * 1e6, "launches_timed": len(k1_us)}
-    strong = world > 1
+    strong = world > 1 and args.config in STRONG_SCALED
+    weak_multi = world > 1 and not strong
     return {
         "metric": METRIC, "value": bs_all / (ms_all / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
@@ -454,15 +469,17 @@ def run_serving(args, cfg, rank, world, local_rank):
         "data": "synthetic (counter-hashed N(0,1) activations with outlier channels; "
                 "generate_synthetic workload, random-init probe)",
         "config": {"workload": f"{args.config.upper()}: {cfg['R']} request slots x {C} branches"
-                   f"{f' split over {world} GPUs ({R} per GPU)' if strong else ''}, hidden {H}, "
+                   f"{f' split over {world} GPUs ({R} per GPU)' if strong else ''}"
+                   f"{f' on each of {world} GPUs' if weak_multi else ''}, hidden {H}, "
                    f"{L} probe layer(s){' (mean of probabilities)' if L > 1 else ''}, T={T} "
                    f"pooling window, {cfg['dtype']}, {cfg['preset']} knobs, cycling pool of "
-                   f"{cfg['pool']} requests (easiest-first{', split over the GPUs' if strong else ''}), "
+                   f"{pool} requests (easiest-first{', split over the GPUs' if world > 1 else ''}), "
                    f"{n_slabs} rotating activation buffers per shard "
                    f"({slab_bytes * S / 2**30:.2f} GiB per rotation step, > L2); {S} request "
                    f"shard(s) per GPU on {S} CUDA stream(s)",
-                   "requests": cfg["R"], "branches": C, "hidden": H, "layers": L, "window": T,
-                   "pool": cfg["pool"], "slots_per_gpu": R, "shards_per_gpu": S,
+                   "requests": cfg["R"] * (world if weak_multi else 1), "branches": C,
+                   "hidden": H, "layers": L, "window": T,
+                   "pool": pool, "slots_per_gpu": R, "shards_per_gpu": S,
                    "launch": "CUDA graph replay" if graph is not None else "eager streams (PDL)",
                    "l2": "inputs larger than L2 (rotating buffers)",
                    "burn_in_rounds": BURN_IN_ROUNDS,
@@ -1409,8 +1426,9 @@ def main():
     ap.add_argument("--config", default=None,
                     choices=sorted(CONFIGS) + ["c3tc", "c4", "c5", "difficulty", "sim",
                                                "baselines"],
-                    help="default: c2 on one GPU (BASELINE.json configs[1]); c3 strong-scaled "
-                         "over the GPUs when N > 1 (configs[2], 1024 requests sharded)")
+                    help="default: c2 (BASELINE.json configs[1]; weak-scaled, one GPU's "
+                         "workload per rank, when N > 1); c3 / c3t1 / c3mlp strong-scale "
+                         "their 1024 requests over the N GPUs (configs[2])")
     ap.add_argument("--shards", type=int, default=None,
                     help="independent request shards (engines on separate CUDA streams) per "
                          "GPU; default 2 for c2 / c3 / c3t1, 1 otherwise")
@@ -1429,9 +1447,8 @@ def main():
                          f"default on the plain N = 1 run: {','.join(SECONDARY)}; 'none' skips")
     args = ap.parse_args()
     default_run = args.config is None
-    world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config is None:
-        args.config = "c2" if world_env == 1 else "c3"
+        args.config = "c2"
     cfg = CONFIGS.get(args.config)
     if args.slots and cfg is not None:
         CONFIGS[args.config] = cfg = dict(cfg, R=args.slots, pool=max(8 * args.slots, 64))

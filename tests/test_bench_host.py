@@ -45,3 +45,23 @@ def test_cpu_reference_helpers_report_value_unit_cores_kind():
     cb = bench.cpu_c3tc(n=256, reps=1)
     assert cb["value"] > 0 and cb["unit"] == "branch-steps/s" and cb["kind"] == "port"
     assert cb["cores"] >= 1 and "sample" in cb
+
+
+def test_serving_plan_weak_c2_strong_c3():
+    """N > 1: C2 (the default) keeps one GPU's workload per rank (weak
+    scaling, each rank its own share of an N-times pool); the C3 variants split
+    BASELINE configs[2]'s 1024 requests and pool over the ranks (strong)."""
+    import bench
+    for world in (1, 2, 4, 8):
+        shares, slots = [], []
+        for rank in range(world):
+            R, (lo, hi), pool = bench.serving_plan("c2", world, rank)
+            assert R == bench.CONFIGS["c2"]["R"] and pool == bench.CONFIGS["c2"]["pool"] * world
+            shares.append((lo, hi))
+            slots.append(R)
+        assert shares[0][0] == 0 and shares[-1][1] == pool
+        assert all(a[1] == b[0] for a, b in zip(shares, shares[1:]))
+        for name in bench.STRONG_SCALED:
+            got = [bench.serving_plan(name, world, r) for r in range(world)]
+            assert sum(R for R, _, _ in got) == bench.CONFIGS[name]["R"]
+            assert got[0][1][0] == 0 and got[-1][1][1] == bench.CONFIGS[name]["pool"]

@@ -21,11 +21,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("config,extra", [("c3", ["--slots", "64"]), ("c2", []),
+@pytest.mark.parametrize("config,extra", [("c3", ["--slots", "64"]), ("c2", ["--slots", "64"]),
                                           ("c5", [])])
 def test_bench_two_ranks_prints_one_aggregate_line(config, extra):
-    """Strong scaling: the config's slots / pool (C3: 1024 requests, here 64
-    slots so two ranks fit one GPU) and C5's 4M rows are split over the ranks."""
+    """Strong scaling: C3's slots / pool (1024 requests, here 64 slots so two
+    ranks fit one GPU) and C5's 4M rows are split over the ranks. Weak scaling:
+    C2 (the default) runs one GPU's workload per rank."""
     env = dict(os.environ, DUCHESS_BENCH_BACKEND="gloo")
     if config == "c5":
         env["DUCHESS_C5_ROWS"] = str(1 << 20)
@@ -39,9 +40,12 @@ def test_bench_two_ranks_prints_one_aggregate_line(config, extra):
     assert len(lines) == 1, r.stdout[-2000:]
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["steps"] == 3 and out["value"] > 0
-    assert out["scaling"] == "strong" and out["gpu_launches"] > 0
+    assert out["gpu_launches"] > 0
+    assert out["scaling"] == ("weak" if config == "c2" else "strong")
     if config == "c5":
         assert out["config"]["rows"] == 1 << 20 and out["config"]["rows_per_gpu"] == 1 << 19
         assert out["allreduce"]["backend"] == "gloo"
+    elif config == "c2":
+        assert out["config"]["slots_per_gpu"] == 64 and out["config"]["requests"] == 128
     else:
         assert out["config"]["slots_per_gpu"] * 2 == out["config"]["requests"]
