@@ -879,6 +879,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     // The serial part: fork k picks entry idx_k of the list alive + children
     // 0..k-1 (each child repeats its source's raw); lane k % 32 records idx_k.
     // Child fields are resolved after the loop.
+    trace_mark(s, r, 20, lane);
     int pick0 = -1, pick1 = -1, n = n_alive, amb = 0;
     // Tree prefix of the last entry, tracked in a register: each child's prefix
     // is p_last + raw, the same sum the appending lane stores. It is also the
@@ -937,6 +938,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       ++n;
     }
     __syncwarp();
+    trace_mark(s, r, 21, lane);
     // Resolve children by pointer jumping over the pick chains: a child's
     // source is an alive entry or an earlier child. Root / last_prediction
     // come from the alive entry at the chain's end; the offset is the
@@ -998,6 +1000,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       }
       __syncwarp();
     }
+    trace_mark(s, r, 22, lane);
     if (lane == 0) {
       if (amb) add_counter(&s.counters[DUCHESS_CNT_AMBIGUOUS], (long long)(amb));
       add_counter(&s.counters[DUCHESS_CNT_FORKS], (long long)(n_forks));

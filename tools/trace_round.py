@@ -47,7 +47,7 @@ if use_kv:
     kv.round()
 tr = None
 names = ["w123", "p23", "alive", "forks", "p5", "end", "prologue", "phase1", "exit"]
-agg, durs, allph, kvph = [], [], [], []
+agg, durs, allph, kvph, forkph = [], [], [], [], []
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for step in range(140):
     if step == 60:
@@ -76,6 +76,9 @@ for step in range(140):
     ph_all = np.stack([marks[i + 1] - marks[i] for i in range(9)], 1)[live]
     allph.append(ph_all)
     worst = np.argsort(np.where(live, endt, -1))[-5:]
+    fr = live & (t[:, 20] > 0)
+    forkph.append(np.stack([rel(20) - rel(3), rel(21) - rel(20), rel(22) - rel(21),
+                            rel(4) - rel(22)], 1)[fr])
     if kv is not None:
         forked = live & (t[:, 17] > 0)         # decided, not reset (the fork / release phases)
         kvp = np.stack([rel(17) - rel(16), rel(18) - rel(17), rel(19) - rel(18),
@@ -95,6 +98,13 @@ print("slowest-slot phase medians (us):",
 print("slowest end (us from first start) median", round(float(np.median(a[:, 9])), 2),
       "| first mark after start median", round(float(np.median(a[:, 10])), 2),
       "| forks", float(np.median(a[:, 11])), "terms", float(np.median(a[:, 12])))
+fk = np.concatenate(forkph) if forkph else None
+if fk is not None and len(fk):
+    print("fork sub-phases of slots that forked, median / p95 / max (us):",
+          {n: (round(float(np.median(fk[:, i])), 2), round(float(np.percentile(fk[:, i], 95)), 2),
+               round(float(fk[:, i].max()), 2))
+           for i, n in enumerate(["setup (words, scans, draws)", "pick loop", "children",
+                                  "stores"])})
 if kvph:
     k = np.concatenate(kvph)
     print("K3 phases, all-slot median / p95 / max (us):",
