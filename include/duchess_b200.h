@@ -196,8 +196,10 @@ typedef struct DuchessState {
   int32_t* queue_head; /* [2] */
   int32_t* active_rows;  /* [2*R*C] compacted survivor rows (r*C + slot) for K1 per list
                             parity, or NULL */
-  int32_t* active_count; /* [4]: rows listed per parity [0..1], parity of the list the next
-                            scorer reads [2], duchess_round exit counter [3] */
+  int32_t* active_count; /* [8], 8-byte aligned: rows listed per parity [0..1], parity of
+                            the list the next scorer reads [2], zero [3], duchess_round's
+                            64-bit accumulator [4..5] (rows listed | slots done << 32),
+                            zero [6..7] */
   /* outcomes by pool index [P] */
   int32_t* out_final;
   int32_t* out_reason;

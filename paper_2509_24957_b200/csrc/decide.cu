@@ -34,9 +34,9 @@ constexpr int kWarpsPerBlock = DUCHESS_K2_WARPS;
 constexpr int kMaxC = DUCHESS_MAX_SLOTS;
 constexpr int kMtN = 624, kMtM = 397;
 // DuchessState.active_count words: [0], [1] survivor rows listed per parity,
-// [2] parity of the list the next scorer launch reads, [3] duchess_round exit
-// counter.
-enum : int { kListPar = 2, kListExit = 3 };
+// [2] parity of the list the next scorer launch reads, [3] unused (zero),
+// [4..5] duchess_round's 64-bit accumulator (rows listed | slots out << 32).
+enum : int { kListPar = 2, kListAcc = 4 };
 constexpr double kProbFloor = 1e-6;   // orchestrator.py:56 BRANCH_PROB_FLOOR
 
 // ---------------------------------------------------------------------------
@@ -545,6 +545,8 @@ __device__ int slot_prologue(const DuchessPolicy& pol, const DuchessWorkload& w,
 struct Phase1Out {
   int32_t* rows;
   int32_t* count;
+  bool defer;            // do not append: report the survivor masks instead
+  unsigned mask[2];      // (defer) survivor branch slots, 32 per word
 };
 
 __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
@@ -599,7 +601,9 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     // compacted list of windows for the persistent scorer (order irrelevant)
     const unsigned m = __ballot_sync(0xffffffffu, surv);
     n_listed += __popc(m);
-    if (m && list_rows) {
+    if (fo && fo->defer) {
+      const_cast<Phase1Out*>(fo)->mask[base >> 5] = m;
+    } else if (m && list_rows) {
       int basei = 0;
       if (lane == 0) basei = atomicAdd(list_count, __popc(m));
       basei = __shfl_sync(0xffffffffu, basei, 0);
@@ -639,11 +643,32 @@ __device__ void clear_round_inputs(const DuchessPolicy& pol, const DuchessState&
   __syncwarp();
 }
 
+// Queue records a round's refills will most likely take: lane i holds the
+// record at queue position head + i, head = the pop counter read when the
+// round starts (pops happen late in the round; a position outside the window,
+// e.g. after a stale head, is loaded when popped). Read in the decision's
+// gather waves, so it overlaps the scorer's tail.
+struct QueuePrefetch {
+  int head;
+  int4 rec;
+};
+
+__device__ __forceinline__ void prefetch_queue_rec(const DuchessWorkload& w, QueuePrefetch& qp,
+                                                   int lane) {
+  qp.rec = make_int4(-1, 0, 0, 0);
+  if (w.queue_rec && w.queue_len > 0) {
+    const int q = qp.head + lane;
+    if (w.cycle || q < w.queue_len)
+      qp.rec = __ldg(reinterpret_cast<const int4*>(w.queue_rec) + (w.cycle ? q % w.queue_len : q));
+  }
+}
+
 // Phases 2-5 for slot r whose phase-1 record is live (cache not yet loaded
 // unless cache_loaded). Completes round_rec. Returns the pool request decided.
 __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, SlotCache& c, int lane,
-                            const double* probs, bool wait_inputs = false) {
+                            const double* probs, bool wait_inputs = false,
+                            QueuePrefetch* qp = nullptr) {
   const int C = pol.max_branches;
   const int64_t rC = int64_t(r) * C, rB = int64_t(r) * s.branch_cap;
   const int64_t rA = int64_t(r) * s.answer_cap;
@@ -668,6 +693,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     if (lane + 32 < s.answer_cap) tl1 = __ldcg(s.tally + rA + lane + 32);
   }
   const uint32_t mt_iw = __ldcg(mt_g + kMtN);
+  if (qp) qp->head = __ldcg(s.queue_head + 1);
   uint32_t mt_flag = mt_iw & kMtPristine;
   int mt_idx = int(mt_iw & ~kMtPristine);
   const int nb = __ldcg(s.n_branches + r);
@@ -733,6 +759,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
   __syncwarp();
   const int n_surv = order_slots(c, C, s.branch_cap, lane);
+  if (qp) prefetch_queue_rec(w, *qp, lane);
   if (wait_inputs) pdl_wait();                     // the scorer's probabilities are final
   double pr0 = 0.0, pr1 = 0.0;
   if (dev_probs) {
@@ -1158,7 +1185,8 @@ decide_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double
 // completion order (the round kernel has no grid-wide barrier to rank slots).
 __device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkload& w,
                                    const DuchessState& s, int r, SlotCache& c, int lane,
-                                   bool cache_valid, int32_t* pop, int p_decided = -1) {
+                                   bool cache_valid, int32_t* pop, int p_decided = -1,
+                                   const QueuePrefetch* qp = nullptr) {
   const int C = pol.max_branches;
   if (cache_valid ? c.need_refill : s.needs_refill[r]) {
     int q = 0;
@@ -1170,7 +1198,15 @@ __device__ int slot_prologue_atomic(const DuchessPolicy& pol, const DuchessWorkl
     if (w.queue_len > 0 && (w.cycle || q < w.queue_len)) {
       const int qi = w.cycle ? q % w.queue_len : q;
       if (w.queue_rec) {
-        rec = reinterpret_cast<const int4*>(w.queue_rec)[qi];
+        const int d = qp ? q - qp->head : -1;
+        if (d >= 0 && d < 32) {                        // prefetched at kernel start
+          rec.x = __shfl_sync(0xffffffffu, qp->rec.x, d);
+          rec.y = __shfl_sync(0xffffffffu, qp->rec.y, d);
+          rec.z = __shfl_sync(0xffffffffu, qp->rec.z, d);
+          rec.w = __shfl_sync(0xffffffffu, qp->rec.w, d);
+        } else {
+          rec = reinterpret_cast<const int4*>(w.queue_rec)[qi];
+        }
         p = rec.x;
         qr = &rec;
       } else {
@@ -1219,10 +1255,13 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   if (r >= s.n_slots) return;
   trace_mark(s, r, 12, lane);
   const bool had_round = __ldcg(s.p1_rec + int64_t(r) * kP1Words) != 0;
+  QueuePrefetch qp;
   int p_dec = -1;
   if (had_round) {
-    p_dec = decide_slot(pol, w, s, r, c, lane, probs, true);   // waits for the scorer inside
+    p_dec = decide_slot(pol, w, s, r, c, lane, probs, true, &qp);   // waits for the scorer
   } else {
+    qp.head = __ldcg(s.queue_head + 1);
+    prefetch_queue_rec(w, qp, lane);
     pdl_wait();
     if (lane == 0) s.round_rec[int64_t(r) * DUCHESS_REC_WORDS + DUCHESS_REC_ROUND] = 0;
   }
@@ -1230,27 +1269,37 @@ round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s, const double*
   trace_mark(s, r, 8, lane);
   clear_round_inputs(pol, s, r, lane);
   const int p = slot_prologue_atomic(pol, w, s, r, c, lane, had_round, s.queue_head + 1,
-                                     p_dec);
+                                     p_dec, &qp);
   trace_mark(s, r, 10, lane);
-  if (p >= 0) {
-    Phase1Out fo{};
-    fo.rows = s.active_rows + int64_t(par ^ 1) * s.n_slots * pol.max_branches;
-    fo.count = s.active_count + (par ^ 1);
-    phase1_slot(pol, w, s, r, p, c, lane, &fo);
-  }
+  Phase1Out fo{};
+  fo.defer = true;
+  if (p >= 0) phase1_slot(pol, w, s, r, p, c, lane, &fo);
   trace_mark(s, r, 11, lane);
-  // Exit counter: the last warp out flips the list parity. No fence before
-  // the increment: everything this warp wrote is read only after the kernel
+  // One 64-bit atomic per slot both reserves the slot's run of the next list
+  // (low word: rows listed so far) and counts the slot out (high word): the
+  // last warp out publishes the count and flips the list parity. No fence
+  // before it: everything this warp wrote is read only after the kernel
   // boundary, and its queue pop (a returning atomic, consumed above) was
-  // performed before this increment was issued; the last warp reads the pop
-  // counter with an atomic, at L2.
-  if (lane == 0) {
-    if (atomicAdd(s.active_count + kListExit, 1) == s.n_slots - 1) {
-      s.active_count[par] = 0;                   // consumed by the scorer this round
-      s.active_count[kListPar] = par ^ 1;
-      s.active_count[kListExit] = 0;
-      s.queue_head[0] = atomicAdd(s.queue_head + 1, 0);
-    }
+  // performed before this one was issued; the last warp reads the pop counter
+  // with an atomic, at L2.
+  const int n0 = __popc(fo.mask[0]), n1 = __popc(fo.mask[1]);
+  unsigned long long old = 0;
+  if (lane == 0)
+    old = atomicAdd(reinterpret_cast<unsigned long long*>(s.active_count + kListAcc),
+                    (1ull << 32) | unsigned(n0 + n1));
+  old = __shfl_sync(0xffffffffu, old, 0);
+  const int base = int(uint32_t(old));
+  int32_t* rows = s.active_rows + int64_t(par ^ 1) * s.n_slots * pol.max_branches;
+  const int64_t rC = int64_t(r) * pol.max_branches;
+  const unsigned below = (1u << lane) - 1u;
+  if (fo.mask[0] >> lane & 1u) rows[base + __popc(fo.mask[0] & below)] = int32_t(rC + lane);
+  if (fo.mask[1] >> lane & 1u) rows[base + n0 + __popc(fo.mask[1] & below)] = int32_t(rC + 32 + lane);
+  if (lane == 0 && int(old >> 32) == s.n_slots - 1) {
+    s.active_count[par ^ 1] = base + n0 + n1;    // the list the next scorer reads
+    s.active_count[par] = 0;                     // consumed by the scorer this round
+    s.active_count[kListPar] = par ^ 1;
+    *reinterpret_cast<unsigned long long*>(s.active_count + kListAcc) = 0ull;
+    s.queue_head[0] = atomicAdd(s.queue_head + 1, 0);
   }
   trace_mark(s, r, 13, lane);
 }

@@ -330,7 +330,7 @@ class BatchedDuchess:
         t["step_pred"] = torch.zeros(R * C, dtype=torch.float64, device=dev)
         t["queue_head"] = torch.zeros(2, **i32)
         t["active_rows"] = torch.zeros(2 * R * C, **i32)
-        t["active_count"] = torch.zeros(4, **i32)
+        t["active_count"] = torch.zeros(8, **i32)       # see DuchessState.active_count
         P = max(self.P, 1)
         for name in ("out_final", "out_reason", "out_tokens_decode", "out_tokens_probe",
                      "out_rounds", "out_error"):
