@@ -551,7 +551,7 @@ struct Phase1Out {
 
 __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
                             const DuchessState& s, int r, int p, SlotCache& c, int lane,
-                            const Phase1Out* fo = nullptr) {
+                            Phase1Out* fo = nullptr) {
   int32_t* list_rows = fo ? fo->rows : s.active_rows;
   int32_t* list_count = fo ? fo->count : s.active_count;
   if (!fo && s.active_rows) {                      // split launches: the current parity
@@ -602,7 +602,7 @@ __device__ void phase1_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
     const unsigned m = __ballot_sync(0xffffffffu, surv);
     n_listed += __popc(m);
     if (fo && fo->defer) {
-      const_cast<Phase1Out*>(fo)->mask[base >> 5] = m;
+      fo->mask[base >> 5] = m;
     } else if (m && list_rows) {
       int basei = 0;
       if (lane == 0) basei = atomicAdd(list_count, __popc(m));

@@ -16,6 +16,8 @@
 // per-row mbarriers, so one row's reduction overlaps the next row's dot,
 // measured slower: 0.74 vs 0.87 of HBM.) Per-CTA partial gradients are reduced in a
 // fixed order by a second kernel (deterministic).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
 
@@ -345,10 +347,13 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   int vpt = 1;
   while (vpt < vpt_needed) vpt <<= 1;
   if (vpt > 8) return DUCHESS_EINVAL;
-  int rb = int(lmax(1, lmin(kMaxRB, kStageBytesTarget / row_bytes)));
+  // Tunables (env, for sweeps): stage bytes target, keep the stage in registers.
+  static const int stage_target = [] { const char* e = getenv("DUCHESS_K4_STAGE"); int v = e ? atoi(e) : kStageBytesTarget; return v < 1024 ? 1024 : v; }();
+  static const int keep_mode = [] { const char* e = getenv("DUCHESS_K4_KEEP"); return e ? atoi(e) : -1; }();
+  int rb = int(lmax(1, lmin(kMaxRB, stage_target / row_bytes)));
   rb = rb >= 8 ? 8 : rb >= 4 ? 4 : rb >= 2 ? 2 : 1;   // compile-time rows per stage
   // g, w and the kept stage: VPT * (16 / esz) * (2 + rb) floats per thread
-  const bool keep = vpt * (16 / esz) * (2 + rb) <= kKeepFloats;
+  const bool keep = keep_mode != 0 && vpt * (16 / esz) * (2 + rb) <= kKeepFloats;
   const int grid = num_sms();          // one CTA per SM (3 warps per sub-partition)
   const int smem_budget = 200 * 1024;
   if (!workspace || workspace_bytes < size_t(grid) * size_t(H + 1) * sizeof(float))
