@@ -13,6 +13,7 @@
 // scheduling. Chains (a child forked from a child of the same round) arrive
 // pre-resolved to the table root by duchess_decide, and the root's rows are
 // never written here, so forks are independent and run one CTA each.
+#include <cstdlib>
 #include <utility>
 
 #include "common.cuh"
@@ -117,6 +118,7 @@ fork_plan_kernel(const int32_t* forks, int group_cap, const int32_t* counts, int
 // One CTA per (group, record) slot: copy the root's full blocks into the
 // child's row (refcount += 1 each, order-independent), the reserved tail
 // block + its KV bytes, -1 for the rest.
+template <int UNROLL>
 __global__ void __launch_bounds__(128)
 fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, ForkWs ws,
                  int32_t* table, int table_stride, int32_t* refcount, const int32_t* free_list,
@@ -158,13 +160,20 @@ fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, ForkWs
     const int64_t nv = nbytes / 16;
     const uint4* s4 = reinterpret_cast<const uint4*>(s);
     uint4* d4 = reinterpret_cast<uint4*>(d);
-    int64_t i = threadIdx.x;
-    for (; i + 3 * 128 < nv; i += 4 * 128) {
-      const uint4 a = ldg_stream(s4 + i), b = ldg_stream(s4 + i + 128);
-      const uint4 c = ldg_stream(s4 + i + 256), e = ldg_stream(s4 + i + 384);
-      __stcs(d4 + i, a); __stcs(d4 + i + 128, b); __stcs(d4 + i + 256, c); __stcs(d4 + i + 384, e);
+    // UNROLL 16-byte loads per thread in flight before their stores
+    for (int64_t i0 = 0; i0 < nv; i0 += UNROLL * 128) {
+      uint4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t i = i0 + u * 128 + threadIdx.x;
+        if (i < nv) v[u] = ldg_stream(s4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t i = i0 + u * 128 + threadIdx.x;
+        if (i < nv) __stcs(d4 + i, v[u]);
+      }
     }
-    for (; i < nv; i += 128) __stcs(d4 + i, ldg_stream(s4 + i));
   } else {
     for (int64_t i = threadIdx.x; i < nbytes; i += blockDim.x) d[i] = s[i];
   }
@@ -351,10 +360,14 @@ extern "C" int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const i
   fork_plan_kernel<<<unsigned((n_groups + kPlanWarps - 1) / kPlanWarps), kPlanWarps * 32, 0, s>>>(
       forks, group_cap, group_counts, counts_stride, n_groups, block_tokens, ws, free_cursor,
       free_list_len, status);
-  fork_exec_kernel<<<unsigned(nf), 128, 0, s>>>(forks, rows_per_group, group_cap, ws, block_table,
-                                                table_stride, refcount, free_list,
-                                                static_cast<char*>(kv_pool), kv_bytes_per_token,
-                                                block_tokens);
+  // tail-copy loads in flight per thread (env DUCHESS_K3_UNROLL, for sweeps;
+  // C4: 4 -> 0.824, 8 -> 0.83, 16 -> 0.68 of the copy peak)
+  static const int unroll = [] { const char* e = getenv("DUCHESS_K3_UNROLL"); return e ? atoi(e) : 8; }();
+  auto k = unroll >= 16 ? fork_exec_kernel<16> : unroll >= 8 ? fork_exec_kernel<8>
+         : fork_exec_kernel<4>;
+  k<<<unsigned(nf), 128, 0, s>>>(forks, rows_per_group, group_cap, ws, block_table, table_stride,
+                                 refcount, free_list, static_cast<char*>(kv_pool),
+                                 kv_bytes_per_token, block_tokens);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
