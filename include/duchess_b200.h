@@ -496,6 +496,10 @@ int duchess_sgd_update(float* w, const float* grad, int32_t n, float lr, void* s
 /* Measurement: stream `bytes` of device memory (16-byte aligned) through a
  * read-only persistent kernel (the read-only HBM ceiling, bench.py roofline). */
 int duchess_read_stream(const void* buf, int64_t bytes, uint32_t* sink, void* stream);
+/* Measurement: hold `stream` until the host writes nonzero to *host_flag
+ * (pinned host memory) or timeout_ns elapses (then *timed_out = 1, device
+ * memory), so a benchmark can enqueue its whole timed region first. */
+int duchess_gate(const int32_t* host_flag, int64_t timeout_ns, int32_t* timed_out, void* stream);
 
 const char* duchess_version(void);
 int duchess_device_arch(void);
