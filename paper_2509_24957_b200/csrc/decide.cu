@@ -757,6 +757,17 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   const bool words_ready = dev_probs && mt_idx + 2 * C <= kMtN;
   if (words_ready)
     for (int k = lane; k < 2 * C; k += 32) c.words[k] = mt_temper(__ldcg(mt_src + mt_idx + k));
+  // Each survivor's CoT-probe answer at its position (probe_answer,
+  // workload.py:82-94), searched now — speculatively, before the scorer's
+  // results are needed — for the branch that terminates this round and for
+  // the synthetic predictor's oracle term.
+  int pans[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if ((q == 0 ? sb0 : sb1) >= 0)
+      pans[q] = probe_answer_pref(w, hconv[q], hlo[q], hhi[q], hfin[q], c.off[j] + c.dec[j]);
+  }
   __syncwarp();
   const int n_surv = order_slots(c, C, s.branch_cap, lane);
   if (qp) prefetch_queue_rec(w, *qp, lane);
@@ -808,7 +819,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
           for (int qq = 0; qq < C; ++qq) k += (c.bid[qq] >= 0 && c.bid[qq] < b && c.need[qq]);
           const double u = c.draws[k];
           // synthetic_predict (predictor.py:328-335) on probe_answer == ground truth
-          const int pa = probe_answer_pref(w, hconv[q], hlo[q], hhi[q], hfin[q], pos);
+          const int pa = pans[q];
           const double oracle = pa == w.ground_truth[p] ? 1.0 : 0.0;
           const double v = __dadd_rn(__dmul_rn(pol.rho, oracle), __dmul_rn(__dsub_rn(1.0, pol.rho), u));
           pr = fmin(fmax(v, 0.0), 1.0);
@@ -838,7 +849,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       act[k * 3 + 1] = b;
       act[k * 3 + 2] = -1;
       if (term) {
-        const int ans = probe_answer_pref(w, hconv[q], hlo[q], hhi[q], hfin[q], pos);
+        const int ans = pans[q];
         c.status[j] = DUCHESS_EARLY_TERMINATED;
         s.br_status[bi] = DUCHESS_EARLY_TERMINATED;
         s.br_final[bi] = ans;

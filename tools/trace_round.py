@@ -86,7 +86,7 @@ for step in range(140):
         kvph.append(kvp)
     for r in worst:
         agg.append([marks[i + 1][r] - marks[i][r] for i in range(9)]
-                   + [endt[r], rel(0)[r], t[r, 6], t[r, 7]])
+                   + [endt[r], rel(0)[r], t[r, 6], t[r, 7], endt[r] - rel(1)[r]])
 a = np.array(agg)
 ph = np.concatenate(allph)
 print(f"config {name} R={R}: round kernel alone (events, untraced) median "
@@ -97,7 +97,9 @@ print("slowest-slot phase medians (us):",
       {n: round(float(np.median(a[:, i])), 2) for i, n in enumerate(names)})
 print("slowest end (us from first start) median", round(float(np.median(a[:, 9])), 2),
       "| first mark after start median", round(float(np.median(a[:, 10])), 2),
-      "| forks", float(np.median(a[:, 11])), "terms", float(np.median(a[:, 12])))
+      "| forks", float(np.median(a[:, 11])), "terms", float(np.median(a[:, 12])),
+      "| after the scorer wait (the part not overlapped in the pipeline)",
+      round(float(np.median(a[:, 13])), 2))
 fk = np.concatenate(forkph) if forkph else None
 if fk is not None and len(fk):
     print("fork sub-phases of slots that forked, median / p95 / max (us):",
