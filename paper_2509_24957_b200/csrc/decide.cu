@@ -941,12 +941,12 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       const double margin = mfac * p_last;
       const bool v0 = lane < n, v1 = lane + 32 < n;
       const bool near = (v0 && fabs(thr - P0) <= margin) || (v1 && fabs(thr - P1) <= margin);
-      int idx;
-      if (!(pol.flags & DUCHESS_FLAG_EXACT_CDF) && !__any_sync(0xffffffffu, near)) {
-        const unsigned b0 = __ballot_sync(0xffffffffu, v0 && thr < P0);
-        const unsigned b1 = __ballot_sync(0xffffffffu, v1 && thr < P1);
-        idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
-      } else {
+      // the prefix-sum pick and the margin vote side by side (no branch between)
+      const unsigned b0 = __ballot_sync(0xffffffffu, v0 && thr < P0);
+      const unsigned b1 = __ballot_sync(0xffffffffu, v1 && thr < P1);
+      const bool any_near = __any_sync(0xffffffffu, near);
+      int idx = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : n - 1);
+      if ((pol.flags & DUCHESS_FLAG_EXACT_CDF) || any_near) {
         __syncwarp();                                       // c.raw[0, n) written
         NeumaierSum sum;
         for (int q = 0; q < n; ++q) sum.add(c.raw[q]);
