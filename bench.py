@@ -829,7 +829,7 @@ def run_difficulty_bench(args, rank, world, local_rank):
                         "frac": tf / peak, "peak_kind": kind,
                         "kernel": "duchess_tc_linear (3 layers) + head", "flops_per_launch": flops,
                         "traffic": None},
-           "gpu_launches": 4 * args.steps, "clocks": clk}
+           "gpu_launches": (len(dims) + 1) * args.steps, "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_difficulty(w)
     return out
@@ -1425,8 +1425,10 @@ def run_reference(args, cfg):
 # BASELINE configs measured after the C2 headline on the plain `python bench.py`
 # run (N = 1), so every config's number comes from the driver's own run:
 # configs[0] (c1), configs[2] per GPU (c3, its T = 1 row c3t1, its tensor-core
-# MLP-probe variant c3mlp), configs[3] (c4), configs[4] per GPU (c5).
-SECONDARY = ["c1", "c3", "c3t1", "c3mlp", "c4", "c5"]
+# MLP-probe variant c3mlp), configs[3] (c4), configs[4] per GPU (c5), and the
+# the difficulty classifier, the baseline policies and
+# run_simulation.
+SECONDARY = ["c1", "c3", "c3t1", "c3mlp", "c4", "c5", "difficulty", "baselines", "sim"]
 SECONDARY_TIMEOUT_S = 300
 SECONDARY_KEYS = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "dtype",
                   "scaling", "config", "roofline", "e2e", "cpu_baseline", "clocks",
@@ -1443,7 +1445,8 @@ def run_secondary(names):
         cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", name,
                "--secondary", "none"]
         if name in ("c3t1", "c3mlp"):
-            cmd += ["--e2e-steps", "4"]
+            # C3's own line carries the CPU baseline of this workload
+            cmd += ["--e2e-steps", "4", "--no-cpu-baseline"]
         t0 = time.time()
         try:
             p = subprocess.run(cmd, capture_output=True, text=True, timeout=SECONDARY_TIMEOUT_S,

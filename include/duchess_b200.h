@@ -386,7 +386,8 @@ int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, int32_t G,
                               int32_t act, void* out, void* workspace, size_t workspace_bytes,
                               void* stream);
 /* Input LayerNorm as a pass: Z (bf16 [M, K]) = (X - mean) / sqrt(var + 1e-5)
- * per row of X ([M, K], DUCHESS_F32 or DUCHESS_F64), statistics in fp64
+ * per row of X ([M, K], DUCHESS_F32, DUCHESS_F64 or DUCHESS_BF16 — bf16 needs
+ * K % 8 == 0, K <= 8192 and 16-byte aligned rows), statistics in fp64
  * (predictor.py:134-136). */
 int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, int32_t K, void* Z,
                           void* stream);

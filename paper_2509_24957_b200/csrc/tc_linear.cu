@@ -371,6 +371,82 @@ __global__ void __launch_bounds__(256) row_normalize_kernel(const TX* X, int64_t
     Z[row * K + k] = f32_to_bf16_rne(float((double(x[k]) - mean) * inv));
 }
 
+// Vectorised variant for bf16 / fp32 rows with K % 8 == 0 and K <= 256 * 8 *
+// RV: each thread loads its 8-element chunks once (16 B of bf16 or 32 B of
+// fp32 per chunk) and keeps them in registers for the mean, the centred
+// square sum (fp64 accumulation) and the normalised output, stored 16 B at a
+// time.
+template <bool BF16, int RV>
+__global__ void __launch_bounds__(256) row_normalize_vec_kernel(const void* X, int64_t M, int K,
+                                                                uint16_t* Z) {
+  __shared__ double red[8];
+  const int64_t row = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nch = K / 8;
+  auto block_sum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    __syncthreads();
+    return t;
+  };
+  float v[RV][8];
+#pragma unroll
+  for (int c = 0; c < RV; ++c) {
+    const int ch = c * 256 + threadIdx.x;
+    if (ch < nch) {
+      if constexpr (BF16) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(X) + row * K) + ch);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { v[c][2 * e] = bf16lo(w4[e]); v[c][2 * e + 1] = bf16hi(w4[e]); }
+      } else {
+        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(X) + row * K) + 2 * ch;
+        const float4 a = __ldg(p), b = __ldg(p + 1);
+        v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+        v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[c][e] = 0.f;
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < RV; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += double(v[c][e]);
+  const double mean = block_sum(s) / K;
+  double q = 0.0;
+#pragma unroll
+  for (int c = 0; c < RV; ++c) {
+    if (c * 256 + int(threadIdx.x) < nch) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double d = double(v[c][e]) - mean;
+        q += d * d;
+      }
+    }
+  }
+  const double inv = 1.0 / sqrt(block_sum(q) / K + double(kLayerNormEps));
+#pragma unroll
+  for (int c = 0; c < RV; ++c) {
+    const int ch = c * 256 + threadIdx.x;
+    if (ch < nch) {
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        o[e] = uint32_t(f32_to_bf16_rne(float((double(v[c][2 * e]) - mean) * inv))) |
+               (uint32_t(f32_to_bf16_rne(float((double(v[c][2 * e + 1]) - mean) * inv))) << 16);
+      reinterpret_cast<uint4*>(Z + row * K)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 // Classifier head (N small, e.g. 5): one warp per row, fp32 dots over the
 // bf16 hidden vector, logits out.
 __global__ void head_kernel(const uint16_t* Hm, int64_t M, int K, const float* W, const float* b,
@@ -553,10 +629,25 @@ extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void
 
 extern "C" int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, int32_t K, void* Z,
                                      void* stream) {
-  if (!X || !Z || M < 0 || K < 1 || (dtype != DUCHESS_F32 && dtype != DUCHESS_F64))
+  if (!X || !Z || M < 0 || K < 1 ||
+      (dtype != DUCHESS_F32 && dtype != DUCHESS_F64 && dtype != DUCHESS_BF16))
     return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec = K % 8 == 0 && K <= 256 * 8 * 4 &&
+                   (reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Z)) % 16 == 0;
+  if (dtype == DUCHESS_BF16 || (dtype == DUCHESS_F32 && vec)) {
+    if (!vec) return DUCHESS_EINVAL;               // bf16 rows: vectorised path only
+    const int rv = (K / 8 + 255) / 256;
+    const bool bf = dtype == DUCHESS_BF16;
+    if (rv <= 1) (bf ? tcl::row_normalize_vec_kernel<true, 1> : tcl::row_normalize_vec_kernel<false, 1>)
+                     <<<unsigned(M), 256, 0, st>>>(X, M, K, static_cast<uint16_t*>(Z));
+    else if (rv <= 2) (bf ? tcl::row_normalize_vec_kernel<true, 2> : tcl::row_normalize_vec_kernel<false, 2>)
+                     <<<unsigned(M), 256, 0, st>>>(X, M, K, static_cast<uint16_t*>(Z));
+    else (bf ? tcl::row_normalize_vec_kernel<true, 4> : tcl::row_normalize_vec_kernel<false, 4>)
+             <<<unsigned(M), 256, 0, st>>>(X, M, K, static_cast<uint16_t*>(Z));
+    return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  }
   if (dtype == DUCHESS_F64)
     tcl::row_normalize_kernel<double><<<unsigned(M), 256, 0, st>>>(
         static_cast<const double*>(X), M, K, static_cast<uint16_t*>(Z));

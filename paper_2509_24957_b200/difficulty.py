@@ -101,14 +101,19 @@ class TensorCoreClassifier:
             raise WeightFormatError(f"activation shape {tuple(x.shape[1:])} does not match "
                                     f"expected ({self.weights.input_dim},)")
         # fp64 inputs stay fp64 until normalised (a large common offset would
-        # swallow an fp32 row's signal); everything else is read as fp32
-        f64 = x.dtype == torch.float64
-        xf = (x if f64 else x.to(torch.float32)).contiguous()
+        # swallow an fp32 row's signal); bf16 / fp32 rows are read as they are;
+        # anything else is read as fp32
+        K = x.shape[1]
+        if x.dtype == torch.bfloat16 and K % 8 == 0 and K <= 8192:
+            xf, dt = x.contiguous(), _lib.BF16
+        elif x.dtype == torch.float64:
+            xf, dt = x.contiguous(), _lib.F64
+        else:
+            xf, dt = x.to(torch.float32).contiguous(), _lib.F32
         M = xf.shape[0]
         stream = _lib.stream_handle()
-        h = torch.empty((M, xf.shape[1]), dtype=torch.bfloat16, device=self.device)
-        _lib.check(self.lib.duchess_row_normalize(xf.data_ptr(), _lib.F64 if f64 else _lib.F32,
-                                                  M, xf.shape[1], h.data_ptr(), stream),
+        h = torch.empty((M, K), dtype=torch.bfloat16, device=self.device)
+        _lib.check(self.lib.duchess_row_normalize(xf.data_ptr(), dt, M, K, h.data_ptr(), stream),
                    "duchess_row_normalize")
         for Wd, _S, C, BS, BT, act, width in self.layers:
             out = torch.empty((M, width), dtype=torch.bfloat16, device=self.device)

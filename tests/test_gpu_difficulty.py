@@ -6,6 +6,7 @@ row; logits within the bf16-chain tolerance stated below."""
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import port
 
@@ -97,3 +98,26 @@ def test_predict_difficulty_batch_equals_single_calls():
     single = [predict_difficulty("mlp", activation=x, weights=w) for x in X[:10]]
     assert batch[:10] == single
     assert set(batch) <= {1, 2, 3, 4, 5}
+
+
+@pytest.mark.parametrize("dtype,K", [(torch.bfloat16, 4096), (torch.bfloat16, 1032),
+                                     (torch.float32, 4096), (torch.float32, 200),
+                                     (torch.float64, 512)])
+def test_row_normalize_matches_fp64(dtype, K):
+    """duchess_row_normalize (the classifier's input LayerNorm pass,
+    predictor.py:134-136) on bf16 / fp32 / fp64 rows: z = (x - mean) / std
+    with fp64 statistics, stored bf16 — equal to the fp64 formula rounded to
+    bf16 up to one bf16 ulp (the fp64 sums' order differs)."""
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(K)
+    x = (torch.randn((300, K), generator=g, device="cuda", dtype=torch.float64) * 3 + 50).to(dtype)
+    z = torch.empty((300, K), dtype=torch.bfloat16, device="cuda")
+    dt = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32, torch.float64: _lib.F64}[dtype]
+    _lib.check(lib.duchess_row_normalize(x.data_ptr(), dt, 300, K, z.data_ptr(),
+                                         _lib.stream_handle()), "row_normalize")
+    xd = x.double()
+    ref = (xd - xd.mean(1, keepdim=True)) / torch.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-5)
+    got = z.double()
+    ulp = ref.abs().clamp_min(2 ** -126) * 2 ** -7
+    assert bool(((got - ref).abs() <= ulp).all())
