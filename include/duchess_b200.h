@@ -278,8 +278,9 @@ int duchess_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
 
 /* One round of a baseline policy for every slot (DefaultScRun.step
  * orchestrator.py:408-435, ShortMkRun.step :466-516, DynasorRun.step
- * :529-561), refill included: a refill launch ranks the slots needing a
- * request, then the policy launch runs the round. No predictions, no forks. */
+ * :529-561), refill included, in one launch: a slot whose request finished
+ * pops the service queue atomically, then the policy round runs. Needs
+ * active_count (the launch's exit count). No predictions, no forks. */
 int duchess_baseline_round(const DuchessPolicy* policy, const DuchessWorkload* workload,
                            const DuchessState* state, void* stream);
 

@@ -1515,14 +1515,15 @@ __device__ void baseline_slot(const DuchessPolicy& pol, const DuchessWorkload& w
   if (cancel || !any_active) close_slot(s, r, p, DUCHESS_REASON_EXHAUSTED, lane, rec);
 }
 
-// Two launches per baseline round, so the refill ranking reads a stable
-// snapshot: baseline_refill_kernel ranks the slots flagged needs_refill (the
-// k-th flagged slot takes queue[head + k]; nothing in this launch writes the
-// flags) and refills them; baseline_kernel then runs the policy round, which
-// clears / sets the flags for the next round. queue_head[1] (written by slot
-// 0's warp) is published to queue_head[0] by the policy launch.
+// One launch per baseline round: each slot's warp refills its slot if the
+// request there finished (the service queue popped atomically, so only its
+// own flag is read — no ranking over other slots' flags, which this launch
+// rewrites), then runs the policy round (which sets / clears the slot's flag
+// for the next round). Requests are independent, so which free slot a request
+// lands in does not change its outcome. The last warp out (one 64-bit atomic,
+// DuchessState.active_count[4..5]) publishes the pop counter to queue_head[0].
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-baseline_refill_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
+baseline_round_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
   __shared__ SlotCache cache[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -1530,23 +1531,17 @@ baseline_refill_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
   int32_t* rec0 = s.round_rec + int64_t(r) * DUCHESS_REC_WORDS;
   if (lane < DUCHESS_REC_WORDS) rec0[lane] = 0;
   __syncwarp();
-  slot_prologue(pol, w, s, r, cache[threadIdx.x >> 5], lane, /*cache_valid=*/true);
-}
-
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-baseline_kernel(DuchessPolicy pol, DuchessWorkload w, DuchessState s) {
-  __shared__ SlotCache cache[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (blockIdx.x == 0 && threadIdx.x == 0) s.queue_head[0] = s.queue_head[1];
-  if (r >= s.n_slots) return;
-  if (s.done[r]) return;
-  const int p = s.slot_req[r];
-  if (p < 0) return;
   SlotCache& c = cache[threadIdx.x >> 5];
-  load_slot(s, int64_t(r) * pol.max_branches, int64_t(r) * s.branch_cap, pol.max_branches, c, lane);
-  load_meta(w, s, r, p, pol.max_branches, c, lane);
-  baseline_slot(pol, w, s, r, p, c, lane);
+  const int p = slot_prologue_atomic(pol, w, s, r, c, lane, /*cache_valid=*/false,
+                                     s.queue_head + 1);
+  if (p >= 0) baseline_slot(pol, w, s, r, p, c, lane);
+  if (lane == 0) {
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(s.active_count + kListAcc);
+    if (int(atomicAdd(acc, 1ull << 32) >> 32) == s.n_slots - 1) {
+      s.queue_head[0] = atomicAdd(s.queue_head + 1, 0);
+      *acc = 0ull;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1804,10 +1799,10 @@ extern "C" int duchess_baseline_round(const DuchessPolicy* policy, const Duchess
       (!state->br_probe_last || !state->br_probe_run || policy->dynasor_window < 2))
     return DUCHESS_EINVAL;
   if (state->n_slots == 0) return DUCHESS_OK;
+  if (!state->active_count) return DUCHESS_EINVAL;     // the round's exit count
   const unsigned grid = unsigned((state->n_slots + kWarpsPerBlock - 1) / kWarpsPerBlock);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  baseline_refill_kernel<<<grid, 32 * kWarpsPerBlock, 0, st>>>(*policy, *workload, *state);
-  baseline_kernel<<<grid, 32 * kWarpsPerBlock, 0, st>>>(*policy, *workload, *state);
+  baseline_round_kernel<<<grid, 32 * kWarpsPerBlock, 0, st>>>(*policy, *workload, *state);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
