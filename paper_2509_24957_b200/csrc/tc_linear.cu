@@ -23,6 +23,7 @@
 // the epilogue (tcgen05.ld 32 columns at a time, fold, activation, bf16
 // store). With ln_fold each tile sums its 1/n_col_tiles share of its rows for
 // the LN statistics and the row tile's tiles combine the shares (fixed order).
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -34,10 +35,15 @@ namespace tcl {
 
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
-constexpr int B_BYTES = BN * BK * 2;            // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
 constexpr int THREADS = 192;
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+// CTA pair (cta_group::2): a 256 x 256 tile per pair, each CTA holding its 128
+// rows of A and half (128 columns) of B per stage, so a stage is 32 KB
+template <int CG> struct Cfg {
+  static constexpr int B_ROWS = BN / CG;                    // B rows this CTA loads
+  static constexpr int STAGE = A_BYTES + B_ROWS * BK * 2;   // 48 / 32 KB
+  static constexpr int NST = CG == 1 ? STAGES : 6;
+  static constexpr int SMEM_BYTES = NST * STAGE + 1024;
+};
 
 struct Args {
   int64_t M;
@@ -70,6 +76,44 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- CTA-pair helpers (sm_100a): the peer signals the leader's (rank 0's)
+// barriers; `mapa` gives the shared::cluster address of a variable in CTA 0.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(p)));
+  return a;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA load whose completion is signalled on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t bar_leader) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_leader)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int x, int y,
+                                                 int z, uint32_t bar_leader) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar_leader)
       : "memory");
 }
 
@@ -115,6 +159,27 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(IDESC), "r"(acc));
 }
 
+// the pair's MMA: M = 256 (128 rows per CTA), N = 256 (128 B columns per CTA)
+constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                            (uint32_t(256 >> 4) << 24);
+
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(acc));
+}
+
+// completion of the pair's MMAs signalled on the same barrier in both CTAs
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -145,36 +210,59 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 
 // LNF / ACT are compile-time (one instantiation per layer kind), so the
 // epilogue evaluates only its own activation (no GeLU computed and discarded).
-template <bool LNF, int ACT>
+// CG = 2: CTA pairs (cluster of 2, cta_group::2). A unit is then a 256-row x
+// 256-column tile: each CTA loads its 128 rows of A and 128 of the tile's 256
+// B columns, both TMA loads signal the leader's stage barrier, the leader's
+// single thread issues M256 N256 K16 MMAs reading both CTAs' shared memory,
+// and each CTA's TMEM holds its 128 rows (the commit reaches both CTAs); the
+// epilogue is per CTA as with CG = 1 and hands the accumulator back to the
+// leader's MMA thread. Per CTA a stage is 32 KB instead of 48 KB for the same
+// MMA work, so each SM moves a third less operand data per FLOP.
+template <bool LNF, int ACT, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
 linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               Args a) {
+  using CF = Cfg<CG>;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full[2], tmem_empty[2];
+  __shared__ uint64_t full_bar[CF::NST], empty_bar[CF::NST], tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k_blocks = a.K / BK;
   const int n_tiles = a.N / BN;
+  const int rank = CG == 2 ? int(cluster_rank()) : 0;
+  const bool leader = rank == 0;
+  // work-unit walk: one per CTA (CG = 1) or per pair (CG = 2)
+  const int64_t u0 = CG == 2 ? int64_t(blockIdx.x >> 1) : int64_t(blockIdx.x);
+  const int64_t ustep = CG == 2 ? int64_t(gridDim.x >> 1) : int64_t(gridDim.x);
+  const int64_t n_rt_u = CG == 2 ? (a.n_rt + 1) / 2 : a.n_rt;     // unit row tiles
+  const int64_t n_units = int64_t(a.G) * n_rt_u * n_tiles;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < CF::NST; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4);
+      mbar_init(&tmem_empty[i], 4 * CG);     // the epilogue warps of every CTA of the unit
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();       // the leader's barriers exist before any signal
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const int stamp = LNF ? a.hdr[0] + 1 : 0;
@@ -182,55 +270,67 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {                                   // ---- TMA producer ----
       int it = 0;
-      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-        const Unit w = unit_of(u, a.n_rt, n_tiles);
-        const int m0 = w.mt * BM, n0 = w.g * a.N + w.nt * BN;
+      for (int64_t u = u0; u < n_units; u += ustep) {
+        const Unit w = unit_of(u, n_rt_u, n_tiles);
+        const int m0 = (w.mt * CG + rank) * BM, n0 = w.g * a.N + w.nt * BN + rank * CF::B_ROWS;
         const int ay = a.a_interleaved ? w.g : m0, az = a.a_interleaved ? m0 : w.g;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1u);
-          char* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_3d(st, &map_a, kb * BK, ay, az, &full_bar[s]);
-          tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
+          const int s = it % CF::NST;
+          mbar_wait(&empty_bar[s], ((it / CF::NST) & 1) ^ 1u);
+          char* st = smem + s * CF::STAGE;
+          if constexpr (CG == 2) {
+            const uint32_t lb = leader_addr(&full_bar[s]);
+            if (leader) mbar_expect_tx(&full_bar[s], 2 * CF::STAGE);   // both CTAs' bytes
+            tma_load_3d_pair(st, &map_a, kb * BK, ay, az, lb);
+            tma_load_2d_pair(st + A_BYTES, &map_b, kb * BK, n0, lb);
+          } else {
+            mbar_expect_tx(&full_bar[s], CF::STAGE);
+            tma_load_3d(st, &map_a, kb * BK, ay, az, &full_bar[s]);
+            tma_load_2d(st + A_BYTES, &map_b, kb * BK, n0, &full_bar[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                   // ---- MMA issuer ----
+    if (lane == 0 && leader) {                         // ---- MMA issuer ----
       int it = 0, i = 0;
-      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+      for (int64_t u = u0; u < n_units; u += ustep, ++i) {
         const int acc = i & 1;
         mbar_wait(&tmem_empty[acc], ((i >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * BN);
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&full_bar[s], (it / STAGES) & 1);
+          const int s = it % CF::NST;
+          mbar_wait(&full_bar[s], (it / CF::NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const char* st = smem + s * STAGE_BYTES;
+          const char* st = smem + s * CF::STAGE;
           const uint64_t da = desc_sw128(st), db = desc_sw128(st + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
-          commit(&empty_bar[s]);
+          for (int k = 0; k < BK / 16; ++k) {
+            if constexpr (CG == 2) mma2(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+            else mma(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+          }
+          if constexpr (CG == 2) commit2(&empty_bar[s]);
+          else commit(&empty_bar[s]);
         }
-        commit(&tmem_full[acc]);
+        if constexpr (CG == 2) commit2(&tmem_full[acc]);
+        else commit(&tmem_full[acc]);
       }
     }
   } else {
     // ---- epilogue: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
     const int q = warp & 3;
     int i = 0;
-    for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
-      const Unit w = unit_of(u, a.n_rt, n_tiles);
-      const int g = w.g, mt = w.mt, nt = w.nt;
+    for (int64_t u = u0; u < n_units; u += ustep, ++i) {
+      const Unit w = unit_of(u, n_rt_u, n_tiles);
+      const int g = w.g, mt = w.mt * CG + rank, nt = w.nt;   // mt: this CTA's 128-row tile
+      const bool tile = mt < a.n_rt;                          // (the pair's 2nd half may be past M)
       const int64_t row = int64_t(mt) * BM + 32 * q + lane;
       const int64_t grow = int64_t(g) * a.M + row;       // (group, row) index, group-major
       const int64_t xrow = a.a_interleaved ? row * a.G + g : grow;
       const int64_t gmt = int64_t(g) * a.n_rt + mt;
       float rsig = 1.f, shift = 0.f;
-      if (LNF) {                                       // overlaps this tile's MMAs
+      if (LNF && tile) {                               // overlaps this tile's MMAs
         const int nv = a.K / 8;
         const int v_lo = int(int64_t(nt) * nv / n_tiles), v_hi = int(int64_t(nt + 1) * nv / n_tiles);
         float sx = 0.f, sxx = 0.f;
@@ -316,14 +416,21 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(leader_addr(&tmem_empty[acc]));
+        else mbar_arrive(&tmem_empty[acc]);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();       // both CTAs done with the pair's TMEM
+  else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
   if (LNF && threadIdx.x == 0) {                     // last CTA out advances the epoch
     __threadfence();
@@ -577,10 +684,14 @@ extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, in
                   reinterpret_cast<uintptr_t>(workspace) % 16))
     return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
+  // CTA pairs (cta_group::2) unless DUCHESS_TC_PAIR=0 (1-CTA tiles, for comparison)
+  static const int pair_mode = [] { const char* e = getenv("DUCHESS_TC_PAIR"); return e ? atoi(e) : 1; }();
+  const int CG = pair_mode ? 2 : 1;
   CUtensorMap ma, mb;
   if (!tcl::make_map_a(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
     return DUCHESS_ECUDA;
-  if (!tcl::make_map(&mb, W, uint64_t(G) * N, uint64_t(K), tcl::BN)) return DUCHESS_ECUDA;
+  if (!tcl::make_map(&mb, W, uint64_t(G) * N, uint64_t(K), uint32_t(tcl::BN / CG)))
+    return DUCHESS_ECUDA;
   const int64_t mt = (M + tcl::BM - 1) / tcl::BM, nt = N / tcl::BN;
   tcl::Args a{};
   a.M = M;
@@ -603,20 +714,40 @@ extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, in
     a.stats = reinterpret_cast<float2*>(ws + 16);
     a.ready = reinterpret_cast<int*>(ws + 16 + int64_t(G) * M * nt * 8);
   }
-  a.n_units = int64_t(G) * mt * nt;
-  void (*kern)(CUtensorMap, CUtensorMap, tcl::Args) =
-      ln_fold ? (act == 2 ? tcl::linear_kernel<true, 2> : act == 1 ? tcl::linear_kernel<true, 1>
-                                                                   : tcl::linear_kernel<true, 0>)
-              : (act == 2 ? tcl::linear_kernel<false, 2> : act == 1 ? tcl::linear_kernel<false, 1>
-                                                                    : tcl::linear_kernel<false, 0>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl::SMEM);
+  a.n_units = int64_t(G) * ((mt + CG - 1) / CG) * nt;   // per CTA (CG 1) or per pair (CG 2)
+  void (*kern)(CUtensorMap, CUtensorMap, tcl::Args);
+  if (CG == 2)
+    kern = ln_fold ? (act == 2 ? tcl::linear_kernel<true, 2, 2> : act == 1 ? tcl::linear_kernel<true, 1, 2>
+                                                                           : tcl::linear_kernel<true, 0, 2>)
+                   : (act == 2 ? tcl::linear_kernel<false, 2, 2> : act == 1 ? tcl::linear_kernel<false, 1, 2>
+                                                                            : tcl::linear_kernel<false, 0, 2>);
+  else
+    kern = ln_fold ? (act == 2 ? tcl::linear_kernel<true, 2, 1> : act == 1 ? tcl::linear_kernel<true, 1, 1>
+                                                                           : tcl::linear_kernel<true, 0, 1>)
+                   : (act == 2 ? tcl::linear_kernel<false, 2, 1> : act == 1 ? tcl::linear_kernel<false, 1, 1>
+                                                                            : tcl::linear_kernel<false, 0, 1>);
+  const int smem = CG == 2 ? tcl::Cfg<2>::SMEM_BYTES : tcl::Cfg<1>::SMEM_BYTES;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one CTA per SM, all resident: with ln_fold tiles wait on statistics shares
-  const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
-  kern<<<grid, tcl::THREADS, tcl::SMEM, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
-  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  const int64_t units_cap = CG == 2 ? sms / 2 : sms;
+  const unsigned grid = unsigned(CG * (a.n_units < units_cap ? a.n_units : units_cap));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tcl::THREADS);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(CG);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, a);
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
 extern "C" int duchess_tc_linear(const void* X, int64_t M, int32_t K, const void* W, int32_t N,
