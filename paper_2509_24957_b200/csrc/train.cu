@@ -174,12 +174,41 @@ __device__ __forceinline__ void lr_grad_body(const GradArgs& a) {
       }
     }
     const int buf = int(it & 1);
+    // The RB rows' warp sums in one butterfly: each of the first log2(RB)
+    // levels halves the rows a lane carries (lane bit 4, 3, ... picks which
+    // half it keeps), the remaining levels sum within lane groups, so the warp
+    // does 5 shuffles for all RB rows instead of 5 per row. Row q's sum ends
+    // in the lanes whose top log2(RB) bits equal q's bit-reversed index;
+    // rows past nr carry zeros.
+    float v[RB];
 #pragma unroll
-    for (int q = 0; q < RB; ++q) {
-      if (q < nr) {
-        const float d = warp_sum(dots[q] + dots2[q]);
-        if (lane == 0) red[buf][warp][q] = d;
+    for (int q = 0; q < RB; ++q) v[q] = dots[q] + dots2[q];
+    int width = RB;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      if (width > 1) {
+        const bool upper = lane & o;
+#pragma unroll
+        for (int h = 0; h < RB / 2; ++h) {
+          if (2 * h >= width) break;
+          const float keep = upper ? v[2 * h + 1] : v[2 * h];
+          const float send = upper ? v[2 * h] : v[2 * h + 1];
+          v[h] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        width >>= 1;
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
       }
+    }
+    {
+      // after the pairing levels lane l holds the row whose index bits are
+      // (bit 4 of l) for the first level, (bit 3) for the second, ...
+      constexpr int LB = RB == 1 ? 0 : RB == 2 ? 1 : RB == 4 ? 2 : 3;
+      int q = 0;
+#pragma unroll
+      for (int b = 0; b < LB; ++b) q |= ((lane >> (4 - b)) & 1) << b;
+      const bool writer = (lane & ((1 << (5 - LB)) - 1)) == 0;   // first lane of its group
+      if (writer && q < nr) red[buf][warp][q] = v[0];
     }
     if constexpr (KEEP) {
       // the stage's bytes are all in registers: hand the slot back now
@@ -197,7 +226,7 @@ __device__ __forceinline__ void lr_grad_body(const GradArgs& a) {
       float yl = 0.f;
 #pragma unroll
       for (int q = 0; q < RB; ++q) yl = lane == q ? yv[q] : yl;
-      mine = 1.0f / (1.0f + expf(-z)) - yl;
+      mine = 1.0f / (1.0f + __expf(-z)) - yl;
     }
     float res[RB];
 #pragma unroll
