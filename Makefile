@@ -9,7 +9,7 @@ OBJ_DIR := build/obj
 LIB     := $(PKG)/libduchess_b200.so
 SRCS    := score decide fork kv train mlp mlp_tc tc_linear bw
 OBJS    := $(addprefix $(OBJ_DIR)/,$(addsuffix .o,$(SRCS)))
-HDRS    := $(SRC_DIR)/common.cuh $(SRC_DIR)/kv_core.cuh include/duchess_b200.h
+HDRS    := $(SRC_DIR)/common.cuh $(SRC_DIR)/kv_core.cuh $(SRC_DIR)/tc_pair.cuh include/duchess_b200.h
 
 all: $(LIB)
 

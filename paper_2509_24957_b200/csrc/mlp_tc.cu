@@ -30,7 +30,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "tc_pair.cuh"
 #include "../../include/duchess_b200.h"
 
 namespace duchess {
@@ -38,9 +41,15 @@ namespace duchess {
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 64, kTcStages = 4;
 constexpr int kTcABytes = kTcBM * kTcBK * 2;            // 16 KB
 constexpr int kTcBBytes = kTcBN * kTcBK * 2;            // 32 KB
-constexpr int kTcStageBytes = kTcABytes + kTcBBytes;    // 48 KB
 constexpr int kTcThreads = 192;                         // 6 warps
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024;  // + alignment slack
+// CTA pairs (cta_group::2, tc_pair.cuh): 256 x 256 units, each CTA loading its
+// 128 rows of A and 128 of the unit's 256 hidden columns of B per 32 KB stage
+template <int CG> struct TcCfg {
+  static constexpr int B_ROWS = kTcBN / CG;
+  static constexpr int STAGE = kTcABytes + B_ROWS * kTcBK * 2;
+  static constexpr int NST = CG == 1 ? kTcStages : 6;
+  static constexpr int SMEM_BYTES = NST * STAGE + 1024;
+};
 
 struct TcArgs {
   int64_t M;
@@ -145,12 +154,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// CG = 2: on CTA pairs, as linear_kernel (tc_linear.cu): the leader issues the
+// M256 N256 MMAs, both CTAs' TMA loads signal its stage barrier, each CTA's
+// epilogue works on its own 128 rows and hands the accumulator back by a
+// remote arrive on the leader's barrier.
+template <int CG>
 __global__ void __launch_bounds__(kTcThreads, 1)
 mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, TcArgs a) {
+  using namespace tcpair;
+  using CF = TcCfg<CG>;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[kTcStages], empty_bar[kTcStages];
+  __shared__ uint64_t full_bar[CF::NST], empty_bar[CF::NST];
   __shared__ uint64_t tmem_full[2], tmem_empty[2];
   __shared__ uint32_t tmem_base;
   __shared__ int last_flag;
@@ -158,25 +174,38 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = a.NH / kTcBN;
   const int k_blocks = a.K / kTcBK;
+  const int rank = CG == 2 ? int(cluster_rank()) : 0;
+  const bool leader = rank == 0;
+  const int64_t u0 = CG == 2 ? int64_t(blockIdx.x >> 1) : int64_t(blockIdx.x);
+  const int64_t ustep = CG == 2 ? int64_t(gridDim.x >> 1) : int64_t(gridDim.x);
+  const int64_t n_rt_u = CG == 2 ? (a.n_rt + 1) / 2 : a.n_rt;
+  const int64_t n_units = int64_t(a.G) * n_rt_u * n_tiles;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kTcStages; ++i) {
+    for (int i = 0; i < CF::NST; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);          // MMA commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4);
+      mbar_init(&tmem_empty[i], 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {   // 2 x 256 fp32 accumulator columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const int stamp = a.hdr[0] + 1;          // this launch's "stats ready" stamp
@@ -184,58 +213,71 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (warp == 0) {
     if (lane == 0) {   // ---- TMA producer ----
       int it = 0;
-      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+      for (int64_t u = u0; u < n_units; u += ustep) {
         int g, mt, h;
-        tc_unit(u, a.n_rt, n_tiles, g, mt, h);
-        const int m0 = mt * kTcBM, n0 = g * a.NH + h * kTcBN;
+        tc_unit(u, n_rt_u, n_tiles, g, mt, h);
+        const int m0 = (mt * CG + rank) * kTcBM, n0 = g * a.NH + h * kTcBN + rank * CF::B_ROWS;
         const int ay = a.a_interleaved ? g : m0, az = a.a_interleaved ? m0 : g;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
-          const int s = it % kTcStages;
-          const uint32_t ph = (it / kTcStages) & 1;
+          const int s = it % CF::NST;
+          const uint32_t ph = (it / CF::NST) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1u);
-          char* st = smem + s * kTcStageBytes;
-          mbar_expect_tx(&full_bar[s], kTcStageBytes);
-          tma_load_3d(st, &map_a, kb * kTcBK, ay, az, &full_bar[s]);
-          tma_load_2d(st + kTcABytes, &map_b, kb * kTcBK, n0, &full_bar[s]);
+          char* st = smem + s * CF::STAGE;
+          if constexpr (CG == 2) {
+            const uint32_t lb = leader_addr(&full_bar[s]);
+            if (leader) mbar_expect_tx(&full_bar[s], 2 * CF::STAGE);
+            tma_load_3d_pair(st, &map_a, kb * kTcBK, ay, az, lb);
+            tma_load_2d_pair(st + kTcABytes, &map_b, kb * kTcBK, n0, lb);
+          } else {
+            mbar_expect_tx(&full_bar[s], CF::STAGE);
+            tma_load_3d(st, &map_a, kb * kTcBK, ay, az, &full_bar[s]);
+            tma_load_2d(st + kTcABytes, &map_b, kb * kTcBK, n0, &full_bar[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {   // ---- MMA issuer ----
+    if (lane == 0 && leader) {   // ---- MMA issuer ----
       int it = 0, i = 0;
-      for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+      for (int64_t u = u0; u < n_units; u += ustep, ++i) {
         const int acc = i & 1;
         mbar_wait(&tmem_empty[acc], ((i >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + uint32_t(acc * kTcBN);
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
-          const int s = it % kTcStages;
-          const uint32_t ph = (it / kTcStages) & 1;
+          const int s = it % CF::NST;
+          const uint32_t ph = (it / CF::NST) & 1;
           mbar_wait(&full_bar[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const char* st = smem + s * kTcStageBytes;
+          const char* st = smem + s * CF::STAGE;
           const uint64_t da = umma_desc_sw128(st), db = umma_desc_sw128(st + kTcABytes);
 #pragma unroll
-          for (int k = 0; k < kTcBK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
-            umma_bf16(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
-          umma_commit(&empty_bar[s]);
+          for (int k = 0; k < kTcBK / 16; ++k) {  // +32 B per K=16 step inside the swizzle atom
+            if constexpr (CG == 2) mma2(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+            else umma_bf16(d, da + uint64_t(2 * k), db + uint64_t(2 * k), (kb | k) ? 1u : 0u);
+          }
+          if constexpr (CG == 2) commit2(&empty_bar[s]);
+          else umma_commit(&empty_bar[s]);
         }
-        umma_commit(&tmem_full[acc]);
+        if constexpr (CG == 2) commit2(&tmem_full[acc]);
+        else umma_commit(&tmem_full[acc]);
       }
     }
   } else {
     // ---- epilogue warps: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
     const int q = warp & 3;
     int i = 0;
-    for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++i) {
+    for (int64_t u = u0; u < n_units; u += ustep, ++i) {
       int g, mt, h;
-      tc_unit(u, a.n_rt, n_tiles, g, mt, h);
+      tc_unit(u, n_rt_u, n_tiles, g, mt, h);
+      mt = mt * CG + rank;                           // this CTA's 128-row tile
+      const bool tile = mt < a.n_rt;                 // (a pair's 2nd half may be past M)
       const int64_t row = int64_t(mt) * kTcBM + 32 * q + lane;
       const int64_t grow = int64_t(g) * a.M + row;          // (group, row), group-major
       const int64_t xrow = a.a_interleaved ? row * a.G + g : grow;
       const int64_t gmt = int64_t(g) * a.n_rt + mt;
       float rsig = 1.f, shift = 0.f;
-      if (a.ln) {
+      if (a.ln && tile) {
         // LN statistics: unit h sums its 1/n_tiles share of each row's columns
         // (while its MMAs run) and publishes the partial; every unit of the row
         // tile then combines the n_tiles partials in fixed order.
@@ -312,7 +354,11 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       const float logit = (lg[0] + lg[1]) + (lg[2] + lg[3]);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(leader_addr(&tmem_empty[acc]));
+        else mbar_arrive(&tmem_empty[acc]);
+      }
+      if (!tile) continue;
       if (row < a.M) a.partial[grow * n_tiles + h] = logit;
       // the row tile's last finished hidden tile sums the partials in fixed order
       epi_bar();
@@ -335,10 +381,14 @@ mlp_probe_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
   if (threadIdx.x == 0) {                        // last CTA out advances the epoch
     __threadfence();
@@ -422,7 +472,10 @@ extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K,
   CUtensorMap ma, mb;
   if (!make_map_a3(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
     return DUCHESS_ECUDA;
-  if (!make_map(&mb, W1, uint64_t(G) * NH, uint64_t(K), kTcBN)) return DUCHESS_ECUDA;
+  // CTA pairs (cta_group::2) unless DUCHESS_TC_PAIR=0 (1-CTA tiles, for comparison)
+  static const int pair_mode = [] { const char* e = getenv("DUCHESS_TC_PAIR"); return e ? atoi(e) : 1; }();
+  const int CG = pair_mode ? 2 : 1;
+  if (!make_map(&mb, W1, uint64_t(G) * NH, uint64_t(K), uint32_t(kTcBN / CG))) return DUCHESS_ECUDA;
   const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
   char* ws = static_cast<char*>(workspace);
   TcArgs a{};
@@ -445,15 +498,31 @@ extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K,
   a.partial = reinterpret_cast<float*>(ws + 16 + int64_t(G) * M * nt * 8);
   a.ready = reinterpret_cast<int*>(ws + 16 + int64_t(G) * M * nt * 8 + int64_t(G) * M * nt * 4);
   a.done = a.ready + int64_t(G) * mt;
-  a.n_units = int64_t(G) * mt * nt;
-  cudaFuncSetAttribute(mlp_probe_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+  a.n_units = int64_t(G) * ((mt + CG - 1) / CG) * nt;   // per CTA (CG 1) or per pair (CG 2)
+  void (*kern)(CUtensorMap, CUtensorMap, TcArgs) =
+      CG == 2 ? mlp_probe_tc_kernel<2> : mlp_probe_tc_kernel<1>;
+  const int smem = CG == 2 ? TcCfg<2>::SMEM_BYTES : TcCfg<1>::SMEM_BYTES;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // every CTA resident (one per SM): units wait on statistics other CTAs publish
-  const unsigned grid = unsigned(a.n_units < sms ? a.n_units : sms);
-  mlp_probe_tc_kernel<<<grid, kTcThreads, kTcSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, a);
-  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  const int64_t units_cap = CG == 2 ? sms / 2 : sms;
+  const unsigned grid = unsigned(CG * (a.n_units < units_cap ? a.n_units : units_cap));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(CG);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, a);
+  return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
 
 extern "C" int duchess_mlp_probe_tc(const void* X, int64_t M, int32_t K, const void* W1,
