@@ -40,7 +40,6 @@ namespace duchess {
 
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 64, kTcStages = 4;
 constexpr int kTcABytes = kTcBM * kTcBK * 2;            // 16 KB
-constexpr int kTcBBytes = kTcBN * kTcBK * 2;            // 32 KB
 constexpr int kTcThreads = 192;                         // 6 warps
 // CTA pairs (cta_group::2, tc_pair.cuh): 256 x 256 units, each CTA loading its
 // 128 rows of A and 128 of the unit's 256 hidden columns of B per 32 KB stage
