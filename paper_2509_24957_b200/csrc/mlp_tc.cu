@@ -506,10 +506,9 @@ extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // every CTA resident (one per SM): units wait on statistics other CTAs publish
-  const int64_t units_cap = CG == 2 ? sms / 2 : sms;
-  const unsigned grid = unsigned(CG * (a.n_units < units_cap ? a.n_units : units_cap));
+  int64_t units_cap = CG == 2 ? sms / 2 : sms;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(unsigned(CG * units_cap));
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = size_t(smem);
   cfg.stream = static_cast<cudaStream_t>(stream);
@@ -520,6 +519,15 @@ extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (CG == 2) {
+    // every pair must be resident at once (units wait on statistics other
+    // CTAs publish): never launch more pairs than can be co-scheduled
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) == cudaSuccess && max_clusters > 0 &&
+        max_clusters < units_cap)
+      units_cap = max_clusters;
+  }
+  cfg.gridDim = dim3(unsigned(CG * (a.n_units < units_cap ? a.n_units : units_cap)));
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, a);
   return e == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }
