@@ -471,9 +471,12 @@ extern "C" int duchess_mlp_probe_tc_grouped(const void* X, int64_t M, int32_t K,
   CUtensorMap ma, mb;
   if (!make_map_a3(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
     return DUCHESS_ECUDA;
-  // CTA pairs (cta_group::2) unless DUCHESS_TC_PAIR=0 (1-CTA tiles, for comparison)
-  static const int pair_mode = [] { const char* e = getenv("DUCHESS_TC_PAIR"); return e ? atoi(e) : 1; }();
-  const int CG = pair_mode ? 2 : 1;
+  // CTA pairs (cta_group::2) for long K loops (K >= 4096: measured faster, e.g.
+  // 2.01 -> 1.83 ms for 5120 -> 2048 x 4 groups), 1-CTA tiles for short ones
+  // (2048 -> 1024 x 4 groups: 347 vs 460 us with pairs); DUCHESS_TC_PAIR=0 / 1
+  // forces one or the other (measurement)
+  static const int pair_mode = [] { const char* e = getenv("DUCHESS_TC_PAIR"); return e ? atoi(e) : 2; }();
+  const int CG = pair_mode == 2 ? (K >= 4096 ? 2 : 1) : (pair_mode ? 2 : 1);
   if (!make_map(&mb, W1, uint64_t(G) * NH, uint64_t(K), uint32_t(kTcBN / CG))) return DUCHESS_ECUDA;
   const int64_t mt = (M + kTcBM - 1) / kTcBM, nt = NH / kTcBN;
   char* ws = static_cast<char*>(workspace);
