@@ -1,7 +1,8 @@
 """Body of __graft_entry__.smoke(): one short run of the serving loop
 (serving.ShardedEngine: two request shards on two CUDA streams, each round
-K1 duchess_score_active + K2 duchess_round) on cuda:0, checked against the
-CPU oracle (oracle/ is the checker only)."""
+K1 duchess_score_active_ex + K2 duchess_round + K3 duchess_kv_round on a paged
+KV cache) on cuda:0, checked against the CPU oracle (oracle/ is the checker
+only): logits and every RoundReport; the KV cache must not overflow."""
 
 from __future__ import annotations
 
@@ -30,8 +31,10 @@ def run_smoke() -> None:
     rng = np.random.default_rng(1)
     w = rng.normal(0, 1.5 / np.sqrt(H), size=(1, H))
     bank = ProbeBank.from_linear(w, [0.05])
+    P = 256                                          # KV blocks per slot arena
     srv = ShardedEngine(traces, knobs, seeds, bank, n_slots=R, shards=2, T=T,
-                        dtype=torch.bfloat16)
+                        dtype=torch.bfloat16,
+                        kv=dict(block_tokens=16, blocks_per_slot=P, kv_bytes_per_token=64))
     C = knobs.max_branches
     fill = keyed_fill(seed)
     seen, reports = {}, {}
@@ -66,6 +69,7 @@ def run_smoke() -> None:
 
     srv.run(max_rounds=1000, fill=fill_and_record, after_round=after)
     assert int(srv.counters()[_lib.CNT_AMBIGUOUS]) == 0
+    assert srv.kv_counters()["overflow"] == 0 and srv.kv_counters()["blocks_allocated"] > 0
     for p, trace in enumerate(traces):
         index = {id(x): j for j, x in enumerate(trace.templates)}
         req_o = port.DuchessRequest(trace, knobs, random.Random(seeds[p]),
