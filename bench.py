@@ -538,7 +538,10 @@ def run_serving(args, cfg, rank, world, local_rank):
         "clocks": clk,
         "counters": {"ambiguous_draws": int(cnt[_lib.CNT_AMBIGUOUS]),
                      "finished_requests": int(cnt[_lib.CNT_FINISHED]),
-                     "forks": int(cnt[_lib.CNT_FORKS])},
+                     "forks": int(cnt[_lib.CNT_FORKS]),
+                     # predictions within the probe's 1e-4 logit tolerance of tau:
+                     # an fp64 probe could have decided these `p > tau` the other way
+                     "near_tau_predictions": int(cnt[_lib.CNT_NEAR_TAU])},
         **({"kv_cache": kv_report(kv0, kv1, args.steps, srv, cfg)} if kv1 else {}),
     }
 

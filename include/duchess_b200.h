@@ -103,6 +103,7 @@ extern "C" {
 #define DUCHESS_CNT_FINISHED 2  /* requests finished */
 #define DUCHESS_CNT_BRANCH_STEPS 3
 #define DUCHESS_CNT_FORKS 4
+#define DUCHESS_CNT_NEAR_TAU 5  /* PRED_DEVICE predictions within the probe tolerance of tau */
 #define DUCHESS_N_COUNTERS 8
 
 typedef struct DuchessPolicy {

@@ -28,7 +28,7 @@ MAX_SLOTS = 64
 REC_WORDS = 12
 (REC_ROUND, REC_DECODING, REC_MAX_CHUNK, REC_DECODE, REC_PROBES, REC_NACTIONS, REC_DONE,
  REC_NFORKS, REC_NSURV, REC_REQ, REC_REASON, REC_FINAL) = range(12)
-CNT_AMBIGUOUS, CNT_ERRORS, CNT_FINISHED, CNT_BRANCH_STEPS, CNT_FORKS = range(5)
+CNT_AMBIGUOUS, CNT_ERRORS, CNT_FINISHED, CNT_BRANCH_STEPS, CNT_FORKS, CNT_NEAR_TAU = range(6)
 N_COUNTERS = 8
 
 _i32p = C.POINTER(C.c_int32)

@@ -771,6 +771,17 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   __syncwarp();
   const int n_surv = order_slots(c, C, s.branch_cap, lane);
   if (qp) prefetch_queue_rec(w, *qp, lane);
+  // Probabilities from the device probe (fp32 logits, within 1e-4 *
+  // max(|logit|, 1) of the fp64 reference, BASELINE.json north_star): count
+  // the predictions close enough to tau that an fp64 probe could have put
+  // them on the other side of `p > tau` (expected rare).
+  double band_lo = 2.0, band_hi = -1.0;
+  if (pol.pred_source == DUCHESS_PRED_DEVICE && pol.early_term_threshold > 0.0 && pol.early_term_threshold < 1.0) {
+    const double lt = log(pol.early_term_threshold / (1.0 - pol.early_term_threshold));
+    const double tol = 1e-4 * fmax(fabs(lt), 1.0);
+    band_lo = 1.0 / (1.0 + exp(-(lt - tol)));
+    band_hi = 1.0 / (1.0 + exp(-(lt + tol)));
+  }
   if (wait_inputs) pdl_wait();                     // the scorer's probabilities are final
   double pr0 = 0.0, pr1 = 0.0;
   if (dev_probs) {
@@ -801,6 +812,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
   }
   const double tau = pol.early_term_threshold;
   int n_term = 0;
+  int n_near_tau = 0;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int j = lane + 32 * q;
@@ -831,6 +843,7 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
         for (int l = 0; l < pol.n_layers; ++l) acc = __dadd_rn(acc, __ldcg(probs + (rC + j) * pol.n_layers + l));
         pr = __ddiv_rn(acc, double(pol.n_layers));
       }
+      n_near_tau += pr > band_lo && pr < band_hi;
       const int streak = pr > tau ? c.streak[j] + 1 : 0;   // strict > (:363)
       c.lp[j] = pr;
       // branch-out weight of this prediction (:183), computed here so its pow
@@ -859,6 +872,10 @@ __device__ int decide_slot(const DuchessPolicy& pol, const DuchessWorkload& w,
       }
     }
     n_term += __popc(__ballot_sync(0xffffffffu, term));
+  }
+  if (pol.pred_source == DUCHESS_PRED_DEVICE) {
+    n_near_tau = __reduce_add_sync(0xffffffffu, n_near_tau);
+    if (lane == 0 && n_near_tau) add_counter(&s.counters[DUCHESS_CNT_NEAR_TAU], n_near_tau);
   }
   __syncwarp();
 
