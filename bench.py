@@ -107,6 +107,16 @@ def k3_traffic():
         return json.load(f)["dram_bytes"], os.path.relpath(files[-1], ROOT)
 
 
+def k3_write_bytes():
+    """DRAM bytes written by one fork_exec launch (committed ncu capture)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k3_traffic.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        return json.load(f).get("dram_write_bytes")
+
+
 def k1_traffic_ratio(T=32):
     """DRAM bytes / algorithmic bytes of K1 from the committed ncu --set full
     capture (tools/profile_all.sh -> profiles/<round>/k1_traffic.json; the
@@ -256,6 +266,30 @@ def measure_read_peak(dev, buf=None, reps=6):
         a.record(st)
         _lib.check(lib.duchess_read_stream(buf.data_ptr(), nbytes, sink.data_ptr(),
                                            st.cuda_stream), "duchess_read_stream")
+        b.record(st)
+        b.synchronize()
+        gbs = nbytes / (a.elapsed_time(b) / 1e3) / 1e9
+        best = gbs if best is None else max(best, gbs)
+    del buf
+    return best
+
+
+def measure_write_peak(dev, reps=6):
+    """Write-only HBM ceiling on this GPU, measured live: best of `reps`
+    passes of duchess_write_stream (16-byte streaming stores) over 4 GiB."""
+    import torch
+
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    buf = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
+    nbytes = buf.numel()
+    st = torch.cuda.current_stream(dev)
+    best = None
+    for r in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        _lib.check(lib.duchess_write_stream(buf.data_ptr(), nbytes, r, st.cuda_stream),
+                   "duchess_write_stream")
         b.record(st)
         b.synchronize()
         gbs = nbytes / (a.elapsed_time(b) / 1e3) / 1e9
@@ -720,6 +754,8 @@ def run_fork_bench(args, rank, world, local_rank):
     k3_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     step_ms = e_all0.elapsed_time(e_all1) / args.steps
     peak, kind = load_peaks()
+    del flush
+    wpeak = measure_write_peak(dev) if rank == 0 else None
     achieved = bytes_per_step / (k3_ms / 1e3) / 1e9
     return {"metric": "copy-on-write forks/s (C4 branch-out-heavy trace)",
             "value": R * nf * world / (k3_ms / 1e3), "unit": "forks/s", "n_gpus": world,
@@ -734,7 +770,14 @@ def run_fork_bench(args, rank, world, local_rank):
                          "frac": achieved / peak, "peak_kind": kind, "peak_note": PEAK_NOTE,
                          "kernel": "duchess_fork_cow (plan + exec)",
                          "bytes_per_launch": bytes_per_step, "k3_us_per_launch": k3_ms * 1e3,
-                         "traffic": k3_traffic()[0], "traffic_source": k3_traffic()[1]},
+                         "traffic": k3_traffic()[0], "traffic_source": k3_traffic()[1],
+                         # the launch is write-dominated (ncu: ~4.3x more DRAM bytes
+                         # written than read): its DRAM writes per second against a
+                         # write-only stream measured in this run
+                         "writes_vs_write_stream": (None if k3_write_bytes() is None else {
+                             "write_stream_gbs": wpeak,
+                             "dram_write_gbs": k3_write_bytes() / (k3_ms / 1e3) / 1e9,
+                             "frac": k3_write_bytes() / (k3_ms / 1e3) / 1e9 / wpeak})},
             "gpu_launches": 2 * args.steps, "clocks": clk}
 
 

@@ -499,6 +499,9 @@ int duchess_sgd_update(float* w, const float* grad, int32_t n, float lr, void* s
 /* Measurement: stream `bytes` of device memory (16-byte aligned) through a
  * read-only persistent kernel (the read-only HBM ceiling, bench.py roofline). */
 int duchess_read_stream(const void* buf, int64_t bytes, uint32_t* sink, void* stream);
+/* Measurement: write `bytes` of device memory (16-byte aligned) with a
+ * persistent streaming-store kernel (the write-only HBM ceiling, bench.py). */
+int duchess_write_stream(void* buf, int64_t bytes, uint32_t seed, void* stream);
 /* Measurement: hold `stream` until the host writes nonzero to *host_flag
  * (pinned host memory) or timeout_ns elapses (then *timed_out = 1, device
  * memory), so a benchmark can enqueue its whole timed region first. */

@@ -128,6 +128,7 @@ SYMBOLS = {
                                 C.c_void_p, C.c_void_p]),
     "duchess_read_stream": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "duchess_gate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "duchess_write_stream": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p]),
     "duchess_baseline_round": (C.c_int, [C.POINTER(Policy), C.POINTER(Workload),
                                          C.POINTER(State), C.c_void_p]),
     "duchess_branch_out_sample": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,

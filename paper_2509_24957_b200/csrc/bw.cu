@@ -36,6 +36,21 @@ __global__ void __launch_bounds__(512) read_stream_kernel(const uint4* __restric
   if (acc == 0x9E3779B9u) out[0] = acc;   // keeps the loads; practically never stores
 }
 
+// Write-only HBM stream (measurement): the ceiling of write-dominated kernels
+// (K3's fork copies write ~4x what they read). Persistent grid, 16-byte
+// streaming stores, eight per thread per iteration.
+__global__ void __launch_bounds__(512) write_stream_kernel(uint4* __restrict__ p, int64_t n16,
+                                                           uint32_t seed) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint4 v = make_uint4(seed, seed ^ 0x9E3779B9u, seed + 1u, ~seed);
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) __stcs(p + i + k * stride, v);
+  }
+  for (; i < n16; i += stride) __stcs(p + i, v);
+}
+
 // Launch gate (measurement): one thread waits until the host sets *flag
 // (pinned host memory, read through its device mapping) or `timeout_ns`
 // passes, so a benchmark can enqueue its whole timed region before the GPU
@@ -57,6 +72,16 @@ __global__ void gate_kernel(const volatile int32_t* flag, int64_t timeout_ns, in
 }  // namespace duchess
 
 using namespace duchess;
+
+extern "C" int duchess_write_stream(void* buf, int64_t bytes, uint32_t seed, void* stream) {
+  if (!buf || bytes < 16 || (reinterpret_cast<uintptr_t>(buf) & 15)) return DUCHESS_EINVAL;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  write_stream_kernel<<<unsigned(4 * sms), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint4*>(buf), bytes / 16, seed);
+  return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+}
 
 extern "C" int duchess_gate(const int32_t* host_flag, int64_t timeout_ns, int32_t* timed_out,
                             void* stream) {
