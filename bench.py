@@ -774,7 +774,7 @@ def run_fork_bench(args, rank, world, local_rank):
                          # the launch is write-dominated (ncu: ~4.3x more DRAM bytes
                          # written than read): its DRAM writes per second against a
                          # write-only stream measured in this run
-                         "writes_vs_write_stream": (None if k3_write_bytes() is None else {
+                         "writes_vs_write_stream": (None if k3_write_bytes() is None or wpeak is None else {
                              "write_stream_gbs": wpeak,
                              "dram_write_gbs": k3_write_bytes() / (k3_ms / 1e3) / 1e9,
                              "frac": k3_write_bytes() / (k3_ms / 1e3) / 1e9 / wpeak})},
