@@ -66,6 +66,19 @@ def test_invalid_arguments_are_rejected_before_launch():
     pol.max_branches = 0
     assert lib.duchess_advance(ctypes.byref(pol), ctypes.byref(_lib.Workload()),
                                ctypes.byref(_lib.State()), None) == 1
+    # round-2 entry points: unknown scorer flags, bad sort / KV / measurement arguments
+    fake = ctypes.c_void_p(16)                   # never dereferenced: rejected first
+    assert lib.duchess_score_active_ex(fake, 1, 4, 1, 1, 16, 16, 16, 16, fake, fake, fake,
+                                       fake, fake, fake, 4, None) == 1
+    assert lib.duchess_sort_keys(None, 5, None, None, 0, None) == 1
+    assert lib.duchess_sort_keys(fake, 5, fake, fake, 8, None) == 1      # workspace too small
+    assert lib.duchess_sort_keys(None, 0, None, None, 0, None) == 0       # empty: nothing to do
+    assert lib.duchess_sort_keys_workspace_bytes(5) >= 5 * 24
+    assert lib.duchess_kv_round(ctypes.byref(pol), ctypes.byref(_lib.State()),
+                                ctypes.byref(_lib.KV()), None) == 1
+    assert lib.duchess_gate(None, 1000, None, None) == 1
+    assert lib.duchess_write_stream(None, 1 << 20, 0, None) == 1
+    assert lib.duchess_row_normalize(fake, 7, 4, 16, fake, None) == 1     # unknown dtype
 
 
 @pytest.mark.parametrize("cname,pyname", [("DuchessPolicy", "Policy"),

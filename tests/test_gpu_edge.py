@@ -152,3 +152,31 @@ def test_upload_survivors_rejects_pageable_host_memory():
     cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
     assert lib.duchess_gather_active(host.data_ptr(), dev.data_ptr(), 256, rows.data_ptr(),
                                      cnt.data_ptr(), 4, _lib.stream_handle()) == 1
+
+
+def test_launch_gate_holds_the_stream_until_released_or_timeout():
+    """bench.py's measurement gate (duchess_gate): work queued behind it does
+    not run until the host writes the pinned flag; without the write it gives
+    up after its timeout and reports that."""
+    import time
+
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    st = torch.cuda.current_stream()
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    timed_out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    x = torch.zeros(1, device="cuda")
+    torch.cuda.synchronize()
+    _lib.check(lib.duchess_gate(flag.data_ptr(), 5_000_000_000, timed_out.data_ptr(),
+                                st.cuda_stream), "gate")
+    x.add_(1)
+    time.sleep(0.05)
+    assert not st.query()                        # held
+    flag.fill_(1)
+    torch.cuda.synchronize()
+    assert float(x.item()) == 1.0 and int(timed_out.item()) == 0
+    flag.zero_()
+    _lib.check(lib.duchess_gate(flag.data_ptr(), 20_000_000, timed_out.data_ptr(),
+                                st.cuda_stream), "gate")
+    torch.cuda.synchronize()                     # released by the 20 ms timeout
+    assert int(timed_out.item()) == 1
