@@ -342,9 +342,15 @@ class Gate:
     def release(self):
         self.flag.fill_(1)
 
-    def check(self):
+    def check(self) -> bool:
+        """True when the gate opened by release(); False when it gave up on its
+        timeout (the timed region then includes host enqueue time, reported in
+        the line's config as gate_timed_out)."""
         if self.enabled and int(self.timed_out.item()):
-            raise RuntimeError("launch gate timed out: the timed region was not fully enqueued")
+            print("warning: launch gate timed out; the timed region includes host time",
+                  file=sys.stderr)
+            return False
+        return True
 
 
 # Configs whose N > 1 run splits the config's requests over the ranks (BASELINE
@@ -445,7 +451,9 @@ def run_serving(args, cfg, rank, world, local_rank):
     # The timed steps are enqueued behind a gate kernel (released once the first
     # GATE_STEPS steps are queued), so the device time measures the steps
     # back to back rather than the host's first launches (nvbench's blocking
-    # kernel); the barrier + synchronize bracket is unchanged.
+    # kernel); the barrier + synchronize bracket is unchanged. Every kernel of
+    # a step ran in the warm-up, so no lazy module load (which would wait for
+    # the gate) happens while it holds.
     gate = Gate(dev, enabled=not args.no_gate)
     gate.hold(main)
     ev0.record(main)
@@ -464,7 +472,7 @@ def run_serving(args, cfg, rank, world, local_rank):
     ev1.record(main)
     gate.release()
     torch.cuda.synchronize(dev)
-    gate.check()
+    gate_ok = gate.check()
     clk = clocks.stop() if clocks else None
     cnt = srv.counters() - c0
     kv1 = srv.kv_counters()
@@ -564,6 +572,7 @@ def run_serving(args, cfg, rank, world, local_rank):
                    "timed_region": f"CUDA events on the main stream around K steps; the first "
                                    f"{GATE_STEPS} steps are enqueued behind a launch gate "
                                    f"(duchess_gate) before the GPU starts them",
+                   **({} if gate_ok else {"gate_timed_out": True}),
                    "parallelism": f"request-sharded x{world} GPUs x{S} streams"},
         "branch_steps_per_step": bs_all / args.steps,
         "roofline": roof,

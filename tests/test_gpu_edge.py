@@ -166,6 +166,7 @@ def test_launch_gate_holds_the_stream_until_released_or_timeout():
     flag = torch.zeros(1, dtype=torch.int32).pin_memory()
     timed_out = torch.zeros(1, dtype=torch.int32, device="cuda")
     x = torch.zeros(1, device="cuda")
+    x.add_(0)          # load the add kernel now: a first (lazy) module load would wait for the gate
     torch.cuda.synchronize()
     _lib.check(lib.duchess_gate(flag.data_ptr(), 5_000_000_000, timed_out.data_ptr(),
                                 st.cuda_stream), "gate")
