@@ -8,14 +8,18 @@
 //
 // Blackwell design: one persistent CTA per SM; a producer warp streams row
 // blocks into a shared-memory ring with cp.async.bulk (TMA bulk copies,
-// completion tracked by mbarrier transaction counts), eight consumer warps
-// compute the row dots from shared memory (keeping the stage's converted
-// elements in registers), reduce them with one named barrier per stage, and
-// accumulate residual * x into per-thread fp32 registers, so X is read from
-// HBM and from shared memory exactly once. (Replacing the named barrier with
-// per-row mbarriers, so one row's reduction overlaps the next row's dot,
-// measured slower: 0.74 vs 0.87 of HBM.) Per-CTA partial gradients are reduced in a
-// fixed order by a second kernel (deterministic).
+// completion tracked by mbarrier transaction counts). Default
+// (lr_grad_split_kernel): eight "dot" warps compute each 64 KB stage's partial
+// row dots and pass them through a per-stage mbarrier to eight "grad" warps,
+// which form the residuals and accumulate residual * x into per-thread fp32
+// registers from a second shared read of the stage; the two warp sets
+// pipeline across stages (C5 on B200: 416 vs 350 M rows/s, 0.93 vs 0.78 of
+// a read-only stream). Alternative (DUCHESS_K4_SPLIT=0, lr_grad_kernel):
+// one warp set keeps a 32 KB stage's converted elements in registers and
+// meets at one named barrier per stage. (Per-row mbarriers inside one warp
+// set measured slower still: 0.74 vs 0.87 of the copy peak.) X is read from
+// HBM exactly once. Per-CTA partial gradients are reduced in a fixed order by
+// a second kernel (deterministic).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -25,7 +29,8 @@ namespace duchess {
 
 constexpr int kConsWarps = 8;
 constexpr int kCons = kConsWarps * 32;
-constexpr int kStageBytesTarget = 32 * 1024;
+constexpr int kStageBytesTarget = 32 * 1024;   // one warp set: two 16 KB rows fit the registers
+constexpr int kStageBytesSplit = 64 * 1024;    // split dot / grad warps: fewer hand-offs per byte
 constexpr int kMaxRB = 8;
 constexpr int kKeepFloats = 128;   // g + w + kept stage per thread under 168 registers
 
@@ -281,6 +286,193 @@ __device__ __forceinline__ void lr_grad_body(const GradArgs& a) {
   if (threadIdx.x == 0) out[a.H] = gb;
 }
 
+// Split roles: CW "dot" warps and CW "grad" warps share each stage. The dot
+// warps compute the stage's partial row dots and hand them over through a
+// per-stage mbarrier; the grad warps wait for them, form the residuals and
+// accumulate r * x from a second read of the same shared stage, then release
+// it. The dot chain of stage s + 1 (loads, FFMA2, butterfly) runs while the
+// grad warps still work on stage s, instead of every warp meeting at one
+// named barrier per stage; the price is a second shared read + bf16
+// conversion per element. The grad warps' arrival releases the stage (the
+// dot warps are done with it once they signalled its dots).
+template <bool BF16, int CW, int VPT, int RB, bool FULL>
+__device__ __forceinline__ void lr_grad_split_body(const GradArgs& a) {
+  constexpr int NCONS = CW * 32;
+  constexpr int EPV = BF16 ? 8 : 4;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t full_bar[16], empty_bar[16], dots_bar[16];
+  __shared__ float red[16][CW][RB];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = int64_t(blockIdx.x) * a.rows_per_cta;
+  const int64_t row1 = lmin(a.n_rows, row0 + a.rows_per_cta);
+  const int64_t n_my = lmax(int64_t(0), row1 - row0);
+  const int64_t n_iter = (n_my + a.rb - 1) / a.rb;
+  const int stage_bytes = a.rb * a.row_bytes;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], CW);
+      mbar_init(&dots_bar[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 2 * CW) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t it = 0; it < n_iter; ++it) {
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        const int64_t r = row0 + it * a.rb;
+        const int nr = int(lmin(a.rb, row1 - r));
+        const uint32_t bytes = uint32_t(nr) * uint32_t(a.row_bytes);
+        mbar_expect_tx(&full_bar[s], bytes);
+        bulk_g2s(smem + size_t(s) * stage_bytes, a.X + r * a.row_bytes, bytes, &full_bar[s], pol);
+        if (++s == a.stages) { s = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+
+  const bool dot_role = warp < CW;
+  const int tid = int(threadIdx.x) - (dot_role ? 0 : NCONS);   // column slot within the role
+  const int rw = dot_role ? warp : warp - CW;
+  const int nvec = a.row_bytes / 16;
+  float acc[VPT][EPV];     // dot warps: w; grad warps: g
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = j * NCONS + tid;
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      const int col = v * EPV + e;
+      acc[j][e] = dot_role && v < nvec && col < a.H ? a.w[col] : 0.f;
+    }
+  }
+  const float bias = a.w[a.H];
+  float gb = 0.f;
+
+  auto convert = [&](const uint4& x, float (&xe)[EPV]) {
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (BF16) {
+        xe[2 * e] = bf16lo(xw[e]);
+        xe[2 * e + 1] = bf16hi(xw[e]);
+      } else {
+        xe[e] = __uint_as_float(xw[e]);
+      }
+    }
+  };
+  auto load_vecs = [&](uint4 (&xv)[VPT], const char* base, int q, int nr) {
+    const uint4* rowv = reinterpret_cast<const uint4*>(base + size_t(q) * a.row_bytes);
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int v = j * NCONS + tid;
+      xv[j] = (q < nr && (FULL || v < nvec)) ? rowv[v] : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t it = 0; it < n_iter; ++it) {
+    const int64_t r = row0 + it * a.rb;
+    const int nr = int(lmin(a.rb, row1 - r));
+    const char* base = smem + size_t(s) * stage_bytes;
+    if (dot_role) {
+      mbar_wait(&full_bar[s], ph);
+      float v[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        uint4 xv[VPT];
+        load_vecs(xv, base, q, nr);
+        float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          float xe[EPV];
+          convert(xv[j], xe);
+#pragma unroll
+          for (int e = 0; e < EPV; e += 2) ffma2(p0, p1, acc[j][e], acc[j][e + 1], xe[e], xe[e + 1]);
+        }
+        v[q] = p0 + p1;
+      }
+      // the RB rows' warp sums in one butterfly (see lr_grad_body)
+      int width = RB;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        if (width > 1) {
+          const bool upper = lane & o;
+#pragma unroll
+          for (int h = 0; h < RB / 2; ++h) {
+            if (2 * h >= width) break;
+            const float keep = upper ? v[2 * h + 1] : v[2 * h];
+            const float send = upper ? v[2 * h] : v[2 * h + 1];
+            v[h] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+          width >>= 1;
+        } else {
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+      }
+      constexpr int LB = RB == 1 ? 0 : RB == 2 ? 1 : RB == 4 ? 2 : 3;
+      int q = 0;
+#pragma unroll
+      for (int b = 0; b < LB; ++b) q |= ((lane >> (4 - b)) & 1) << b;
+      if ((lane & ((1 << (5 - LB)) - 1)) == 0 && q < nr) red[s][rw][q] = v[0];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dots_bar[s]);
+    } else {
+      float yl = lane < nr ? __ldg(a.y + r + lane) : 0.f;
+      mbar_wait(&dots_bar[s], ph);   // implies the stage's bytes landed
+      float mine = 0.f;
+      if (lane < nr) {
+        float z = bias;
+#pragma unroll
+        for (int k = 0; k < CW; ++k) z += red[s][k][lane];
+        mine = 1.0f / (1.0f + __expf(-z)) - yl;
+      }
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const float rq = __shfl_sync(0xffffffffu, mine, q);
+        gb += rq;                                   // 0 for q >= nr
+        uint4 xv[VPT];
+        load_vecs(xv, base, q, nr);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          float xe[EPV];
+          convert(xv[j], xe);
+#pragma unroll
+          for (int e = 0; e < EPV; e += 2) ffma2(acc[j][e], acc[j][e + 1], rq, rq, xe[e], xe[e + 1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+    if (++s == a.stages) { s = 0; ph ^= 1u; }
+  }
+  if (dot_role) return;
+
+  float* out = a.partial + int64_t(blockIdx.x) * (a.H + 1);
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = j * NCONS + tid;
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      const int col = v * EPV + e;
+      if (v < nvec && col < a.H) out[col] = acc[j][e];
+    }
+  }
+  if (tid == 0) out[a.H] = gb;
+}
+
+template <bool BF16, int VPT, int RB, bool FULL>
+__global__ void __launch_bounds__(2 * kCons + 32, 1) lr_grad_split_kernel(GradArgs a) {
+  lr_grad_split_body<BF16, kConsWarps, VPT, RB, FULL>(a);
+}
+
 // Default: one CTA per SM (8 + 1 warps = 3 warps per SM sub-partition, so up
 // to 168 registers), the stage's converted elements kept in registers between
 // the two passes. Measured on B200 at H = 8192 bf16: 0.87 of HBM, against 0.78
@@ -313,11 +505,17 @@ __global__ void sgd_kernel(float* w, const float* g, int n, float lr) {
 }
 
 template <bool BF16, int VPT, int RB, bool FULL>
-static cudaError_t launch_grad_full(const GradArgs& a, bool keep, int grid, size_t smem,
+static cudaError_t launch_grad_full(const GradArgs& a, int keep, int grid, size_t smem,
                                     cudaStream_t s) {
+  if (keep == 2) {                       // split dot / grad warps
+    auto k = lr_grad_split_kernel<BF16, VPT, RB, FULL>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k<<<grid, 2 * kCons + 32, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   void (*k)(GradArgs) = lr_grad_kernel_reread<BF16, VPT, RB, FULL>;
   if constexpr (VPT * (BF16 ? 8 : 4) * (2 + RB) <= kKeepFloats) {
-    if (keep) k = lr_grad_kernel<BF16, VPT, RB, FULL>;
+    if (keep == 1) k = lr_grad_kernel<BF16, VPT, RB, FULL>;
   }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<grid, kCons + 32, smem, s>>>(a);
@@ -325,7 +523,7 @@ static cudaError_t launch_grad_full(const GradArgs& a, bool keep, int grid, size
 }
 
 template <bool BF16, int VPT, int RB>
-static cudaError_t launch_grad_rb(const GradArgs& a, bool keep, int grid, size_t smem,
+static cudaError_t launch_grad_rb(const GradArgs& a, int keep, int grid, size_t smem,
                                   cudaStream_t s) {
   return a.row_bytes == VPT * kCons * 16
              ? launch_grad_full<BF16, VPT, RB, true>(a, keep, grid, smem, s)
@@ -333,7 +531,7 @@ static cudaError_t launch_grad_rb(const GradArgs& a, bool keep, int grid, size_t
 }
 
 template <bool BF16, int VPT>
-static cudaError_t launch_grad(const GradArgs& a, bool keep, int grid, size_t smem,
+static cudaError_t launch_grad(const GradArgs& a, int keep, int grid, size_t smem,
                                cudaStream_t s) {
   switch (a.rb) {
     case 1: return launch_grad_rb<BF16, VPT, 1>(a, keep, grid, smem, s);
@@ -377,12 +575,14 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   while (vpt < vpt_needed) vpt <<= 1;
   if (vpt > 8) return DUCHESS_EINVAL;
   // Tunables (env, for sweeps): stage bytes target, keep the stage in registers.
-  static const int stage_target = [] { const char* e = getenv("DUCHESS_K4_STAGE"); int v = e ? atoi(e) : kStageBytesTarget; return v < 1024 ? 1024 : v; }();
+  static const int split = [] { const char* e = getenv("DUCHESS_K4_SPLIT"); return e ? atoi(e) : 1; }();
+  static const int stage_target = [] { const char* e = getenv("DUCHESS_K4_STAGE"); int v = e ? atoi(e) : split ? kStageBytesSplit : kStageBytesTarget; return v < 1024 ? 1024 : v; }();
   static const int keep_mode = [] { const char* e = getenv("DUCHESS_K4_KEEP"); return e ? atoi(e) : -1; }();
   int rb = int(lmax(1, lmin(kMaxRB, stage_target / row_bytes)));
   rb = rb >= 8 ? 8 : rb >= 4 ? 4 : rb >= 2 ? 2 : 1;   // compile-time rows per stage
   // g, w and the kept stage: VPT * (16 / esz) * (2 + rb) floats per thread
-  const bool keep = keep_mode != 0 && vpt * (16 / esz) * (2 + rb) <= kKeepFloats;
+  // 2: split dot / grad warps; 1: one warp set keeping the stage in registers; 0: re-read
+  const int keep = split ? 2 : keep_mode != 0 && vpt * (16 / esz) * (2 + rb) <= kKeepFloats ? 1 : 0;
   const int grid = num_sms();          // one CTA per SM (3 warps per sub-partition)
   const int smem_budget = 200 * 1024;
   if (!workspace || workspace_bytes < size_t(grid) * size_t(H + 1) * sizeof(float))

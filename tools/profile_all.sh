@@ -13,7 +13,7 @@ ncu --set full --clock-control none --import-source on -k regex:score_rows -s 5 
 ncu --set full --cache-control none --clock-control none --import-source on -k regex:^round_kernel -s 40 -c 1 -o $D/round_full -f python bench.py --config c2 --steps 8 --warmup 3 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/round_full.log 2>&1
 ncu --set full --cache-control none --clock-control none --import-source on -k regex:kv_round_kernel -s 40 -c 1 -o $D/kv_full -f python bench.py --config c2 --steps 8 --warmup 3 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/kv_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fork_exec -s 2 -c 1 -o $D/k3_full -f python bench.py --config c4 --steps 3 --warmup 1 --no-cpu-baseline --no-gate > $D/k3_full.log 2>&1
-DUCHESS_C5_ROWS=524288 ncu --set full --clock-control none --import-source on -k regex:lr_grad_kernel -s 2 -c 1 -o $D/k4_full -f python bench.py --config c5 --steps 3 --warmup 1 --no-cpu-baseline --no-gate > $D/k4_full.log 2>&1
+DUCHESS_C5_ROWS=524288 ncu --set full --clock-control none --import-source on -k regex:lr_grad_ -s 2 -c 1 -o $D/k4_full -f python bench.py --config c5 --steps 3 --warmup 1 --no-cpu-baseline --no-gate > $D/k4_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:linear_kernel -s 2 -c 1 -o $D/mlp1_full -f python bench.py --config c3mlp --steps 3 --warmup 1 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/mlp1_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:mlp_probe_tc -s 2 -c 1 -o $D/mlp2_full -f python bench.py --config c3mlp --steps 3 --warmup 1 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/mlp2_full.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
