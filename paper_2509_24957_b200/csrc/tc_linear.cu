@@ -497,6 +497,95 @@ __global__ void __launch_bounds__(256) row_normalize_vec_kernel(const void* X, i
   }
 }
 
+// bf16 rows (K % 8 == 0, 16 B-aligned): one WARP per row, persistent, with
+// the rows staged in shared memory. The CTA-per-row kernel above meets at four
+// __syncthreads per row, so an SM had only ~8 rows' loads in flight and the
+// pass ran at half the copy rate. Here each warp owns two row slots: while it
+// normalises row i from one slot, ONE cp.async.bulk (lane 0, mbarrier
+// transaction count) fills the other with its next row. Statistics: the mean
+// summed in fp64 (four independent chains), then d = (x - mean_hi) - mean_lo
+// in fp32 with the mean split into two floats (no cancellation for rows with
+// a large common offset), the centred square sum in fp32 per lane and fp64
+// across lanes, z = d * inv rounded to bf16.
+constexpr int kNormWarps = 4;
+
+__global__ void __launch_bounds__(kNormWarps * 32) row_normalize_bulk_kernel(const uint16_t* X,
+                                                                            int64_t M, int K,
+                                                                            uint16_t* Z) {
+  extern __shared__ __align__(128) unsigned char norm_smem[];
+  __shared__ uint64_t bars[kNormWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t row_bytes = uint32_t(K) * 2u;
+  const uint32_t slot_bytes = (row_bytes + 127u) & ~127u;
+  unsigned char* slot0 = norm_smem + size_t(warp) * 2 * slot_bytes;
+  const int64_t stride = int64_t(gridDim.x) * kNormWarps;
+  int64_t row = int64_t(blockIdx.x) * kNormWarps + warp;
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t pol = evict_first_policy();
+  if (lane == 0 && row < M) {
+    mbar_expect_tx(&bars[warp][0], row_bytes);
+    bulk_g2s(slot0, X + row * K, row_bytes, &bars[warp][0], pol);
+  }
+  const int nch = K / 8;
+  for (int it = 0; row < M; ++it, row += stride) {
+    const int b = it & 1;
+    const uint4* sv = reinterpret_cast<const uint4*>(slot0 + size_t(b) * slot_bytes);
+    if (lane == 0 && row + stride < M) {
+      // the other slot was last read in iteration it - 1 (its reads completed
+      // before the __syncwarp that ended it)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[warp][b ^ 1], row_bytes);
+      bulk_g2s(slot0 + size_t(b ^ 1) * slot_bytes, X + (row + stride) * K, row_bytes,
+               &bars[warp][b ^ 1], pol);
+    }
+    mbar_wait(&bars[warp][b], uint32_t(it >> 1) & 1u);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint4 u = sv[ch];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] += double(bf16lo(w4[e])) + double(bf16hi(w4[e]));
+    }
+    double sm = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    const double mean = sm / K;
+    const float mh = float(mean), ml = float(mean - double(mh));
+    float q0 = 0.f, q1 = 0.f;
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint4 u = sv[ch];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float d0 = (bf16lo(w4[e]) - mh) - ml, d1 = (bf16hi(w4[e]) - mh) - ml;
+        q0 = fmaf(d0, d0, q0);
+        q1 = fmaf(d1, d1, q1);
+      }
+    }
+    double q = double(q0) + double(q1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = float(1.0 / sqrt(q / K + double(kLayerNormEps)));
+    uint4* zr = reinterpret_cast<uint4*>(Z + row * K);
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint4 u = sv[ch];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        o[e] = uint32_t(f32_to_bf16_rne(((bf16lo(w4[e]) - mh) - ml) * inv)) |
+               (uint32_t(f32_to_bf16_rne(((bf16hi(w4[e]) - mh) - ml) * inv)) << 16);
+      zr[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    __syncwarp();
+  }
+}
+
 // Classifier head (N small, e.g. 5): one warp per row, fp32 dots over the
 // bf16 hidden vector, logits out.
 __global__ void head_kernel(const uint16_t* Hm, int64_t M, int K, const float* W, const float* b,
@@ -551,6 +640,69 @@ __global__ void head_vec_kernel(const uint16_t* Hm, int64_t M, int K, const floa
     }
     const float acc = warp_sum(acc0 + acc1);
     if (lane == 0) logits[row * NO + o] = acc + b[o];
+  }
+}
+
+// Head with the weights in registers (NO outputs, K <= 256 * HC / 32 * 8):
+// persistent warps, each lane holds its 8 * HC columns of every output row
+// of W, so a row costs two 16-byte loads, NO * 8 * HC FMAs and NO warp sums
+// (the vector kernel above re-loaded W for every row and output and ran at
+// 1 TB/s on 33 MB). The next row's vectors are loaded before the current
+// row's sums.
+template <int NO, int HC>
+__global__ void __launch_bounds__(256) head_reg_kernel(const uint16_t* Hm, int64_t M, int K,
+                                                       const float* W, const float* b,
+                                                       float* logits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = K / 8;
+  float w[NO][HC][8];
+#pragma unroll
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int c = 0; c < HC; ++c) {
+      const int ch = c * 32 + lane;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[o][c][e] = ch < nch ? W[int64_t(o) * K + ch * 8 + e] : 0.f;
+    }
+  float bias[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) bias[o] = b[o];
+  auto load = [&](int64_t r, uint4 (&hv)[HC]) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(Hm + r * K);
+#pragma unroll
+    for (int c = 0; c < HC; ++c) {
+      const int ch = c * 32 + lane;
+      hv[c] = r < M && ch < nch ? ldg_stream(h4 + ch) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  uint4 cur[HC];
+  load(row, cur);
+  for (; row < M; row += stride) {
+    uint4 nxt[HC];
+    load(row + stride, nxt);
+    float acc[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) {
+      const uint32_t x4[4] = {cur[c].x, cur[c].y, cur[c].z, cur[c].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = bf16lo(x4[e]), hi = bf16hi(x4[e]);
+#pragma unroll
+        for (int o = 0; o < NO; ++o) acc[o] = fmaf(hi, w[o][c][2 * e + 1], fmaf(lo, w[o][c][2 * e], acc[o]));
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[o] = warp_sum(acc[o]);
+    float mine = 0.f;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) mine = lane == o ? acc[o] + bias[o] : mine;
+    if (lane < NO) logits[row * NO + lane] = mine;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) cur[c] = nxt[c];
   }
 }
 
@@ -721,6 +873,23 @@ extern "C" int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec = K % 8 == 0 && K <= 256 * 8 * 4 &&
                    (reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Z)) % 16 == 0;
+  if (dtype == DUCHESS_BF16 && vec && K <= 8192) {   // one warp per row, rows staged in smem
+    const size_t slot = (size_t(K) * 2 + 127) & ~size_t(127);
+    const size_t smem = slot * 2 * tcl::kNormWarps;
+    cudaFuncSetAttribute(tcl::row_normalize_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcl::row_normalize_bulk_kernel,
+                                                  tcl::kNormWarps * 32, smem);
+    const int64_t need = (M + tcl::kNormWarps - 1) / tcl::kNormWarps;
+    const unsigned grid = unsigned(need < int64_t(sms) * (per_sm < 1 ? 1 : per_sm)
+                                       ? need : int64_t(sms) * (per_sm < 1 ? 1 : per_sm));
+    tcl::row_normalize_bulk_kernel<<<grid, tcl::kNormWarps * 32, smem, st>>>(
+        static_cast<const uint16_t*>(X), M, K, static_cast<uint16_t*>(Z));
+    return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
+  }
   if (dtype == DUCHESS_BF16 || (dtype == DUCHESS_F32 && vec)) {
     if (!vec) return DUCHESS_EINVAL;               // bf16 rows: vectorised path only
     const int rv = (K / 8 + 255) / 256;
@@ -751,7 +920,15 @@ extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const fl
   const uint16_t* h = static_cast<const uint16_t*>(H);
   const bool vec = K % 8 == 0 && reinterpret_cast<uintptr_t>(H) % 16 == 0 &&
                    reinterpret_cast<uintptr_t>(W) % 16 == 0 && K <= 256 * 8;
-  if (vec && K <= 256 * 2) tcl::head_vec_kernel<2><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
+  if (vec && n_out == 5 && K <= 32 * 8 * 2) {      // the classifier's 5 levels
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcl::head_reg_kernel<5, 2>, 256, 0);
+    const int64_t cap = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
+    const unsigned g = unsigned(int64_t(grid) < cap ? int64_t(grid) : cap);
+    tcl::head_reg_kernel<5, 2><<<g, 256, 0, s>>>(h, M, K, W, b, logits);
+  } else if (vec && K <= 256 * 2) tcl::head_vec_kernel<2><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   else if (vec) tcl::head_vec_kernel<8><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   else tcl::head_kernel<<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;

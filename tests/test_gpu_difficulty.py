@@ -101,6 +101,7 @@ def test_predict_difficulty_batch_equals_single_calls():
 
 
 @pytest.mark.parametrize("dtype,K", [(torch.bfloat16, 4096), (torch.bfloat16, 1032),
+                                     (torch.bfloat16, 512), (torch.bfloat16, 8192),
                                      (torch.float32, 4096), (torch.float32, 200),
                                      (torch.float64, 512)])
 def test_row_normalize_matches_fp64(dtype, K):
@@ -121,3 +122,23 @@ def test_row_normalize_matches_fp64(dtype, K):
     got = z.double()
     ulp = ref.abs().clamp_min(2 ** -126) * 2 ** -7
     assert bool(((got - ref).abs() <= ulp).all())
+
+
+@pytest.mark.parametrize("K,n_out,M", [(512, 5, 3001), (256, 5, 17), (200, 5, 40), (1024, 5, 999),
+                                       (512, 3, 500)])
+def test_head_logits_match_fp64(K, n_out, M):
+    """duchess_head_logits (the classifier's output layer over the last hidden
+    bf16 vectors): the register-weight kernel (5 outputs, K <= 512), the
+    vector kernel and the scalar fallback all equal the fp64 dot of the same
+    bf16 inputs within fp32 accumulation error."""
+    from paper_2509_24957_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(K * 7 + n_out)
+    h = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
+    W = torch.randn((n_out, K), generator=g, device="cuda") / np.sqrt(K)
+    b = torch.randn(n_out, generator=g, device="cuda")
+    out = torch.empty((M, n_out), device="cuda")
+    _lib.check(lib.duchess_head_logits(h.data_ptr(), M, K, W.data_ptr(), b.data_ptr(), n_out,
+                                       out.data_ptr(), _lib.stream_handle()), "head_logits")
+    ref = h.double() @ W.double().T + b.double()
+    np.testing.assert_allclose(out.double().cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-5)
