@@ -207,6 +207,10 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   if constexpr (CG == 2) cluster_sync_all();       // the leader's barriers exist before any signal
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // PDL: the setup above (barriers, TMEM allocation) overlaps the previous
+  // layer's tail; its output is read only after this point.
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t tmem = tmem_base;
   const int stamp = LNF ? a.hdr[0] + 1 : 0;
 
@@ -527,6 +531,8 @@ __global__ void __launch_bounds__(kNormWarps * 32) row_normalize_bulk_kernel(con
   }
   __syncwarp();
   const uint64_t pol = evict_first_policy();
+  pdl_wait();                  // rows may come from the previous kernel
+  pdl_launch_dependents();     // the first layer's setup may start on freed SMs
   if (lane == 0 && row < M) {
     mbar_expect_tx(&bars[warp][0], row_bytes);
     bulk_g2s(slot0, X + row * K, row_bytes, &bars[warp][0], pol);
@@ -669,6 +675,8 @@ __global__ void __launch_bounds__(256) head_reg_kernel(const uint16_t* Hm, int64
   float bias[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) bias[o] = b[o];
+  pdl_wait();                  // the weights above overlap the last layer's tail
+  pdl_launch_dependents();
   auto load = [&](int64_t r, uint4 (&hv)[HC]) {
     const uint4* h4 = reinterpret_cast<const uint4*>(Hm + r * K);
 #pragma unroll
@@ -836,13 +844,15 @@ extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, in
   cfg.blockDim = dim3(tcl::THREADS);
   cfg.dynamicSmemBytes = size_t(smem);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = unsigned(CG);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (CG == 2) {
     // every pair must be resident at once (units wait on statistics other
     // CTAs publish): never launch more pairs than can be co-scheduled
@@ -927,7 +937,16 @@ extern "C" int duchess_head_logits(const void* H, int64_t M, int32_t K, const fl
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcl::head_reg_kernel<5, 2>, 256, 0);
     const int64_t cap = int64_t(sms) * (per_sm < 1 ? 1 : per_sm);
     const unsigned g = unsigned(int64_t(grid) < cap ? int64_t(grid) : cap);
-    tcl::head_reg_kernel<5, 2><<<g, 256, 0, s>>>(h, M, K, W, b, logits);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tcl::head_reg_kernel<5, 2>, h, M, K, W, b, logits);
   } else if (vec && K <= 256 * 2) tcl::head_vec_kernel<2><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   else if (vec) tcl::head_vec_kernel<8><<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
   else tcl::head_kernel<<<grid, 256, 0, s>>>(h, M, K, W, b, n_out, logits);
