@@ -58,6 +58,14 @@ __device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
   return uint16_t(u >> 16);
 }
 
+// Two fp32 values -> packed bf16x2 (lo in bits 15:0), round-to-nearest-even:
+// one F2FP.BF16.F32.PACK_AB; equal to f32_to_bf16_rne for finite inputs.
+__device__ __forceinline__ uint32_t pack_bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // acc_lo += bf16(w[15:0]), acc_hi += bf16(w[31:16]) in fp32, round to nearest:
 // one mixed-precision add per element (FHADD.BF16 on sm_100a), bit-identical
 // to widening the bf16 and adding in fp32.

@@ -37,7 +37,8 @@ using namespace tcpair;
 
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
-constexpr int THREADS = 192;
+constexpr int THREADS = 192;       // producer + MMA + 4 epilogue warps
+constexpr int THREADS_EW8 = 320;   // producer + MMA + 8 epilogue warps (two per TMEM lane quarter)
 // CTA pair (cta_group::2): a 256 x 256 tile per pair, each CTA holding its 128
 // rows of A and half (128 columns) of B per stage, so a stage is 32 KB
 template <int CG> struct Cfg {
@@ -162,10 +163,14 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 // leader's MMA thread. Per CTA a stage is 32 KB instead of 48 KB for the same
 // MMA work, so each SM moves a third less operand data per FLOP.
 template <bool LNF, int ACT, int CG>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(LNF ? THREADS : THREADS_EW8, 1)
 linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               Args a) {
   using CF = Cfg<CG>;
+  // Epilogue warps: without the LN fold the epilogue is per column only, so
+  // two warps share each TMEM lane quarter (one half of the tile's columns
+  // each) and a short-K layer's BN + GeLU epilogue keeps up with its MMAs.
+  constexpr int EW = LNF ? 4 : 8;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[CF::NST], empty_bar[CF::NST], tmem_full[2], tmem_empty[2];
@@ -188,7 +193,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4 * CG);     // the epilogue warps of every CTA of the unit
+      mbar_init(&tmem_empty[i], EW * CG);    // the epilogue warps of every CTA of the unit
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -267,6 +272,8 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
   } else {
     // ---- epilogue: row = 32 * (warp % 4) + lane (TMEM lane quarter) ----
     const int q = warp & 3;
+    constexpr int COLS = BN / (EW / 4);                     // columns per epilogue warp
+    const int c_lo = EW == 8 ? ((warp - 2) >> 2) * COLS : 0;
     int i = 0;
     for (int64_t u = u0; u < n_units; u += ustep, ++i) {
       const Unit w = unit_of(u, n_rt_u, n_tiles);
@@ -328,7 +335,7 @@ linear_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__
       const int n0 = nt * BN;
       const int64_t gp = int64_t(g) * a.N;               // group's per-column parameters
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = c_lo; c0 < c_lo + COLS; c0 += 32) {
         float v[32];
         tmem_ld32(base + uint32_t(c0), v);
         const int j0 = n0 + c0;
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(256) row_normalize_vec_kernel(const void* X, i
 // pass ran at half the copy rate. Here each warp owns two row slots: while it
 // normalises row i from one slot, ONE cp.async.bulk (lane 0, mbarrier
 // transaction count) fills the other with its next row. Statistics: the mean
-// summed in fp64 (four independent chains), then d = (x - mean_hi) - mean_lo
+// from compensated fp32 sums per lane and fp64 across lanes, then d = (x - mean_hi) - mean_lo
 // in fp32 with the mean split into two floats (no cancellation for rows with
 // a large common offset), the centred square sum in fp32 per lane and fp64
 // across lanes, z = d * inv rounded to bf16.
@@ -550,14 +557,25 @@ __global__ void __launch_bounds__(kNormWarps * 32) row_normalize_bulk_kernel(con
                &bars[warp][b ^ 1], pol);
     }
     mbar_wait(&bars[warp][b], uint32_t(it >> 1) & 1u);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // compensated fp32 sum per lane (TwoSum error terms accumulated apart;
+    // error ~2^-46 of the sum of |x|, no fp64 conversion per element), then
+    // fp64 across lanes
+    float s0 = 0.f, c0 = 0.f, s1 = 0.f, c1 = 0.f;
+    auto two_sum = [](float& s, float& c, float x) {
+      const float t = s + x, bb = t - s;
+      c += (s - (t - bb)) + (x - bb);
+      s = t;
+    };
     for (int ch = lane; ch < nch; ch += 32) {
       const uint4 u = sv[ch];
       const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[e] += double(bf16lo(w4[e])) + double(bf16hi(w4[e]));
+      for (int e = 0; e < 4; ++e) {
+        two_sum(s0, c0, bf16lo(w4[e]));
+        two_sum(s1, c1, bf16hi(w4[e]));
+      }
     }
-    double sm = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    double sm = (double(s0) + double(c0)) + (double(s1) + double(c1));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
     const double mean = sm / K;
@@ -584,8 +602,7 @@ __global__ void __launch_bounds__(kNormWarps * 32) row_normalize_bulk_kernel(con
       uint32_t o[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        o[e] = uint32_t(f32_to_bf16_rne(((bf16lo(w4[e]) - mh) - ml) * inv)) |
-               (uint32_t(f32_to_bf16_rne(((bf16hi(w4[e]) - mh) - ml) * inv)) << 16);
+        o[e] = pack_bf16x2_rn(((bf16lo(w4[e]) - mh) - ml) * inv, ((bf16hi(w4[e]) - mh) - ml) * inv);
       zr[ch] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     __syncwarp();
@@ -655,7 +672,7 @@ __global__ void head_vec_kernel(const uint16_t* Hm, int64_t M, int K, const floa
 // (the vector kernel above re-loaded W for every row and output and ran at
 // 1 TB/s on 33 MB). The next row's vectors are loaded before the current
 // row's sums.
-template <int NO, int HC>
+template <int NO, int HC>   // NO <= 8
 __global__ void __launch_bounds__(256) head_reg_kernel(const uint16_t* Hm, int64_t M, int K,
                                                        const float* W, const float* b,
                                                        float* logits) {
@@ -703,12 +720,32 @@ __global__ void __launch_bounds__(256) head_reg_kernel(const uint16_t* Hm, int64
         for (int o = 0; o < NO; ++o) acc[o] = fmaf(hi, w[o][c][2 * e + 1], fmaf(lo, w[o][c][2 * e], acc[o]));
       }
     }
+    // the NO warp sums in one transposed butterfly (8 value slots): each of the
+    // first three levels halves the slots a lane carries (lane bit 4, 3, 2
+    // picks the half), the last two sum within groups of four lanes — 9
+    // shuffles instead of 5 per output
+    float v[8];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) acc[o] = warp_sum(acc[o]);
-    float mine = 0.f;
+    for (int o = 0; o < 8; ++o) v[o] = o < NO ? acc[o < NO ? o : 0] : 0.f;
 #pragma unroll
-    for (int o = 0; o < NO; ++o) mine = lane == o ? acc[o] + bias[o] : mine;
-    if (lane < NO) logits[row * NO + lane] = mine;
+    for (int lvl = 0, width = 8; lvl < 3; ++lvl, width >>= 1) {
+      const int off = 16 >> lvl;
+      const bool upper = lane & off;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        if (2 * h >= width) break;
+        const float keep = upper ? v[2 * h + 1] : v[2 * h];
+        const float send = upper ? v[2 * h] : v[2 * h + 1];
+        v[h] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int q = ((lane >> 4) & 1) | (((lane >> 3) & 1) << 1) | (((lane >> 2) & 1) << 2);
+    float bq = 0.f;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) bq = q == o ? bias[o] : bq;
+    if ((lane & 3) == 0 && q < NO) logits[row * NO + q] = v[0] + bq;
 #pragma unroll
     for (int c = 0; c < HC; ++c) cur[c] = nxt[c];
   }
@@ -841,7 +878,7 @@ extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, in
   int64_t units_cap = CG == 2 ? sms / 2 : sms;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(CG * units_cap));
-  cfg.blockDim = dim3(tcl::THREADS);
+  cfg.blockDim = dim3(ln_fold ? tcl::THREADS : tcl::THREADS_EW8);
   cfg.dynamicSmemBytes = size_t(smem);
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[2];
