@@ -824,12 +824,13 @@ extern "C" int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, in
                   reinterpret_cast<uintptr_t>(workspace) % 16))
     return DUCHESS_EINVAL;
   if (M == 0) return DUCHESS_OK;
-  // CTA pairs (cta_group::2) for long K loops (K >= 4096: measured faster, e.g.
-  // 2.01 -> 1.83 ms for 5120 -> 2048 x 4 groups), 1-CTA tiles for short ones
-  // (2048 -> 1024 x 4 groups: 347 vs 460 us with pairs); DUCHESS_TC_PAIR=0 / 1
-  // forces one or the other (measurement)
+  // CTA pairs (cta_group::2) for K >= 1024 (measured faster: 2.01 -> 1.83 ms
+  // for 5120 -> 2048 x 4 groups; with the 8-warp epilogue also for the
+  // classifier's 2048 -> 1024 and 1024 -> 512 layers, 0.650 -> 0.641 ms per
+  // batch), 1-CTA tiles for shorter K loops; DUCHESS_TC_PAIR=0 / 1 forces one
+  // or the other (measurement)
   static const int pair_mode = [] { const char* e = getenv("DUCHESS_TC_PAIR"); return e ? atoi(e) : 2; }();
-  const int CG = pair_mode == 2 ? (K >= 4096 ? 2 : 1) : (pair_mode ? 2 : 1);
+  const int CG = pair_mode == 2 ? (K >= 1024 ? 2 : 1) : (pair_mode ? 2 : 1);
   CUtensorMap ma, mb;
   if (!tcl::make_map_a(&ma, X, uint64_t(M), uint64_t(G), uint64_t(K), x_interleaved != 0))
     return DUCHESS_ECUDA;
