@@ -10,7 +10,7 @@
 // blocks into a shared-memory ring with cp.async.bulk (TMA bulk copies,
 // completion tracked by mbarrier transaction counts). Default
 // (lr_grad_split_kernel): eight "dot" warps compute each 64 KB stage's partial
-// row dots and pass them through a per-stage mbarrier to eight "grad" warps,
+// row dots and pass them through per-slot named barriers to eight "grad" warps,
 // which form the residuals and accumulate residual * x into per-thread fp32
 // registers from a second shared read of the stage; the two warp sets
 // pipeline across stages (C5 on B200: 416 vs 350 M rows/s, 0.93 vs 0.78 of
@@ -288,20 +288,34 @@ __device__ __forceinline__ void lr_grad_body(const GradArgs& a) {
 
 // Split roles: CW "dot" warps and CW "grad" warps share each stage. The dot
 // warps compute the stage's partial row dots and hand them over through a
-// per-stage mbarrier; the grad warps wait for them, form the residuals and
-// accumulate r * x from a second read of the same shared stage, then release
-// it. The dot chain of stage s + 1 (loads, FFMA2, butterfly) runs while the
-// grad warps still work on stage s, instead of every warp meeting at one
-// named barrier per stage; the price is a second shared read + bf16
-// conversion per element. The grad warps' arrival releases the stage (the
-// dot warps are done with it once they signalled its dots).
+// named barrier per ring slot (bar.arrive by the dot warps, bar.sync by the
+// grad warps; a second barrier per slot returns the dot buffer); the grad
+// warps form the residuals and accumulate r * x from a second read of the
+// same shared stage, then release it. The dot chain of stage s + 1 (loads,
+// FFMA2, butterfly) runs while the grad warps still work on stage s, instead
+// of every warp meeting at one barrier per stage; the price is a second shared
+// read + bf16 conversion per element. The grad warps' arrival releases the
+// stage (the dot warps are done with it once they handed its dots over).
+// Named barriers: 1 + s (dots of ring slot s ready), kSplitWar + s (slot s's
+// dots consumed); id 0 is __syncthreads.
+constexpr int kSplitMaxStages = 7;
+constexpr int kSplitWar = 1 + kSplitMaxStages;
+template <int BASE>
+__device__ __forceinline__ void named_sync(int s, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(BASE + s), "r"(n) : "memory");
+}
+template <int BASE>
+__device__ __forceinline__ void named_arrive(int s, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(BASE + s), "r"(n) : "memory");
+}
+
 template <bool BF16, int CW, int VPT, int RB, bool FULL>
 __device__ __forceinline__ void lr_grad_split_body(const GradArgs& a) {
   constexpr int NCONS = CW * 32;
   constexpr int EPV = BF16 ? 8 : 4;
   extern __shared__ __align__(128) char smem[];
-  __shared__ uint64_t full_bar[16], empty_bar[16], dots_bar[16];
-  __shared__ float red[16][CW][RB];
+  __shared__ uint64_t full_bar[kSplitMaxStages], empty_bar[kSplitMaxStages];
+  __shared__ float red[kSplitMaxStages][CW][RB];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = int64_t(blockIdx.x) * a.rows_per_cta;
@@ -314,7 +328,6 @@ __device__ __forceinline__ void lr_grad_split_body(const GradArgs& a) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], CW);
-      mbar_init(&dots_bar[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -421,12 +434,16 @@ __device__ __forceinline__ void lr_grad_split_body(const GradArgs& a) {
       int q = 0;
 #pragma unroll
       for (int b = 0; b < LB; ++b) q |= ((lane >> (4 - b)) & 1) << b;
+      // red[s] hand-off by named barriers (producer arrive / consumer sync):
+      // 1 + s orders these writes before the grad warps' reads, kSplitWar + s
+      // the grad warps' reads of the previous lap before these writes
+      if (it >= a.stages) named_sync<kSplitWar>(s, 2 * NCONS);
       if ((lane & ((1 << (5 - LB)) - 1)) == 0 && q < nr) red[s][rw][q] = v[0];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dots_bar[s]);
+      named_arrive<1>(s, 2 * NCONS);
     } else {
       float yl = lane < nr ? __ldg(a.y + r + lane) : 0.f;
-      mbar_wait(&dots_bar[s], ph);   // implies the stage's bytes landed
+      named_sync<1>(s, 2 * NCONS);   // the dots of stage s
+      mbar_wait(&full_bar[s], ph);   // (complete already) the stage's bytes, for this warp
       float mine = 0.f;
       if (lane < nr) {
         float z = bias;
@@ -448,6 +465,7 @@ __device__ __forceinline__ void lr_grad_split_body(const GradArgs& a) {
           for (int e = 0; e < EPV; e += 2) ffma2(acc[j][e], acc[j][e + 1], rq, rq, xe[e], xe[e + 1]);
         }
       }
+      if (it + a.stages < n_iter) named_arrive<kSplitWar>(s, 2 * NCONS);   // red[s] read
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
@@ -597,7 +615,7 @@ extern "C" int duchess_lr_grad(const void* X, int32_t dtype, const float* y, con
   a.row_bytes = int(row_bytes);
   a.rb = rb;
   const int stage_bytes = a.rb * a.row_bytes;
-  a.stages = int(lmin(16, lmax(2, smem_budget / stage_bytes)));
+  a.stages = int(lmin(keep == 2 ? kSplitMaxStages : 16, lmax(2, smem_budget / stage_bytes)));
   if (int64_t(a.stages) * stage_bytes > smem_budget) return DUCHESS_EINVAL;
   a.rows_per_cta = (n_rows + grid - 1) / grid;
   a.partial = static_cast<float*>(workspace);
