@@ -389,8 +389,9 @@ int duchess_tc_linear_grouped(const void* X, int64_t M, int32_t K, int32_t G,
                               void* stream);
 /* Input LayerNorm as a pass: Z (bf16 [M, K]) = (X - mean) / sqrt(var + 1e-5)
  * per row of X ([M, K], DUCHESS_F32, DUCHESS_F64 or DUCHESS_BF16 — bf16 needs
- * K % 8 == 0, K <= 8192 and 16-byte aligned rows), statistics in fp64
- * (predictor.py:134-136). */
+ * K % 8 == 0, K <= 8192 and 16-byte aligned rows), statistics in fp64 (bf16
+ * rows: compensated fp32 sums per lane, fp64 across lanes; the mean is split
+ * into two floats for the centring) (predictor.py:134-136). */
 int duchess_row_normalize(const void* X, int32_t dtype, int64_t M, int32_t K, void* Z,
                           void* stream);
 /* Small classifier head: logits[M, n_out] = H (bf16 [M, K]) . W^T (fp32 [n_out, K]) + b. */
