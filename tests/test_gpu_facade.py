@@ -267,6 +267,54 @@ def test_active_branch_count_never_exceeds_limit():
                 assert len(active) == cfg.max_branches
 
 
+
+def test_early_terminated_branches_satisfy_rule_and_replay_is_deterministic():
+    """test_orchestrator.py:267-296: every early-terminated branch held the
+    threshold for the last early_term_rounds predictions, streak <= history;
+    two runs with equal seeds give equal RoundReports and outcomes."""
+    from paper_2509_24957_b200.orchestrator import EARLY_TERMINATED, DuchessRun, OrchestratorConfig
+    from paper_2509_24957_b200.predictor import SyntheticPredictorConfig
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    wl = generate_synthetic(SyntheticParams(), 10, seed=5)
+    cfg = OrchestratorConfig(max_branches=10, interval_tokens=80, early_term_threshold=0.5,
+                             early_term_rounds=2)
+    for i, tr in enumerate(wl.requests):
+        run = DuchessRun(tr, cfg, random.Random(i), synthetic=SyntheticPredictorConfig(rho=1.0))
+        run.run()
+        for b in run.branches:
+            if b.status == EARLY_TERMINATED:
+                assert len(b.prediction_history) >= 2
+                assert all(p > 0.5 for p in b.prediction_history[-2:])
+            assert b.streak <= len(b.prediction_history)
+    wl = generate_synthetic(SyntheticParams(), 5, seed=6)
+    cfg = OrchestratorConfig(early_term_threshold=0.6, early_term_rounds=1)
+    synth = SyntheticPredictorConfig(rho=0.7)
+    for i, tr in enumerate(wl.requests):
+        a = DuchessRun(tr, cfg, random.Random(i), synthetic=synth)
+        b = DuchessRun(tr, cfg, random.Random(i), synthetic=synth)
+        ra, rb = [], []
+        while not a.done:
+            ra.append(a.step())
+        while not b.done:
+            rb.append(b.step())
+        assert ra == rb and a.outcome == b.outcome
+
+
+def test_policy_reduction_matches_default_sc():
+    """test_orchestrator.py:299-313: with termination disabled and full
+    consensus / coverage bounds the policy is plain self-consistency."""
+    from paper_2509_24957_b200.orchestrator import (TERMINATION_DISABLED, OrchestratorConfig,
+                                                    run_default_sc, run_duchess)
+    from paper_2509_24957_b200.workload import SyntheticParams, generate_synthetic
+    wl = generate_synthetic(SyntheticParams(templates_per_request=8), 30, seed=7)
+    cfg = OrchestratorConfig(max_branches=8, interval_tokens=80,
+                             early_term_threshold=TERMINATION_DISABLED, consensus_frac=1.0,
+                             coverage_frac=1.0)
+    for i, tr in enumerate(wl.requests):
+        sc, du = run_default_sc(tr, cfg), run_duchess(tr, cfg, random.Random(i))
+        assert (du.tokens_decode, du.tokens_probe, du.tally, du.final) == \
+            (sc.tokens_decode, sc.tokens_probe, sc.tally, sc.final)
+
 # ---- predictor (test_predictor.py) + golden fixture -------------------------
 
 def _mlp(case):
