@@ -5,6 +5,8 @@
 //
 // Persistent grid (4 CTAs x 512 threads per SM), eight independent 16-byte
 // non-coherent loads in flight per thread (256 KB per SM), L1 not allocated.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../../include/duchess_b200.h"
 
@@ -39,6 +41,12 @@ __global__ void __launch_bounds__(512) read_stream_kernel(const uint4* __restric
 // Write-only HBM stream (measurement): the ceiling of write-dominated kernels
 // (K3's fork copies write ~4x what they read). Persistent grid, 16-byte
 // streaming stores, eight per thread per iteration.
+template <bool STCS>
+__device__ __forceinline__ void st16(uint4* p, uint4 v) {
+  if constexpr (STCS) __stcs(p, v);
+  else *p = v;
+}
+template <bool STCS>
 __global__ void __launch_bounds__(512) write_stream_kernel(uint4* __restrict__ p, int64_t n16,
                                                            uint32_t seed) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -46,9 +54,9 @@ __global__ void __launch_bounds__(512) write_stream_kernel(uint4* __restrict__ p
   const uint4 v = make_uint4(seed, seed ^ 0x9E3779B9u, seed + 1u, ~seed);
   for (; i + 7 * stride < n16; i += 8 * stride) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) __stcs(p + i + k * stride, v);
+    for (int k = 0; k < 8; ++k) st16<STCS>(p + i + k * stride, v);
   }
-  for (; i < n16; i += stride) __stcs(p + i, v);
+  for (; i < n16; i += stride) st16<STCS>(p + i, v);
 }
 
 // Launch gate (measurement): one thread waits until the host sets *flag
@@ -78,7 +86,10 @@ extern "C" int duchess_write_stream(void* buf, int64_t bytes, uint32_t seed, voi
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  write_stream_kernel<<<unsigned(4 * sms), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+  // store flavour (env DUCHESS_WS_STCS=1: streaming .cs stores; default write-back)
+  static const bool stcs = [] { const char* e = getenv("DUCHESS_WS_STCS"); return e && atoi(e) != 0; }();
+  auto k = stcs ? write_stream_kernel<true> : write_stream_kernel<false>;
+  k<<<unsigned(4 * sms), 512, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<uint4*>(buf), bytes / 16, seed);
   return cudaGetLastError() == cudaSuccess ? DUCHESS_OK : DUCHESS_ECUDA;
 }

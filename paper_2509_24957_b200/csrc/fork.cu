@@ -118,7 +118,7 @@ fork_plan_kernel(const int32_t* forks, int group_cap, const int32_t* counts, int
 // One CTA per (group, record) slot: copy the root's full blocks into the
 // child's row (refcount += 1 each, order-independent), the reserved tail
 // block + its KV bytes, -1 for the rest.
-template <int UNROLL>
+template <int UNROLL, bool STCS>
 __global__ void __launch_bounds__(128)
 fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, ForkWs ws,
                  int32_t* table, int table_stride, int32_t* refcount, const int32_t* free_list,
@@ -171,7 +171,10 @@ fork_exec_kernel(const int32_t* forks, int rows_per_group, int group_cap, ForkWs
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const int64_t i = i0 + u * 128 + threadIdx.x;
-        if (i < nv) __stcs(d4 + i, v[u]);
+        if (i < nv) {
+          if constexpr (STCS) __stcs(d4 + i, v[u]);
+          else d4[i] = v[u];
+        }
       }
     }
   } else {
@@ -361,10 +364,15 @@ extern "C" int duchess_fork_cow(const int32_t* forks, int32_t group_cap, const i
       forks, group_cap, group_counts, counts_stride, n_groups, block_tokens, ws, free_cursor,
       free_list_len, status);
   // tail-copy loads in flight per thread (env DUCHESS_K3_UNROLL, for sweeps;
-  // C4: 4 -> 0.824, 8 -> 0.83, 16 -> 0.68 of the copy peak)
-  static const int unroll = [] { const char* e = getenv("DUCHESS_K3_UNROLL"); return e ? atoi(e) : 8; }();
-  auto k = unroll >= 16 ? fork_exec_kernel<16> : unroll >= 8 ? fork_exec_kernel<8>
-         : fork_exec_kernel<4>;
+  // C4 with write-back stores: 4 -> 0.857, 8 -> 0.849, 16 -> 0.66 of the copy peak)
+  static const int unroll = [] { const char* e = getenv("DUCHESS_K3_UNROLL"); return e ? atoi(e) : 4; }();
+  // tail-copy stores: write-back (default; C4 142 vs 138 M forks/s with streaming
+  // .cs stores, env DUCHESS_K3_WB=0)
+  static const bool wb = [] { const char* e = getenv("DUCHESS_K3_WB"); return e ? atoi(e) != 0 : true; }();
+  auto k = wb ? (unroll >= 16 ? fork_exec_kernel<16, false> : unroll >= 8 ? fork_exec_kernel<8, false>
+                                                            : fork_exec_kernel<4, false>)
+              : (unroll >= 16 ? fork_exec_kernel<16, true> : unroll >= 8 ? fork_exec_kernel<8, true>
+                                                           : fork_exec_kernel<4, true>);
   k<<<unsigned(nf), 128, 0, s>>>(forks, rows_per_group, group_cap, ws, block_table, table_stride,
                                  refcount, free_list, static_cast<char*>(kv_pool),
                                  kv_bytes_per_token, block_tokens);

@@ -34,7 +34,7 @@ __device__ __forceinline__ void kv_copy_bytes(const char* sp, char* dp, int64_t 
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int64_t i = i0 + u * 32 + lane;
-        if (i < nv) __stcs(d4 + i, v[u]);
+        if (i < nv) d4[i] = v[u];          // write-back stores (as K3's C4 copies)
       }
     }
   } else {
