@@ -635,11 +635,27 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
                                   pin_memory=True)
     torch.cuda.synchronize(dev)
 
+    # input path per shard: "gather" = duchess_gather_active (SM reads of the
+    # host mapping), "dma" = the survivor list read back with the round records,
+    # then one DMA per run of consecutive rows (duchess_upload_rows); "mixed" =
+    # shard 0 by DMA, the others by gather, side by side on the link
+    mode = args.e2e_upload
+    dma = [mode == "dma" or (mode == "mixed" and k == 0) for k in range(len(srv.shards))]
+    list_bytes = [0]
+
     def step():
-        for sh in srv.shards:
+        order = [k for k in range(len(srv.shards)) if not dma[k]] + \
+                [k for k in range(len(srv.shards)) if dma[k]]
+        for k in order:
+            sh = srv.shards[k]
             with torch.cuda.stream(sh["stream"]):
                 eng = sh["eng"]
-                eng.upload_survivors(sh["host"], sh["dslab"])
+                if dma[k]:
+                    rws = eng.survivor_rows_host(sh["stream"])
+                    list_bytes[0] += 4 * (8 + len(rws))
+                    eng.upload_rows(sh["host"], sh["dslab"], rws)
+                else:
+                    eng.upload_survivors(sh["host"], sh["dslab"])
                 sh["scorer"].score_active(sh["dslab"], sh["logit"],
                                           eng.probs.view(rows, L), eng)
                 eng.round()
@@ -654,6 +670,7 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
     c0 = srv.counters()
     if world > 1:
         torch.distributed.barrier()
+    list_bytes[0] = 0
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
@@ -671,10 +688,16 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
             sh.pop(k)
     return {"value": bs / dt, "unit": UNIT,
             "h2d_bytes_per_step": bs / steps / max(world, 1) * row_bytes,
-            "h2d": "survivor windows only (duchess_gather_active over each shard's active "
-                   "list), average per rank; host buffers hold the counter-hashed windows",
+            "h2d": {"gather": "survivor windows only (duchess_gather_active over each shard's "
+                              "active list)",
+                    "dma": "survivor windows only, one DMA per run of consecutive survivor "
+                           "rows (duchess_upload_rows; list read back with the round records)",
+                    "mixed": "survivor windows only: shard 0 by DMA runs (duchess_upload_rows), "
+                             "the other shard by duchess_gather_active, side by side"}[mode]
+                   + "; average per rank; host buffers hold the counter-hashed windows",
+            "upload": mode,
             "d2h_bytes_per_step": sum((sh["rec_h"].numel() + sh["act_h"].numel()) * 4
-                                      for sh in srv.shards),
+                                      for sh in srv.shards) + list_bytes[0] / steps,
             "steps": steps, "timing": "host wall clock, streams synchronised each step"}
 
 
@@ -1537,6 +1560,10 @@ def main():
     ap.add_argument("--shards", type=int, default=None,
                     help="independent request shards (engines on separate CUDA streams) per "
                          "GPU; default 2 for c2 / c3 / c3t1, 1 otherwise")
+    ap.add_argument("--e2e-upload", default="dma", choices=["gather", "dma", "mixed"],
+                    help="e2e input path: DMA runs of the survivor rows (default; 0.201-0.205 "
+                         "M branch-steps/s at C2), the SM gather of the host mapping "
+                         "(0.189-0.195), or one shard each (0.197-0.200)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the round loop as a CUDA graph (one buffer rotation per "
                          "graph); auto = on for the launch-bound c1")

@@ -255,6 +255,12 @@ int duchess_score_active_ex(const void* acts, int32_t dtype, int64_t n_rows, int
 int duchess_gather_active(const void* src, void* dst, int64_t row_bytes,
                           const int32_t* active_rows, const int32_t* active_count,
                           int64_t n_rows, void* stream);
+/* The same copy by DMA for a survivor list the caller holds on the HOST (rows[n],
+ * any order, each in [0, n_rows)): consecutive rows are merged into runs and
+ * each run is one cudaMemcpyAsync (src pinned host memory, dst device) on
+ * `stream`. */
+int duchess_upload_rows(const void* src, void* dst, int64_t row_bytes, const int32_t* rows,
+                        int32_t n, int64_t n_rows, void* stream);
 int duchess_fill_activations(void* acts, int32_t dtype, int64_t n_rows, int32_t n_layers,
                              int32_t T, int32_t H, int64_t row_stride, int64_t layer_stride,
                              int64_t token_stride, uint64_t seed, const int64_t* row_req,

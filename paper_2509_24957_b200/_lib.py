@@ -116,6 +116,8 @@ SYMBOLS = {
                                        C.c_void_p, C.c_int32, C.c_void_p]),
     "duchess_gather_active": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                         C.c_void_p, C.c_int64, C.c_void_p]),
+    "duchess_upload_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                      C.c_int32, C.c_int64, C.c_void_p]),
     "duchess_fill_activations": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                            C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                            C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p,

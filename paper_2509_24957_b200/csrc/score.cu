@@ -16,7 +16,9 @@
 // window is split over several CTAs, merges (count, mean, M2, dot) partials
 // with Chan's formula in fixed chunk order in the last-arriving CTA, so the
 // result is deterministic run to run.
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "score_core.cuh"
@@ -1012,6 +1014,37 @@ extern "C" int duchess_score_active(const void* acts, int32_t dtype, int64_t n_r
   return duchess_score_active_ex(acts, dtype, n_rows, n_layers, T, H, row_stride, layer_stride,
                                  token_stride, wg, c1, active_rows, active_count, out_logit,
                                  out_prob, 0, stream);
+}
+
+// DMA variant of the end-to-end input path: the caller holds the survivor
+// rows on the host (e.g. read back with the round records); the rows are
+// sorted, merged into runs of consecutive rows, and each run is one
+// cudaMemcpyAsync from the host array into the same rows of dst, so the copy
+// engines move the bytes (one large H2D DMA reaches ~55 GB/s on the box's
+// link against ~51 GB/s for SM-initiated reads of the host mapping, and the
+// two run side by side on different streams).
+extern "C" int duchess_upload_rows(const void* src, void* dst, int64_t row_bytes,
+                                   const int32_t* rows, int32_t n, int64_t n_rows, void* stream) {
+  if (!src || !dst || row_bytes <= 0 || n < 0 || (n > 0 && !rows) || n_rows < 0)
+    return DUCHESS_EINVAL;
+  if (n == 0) return DUCHESS_OK;
+  std::vector<int32_t> r(rows, rows + n);
+  std::sort(r.begin(), r.end());
+  if (r.front() < 0 || r.back() >= n_rows) return DUCHESS_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  size_t i = 0;
+  while (i < r.size()) {
+    size_t j = i + 1;
+    while (j < r.size() && r[j] <= r[j - 1] + 1) ++j;    // duplicates fold into the run
+    const int64_t a = r[i], b = r[j - 1] + 1;
+    if (cudaMemcpyAsync(d + a * row_bytes, s + a * row_bytes, size_t(b - a) * size_t(row_bytes),
+                        cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return DUCHESS_ECUDA;
+    i = j;
+  }
+  return DUCHESS_OK;
 }
 
 extern "C" int duchess_gather_active(const void* src, void* dst, int64_t row_bytes,

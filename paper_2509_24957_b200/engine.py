@@ -15,6 +15,7 @@ unpacks RoundReports / RequestOutcomes.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import random
 from dataclasses import dataclass
@@ -397,6 +398,36 @@ class BatchedDuchess:
             host_acts.data_ptr(), dev_acts.data_ptr(), row_bytes,
             self.t["active_rows"].data_ptr(), self.t["active_count"].data_ptr(), rows,
             _lib.stream_handle(stream)), "duchess_gather_active")
+
+    def survivor_rows_host(self, stream=None) -> np.ndarray:
+        """The survivor rows the next scorer launch reads, read back to the
+        host (waits for the stream: the round that listed them must be done)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream()
+        st.synchronize()
+        cnt = self.t["active_count"].cpu().numpy()
+        par = int(cnt[2])
+        n = int(cnt[par])
+        rows = self.R * self.C
+        return self.t["active_rows"][par * rows: par * rows + n].cpu().numpy()
+
+    def upload_rows(self, host_acts: torch.Tensor, dev_acts: torch.Tensor, rows,
+                    stream=None) -> None:
+        """DMA flavour of upload_survivors for a survivor list the caller holds
+        on the host (e.g. survivor_rows_host()): runs of consecutive rows, one
+        cudaMemcpyAsync each (duchess_upload_rows)."""
+        if host_acts.shape != dev_acts.shape or host_acts.dtype != dev_acts.dtype:
+            raise ValueError("host and device activation arrays must match")
+        if not host_acts.is_pinned() or not dev_acts.is_cuda:
+            raise ValueError("host_acts must be pinned host memory, dev_acts a CUDA tensor")
+        if not (host_acts.is_contiguous() and dev_acts.is_contiguous()):
+            raise ValueError("activation arrays must be contiguous")
+        r = np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
+        row_bytes = host_acts[0].numel() * host_acts.element_size()
+        _lib.check(self.lib.duchess_upload_rows(
+            host_acts.data_ptr(), dev_acts.data_ptr(), row_bytes,
+            r.ctypes.data_as(ctypes.c_void_p), len(r), host_acts.shape[0],
+            _lib.stream_handle(stream)), "duchess_upload_rows")
 
     def active_list(self):
         """(rows, count) device views of the survivor list the next scorer

@@ -79,6 +79,10 @@ def test_invalid_arguments_are_rejected_before_launch():
     assert lib.duchess_gate(None, 1000, None, None) == 1
     assert lib.duchess_write_stream(None, 1 << 20, 0, None) == 1
     assert lib.duchess_row_normalize(fake, 7, 4, 16, fake, None) == 1     # unknown dtype
+    rows = (ctypes.c_int32 * 3)(5, 1, 9)
+    assert lib.duchess_upload_rows(None, fake, 64, rows, 3, 10, None) == 1
+    assert lib.duchess_upload_rows(fake, fake, 64, rows, 3, 9, None) == 1    # row 9 out of range
+    assert lib.duchess_upload_rows(fake, fake, 64, None, 0, 9, None) == 0    # nothing to copy
 
 
 @pytest.mark.parametrize("cname,pyname", [("DuchessPolicy", "Policy"),

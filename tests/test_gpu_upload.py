@@ -48,3 +48,36 @@ def test_upload_survivors_copies_only_listed_rows():
         assert not d[torch.from_numpy(~mask)].any()
         eng.probs.fill_(0.5)
         eng.round()
+
+
+def test_upload_rows_dma_runs_match_the_gather():
+    """duchess_upload_rows (DMA per run of consecutive rows) over the survivor
+    list read back to the host equals the gather over the device list, round
+    after round; arbitrary order and duplicates in a caller's list are fine."""
+    from paper_2509_24957_b200 import _lib
+    from paper_2509_24957_b200.engine import BatchedDuchess
+    knobs, traces, seeds = _setup(40, 8, 1.0)
+    R, C = 6, 8
+    eng = BatchedDuchess(traces, knobs, seeds, n_slots=R, pred_source=_lib.PRED_DEVICE,
+                         queue=list(range(len(traces))), cycle=True)
+    host = torch.randint(-1000, 1000, (R * C, 1, 3, 64), dtype=torch.int16).view(
+        torch.bfloat16).pin_memory()
+    eng.advance()
+    for step in range(6):
+        a = torch.zeros_like(host, device="cuda")
+        b = torch.zeros_like(host, device="cuda")
+        eng.upload_survivors(host, a)
+        rows = eng.survivor_rows_host()
+        assert len(rows) and sorted(rows) == sorted(np.nonzero(eng.t["row_mask"].cpu().numpy())[0])
+        eng.upload_rows(host, b, rows[::-1].copy())
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+        eng.probs.fill_(0.5)
+        eng.round()
+    c = torch.zeros_like(host, device="cuda")
+    eng.upload_rows(host, c, [5, 3, 4, 4, 40, 7])
+    torch.cuda.synchronize()
+    d, h = c.cpu().view(torch.int16), host.view(torch.int16)
+    for r in range(R * C):
+        listed = r in (3, 4, 5, 7, 40)
+        assert torch.equal(d[r], h[r]) if listed else not d[r].any()
