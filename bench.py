@@ -640,6 +640,11 @@ def run_serving_e2e(args, srv, rows, L, T, H, tdtype, dev, world):
     # then one DMA per run of consecutive rows (duchess_upload_rows); "mixed" =
     # shard 0 by DMA, the others by gather, side by side on the link
     mode = args.e2e_upload
+    if mode == "auto":
+        # DMA runs pay ~4 us of copy-engine setup per run: a win for big windows
+        # (C2 256 KB: 0.20 vs 0.19 M/s; C3 1.3 MB: 41.6 vs 37.5 K/s), a loss for
+        # last-token rows (C1 16 KB: 0.43 vs 0.71 M/s; C3-T1 40 KB: 0.92 vs 1.25 M/s)
+        mode = "dma" if row_bytes >= (128 << 10) else "gather"
     dma = [mode == "dma" or (mode == "mixed" and k == 0) for k in range(len(srv.shards))]
     list_bytes = [0]
 
@@ -1560,10 +1565,10 @@ def main():
     ap.add_argument("--shards", type=int, default=None,
                     help="independent request shards (engines on separate CUDA streams) per "
                          "GPU; default 2 for c2 / c3 / c3t1, 1 otherwise")
-    ap.add_argument("--e2e-upload", default="dma", choices=["gather", "dma", "mixed"],
-                    help="e2e input path: DMA runs of the survivor rows (default; 0.201-0.205 "
-                         "M branch-steps/s at C2), the SM gather of the host mapping "
-                         "(0.189-0.195), or one shard each (0.197-0.200)")
+    ap.add_argument("--e2e-upload", default="auto", choices=["auto", "gather", "dma", "mixed"],
+                    help="e2e input path: DMA runs of the survivor rows (C2: 0.201-0.205 "
+                         "M branch-steps/s), the SM gather of the host mapping (0.189-0.195), "
+                         "one shard each (0.197-0.200); auto = DMA for windows >= 128 KB")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the round loop as a CUDA graph (one buffer rotation per "
                          "graph); auto = on for the launch-bound c1")
