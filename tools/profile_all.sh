@@ -16,6 +16,9 @@ ncu --set full --clock-control none --import-source on -k regex:fork_exec -s 2 -
 DUCHESS_C5_ROWS=524288 ncu --set full --clock-control none --import-source on -k regex:lr_grad_ -s 2 -c 1 -o $D/k4_full -f python bench.py --config c5 --steps 3 --warmup 1 --no-cpu-baseline --no-gate > $D/k4_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:linear_kernel -s 2 -c 1 -o $D/mlp1_full -f python bench.py --config c3mlp --steps 3 --warmup 1 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/mlp1_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:mlp_probe_tc -s 2 -c 1 -o $D/mlp2_full -f python bench.py --config c3mlp --steps 3 --warmup 1 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/mlp2_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:linear_kernel -s 4 -c 1 -o $D/tc_full -f python bench.py --config difficulty --steps 3 --warmup 1 --no-cpu-baseline > $D/tc_full.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"linear_kernel|row_normalize_bulk|head_reg" -s 20 -c 5 \
+    --csv --log-file $D/launches_difficulty.csv python bench.py --config difficulty --steps 6 --warmup 3 --no-cpu-baseline > $D/bench_difficulty_under_ncu.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $D/launches_c3mlp.csv python bench.py --config c3mlp --steps 4 --warmup 2 --no-cpu-baseline --no-gate --e2e-steps 2 > $D/bench_c3mlp_under_ncu.log 2>&1
 ls -la $D

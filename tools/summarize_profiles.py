@@ -97,4 +97,6 @@ launch_list("launches_c2", "ncu --metrics gpu__time_duration.sum,dram__bytes_rea
             "dram__bytes_write.sum --clock-control none  python bench.py --steps 8 --warmup 3 "
             "(cold-cache, serialised: compare shares, not absolutes)")
 launch_list("launches_c3mlp", "the same for python bench.py --config c3mlp --steps 4 --warmup 2")
+launch_list("launches_difficulty", "ncu --metrics gpu__time_duration.sum, the classifier's "
+            "kernels in python bench.py --config difficulty (normalise, 3 layers, head)")
 print(json.dumps(summary, indent=1))
