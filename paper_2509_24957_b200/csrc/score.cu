@@ -861,9 +861,10 @@ static int score_impl(const void* acts, int32_t dtype, int64_t n_rows, int32_t n
     t.contiguous = token_stride == H;
     // Tunables (env, for sweeps): CTAs per SM and stage size target.
     static const int cps = [] { const char* e = getenv("DUCHESS_K1_CPS"); int v = e ? atoi(e) : 2; return v < 1 ? 1 : (v > 4 ? 4 : v); }();
-    // ~20 KB bulk copies (2 token rows at H = 4096 / 5120 bf16): with two request
-    // shards' scorers in flight they stream at 1.05-1.10 of the copy-measured
-    // peak vs 0.95-0.98 with one row per copy
+    // ~32 KB bulk copies (4 / 3 token rows at H = 4096 / 5120 bf16; three stages
+    // per CTA at 2 CTAs/SM): C2 26.6-26.7 M branch-steps/s vs 26.1-26.2 with
+    // ~20 KB copies and 0.95-0.98 of the copy peak with one row per copy; C3
+    // 5.67-5.70 vs 5.58 M/s (DUCHESS_K1_STAGE sweeps)
     static const int stage_target = [] { const char* e = getenv("DUCHESS_K1_STAGE"); int v = e ? atoi(e) : kScoreStageTarget; return v < 4096 ? 4096 : v; }();
     const int nvec_row = int(row_bytes / 16);
     // 0: no warp-per-window kernel, 1: register pipeline, 2 (default): bulk-copy slots

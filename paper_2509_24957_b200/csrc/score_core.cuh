@@ -50,7 +50,7 @@ __device__ __forceinline__ void write_score(const ScoreArgs& a, int64_t unit, fl
 constexpr int kTmaConsWarps = 8;
 constexpr int kTmaCons = kTmaConsWarps * 32;
 constexpr int kTmaStageTarget = 8 * 1024;     // fused step kernel; row-size bound (4x) of the TMA path
-constexpr int kScoreStageTarget = 20 * 1024;  // stand-alone scorer's stage (bulk copy) target
+constexpr int kScoreStageTarget = 32 * 1024;  // stand-alone scorer's stage (bulk copy) target
 constexpr int kTmaSmemBudget = 196 * 1024;
 
 struct TmaArgs {
